@@ -1,0 +1,90 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and
+bench.py.  Holds NONE of the method's arithmetic (no exp, no scan, no search):
+it only draws log-weights / states and derives per-replicate seeds.
+
+Recipe:
+  * Gaussian log-weights logw_i = sigma * z_i, z ~ N(0,1) from numpy PCG64,
+    cast to float32; sigma^2 in {0.1, 1, 10}.
+  * Paper-matched Dirichlet(alpha) weights as log Gamma(alpha)
+    draws: logw_i = log G_i, G_i ~ Gamma(alpha) (normalisation is irrelevant
+    to every scheme: only ratios enter).
+  * Edge-case sets: all-equal, single support (-inf elsewhere), runs of -inf,
+    NaN / +inf / all -inf (invalid).
+  * Replicate r uses resampling seed splitmix64(BASE_SEED + r).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+BASE_SEED = 0x12026163
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    """Vigna's splitmix64 finaliser (seed derivation only)."""
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    z = x
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def seed_for(replicate: int, base: int = BASE_SEED) -> int:
+    return splitmix64(base + replicate)
+
+
+def gaussian_logw(P: int, var: float = 1.0, seed: int = BASE_SEED, N: int | None = None) -> np.ndarray:
+    """float32 logw of shape (P,) or (N, P): sqrt(var) * N(0,1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shape = (P,) if N is None else (N, P)
+    z = rng.standard_normal(size=shape, dtype=np.float32)
+    return (np.float32(np.sqrt(var)) * z).astype(np.float32)
+
+
+def gaussian_logw_torch(P: int, var: float, seed: int, N: int, device):
+    """Same distribution generated directly on a torch device (bench-size inputs;
+    parity at bench size is checked on sampled outputs against numpy copies)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    z = torch.randn((N, P), generator=g, device=device, dtype=torch.float32)
+    return z * float(np.sqrt(var))
+
+
+def dirichlet_logw(P: int, alpha: float, seed: int = BASE_SEED) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    g = rng.standard_gamma(alpha, size=P)
+    with np.errstate(divide="ignore"):
+        return np.log(g).astype(np.float32)
+
+
+def equal_logw(P: int, value: float = 0.0) -> np.ndarray:
+    return np.full(P, value, dtype=np.float32)
+
+
+def single_support_logw(P: int, index: int) -> np.ndarray:
+    x = np.full(P, -np.inf, dtype=np.float32)
+    x[index] = 0.0
+    return x
+
+
+def with_neg_inf_runs(logw: np.ndarray, frac: float = 0.3, seed: int = 7) -> np.ndarray:
+    """Replace random runs of entries by -inf (zero weight), keeping >= 1 finite."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = logw.copy()
+    P = x.shape[-1]
+    n_runs = max(1, int(P * frac / 16))
+    for _ in range(n_runs):
+        s = int(rng.integers(0, P))
+        x[..., s:s + int(rng.integers(1, 32))] = -np.inf
+    flat = x.reshape(-1, P)
+    for row in flat:
+        if not np.isfinite(row).any():
+            row[0] = 0.0
+    return x
+
+
+def state_matrix(P: int, D: int, seed: int = BASE_SEED) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed ^ 0x5A5A))
+    return rng.standard_normal(size=(P, D), dtype=np.float32)
