@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""bench.py — particle-filter resampling throughput on B200.
+
+One step = one pass of the whole hot path over a batch of synthetic filters
+(BASELINE.json configs[2], "batched PMCMC: 1024 independent filters x 2^16"):
+  pf_resample_batched (log-weight max, dexp + u64 lookback scan, ancestor search)
+  -> pf_permute_batched (offspring histogram + canonical permutation)
+  -> pf_gather_state_batched (in-place gather of a D=16 float32 state).
+Metric: resampled particles/s (whole job, all ranks).  Multi-GPU: one process
+per GPU (torchrun); rank g owns filters [g*N, (g+1)*N) (global Philox filter
+indices), no data-path collective -> weak scaling; --strong splits a fixed N.
+
+--impl reference runs the CPU oracle (oracle/, the reference arm of this tier)
+on a bounded sample of the same workload on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "resampled particles/sec vs P and weight variance; % of B200 HBM/L2 roofline"
+UNIT = "particles/s"
+
+WORKLOADS = {
+    # name: (N filters per GPU, P particles, description)
+    "c3": (1024, 1 << 16, "C3 batched PMCMC: 1024 filters x 2^16 particles per GPU"),
+    "c2": (1, 1 << 20, "C2 single filter P=2^20"),
+    "p24": (1, 1 << 24, "single filter P=2^24"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--scheme", default="systematic", choices=["multinomial", "stratified", "systematic", "metropolis"])
+    ap.add_argument("--B", type=int, default=32, help="Metropolis steps (Metropolis scheme / extras)")
+    ap.add_argument("--var", type=float, default=1.0, help="log-weight variance sigma^2")
+    ap.add_argument("--D", type=int, default=16, help="state dimension (float32) for the gather")
+    ap.add_argument("--strong", action="store_true", help="split a fixed N over ranks (strong scaling)")
+    ap.add_argument("--no-extras", action="store_true", help="skip per-scheme / e2e / cpu_baseline extras")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is under load."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nme)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        top = max(sm)
+        loaded = [v for v in sm if v >= 0.5 * top] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1202_6163_b200 as pf
+    import pfinputs
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N0, P, desc = WORKLOADS[args.workload]
+    if args.strong and world > 1:
+        N = N0 // world
+        first = rank * N
+    else:
+        N = N0
+        first = rank * N0
+    stream = torch.cuda.current_stream(dev)
+    scheme = args.scheme
+    B = args.B if scheme == "metropolis" else 0
+    seed = pfinputs.seed_for(0)
+
+    # inputs resident in HBM before timing (weak scaling: each rank its own filters)
+    logw = pfinputs.gaussian_logw_torch(P, args.var, pfinputs.BASE_SEED + first, N, dev)
+    X = torch.randn((N, P, args.D), generator=torch.Generator(device=dev).manual_seed(first + 1), device=dev,
+                    dtype=torch.float32)
+    anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+    perm = torch.empty((N, P), dtype=torch.int32, device=dev)
+
+    def step():
+        pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
+        pf.pf_permute(anc, permuted=perm, stream=stream)
+        pf.pf_gather_state(X, perm, stream=stream)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: exactly K steps
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = pf.pf_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = pf.pf_launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    units = N * P * world * args.steps
+    value = units / (ms_max / 1e3)
+
+    # ---------------- per-kernel live durations (separate traced pass, same stream)
+    pf.pf_profile_enable(True)
+    kprof_steps = min(args.steps, 5)
+    for _ in range(kprof_steps):
+        step()
+    kt = pf.pf_profile_collect()
+    pf.pf_profile_enable(False)
+    torch.cuda.synchronize(dev)
+
+    # algorithmic bytes per launch of each kernel of the step
+    o = pf.pf_ancestors_to_offspring(anc)
+    survivors = int((o > 0).sum().item())
+    free = N * P - survivors
+    row = args.D * 4
+    NP = N * P
+    alg = {
+        "k_max": 4 * NP,
+        "k_scan": 12 * NP,
+        "k_merge": 12 * NP,
+        "k_bsearch": 12 * NP,
+        "k_mexp_vec": 8 * NP,
+        "k_mexp": 8 * NP,
+        "k_metro": 8 * NP,
+        "k_hist": 8 * NP,
+        "k_pscan": 12 * NP,
+        "k_merge_perm": 4 * NP + 8 * free,
+        "k_gather_inplace": 4 * NP + 2 * row * free,
+    }
+    hbm, peak_src = peaks()
+    kernels = {}
+    for name, (cnt, tot) in kt.items():
+        per = tot / max(cnt, 1)
+        ent = {"launches_per_step": cnt / kprof_steps, "avg_ms": per}
+        if name in alg:
+            ent["alg_bytes"] = alg[name]
+            ent["gbs"] = alg[name] / (per / 1e3) / 1e9
+            ent["frac_hbm"] = ent["gbs"] / hbm
+        kernels[name] = ent
+    dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
+    step_kernel_ms = sum(v["avg_ms"] * v["launches_per_step"] for v in kernels.values())
+    roofline = None
+    if dom:
+        d = kernels[dom]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(d.get("gbs", 0.0), 1), "peak": hbm,
+                    "unit": "GB/s", "frac": round(d.get("frac_hbm", 0.0), 4), "traffic": None,
+                    "alg_bytes_per_launch": d.get("alg_bytes"), "avg_ms": round(d["avg_ms"], 5),
+                    "share_of_step": round(d["avg_ms"] * d["launches_per_step"] / max(step_kernel_ms, 1e-9), 3),
+                    "peak_source": peak_src}
+
+    extras = {}
+    e2e = None
+    if not args.no_extras:
+        # ---------------- per-scheme resample-only throughput (same inputs)
+        per_scheme = {}
+        for sch in ("systematic", "stratified", "multinomial", "metropolis"):
+            b = args.B if sch == "metropolis" else 0
+            for _ in range(2):
+                pf.pf_resample_batched(sch, logw, seed, B=b, first_filter=first, ancestors=anc, stream=stream)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            reps = max(3, min(args.steps, 10))
+            a0.record(stream)
+            for _ in range(reps):
+                pf.pf_resample_batched(sch, logw, seed, B=b, first_filter=first, ancestors=anc, stream=stream)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            sms = a0.elapsed_time(a1) / reps
+            per_scheme[sch if sch != "metropolis" else f"metropolis_B{b}"] = {
+                "ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
+        extras["resample_only"] = per_scheme
+
+        # ---------------- end to end through the public API with host buffers
+        h_logw = logw.cpu().pin_memory()
+        h_out = torch.empty((N, P), dtype=torch.int32).pin_memory()
+        d_logw = torch.empty_like(logw)
+
+        def e2e_step():
+            d_logw.copy_(h_logw, non_blocking=True)
+            pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
+            pf.pf_permute(anc, permuted=perm, stream=stream)
+            pf.pf_gather_state(X, perm, stream=stream)
+            h_out.copy_(perm, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        et = torch.tensor([b0.elapsed_time(b1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": N * P * world * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": N * P * 4, "d2h_bytes_per_step": N * P * 4,
+               "note": "host logw (pinned) -> H2D -> resample/permute/gather -> D2H permuted ancestors; "
+                       "state X stays resident"}
+    clocks = sampler.stop()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        cpu = cpu_baseline(args, logw.cpu().numpy(), seed, first, budget_s=12.0)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if (args.strong and world > 1) else "weak", "vs_baseline": None,
+            "dtype": "f32 log-weights / u64 fixed-point scan / int32 indices", "data": "synthetic",
+            "config": {"workload": desc + f", sigma^2={args.var}, scheme={scheme}"
+                                  + (f", B={B}" if scheme == "metropolis" else "")
+                                  + f", in-place gather of a D={args.D} f32 state",
+                       "filters_per_gpu": N, "P": P, "var": args.var, "scheme": scheme, "D": args.D,
+                       "global_filters": N * world, "parallelism": f"filter-sharded x{world} (no collective)",
+                       "l2": "inputs larger than L2 (logw N*P*4 B, state N*P*D*4 B), no flush"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "kernels": kernels,
+            "stage_survivor_fraction": survivors / NP,
+            "extras": extras,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+def _oracle_pass(scheme, logw_np, X_np, seed, first, B, threads):
+    """Oracle pipeline (resample -> permute -> in-place gather) over the given filters, one filter
+    per task on `threads` host threads (ctypes releases the GIL; each call is single-threaded C)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    def one(n):
+        _, a = oracle.resample(scheme, logw_np[n], seed, B=B, filter_index=first + n)
+        p = oracle.permute(a)
+        X_np[n] = oracle.gather_inplace(X_np[n], p)
+        return 0
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, range(logw_np.shape[0])))
+
+
+def cpu_baseline(args, logw_np, seed, first, budget_s=12.0, n_sample=None):
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    scheme = args.scheme
+    B = args.B if scheme == "metropolis" else 0
+    N, P = logw_np.shape
+    n_s = n_sample or min(N, max(cores, 32))
+    sample = np.ascontiguousarray(logw_np[:n_s])
+    X = np.random.default_rng(0).standard_normal((n_s, P, args.D), dtype=np.float32)
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        _oracle_pass(scheme, sample, X, seed, first, B, cores)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or passes >= 50:
+            break
+    return {"value": n_s * P * passes / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{passes} pass(es) over the first {n_s} of {N} filters (P={P}, D={args.D}) of the same "
+                      f"workload: oracle resample({scheme}) -> permute -> gather, one filter per thread",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    import numpy as np
+
+    import oracle
+    import pfinputs
+
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    oracle.build()
+    N, P, desc = WORKLOADS[args.workload]
+    scheme = args.scheme
+    B = args.B if scheme == "metropolis" else 0
+    seed = pfinputs.seed_for(0)
+    cores = os.cpu_count() or 1
+    n_s = min(N, cores)  # bounded sample per step
+    logw = pfinputs.gaussian_logw(P, args.var, pfinputs.BASE_SEED, N=n_s)
+    X = np.random.default_rng(0).standard_normal((n_s, P, args.D), dtype=np.float32)
+    for _ in range(args.warmup):
+        _oracle_pass(scheme, logw, X, seed, 0, B, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _oracle_pass(scheme, logw, X, seed, 0, B, cores)
+    el = time.perf_counter() - t0
+    value = n_s * P * args.steps / el
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 log-weights / u64 fixed-point scan / int32 indices", "data": "synthetic",
+        "config": {"workload": desc + f", sigma^2={args.var}, scheme={scheme}, in-place gather of a D={args.D} "
+                              "f32 state", "filters_per_gpu": N, "P": P, "var": args.var, "scheme": scheme,
+                   "D": args.D},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: {n_s} of {N} filters (P={P}) through oracle resample -> permute "
+                                   f"-> gather, one filter per host thread", "cpu_model": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

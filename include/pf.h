@@ -1,0 +1,196 @@
+/*
+ * pf.h — C ABI of libpfresample: B200 (sm_100a) particle-filter resampling,
+ * after Murray, "GPU acceleration of the particle filter: the Metropolis
+ * resampler" (arXiv 1202.6163).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper's text); NS-n / R-n =
+ * DESIGN.md §3 numeric spec / §3.2 readings.  The problem statement is P:64-68:
+ * "Redraw, with replacement, P samples from the weighted sample set, using
+ * weights as unnormalised probabilities".
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every data pointer is CALLER-OWNED DEVICE memory (cudaMalloc / torch),
+ *    unless stated otherwise.  The library never frees caller memory.
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *    Calls only ENQUEUE work: they never synchronise the stream, never abort
+ *    and never throw.  Results are ready when the stream reaches them.
+ *  - Argument errors (NULL pointer, P < 1, N < 1, B < 0, ld < P, bad scheme,
+ *    too-small explicit workspace) are reported synchronously by the return
+ *    value and nothing is enqueued.  A failed launch returns PF_ERR_CUDA
+ *    (cudaPeekAtLastError after the launch).
+ *  - Data-dependent errors are reported asynchronously, per filter, in the
+ *    optional device array status_out (PF_FILTER_*): any NaN or +inf
+ *    log-weight, or all log-weights -inf, is invalid (NS-1); the ancestors of
+ *    an invalid filter are the identity and its lse/ess/normw are NaN.
+ *  - Log-weights are float32; -inf means zero weight.  Ancestors, offspring
+ *    and permutations are int32, 0-based.
+ *  - Randomness is a pure function of (seed, scheme, filter_index, slot): the
+ *    Philox4x32-10 counter is (c0, c1, scheme tag, filter_index) and the key
+ *    is the 64-bit seed (NS-6).  Results are bit-identical to the CPU oracle
+ *    (oracle/pfo.c) and independent of launch configuration and GPU count.
+ *  - Workspace: by default the library uses its own pool keyed by (device,
+ *    stream), grown on demand outside steady state ("pooled memory").
+ *    Concurrent calls must use different streams or explicit workspaces.
+ *  - Thread safety: distinct streams may be driven from distinct host threads.
+ */
+#ifndef PF_H
+#define PF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* pf_stream_t; /* cudaStream_t */
+
+typedef enum {
+    PF_OK = 0,
+    PF_ERR_INVALID_ARG = 1,
+    PF_ERR_WORKSPACE = 2,
+    PF_ERR_CUDA = 3,
+    PF_ERR_UNSUPPORTED = 4
+} pf_status;
+
+/* Scheme ids double as the Philox counter tag c2 (NS-6). */
+typedef enum {
+    PF_MULTINOMIAL = 1, /* Fig. 1(a): i.i.d. uniform positions      */
+    PF_STRATIFIED = 2,  /* Fig. 1(b): one offset per stratum       */
+    PF_SYSTEMATIC = 3,  /* Fig. 1(c): one shared offset (Kitagawa) */
+    PF_METROPOLIS = 4   /* Fig. 1(d): B-step chains    */
+} pf_scheme;
+
+enum { PF_FILTER_OK = 0, PF_FILTER_INVALID_WEIGHTS = 1 };
+
+/*
+ * Optional outputs and controls of pf_resample_ex / pf_resample_batched.
+ * All device pointers are nullable.  A zero-initialised struct means "none".
+ */
+typedef struct {
+    uint32_t filter_index; /* Philox c3 of a single-filter call (batched: first_filter+n) */
+    uint32_t flags;        /* reserved, must be 0 */
+    double* lse_out;       /* [N] ln sum_i exp(logw_i)  (NS-13; 1e-6 rel. of oracle)       */
+    float* normw_out;      /* [N][P] (row stride P) v_i = w_i / sum_j w_j  (NS-13)          */
+    double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */
+    int32_t* status_out;   /* [N] PF_FILTER_* per filter                                    */
+    void* workspace;       /* device, nullable -> library pool                              */
+    size_t workspace_bytes;
+} pf_opts;
+
+/*
+ * Single-filter resamplers with the north-star signature.
+ *   logw      [P] float32 log-weights (device).
+ *   P         particle count, 1 <= P <= 2^31-1.
+ *   seed      64-bit Philox key.
+ *   B         Metropolis steps per chain; ignored (must be >= 0)
+ *             by the prefix-sum schemes.  B = 0 yields the identity.
+ *   ancestors [P] int32 output (device): a_k = ancestor of slot k.
+ * The multinomial, stratified and systematic schemes compute the exact u64
+ * fixed-point inclusive scan of the weights and search it
+ * (NS-5..NS-10); stratified and systematic ancestors are nondecreasing.
+ * The Metropolis scheme needs no collective (NS-11).
+ */
+pf_status pf_resample_multinomial(const float* logw, int32_t P, uint64_t seed, int32_t B,
+                                  int32_t* ancestors, pf_stream_t stream);
+pf_status pf_resample_stratified(const float* logw, int32_t P, uint64_t seed, int32_t B,
+                                 int32_t* ancestors, pf_stream_t stream);
+pf_status pf_resample_systematic(const float* logw, int32_t P, uint64_t seed, int32_t B,
+                                 int32_t* ancestors, pf_stream_t stream);
+pf_status pf_resample_metropolis(const float* logw, int32_t P, uint64_t seed, int32_t B,
+                                 int32_t* ancestors, pf_stream_t stream);
+
+/* Same with a scheme id and optional outputs (opts nullable). */
+pf_status pf_resample_ex(pf_scheme scheme, const float* logw, int32_t P, uint64_t seed, int32_t B,
+                         int32_t* ancestors, const pf_opts* opts, pf_stream_t stream);
+
+/*
+ * Batched resampling of N independent filters (PMCMC): filter n reads
+ * logw[n*ld_logw .. +P) and writes ancestors[n*ld_anc .. +P).  Filter n is
+ * bit-identical to pf_resample_ex with filter_index = first_filter + n, so
+ * disjoint filter ranges may be resampled on different GPUs.
+ * opts->filter_index is ignored here.
+ */
+pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_logw, int32_t N, int32_t P,
+                              uint64_t seed, uint32_t first_filter, int32_t B,
+                              int32_t* ancestors, int64_t ld_anc, const pf_opts* opts, pf_stream_t stream);
+
+/* Workspace bytes a call with these sizes needs (for explicit workspaces). */
+size_t pf_workspace_bytes(pf_scheme scheme, int32_t N, int32_t P);
+
+/*
+ * Ancestors -> offspring (NS-14): offspring[i] = #{k : anc[k] == i}.
+ * anc entries must lie in [0, P).  Batched form: N rows with strides.
+ */
+pf_status pf_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* offspring, pf_stream_t stream);
+pf_status pf_ancestors_to_offspring_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P,
+                                            int32_t* offspring, int64_t ld_off, pf_stream_t stream);
+
+/*
+ * In-place permutation (NS-15; BJ north_star): permuted is a permutation of
+ * the multiset anc with permuted[i] == i for every surviving particle i
+ * (offspring > 0); the free slots, ascending, receive the extra copies in
+ * ascending survivor order.  Unique given the offspring; independent of the
+ * order of anc.  Batched form: N rows with strides.
+ */
+pf_status pf_permute(const int32_t* anc, int32_t P, int32_t* permuted, pf_stream_t stream);
+pf_status pf_permute_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P,
+                             int32_t* permuted, int64_t ld_perm, pf_stream_t stream);
+
+/*
+ * State gather in place (NS-16): for each i with permuted[i] != i,
+ * row i of X (row_bytes bytes at X + i*ld_bytes) <- row permuted[i].  Safe in
+ * place ONLY for a pf_permute output (reads touch survivors, writes touch
+ * non-survivors).  Batched: filter n's rows start at X + n*ld_filter_bytes and
+ * its permutation at permuted + n*ld_perm.
+ */
+pf_status pf_gather_state(void* X, int64_t row_bytes, int64_t ld_bytes, int32_t P,
+                          const int32_t* permuted, pf_stream_t stream);
+pf_status pf_gather_state_batched(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes,
+                                  int32_t N, int32_t P, const int32_t* permuted, int64_t ld_perm,
+                                  pf_stream_t stream);
+
+/* Out-of-place gather for arbitrary ancestors: Y[i] <- X[anc[i]]. X and Y must not overlap. */
+pf_status pf_gather_state_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y,
+                              int32_t P, const int32_t* anc, pf_stream_t stream);
+
+/*
+ * Host helper: minimum B with lambda^B <= eps (alpha+beta)/max(alpha,beta)
+ * (Eq. (4)-(5)), alpha = (1 - w_max)/(P w_max) (Eq. (2)), beta = 1/P.  Returns 0 if
+ * B = 0 already satisfies Eq. (4), -1 on invalid arguments.  Host-only, no GPU.
+ */
+int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps);
+
+const char* pf_status_string(pf_status s);
+
+/* Number of kernels this library has launched in this process (diagnostics / bench). */
+uint64_t pf_launch_count(void);
+
+/*
+ * Per-kernel tracing (SURVEY §5 "tracing"): when enabled, every kernel launch
+ * is bracketed by two CUDA events recorded on its own stream (the launching
+ * stream, so the interval is that kernel's device duration).
+ * pf_profile_collect waits for the recorded events, writes up to max_entries
+ * aggregated {kernel name, launches, total milliseconds} records, clears the
+ * record and returns the number of distinct kernels (or -1 on a CUDA error).
+ * Not for use inside CUDA-graph capture.
+ */
+typedef struct {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+} pf_kernel_time;
+void pf_profile_enable(int32_t on);
+int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries);
+
+/* Library version string. */
+const char* pf_version(void);
+
+/* Free the library workspace pool (all devices/streams).  Must not race with calls. */
+void pf_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_H */

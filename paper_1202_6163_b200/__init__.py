@@ -1,0 +1,331 @@
+"""paper_1202_6163_b200 — Python binding of libpfresample (include/pf.h).
+
+Argument marshalling only: every step of the resampling path runs in the
+sm_100a kernels of ``libpfresample.so``.  There is NO CPU fallback: if the
+library or a CUDA device is missing, every entry point raises.
+
+Function names are the C names (``pf_resample_systematic``...).  Tensors are
+torch CUDA tensors (PyTorch supplies device memory and streams only); the
+stream defaults to torch's current stream on the tensor's device.
+
+Citations: P:n = PAPER.md line n; NS-n = DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._build import LIB as _LIB_PATH
+
+PF_MULTINOMIAL, PF_STRATIFIED, PF_SYSTEMATIC, PF_METROPOLIS = 1, 2, 3, 4
+SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
+PF_FILTER_OK, PF_FILTER_INVALID_WEIGHTS = 0, 1
+
+
+class PfError(RuntimeError):
+    pass
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [
+        ("filter_index", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("lse_out", ctypes.c_void_p),
+        ("normw_out", ctypes.c_void_p),
+        ("ess_out", ctypes.c_void_p),
+        ("status_out", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_size_t),
+    ]
+
+
+_lib = None
+
+# (name, argtypes, restype) of every exported symbol of include/pf.h
+_V, _I32, _U32, _I64, _U64, _F64, _SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64,
+                                         ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t)
+_SIGS = {
+    "pf_resample_multinomial": ([_V, _I32, _U64, _I32, _V, _V], ctypes.c_int),
+    "pf_resample_stratified": ([_V, _I32, _U64, _I32, _V, _V], ctypes.c_int),
+    "pf_resample_systematic": ([_V, _I32, _U64, _I32, _V, _V], ctypes.c_int),
+    "pf_resample_metropolis": ([_V, _I32, _U64, _I32, _V, _V], ctypes.c_int),
+    "pf_resample_ex": ([ctypes.c_int, _V, _I32, _U64, _I32, _V, _V, _V], ctypes.c_int),
+    "pf_resample_batched": ([ctypes.c_int, _V, _I64, _I32, _I32, _U64, _U32, _I32, _V, _I64, _V, _V], ctypes.c_int),
+    "pf_workspace_bytes": ([ctypes.c_int, _I32, _I32], _SZ),
+    "pf_ancestors_to_offspring": ([_V, _I32, _V, _V], ctypes.c_int),
+    "pf_ancestors_to_offspring_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
+    "pf_permute": ([_V, _I32, _V, _V], ctypes.c_int),
+    "pf_permute_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
+    "pf_gather_state": ([_V, _I64, _I64, _I32, _V, _V], ctypes.c_int),
+    "pf_gather_state_batched": ([_V, _I64, _I64, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
+    "pf_gather_state_out": ([_V, _V, _I64, _I64, _I64, _I32, _V, _V], ctypes.c_int),
+    "pf_metropolis_required_B": ([_I64, _F64, _F64], _I32),
+    "pf_status_string": ([ctypes.c_int], ctypes.c_char_p),
+    "pf_launch_count": ([], _U64),
+    "pf_profile_enable": ([_I32], None),
+    "pf_profile_collect": ([_V, _I32], _I32),
+    "pf_version": ([], ctypes.c_char_p),
+    "pf_release": ([], None),
+}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libpfresample.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise PfError(f"libpfresample.so not built at {_LIB_PATH}: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+        L = ctypes.CDLL(_LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().pf_status_string(rc).decode()
+        raise PfError(f"{what} failed: {msg}")
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream(t, stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device)
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _need_cuda(t, dtype, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise PfError(f"{name} must be a CUDA tensor (libpfresample has no CPU path)")
+    if t.dtype != dtype:
+        raise PfError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _rows(t, name):
+    """(ptr, ld) of a 1-D contiguous or 2-D row-strided tensor."""
+    if t.dim() == 1:
+        if t.stride(0) != 1:
+            raise PfError(f"{name} must be contiguous")
+        return t.data_ptr(), t.shape[0]
+    if t.dim() == 2:
+        if t.stride(1) != 1:
+            raise PfError(f"{name} rows must be contiguous")
+        return t.data_ptr(), t.stride(0)
+    raise PfError(f"{name} must be 1-D or 2-D")
+
+
+def _scheme(s):
+    return SCHEMES[s] if isinstance(s, str) else int(s)
+
+
+# ----------------------------------------------------------------------------- resamplers
+def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
+                   lse_out=None, normw_out=None, ess_out=None, status_out=None, stream=None):
+    """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor."""
+    torch = _torch()
+    _need_cuda(logw, torch.float32, "logw")
+    if logw.dim() != 1 or logw.stride(0) != 1:
+        raise PfError("logw must be a contiguous 1-D tensor")
+    P = logw.shape[0]
+    if ancestors is None:
+        ancestors = torch.empty(P, dtype=torch.int32, device=logw.device)
+    _need_cuda(ancestors, torch.int32, "ancestors")
+    opts = _Opts(filter_index=filter_index)
+    if lse_out is not None:
+        _need_cuda(lse_out, torch.float64, "lse_out"); opts.lse_out = lse_out.data_ptr()
+    if ess_out is not None:
+        _need_cuda(ess_out, torch.float64, "ess_out"); opts.ess_out = ess_out.data_ptr()
+    if normw_out is not None:
+        _need_cuda(normw_out, torch.float32, "normw_out"); opts.normw_out = normw_out.data_ptr()
+    if status_out is not None:
+        _need_cuda(status_out, torch.int32, "status_out"); opts.status_out = status_out.data_ptr()
+    rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
+                              ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
+    _check(rc, "pf_resample_ex")
+    return ancestors
+
+
+def _single(name, scheme):
+    def f(logw, seed: int, B: int = 0, ancestors=None, stream=None):
+        torch = _torch()
+        _need_cuda(logw, torch.float32, "logw")
+        if logw.dim() != 1 or logw.stride(0) != 1:
+            raise PfError("logw must be a contiguous 1-D tensor")
+        P = logw.shape[0]
+        if ancestors is None:
+            ancestors = torch.empty(P, dtype=torch.int32, device=logw.device)
+        _need_cuda(ancestors, torch.int32, "ancestors")
+        rc = getattr(lib(), name)(logw.data_ptr(), P, seed & (2 ** 64 - 1), B, ancestors.data_ptr(),
+                                  _stream(logw, stream))
+        _check(rc, name)
+        return ancestors
+
+    f.__name__ = name
+    f.__doc__ = f"{name}(logw[P] f32, seed, B, ancestors=None) -> int32 ancestors (scheme {scheme})."
+    return f
+
+
+pf_resample_multinomial = _single("pf_resample_multinomial", "multinomial, Fig. 1(a)")
+pf_resample_stratified = _single("pf_resample_stratified", "stratified, Fig. 1(b)")
+pf_resample_systematic = _single("pf_resample_systematic", "systematic, Fig. 1(c)")
+pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d), P:128-140")
+
+
+def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
+                        lse_out=None, normw_out=None, ess_out=None, status_out=None, stream=None):
+    """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P]."""
+    torch = _torch()
+    _need_cuda(logw, torch.float32, "logw")
+    if logw.dim() != 2:
+        raise PfError("logw must be [N, P]")
+    N, P = logw.shape
+    ptr, ld = _rows(logw, "logw")
+    if ancestors is None:
+        ancestors = torch.empty((N, P), dtype=torch.int32, device=logw.device)
+    _need_cuda(ancestors, torch.int32, "ancestors")
+    aptr, ald = _rows(ancestors, "ancestors")
+    opts = _Opts()
+    for name, t, dt in (("lse_out", lse_out, torch.float64), ("ess_out", ess_out, torch.float64),
+                        ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32)):
+        if t is not None:
+            _need_cuda(t, dt, name)
+            setattr(opts, name, t.data_ptr())
+    rc = lib().pf_resample_batched(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
+                                   aptr, ald, ctypes.byref(opts), _stream(logw, stream))
+    _check(rc, "pf_resample_batched")
+    return ancestors
+
+
+def pf_workspace_bytes(scheme, N: int, P: int) -> int:
+    return int(lib().pf_workspace_bytes(_scheme(scheme), N, P))
+
+
+# ----------------------------------------------------------------------------- conversions
+def pf_ancestors_to_offspring(anc, offspring=None, stream=None):
+    """int32 [P] or [N, P] ancestors -> int32 offspring (NS-14)."""
+    torch = _torch()
+    _need_cuda(anc, torch.int32, "anc")
+    if offspring is None:
+        offspring = torch.empty_like(anc)
+    _need_cuda(offspring, torch.int32, "offspring")
+    if anc.dim() == 1:
+        rc = lib().pf_ancestors_to_offspring(anc.data_ptr(), anc.shape[0], offspring.data_ptr(), _stream(anc, stream))
+    else:
+        N, P = anc.shape
+        ap, ald = _rows(anc, "anc")
+        op, old = _rows(offspring, "offspring")
+        rc = lib().pf_ancestors_to_offspring_batched(ap, ald, N, P, op, old, _stream(anc, stream))
+    _check(rc, "pf_ancestors_to_offspring")
+    return offspring
+
+
+def pf_permute(anc, permuted=None, stream=None):
+    """Canonical in-place permutation (NS-15) of int32 [P] or [N, P] ancestors."""
+    torch = _torch()
+    _need_cuda(anc, torch.int32, "anc")
+    if permuted is None:
+        permuted = torch.empty_like(anc)
+    _need_cuda(permuted, torch.int32, "permuted")
+    if anc.dim() == 1:
+        rc = lib().pf_permute(anc.data_ptr(), anc.shape[0], permuted.data_ptr(), _stream(anc, stream))
+    else:
+        N, P = anc.shape
+        ap, ald = _rows(anc, "anc")
+        pp, pld = _rows(permuted, "permuted")
+        rc = lib().pf_permute_batched(ap, ald, N, P, pp, pld, _stream(anc, stream))
+    _check(rc, "pf_permute")
+    return permuted
+
+
+def pf_gather_state(X, permuted, stream=None):
+    """In place X[i] <- X[permuted[i]] (NS-16).  X: [P, ...] or [N, P, ...] CUDA tensor with
+    contiguous rows; permuted from pf_permute."""
+    torch = _torch()
+    _need_cuda(permuted, torch.int32, "permuted")
+    if not X.is_cuda:
+        raise PfError("X must be a CUDA tensor")
+    es = X.element_size()
+    if permuted.dim() == 1:
+        P = permuted.shape[0]
+        row = X[0].numel() * es if X.dim() > 1 else es
+        ld = X.stride(0) * es
+        rc = lib().pf_gather_state(X.data_ptr(), row, ld, P, permuted.data_ptr(), _stream(X, stream))
+    else:
+        N, P = permuted.shape
+        row = X[0, 0].numel() * es if X.dim() > 2 else es
+        ld = X.stride(1) * es
+        ldf = X.stride(0) * es
+        pp, pld = _rows(permuted, "permuted")
+        rc = lib().pf_gather_state_batched(X.data_ptr(), row, ld, ldf, N, P, pp, pld, _stream(X, stream))
+    _check(rc, "pf_gather_state")
+    return X
+
+
+def pf_gather_state_out(X, anc, Y=None, stream=None):
+    """Out of place Y[i] <- X[anc[i]] for arbitrary ancestors."""
+    torch = _torch()
+    _need_cuda(anc, torch.int32, "anc")
+    if Y is None:
+        Y = torch.empty_like(X)
+    es = X.element_size()
+    P = anc.shape[0]
+    row = X[0].numel() * es if X.dim() > 1 else es
+    rc = lib().pf_gather_state_out(X.data_ptr(), Y.data_ptr(), row, X.stride(0) * es, Y.stride(0) * es, P,
+                                   anc.data_ptr(), _stream(X, stream))
+    _check(rc, "pf_gather_state_out")
+    return Y
+
+
+# ----------------------------------------------------------------------------- host helpers
+def pf_metropolis_required_B(P: int, w_max: float, eps: float) -> int:
+    """Eq. (5), alpha Eq. (2), beta = 1/P."""
+    return int(lib().pf_metropolis_required_B(P, w_max, eps))
+
+
+def pf_launch_count() -> int:
+    return int(lib().pf_launch_count())
+
+
+class _KernelTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
+
+
+def pf_profile_enable(on: bool = True) -> None:
+    """Bracket every kernel launch with CUDA events on its own stream (tracing)."""
+    lib().pf_profile_enable(1 if on else 0)
+
+
+def pf_profile_collect() -> dict:
+    """{kernel name: (launches, total_ms)} since the last collect (waits for the events)."""
+    buf = (_KernelTime * 64)()
+    n = lib().pf_profile_collect(buf, 64)
+    if n < 0:
+        raise PfError("pf_profile_collect: CUDA error")
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(n, 64))}
+
+
+def pf_version() -> str:
+    return lib().pf_version().decode()
+
+
+def pf_release() -> None:
+    lib().pf_release()

@@ -1,0 +1,321 @@
+// pf_api.cu — C ABI of libpfresample (include/pf.h): argument validation,
+// the (device, stream)-keyed workspace pool ("pooled memory") and
+// the stage sequence of each entry point.  No torch types, no host sync.
+#include <atomic>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/pf.h"
+#include "pf_device.cuh"
+#include "pf_internal.h"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+struct PoolBlock {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+std::mutex g_pool_mu;
+std::map<std::pair<int, void*>, PoolBlock>& pool() {
+    static auto* m = new std::map<std::pair<int, void*>, PoolBlock>();
+    return *m;
+}
+
+// Returns a device workspace of >= bytes for (current device, stream).  Growth
+// is stream-ordered (cudaFreeAsync / cudaMallocAsync) and happens only when a
+// call needs more than any earlier call on that stream.
+pf_status pool_get(size_t bytes, cudaStream_t s, void** out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PF_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    PoolBlock& b = pool()[{dev, static_cast<void*>(s)}];
+    if (b.bytes < bytes) {
+        if (b.ptr) cudaFreeAsync(b.ptr, s);
+        b.ptr = nullptr;
+        b.bytes = 0;
+        const size_t want = bytes + bytes / 4 + (1u << 20);
+        if (cudaMallocAsync(&b.ptr, want, s) != cudaSuccess) {
+            cudaGetLastError();
+            b.ptr = nullptr;
+            return PF_ERR_WORKSPACE;
+        }
+        b.bytes = want;
+    }
+    *out = b.ptr;
+    return PF_OK;
+}
+
+pf_status get_workspace(const pf_opts* opts, size_t bytes, cudaStream_t s, void** out) {
+    if (opts && opts->workspace) {
+        if (opts->workspace_bytes < bytes) return PF_ERR_WORKSPACE;
+        *out = opts->workspace;
+        return PF_OK;
+    }
+    return pool_get(bytes, s, out);
+}
+
+// ---------------------------------------------------------------- tracing
+struct ProfRecord {
+    const char* name;
+    cudaEvent_t start, stop;
+};
+std::atomic<bool> g_prof_on{false};
+std::mutex g_prof_mu;
+std::vector<ProfRecord>& prof_records() {
+    static auto* v = new std::vector<ProfRecord>();
+    return *v;
+}
+std::vector<cudaEvent_t>& prof_free_events() {
+    static auto* v = new std::vector<cudaEvent_t>();
+    return *v;
+}
+cudaEvent_t prof_event() {
+    auto& fr = prof_free_events();
+    if (!fr.empty()) {
+        cudaEvent_t e = fr.back();
+        fr.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+pf_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
+
+unsigned needs_for(int scheme) { return scheme == PF_METROPOLIS ? pf::kNeedW : pf::kNeedQ; }
+
+pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                        uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
+                        cudaStream_t s) {
+    if (!logw || !anc) return PF_ERR_INVALID_ARG;
+    if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
+    if (N < 1 || P < 1 || B < 0 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
+    if (opts && opts->flags != 0) return PF_ERR_UNSUPPORTED;
+    double* lse = opts ? opts->lse_out : nullptr;
+    double* ess = opts ? opts->ess_out : nullptr;
+    float* normw = opts ? opts->normw_out : nullptr;
+    int32_t* status_out = opts ? opts->status_out : nullptr;
+
+    const pf::Layout L = pf::make_layout(N, P, needs_for(scheme));
+    void* base = nullptr;
+    pf_status st = get_workspace(opts, L.total, s, &base);
+    if (st != PF_OK) return st;
+    const pf::Ws ws = pf::carve(base, L);
+    uint64_t nl = 0;
+    cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e == cudaSuccess) e = pf::launch_max(logw, ld, N, P, L, ws, status_out, s, &nl);
+    const bool side = lse || ess || normw;
+    if (scheme != PF_METROPOLIS) {
+        if (e == cudaSuccess) e = pf::launch_scan(logw, ld, N, P, L, ws, P > 1, lse, ess, s, &nl);
+        if (e == cudaSuccess) {
+            if (P == 1) e = pf::launch_identity(N, P, anc, ld_anc, s, &nl);
+            else e = pf::launch_search(scheme, N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl);
+        }
+    } else {
+        if (side && e == cudaSuccess) e = pf::launch_scan(logw, ld, N, P, L, ws, false, lse, ess, s, &nl);
+        if (e == cudaSuccess)
+            e = pf::launch_metropolis(logw, ld, N, P, L, ws, seed, first_filter, B, anc, ld_anc, s, &nl);
+    }
+    if (normw && e == cudaSuccess) e = pf::launch_normw(logw, ld, N, P, ws, normw, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+}  // namespace
+
+namespace pf {
+ProfScope::ProfScope(const char* name, cudaStream_t s) : slot(-1), stream(s) {
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    ProfRecord r{name, prof_event(), prof_event()};
+    cudaEventRecord(r.start, s);
+    prof_records().push_back(r);
+    slot = static_cast<int>(prof_records().size()) - 1;
+}
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(prof_records()[slot].stop, stream);
+}
+}  // namespace pf
+
+extern "C" {
+
+void pf_profile_enable(int32_t on) { g_prof_on.store(on != 0); }
+
+int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<std::pair<std::string, std::pair<uint64_t, double>>> agg;
+    int32_t rc = 0;
+    for (auto& r : prof_records()) {
+        float ms = 0.0f;
+        if (cudaEventSynchronize(r.stop) != cudaSuccess || cudaEventElapsedTime(&ms, r.start, r.stop) != cudaSuccess)
+            rc = -1;
+        bool found = false;
+        for (auto& a : agg)
+            if (a.first == r.name) {
+                a.second.first += 1;
+                a.second.second += ms;
+                found = true;
+            }
+        if (!found) agg.push_back({r.name, {1, static_cast<double>(ms)}});
+        prof_free_events().push_back(r.start);
+        prof_free_events().push_back(r.stop);
+    }
+    prof_records().clear();
+    if (rc < 0) return -1;
+    int32_t n = 0;
+    for (auto& a : agg) {
+        if (n >= max_entries) break;
+        std::memset(out[n].name, 0, sizeof(out[n].name));
+        std::strncpy(out[n].name, a.first.c_str(), sizeof(out[n].name) - 1);
+        out[n].launches = a.second.first;
+        out[n].total_ms = a.second.second;
+        ++n;
+    }
+    return static_cast<int32_t>(agg.size());
+}
+
+
+pf_status pf_resample_ex(pf_scheme scheme, const float* logw, int32_t P, uint64_t seed, int32_t B,
+                         int32_t* ancestors, const pf_opts* opts, pf_stream_t stream) {
+    const uint32_t f = opts ? opts->filter_index : 0u;
+    return resample_impl(scheme, logw, P, 1, P, seed, f, B, ancestors, P, opts, static_cast<cudaStream_t>(stream));
+}
+
+pf_status pf_resample_multinomial(const float* logw, int32_t P, uint64_t seed, int32_t B, int32_t* ancestors,
+                                  pf_stream_t stream) {
+    return pf_resample_ex(PF_MULTINOMIAL, logw, P, seed, B, ancestors, nullptr, stream);
+}
+pf_status pf_resample_stratified(const float* logw, int32_t P, uint64_t seed, int32_t B, int32_t* ancestors,
+                                 pf_stream_t stream) {
+    return pf_resample_ex(PF_STRATIFIED, logw, P, seed, B, ancestors, nullptr, stream);
+}
+pf_status pf_resample_systematic(const float* logw, int32_t P, uint64_t seed, int32_t B, int32_t* ancestors,
+                                 pf_stream_t stream) {
+    return pf_resample_ex(PF_SYSTEMATIC, logw, P, seed, B, ancestors, nullptr, stream);
+}
+pf_status pf_resample_metropolis(const float* logw, int32_t P, uint64_t seed, int32_t B, int32_t* ancestors,
+                                 pf_stream_t stream) {
+    return pf_resample_ex(PF_METROPOLIS, logw, P, seed, B, ancestors, nullptr, stream);
+}
+
+pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_logw, int32_t N, int32_t P,
+                              uint64_t seed, uint32_t first_filter, int32_t B, int32_t* ancestors, int64_t ld_anc,
+                              const pf_opts* opts, pf_stream_t stream) {
+    return resample_impl(scheme, logw, ld_logw, N, P, seed, first_filter, B, ancestors, ld_anc, opts,
+                         static_cast<cudaStream_t>(stream));
+}
+
+size_t pf_workspace_bytes(pf_scheme scheme, int32_t N, int32_t P) {
+    if (N < 1 || P < 1) return 0;
+    const pf::Layout a = pf::make_layout(N, P, needs_for(scheme));
+    return a.total;
+}
+
+pf_status pf_ancestors_to_offspring_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P,
+                                            int32_t* offspring, int64_t ld_off, pf_stream_t stream) {
+    if (!anc || !offspring || N < 1 || P < 1 || ld_anc < P || ld_off < P) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e =
+        pf::launch_offspring(anc, ld_anc, N, P, offspring, ld_off, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* offspring, pf_stream_t stream) {
+    return pf_ancestors_to_offspring_batched(anc, P, 1, P, offspring, P, stream);
+}
+
+pf_status pf_permute_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, int32_t* permuted,
+                             int64_t ld_perm, pf_stream_t stream) {
+    if (!anc || !permuted || N < 1 || P < 1 || ld_anc < P || ld_perm < P) return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const pf::Layout L = pf::make_layout(N, P, pf::kNeedPermute);
+    void* base = nullptr;
+    pf_status st = pool_get(L.total, s, &base);
+    if (st != PF_OK) return st;
+    const pf::Ws ws = pf::carve(base, L);
+    uint64_t nl = 0;
+    cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e == cudaSuccess) e = pf::launch_permute(anc, ld_anc, N, P, L, ws, permuted, ld_perm, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_permute(const int32_t* anc, int32_t P, int32_t* permuted, pf_stream_t stream) {
+    return pf_permute_batched(anc, P, 1, P, permuted, P, stream);
+}
+
+pf_status pf_gather_state_batched(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes, int32_t N,
+                                  int32_t P, const int32_t* permuted, int64_t ld_perm, pf_stream_t stream) {
+    if (!X || !permuted || N < 1 || P < 1 || row_bytes < 1 || ld_bytes < row_bytes || ld_perm < P)
+        return PF_ERR_INVALID_ARG;
+    if (N > 1 && ld_filter_bytes < ld_bytes * P) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_gather_inplace(X, row_bytes, ld_bytes, ld_filter_bytes, N, P, permuted, ld_perm,
+                                                    static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_gather_state(void* X, int64_t row_bytes, int64_t ld_bytes, int32_t P, const int32_t* permuted,
+                          pf_stream_t stream) {
+    return pf_gather_state_batched(X, row_bytes, ld_bytes, ld_bytes * P, 1, P, permuted, P, stream);
+}
+
+pf_status pf_gather_state_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y, int32_t P,
+                              const int32_t* anc, pf_stream_t stream) {
+    if (!X || !Y || !anc || P < 1 || row_bytes < 1 || ld_x < row_bytes || ld_y < row_bytes)
+        return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e =
+        pf::launch_gather_out(X, Y, row_bytes, ld_x, ld_y, P, anc, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps) {
+    if (P < 1 || !(w_max > 0.0) || w_max > 1.0 || !(eps > 0.0)) return -1;
+    const double beta = 1.0 / static_cast<double>(P);
+    const double alpha = (1.0 - w_max) / (static_cast<double>(P) * w_max);    // Eq. (2)
+    const double lambda = 1.0 - alpha - beta;
+    const double bound = eps * (alpha + beta) / (alpha > beta ? alpha : beta);  // Eq. (4)
+    if (bound >= 1.0) return 0;
+    if (lambda <= 0.0) return 1;
+    return static_cast<int32_t>(std::ceil(std::log(bound) / std::log(lambda)));  // Eq. (5)
+}
+
+const char* pf_status_string(pf_status s) {
+    switch (s) {
+        case PF_OK: return "PF_OK";
+        case PF_ERR_INVALID_ARG: return "PF_ERR_INVALID_ARG";
+        case PF_ERR_WORKSPACE: return "PF_ERR_WORKSPACE";
+        case PF_ERR_CUDA: return "PF_ERR_CUDA";
+        case PF_ERR_UNSUPPORTED: return "PF_ERR_UNSUPPORTED";
+    }
+    return "PF_ERR_UNKNOWN";
+}
+
+uint64_t pf_launch_count(void) { return g_launches.load(); }
+
+const char* pf_version(void) { return "libpfresample 0.1 (sm_100a)"; }
+
+void pf_release(void) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto& kv : pool()) {
+        if (kv.second.ptr) cudaFree(kv.second.ptr);
+    }
+    pool().clear();
+}
+
+}  // extern "C"

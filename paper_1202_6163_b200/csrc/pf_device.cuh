@@ -1,0 +1,170 @@
+// pf_device.cuh — device primitives of libpfresample (sm_100a).
+//
+// Implements the numeric spec of DESIGN.md §3 (NS-n) for the GPU.  Shares no
+// code with oracle/ (which implements the same text on the host); bit-exact
+// agreement is the parity test.  Every float operation that decides an
+// integer is spelled out with an explicit IEEE intrinsic (__fmul_rn,
+// __fmaf_rn, __fsub_rn) so that nvcc can neither contract nor reorder it.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pf {
+
+// ---------------------------------------------------------------- NS-6
+// Philox4x32-10 (Salmon et al., SC'11).  Counter (c0, c1, tag, filter),
+// key (lo32(seed), hi32(seed)).
+struct u32x4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return {c0, c1, c2, c3};
+}
+
+struct Key {
+    uint32_t k0, k1;
+};
+__host__ __device__ __forceinline__ Key make_key(uint64_t seed) {
+    return {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)};
+}
+
+__device__ __forceinline__ uint64_t lo_word(const u32x4& v) {
+    return (static_cast<uint64_t>(v.y) << 32) | v.x;
+}
+__device__ __forceinline__ uint64_t hi_word(const u32x4& v) {
+    return (static_cast<uint64_t>(v.w) << 32) | v.z;
+}
+
+// ---------------------------------------------------------------- NS-4
+// Deterministic float32 exp of t <= 0; constants are the NS-4 bit patterns.
+__device__ __forceinline__ float dexp(float t) {
+    if (!(t >= -88.0f)) return 0.0f;                        // step 1
+    if (fabsf(t) < __uint_as_float(0x00800000u)) t = 0.0f;  // step 2
+    const float n = rintf(__fmul_rn(t, __uint_as_float(0x3FB8AA3Bu)));  // step 3
+    float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), t);            // step 4
+    r = __fmaf_rn(-n, __uint_as_float(0x35BFBE8Eu), r);
+    float p = __uint_as_float(0x39500D01u);                               // step 5
+    p = __fmaf_rn(p, r, __uint_as_float(0x3AB60B61u));
+    p = __fmaf_rn(p, r, __uint_as_float(0x3C088889u));
+    p = __fmaf_rn(p, r, __uint_as_float(0x3D2AAAABu));
+    p = __fmaf_rn(p, r, __uint_as_float(0x3E2AAAABu));
+    p = __fmaf_rn(p, r, 0.5f);
+    p = __fmaf_rn(p, r, 1.0f);
+    p = __fmaf_rn(p, r, 1.0f);
+    const int ni = static_cast<int>(n);                                   // step 6
+    if (ni < -126) return 0.0f;
+    float w = __fmul_rn(p, __uint_as_float(static_cast<uint32_t>(ni + 127) << 23));
+    if (w < __uint_as_float(0x00800000u)) return 0.0f;                   // step 7
+    return fminf(w, 1.0f);
+}
+
+// ---------------------------------------------------------------- NS-5
+// q = trunc(w * 2^kfx) computed on the float's bit fields (exact).
+__device__ __forceinline__ uint64_t quantise(float w, int kfx) {
+    const uint32_t b = __float_as_uint(w);
+    const int e = static_cast<int>(b >> 23);
+    if (e == 0) return 0ull;  // zero (dexp never returns subnormals)
+    const uint64_t mant = (b & 0x7FFFFFu) | 0x800000u;
+    const int s = e - 150 + kfx;
+    if (s >= 0) return mant << s;
+    if (s <= -24) return 0ull;
+    return mant >> (-s);
+}
+
+// w_i = dexp(fl(logw_i - lmax)) (NS-3)
+__device__ __forceinline__ float weight(float logw, float lmax) { return dexp(__fsub_rn(logw, lmax)); }
+
+// ---------------------------------------------------------------- NS-7..10
+__device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// ---------------------------------------------------------------- warp helpers
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------- lookback status words
+// 64-bit word: [63:62] flag (0 empty, 1 aggregate, 2 inclusive prefix), [61:0] value.
+// Values are <= 2^61 (NS-5) or packed pairs < 2^62 (permute).
+constexpr uint64_t kFlagShift = 62;
+constexpr uint64_t kFlagAgg = 1ull << kFlagShift;
+constexpr uint64_t kFlagInc = 2ull << kFlagShift;
+constexpr uint64_t kValueMask = (1ull << kFlagShift) - 1;
+
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Warp-cooperative decoupled lookback (Merrill & Garland 2016) over the
+// status words of tiles [0, tile) of one segment.  Returns the exclusive
+// prefix of `tile`.  Must be called by a full warp.
+__device__ __forceinline__ uint64_t lookback(const uint64_t* status, int64_t tile, int lane) {
+    uint64_t prefix = 0;
+    int64_t pred = tile - 1;
+    while (true) {
+        const int64_t idx = pred - lane;
+        uint64_t s = (idx >= 0) ? ld_acquire(status + idx) : kFlagInc;
+        while (__any_sync(0xFFFFFFFFu, (s >> kFlagShift) == 0)) {
+            if ((s >> kFlagShift) == 0) {
+                __nanosleep(20);
+                s = ld_acquire(status + idx);
+            }
+        }
+        const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (s >> kFlagShift) == 2);
+        if (inc) {
+            const int L = __ffs(inc) - 1;  // nearest inclusive predecessor
+            const uint64_t v = (lane <= L) ? (s & kValueMask) : 0ull;
+            prefix += warp_sum_u64(v);
+            return prefix;
+        }
+        prefix += warp_sum_u64(s & kValueMask);
+        pred -= 32;
+    }
+}
+
+// Host/device shared integer helpers (no method arithmetic beyond NS-5/NS-7 sizes).
+__host__ __device__ __forceinline__ int ceil_log2(int64_t P) {
+    int m = 0;
+    while ((int64_t{1} << m) < P) ++m;
+    return m;
+}
+
+}  // namespace pf

@@ -1,0 +1,84 @@
+// pf_internal.h — internal launcher interface between the C ABI (pf_api.cu)
+// and the kernels (pf_kernels.cu).  Not installed; no torch types.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pf {
+
+constexpr int kThreads = 256;           // every kernel: 8 warps
+constexpr int kItems = 16;              // items per thread in scan / merge tiles
+constexpr int kTile = kThreads * kItems;  // 4096 particles per scan tile
+constexpr int kMergeItems = kTile;      // merged (slot + particle) items per merge CTA
+constexpr int kSplitters = 4096;        // smem splitters of the multinomial search
+
+// Per-kernel event tracing (pf_profile_enable); a no-op unless enabled.
+struct ProfScope {
+    ProfScope(const char* name, cudaStream_t s);
+    ~ProfScope();
+    int slot;
+    cudaStream_t stream;
+};
+
+// Per-call device workspace (carved from the pool or a caller buffer).
+struct Ws {
+    float* lmax;         // [N]
+    int32_t* fstatus;    // [N]
+    float* max_part;     // [N*cpf]
+    int32_t* max_bad;    // [N*cpf]
+    uint32_t* max_cnt;   // [N]       zeroed per call
+    uint32_t* tile_ctr;  // [1]       zeroed per call
+    uint64_t* tstatus;   // [N*T]     zeroed per call
+    double* tsum;        // [N*T]
+    double* tsum2;       // [N*T]
+    uint64_t* Q;         // [N*ldq]   inclusive fixed-point scan
+    uint64_t* Qtot;      // [N]
+    double* S;           // [N]       sum of w (double)
+    float* w;            // [N*ldq]   Metropolis weights
+    int32_t* o;          // [N*ldq]   permute: offspring
+    uint32_t* Qe;        // [N*ldq]   permute: inclusive extras count
+    int32_t* freeslot;   // [N*ldq]   permute: r-th free slot
+    int32_t* F;          // [N]       permute: number of free slots
+};
+
+struct Layout {
+    size_t lmax, fstatus, max_part, max_bad, zero_begin, max_cnt, tile_ctr, tstatus, zero_end;
+    size_t tsum, tsum2, Q, Qtot, S, w, o, Qe, freeslot, F, total;
+    int cpf_max;  // CTAs per filter of k_max
+    int T;        // scan tiles per filter
+    int64_t ldq;  // padded row length (multiple of 4)
+};
+
+enum Need : unsigned { kNeedQ = 1u, kNeedW = 2u, kNeedPermute = 4u };
+
+Layout make_layout(int32_t N, int32_t P, unsigned need);
+Ws carve(void* base, const Layout& L);
+
+// Launchers: enqueue on `s`; return cudaPeekAtLastError().  `launches` is
+// incremented by the number of kernels enqueued.
+cudaError_t launch_max(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
+                       int32_t* status_out, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
+                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                          uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                          uint64_t* launches);
+cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L,
+                              const Ws& ws, uint64_t seed, uint32_t first_filter, int32_t B, int32_t* anc,
+                              int64_t ld_anc, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_normw(const float* logw, int64_t ld, int32_t N, int32_t P, const Ws& ws, float* normw,
+                         cudaStream_t s, uint64_t* launches);
+cudaError_t launch_identity(int32_t N, int32_t P, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                            uint64_t* launches);
+cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, int32_t* o, int64_t ld_o,
+                             cudaStream_t s, uint64_t* launches);
+cudaError_t launch_permute(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, const Layout& L,
+                           const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes, int32_t N,
+                                  int32_t P, const int32_t* perm, int64_t ld_perm, cudaStream_t s,
+                                  uint64_t* launches);
+cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y, int32_t P,
+                              const int32_t* anc, cudaStream_t s, uint64_t* launches);
+
+}  // namespace pf

@@ -1,0 +1,941 @@
+// pf_kernels.cu — sm_100a kernels of libpfresample.
+//
+// Stage map:
+//   k_max       a1      log-weight max-reduce + validation           HBM 4 B/particle
+//   k_scan      a2+a3   dexp -> u64 fixed point -> decoupled-lookback inclusive scan
+//                                                                    HBM 4 B in + 8 B out
+//   k_merge     a4+a5   merge-path search of sorted positions (stratified / systematic)
+//                                                                    HBM 8 B in + 4 B out
+//   k_bsearch   a4+a5   per-slot search of i.i.d. positions (multinomial)
+//   k_mexp/k_metro a7   Metropolis: weights once, then B-step chains (no collective)
+//   k_hist      a8      ancestors -> offspring (warp-aggregated atomics)
+//   k_pscan+k_merge a9  canonical in-place permutation
+//   k_gather_*  a10     state gather (16-byte vectors)
+// Every kernel takes the filter index n as part of a flat grid, so a batch of
+// N independent filters (a11) is one launch per stage.
+#include <cfloat>
+#include <cmath>
+
+#include "pf_device.cuh"
+#include "pf_internal.h"
+
+namespace pf {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ============================================================================ a1: max
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_max(const float* __restrict__ logw, int64_t ld, int32_t P,
+                                                  int cpf, int64_t chunk, Ws ws, int32_t* status_out) {
+    __shared__ float s_m[kThreads / 32];
+    __shared__ int s_b[kThreads / 32];
+    __shared__ int s_last;
+    const int n = blockIdx.x / cpf;
+    const int c = blockIdx.x - n * cpf;
+    const int tid = threadIdx.x;
+    const float* row = logw + static_cast<int64_t>(n) * ld;
+    const int64_t beg = static_cast<int64_t>(c) * chunk;
+    const int64_t end = min(static_cast<int64_t>(P), beg + chunk);
+    float m = -INFINITY;
+    int bad = 0;
+    auto upd = [&](float v) {
+        if (isnan(v) || v == INFINITY) bad = 1;
+        else m = fmaxf(m, v);
+    };
+    int64_t i = beg + tid;
+    if (VEC) {
+        const float4* r4 = reinterpret_cast<const float4*>(row + beg);
+        const int64_t n4 = (end > beg) ? (end - beg) / 4 : 0;
+        for (int64_t t = tid; t < n4; t += kThreads) {
+            const float4 v = __ldg(r4 + t);
+            upd(v.x); upd(v.y); upd(v.z); upd(v.w);
+        }
+        i = beg + n4 * 4 + tid;
+    }
+    for (; i < end; i += kThreads) upd(__ldg(row + i));
+    // block reduce
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        bad |= __shfl_xor_sync(kFull, bad, o);
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) { s_m[warp] = m; s_b[warp] = bad; }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < kThreads / 32; ++w) { m = fmaxf(m, s_m[w]); bad |= s_b[w]; }
+        bool finalize = true;
+        if (cpf > 1) {
+            ws.max_part[static_cast<int64_t>(n) * cpf + c] = m;
+            ws.max_bad[static_cast<int64_t>(n) * cpf + c] = bad;
+            __threadfence();
+            const unsigned prev = atomicAdd(ws.max_cnt + n, 1u);
+            finalize = (prev == static_cast<unsigned>(cpf - 1));
+        }
+        s_last = finalize ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (cpf > 1) {
+        __threadfence();
+        m = -INFINITY;
+        bad = 0;
+        for (int t = tid; t < cpf; t += kThreads) {
+            m = fmaxf(m, __ldcg(ws.max_part + static_cast<int64_t>(n) * cpf + t));
+            bad |= __ldcg(ws.max_bad + static_cast<int64_t>(n) * cpf + t);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+            bad |= __shfl_xor_sync(kFull, bad, o);
+        }
+        __syncthreads();
+        if (lane == 0) { s_m[warp] = m; s_b[warp] = bad; }
+        __syncthreads();
+        if (tid == 0) for (int w = 0; w < kThreads / 32; ++w) { m = fmaxf(m, s_m[w]); bad |= s_b[w]; }
+    }
+    if (tid == 0) {
+        const int st = (bad || m == -INFINITY) ? 1 : 0;
+        ws.lmax[n] = m;
+        ws.fstatus[n] = st;
+        if (status_out) status_out[n] = st;
+    }
+}
+
+// ============================================================================ a2+a3: scan
+// One tile = 4096 particles = 8 warps x 4 rows x (32 lanes x 4 contiguous items).
+// Tiles are taken in order from an atomic counter (forward progress of the
+// lookback), never straddle filters, and publish (aggregate | inclusive) words.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ logw, int64_t ld, int32_t P, int T,
+                                                   int kfx, Ws ws, int64_t ldq, int write_q, double* lse_out,
+                                                   double* ess_out) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_wtot[kThreads / 32];
+    __shared__ double s_sw[kThreads / 32], s_sw2[kThreads / 32];
+    __shared__ uint64_t s_off[kThreads / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(ws.tile_ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int n = static_cast<int>(tile / T);
+    const int j = static_cast<int>(tile - static_cast<int64_t>(n) * T);
+    if (ws.fstatus[n] != 0) {
+        if (j == T - 1 && tid == 0) {
+            if (lse_out) lse_out[n] = NAN;
+            if (ess_out) ess_out[n] = NAN;
+            ws.S[n] = NAN;
+        }
+        return;
+    }
+    const float lm = ws.lmax[n];
+    const float* row = logw + static_cast<int64_t>(n) * ld;
+    const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
+
+    uint64_t q[16];
+    double sw = 0.0, sw2 = 0.0;
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        float v[4];
+        if (VEC && i0 + 3 < P) {
+            const float4 t = __ldcs(reinterpret_cast<const float4*>(row + i0));
+            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = (i0 + c < P) ? row[i0 + c] : -INFINITY;
+        }
+        uint64_t loc = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float w = weight(v[c], lm);
+            sw += static_cast<double>(w);
+            sw2 += static_cast<double>(w) * static_cast<double>(w);
+            loc += quantise(w, kfx);
+            q[r * 4 + c] = loc;
+        }
+        const uint64_t incl = warp_incl_scan_u64(loc, lane);
+        const uint64_t excl = incl - loc + carry;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[r * 4 + c] += excl;
+        carry += __shfl_sync(kFull, incl, 31);
+    }
+    sw = warp_sum_f64(sw);
+    sw2 = warp_sum_f64(sw2);
+    if (lane == 0) { s_wtot[warp] = carry; s_sw[warp] = sw; s_sw2[warp] = sw2; }
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t wv = (lane < kThreads / 32) ? s_wtot[lane] : 0ull;
+        const uint64_t wi = warp_incl_scan_u64(wv, lane);
+        const uint64_t agg = __shfl_sync(kFull, wi, kThreads / 32 - 1);
+        uint64_t* st = ws.tstatus + static_cast<int64_t>(n) * T;
+        if (lane == 0) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) { a += s_sw[w]; b += s_sw2[w]; }
+            ws.tsum[tile] = a;
+            ws.tsum2[tile] = b;
+        }
+        uint64_t prefix = 0;
+        if (j == 0) {
+            if (lane == 0) st_release(st, kFlagInc | agg);
+        } else {
+            if (lane == 0) st_release(st + j, kFlagAgg | agg);
+            prefix = lookback(st, j, lane);
+            if (lane == 0) st_release(st + j, kFlagInc | (prefix + agg));
+        }
+        if (lane < kThreads / 32) s_off[lane] = prefix + wi - wv;
+        if (j == T - 1) {
+            // last tile of the filter: every predecessor's partial sums are visible
+            // (written before its first status release; acquire chain of the lookback).
+            __threadfence();
+            double a = 0.0, b = 0.0;
+            const int64_t t0 = static_cast<int64_t>(n) * T;
+            for (int t = lane; t < T; t += 32) { a += __ldcg(ws.tsum + t0 + t); b += __ldcg(ws.tsum2 + t0 + t); }
+            a = warp_sum_f64(a);
+            b = warp_sum_f64(b);
+            if (lane == 0) {
+                ws.Qtot[n] = prefix + agg;
+                ws.S[n] = a;
+                if (lse_out) lse_out[n] = static_cast<double>(lm) + log(a);
+                if (ess_out) ess_out[n] = a * a / b;
+            }
+        }
+    }
+    if (!write_q) return;
+    __syncthreads();
+    const uint64_t off = s_off[warp];
+    uint64_t* qrow = ws.Q + static_cast<int64_t>(n) * ldq;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        if (i0 + 3 < P) {
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(qrow + i0);
+            __stcg(dst, make_ulonglong2(q[r * 4 + 0] + off, q[r * 4 + 1] + off));
+            __stcg(dst + 1, make_ulonglong2(q[r * 4 + 2] + off, q[r * 4 + 3] + off));
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (i0 + c < P) qrow[i0 + c] = q[r * 4 + c] + off;
+        }
+    }
+}
+
+// ============================================================================ a4+a5: merge path
+// Merged sequence of A (positions x_k, sorted) and B (cumulative Q_i, sorted);
+// B_i precedes A_k iff Q_i <= x_k, so when x_k is emitted the number of B
+// consumed is #{i : Q_i <= x_k} = min{i : Q_i > x_k} = a_k (G6).
+struct SortedCtx {
+    int n;
+    uint64_t Qtot, D, rho;
+    uint32_t filt;
+    const uint64_t* Q;
+};
+
+template <int SCHEME>  // PF_STRATIFIED = 2, PF_SYSTEMATIC = 3
+struct ModeSorted {
+    const uint64_t* Q;
+    int64_t ldq;
+    const uint64_t* Qtot;
+    const int32_t* fstatus;
+    uint64_t D;
+    Key key;
+    uint32_t filt0;
+    int32_t P;
+    int32_t* anc;
+    int64_t ld_anc;
+
+    using Ctx = SortedCtx;
+    __device__ Ctx ctx(int n) const {
+        Ctx c;
+        c.n = n;
+        c.Qtot = Qtot[n];
+        c.D = D;
+        c.filt = filt0 + static_cast<uint32_t>(n);
+        c.Q = Q + static_cast<int64_t>(n) * ldq;
+        c.rho = 0;
+        if (SCHEME == 3) c.rho = mulhi64(lo_word(philox10(0u, 0u, 3u, c.filt, key.k0, key.k1)), D);
+        return c;
+    }
+    __device__ bool valid(int n) const { return fstatus[n] == 0; }
+    __device__ int64_t nA(const Ctx&) const { return P; }
+    __device__ uint64_t x(const Ctx& c, int64_t k) const {
+        uint64_t rho = c.rho;
+        if (SCHEME == 2) {
+            const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 2u, c.filt, key.k0, key.k1);
+            rho = mulhi64((k & 1) ? hi_word(r) : lo_word(r), c.D);
+        }
+        return mulhi64(static_cast<uint64_t>(k) * c.D + rho, c.Qtot);
+    }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return __ldg(c.Q + i); }
+    __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
+        if (SCHEME == 2) {
+            const int64_t k_even = ka0 & ~int64_t{1};
+            const int npairs = static_cast<int>((ka0 + na - k_even + 1) >> 1);
+            for (int p = threadIdx.x; p < npairs; p += kThreads) {
+                const int64_t k = k_even + 2 * p;
+                const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 2u, c.filt, key.k0, key.k1);
+                if (k >= ka0)
+                    s[k - ka0] = mulhi64(static_cast<uint64_t>(k) * c.D + mulhi64(lo_word(r), c.D), c.Qtot);
+                if (k + 1 < ka0 + na)
+                    s[k + 1 - ka0] = mulhi64(static_cast<uint64_t>(k + 1) * c.D + mulhi64(hi_word(r), c.D), c.Qtot);
+            }
+        } else {
+            for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
+        }
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        int32_t* dst = anc + static_cast<int64_t>(c.n) * ld_anc + ka0;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[t] = s_out[t];
+    }
+    __device__ void identity(int n, int c, int cpf) const {
+        const int64_t per = cdiv(P, cpf);
+        const int64_t b0 = c * per, b1 = min(static_cast<int64_t>(P), b0 + per);
+        int32_t* dst = anc + static_cast<int64_t>(n) * ld_anc;
+        for (int64_t k = b0 + threadIdx.x; k < b1; k += kThreads) dst[k] = static_cast<int32_t>(k);
+    }
+};
+
+struct PermCtx {
+    int n;
+    int64_t F;
+    const uint32_t* Qe;
+};
+
+// Canonical permutation (NS-15): free rank r -> survivor min{j : Qe_j > r}.
+struct ModePermute {
+    const uint32_t* Qe;
+    const int32_t* freeslot;
+    const int32_t* F;
+    int64_t ldq;
+    int32_t P;
+    int32_t* perm;
+    int64_t ld_perm;
+
+    using Ctx = PermCtx;
+    __device__ Ctx ctx(int n) const {
+        return {n, static_cast<int64_t>(F[n]), Qe + static_cast<int64_t>(n) * ldq};
+    }
+    __device__ bool valid(int) const { return true; }
+    __device__ int64_t nA(const Ctx& c) const { return c.F; }
+    __device__ uint64_t x(const Ctx&, int64_t r) const { return static_cast<uint64_t>(r); }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return c.Qe[i]; }
+    __device__ void fill_a(const Ctx&, int64_t ka0, int na, uint64_t* s) const {
+        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = static_cast<uint64_t>(ka0 + t);
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        const int32_t* fs = freeslot + static_cast<int64_t>(c.n) * ldq + ka0;
+        int32_t* dst = perm + static_cast<int64_t>(c.n) * ld_perm;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[fs[t]] = s_out[t];
+    }
+    __device__ void identity(int, int, int) const {}
+};
+
+template <class Mode>
+__device__ __forceinline__ int64_t merge_split(const Mode& md, const typename Mode::Ctx& c, int64_t d, int64_t nA,
+                                               int64_t nB, int lane) {
+    int64_t lo = max(int64_t{0}, d - nB), hi = min(d, nA);
+    while (hi > lo) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t m = lo + lane * step;
+        bool p = false;
+        if (m < hi) p = md.x(c, m) < md.b(c, d - 1 - m);
+        const int L = __popc(__ballot_sync(kFull, p));
+        const int64_t nlo = (L == 0) ? lo : lo + static_cast<int64_t>(L - 1) * step + 1;
+        const int64_t mL = lo + static_cast<int64_t>(L) * step;
+        hi = (mL < hi) ? mL : hi;
+        lo = nlo;
+    }
+    return lo;
+}
+
+template <class Mode>
+__global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf) {
+    __shared__ uint64_t s_keys[kMergeItems];
+    __shared__ __align__(16) int32_t s_out[kMergeItems];
+    // the two split points live in s_out[0..3] until the fill barrier (read before s_out is written)
+    int64_t* s_split = reinterpret_cast<int64_t*>(s_out);
+    const int n = blockIdx.x / cpf;
+    const int cb = blockIdx.x - n * cpf;
+    if (!md.valid(n)) {
+        md.identity(n, cb, cpf);
+        return;
+    }
+    const typename Mode::Ctx c = md.ctx(n);
+    const int64_t nA = md.nA(c), nB = md.P;
+    const int64_t total = nA + nB;
+    const int64_t d0 = static_cast<int64_t>(cb) * kMergeItems;
+    if (d0 >= total) return;
+    const int64_t d1 = min(d0 + kMergeItems, total);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp < 2) {
+        const int64_t ka = merge_split(md, c, warp ? d1 : d0, nA, nB, lane);
+        if (lane == 0) s_split[warp] = ka;
+    }
+    __syncthreads();
+    const int64_t ka0 = s_split[0], ka1 = s_split[1];
+    const int64_t ib0 = d0 - ka0;
+    const int na = static_cast<int>(ka1 - ka0);
+    const int nb = static_cast<int>((d1 - ka1) - ib0);
+    md.fill_a(c, ka0, na, s_keys);
+    for (int t = tid; t < nb; t += kThreads) s_keys[na + t] = md.b(c, ib0 + t);
+    __syncthreads();
+    const int cnt = na + nb;
+    const int dd = tid * kItems;
+    if (dd < cnt) {
+        int lo = max(0, dd - nb), hi = min(dd, na);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_keys[mid] < s_keys[na + dd - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        int a = lo, b = dd - lo;
+        const int end = min(dd + kItems, cnt);
+        for (int it = dd; it < end; ++it) {
+            const bool take_b = (b < nb) && (a >= na || s_keys[na + b] <= s_keys[a]);
+            if (take_b) {
+                ++b;
+            } else {
+                s_out[a] = static_cast<int32_t>(ib0 + b);
+                ++a;
+            }
+        }
+    }
+    __syncthreads();
+    md.emit(c, ka0, na, s_out);
+}
+
+// ============================================================================ a4+a5: multinomial
+__global__ void __launch_bounds__(kThreads) k_bsearch(int32_t P, int cpf, Ws ws, int64_t ldq, Key key,
+                                                      uint32_t filt0, int32_t* anc, int64_t ld_anc) {
+    __shared__ uint64_t spl[kSplitters];
+    const int n = blockIdx.x / cpf;
+    const int cb = blockIdx.x - n * cpf;
+    const int64_t k0 = static_cast<int64_t>(cb) * kTile;
+    const int64_t k1 = min(static_cast<int64_t>(P), k0 + kTile);
+    int32_t* arow = anc + static_cast<int64_t>(n) * ld_anc;
+    if (ws.fstatus[n] != 0) {
+        for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) arow[k] = static_cast<int32_t>(k);
+        return;
+    }
+    const uint64_t* Q = ws.Q + static_cast<int64_t>(n) * ldq;
+    const uint64_t Qtot = ws.Qtot[n];
+    const int64_t chunk = cdiv(P, kSplitters);
+    const int nspl = static_cast<int>(cdiv(P, chunk));
+    for (int s = threadIdx.x; s < nspl; s += kThreads) spl[s] = __ldg(Q + min((s + 1) * chunk, int64_t{P}) - 1);
+    __syncthreads();
+    const uint32_t filt = filt0 + static_cast<uint32_t>(n);
+    auto search = [&](uint64_t R) -> int32_t {
+        const uint64_t pos = mulhi64(R, Qtot);
+        int lo = 0, hi = nspl - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (spl[mid] > pos) hi = mid;
+            else lo = mid + 1;
+        }
+        int64_t alo = lo * chunk, ahi = min((lo + 1) * chunk, int64_t{P}) - 1;
+        while (alo < ahi) {
+            const int64_t mid = (alo + ahi) >> 1;
+            if (__ldg(Q + mid) > pos) ahi = mid;
+            else alo = mid + 1;
+        }
+        return static_cast<int32_t>(alo);
+    };
+    const bool vec = ((reinterpret_cast<uintptr_t>(arow) & 7) == 0);
+    for (int64_t k = k0 + 2 * threadIdx.x; k < k1; k += 2 * kThreads) {
+        const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 1u, filt, key.k0, key.k1);
+        const int32_t a0 = search(lo_word(r));
+        if (k + 1 < k1) {
+            const int32_t a1 = search(hi_word(r));
+            if (vec) *reinterpret_cast<int2*>(arow + k) = make_int2(a0, a1);
+            else { arow[k] = a0; arow[k + 1] = a1; }
+        } else {
+            arow[k] = a0;
+        }
+    }
+}
+
+// ============================================================================ a7: Metropolis
+__global__ void __launch_bounds__(kThreads) k_mexp(const float* __restrict__ logw, int64_t ld, int32_t N,
+                                                   int32_t P, Ws ws, int64_t ldq) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t n = g / P, i = g - n * P;
+        ws.w[n * ldq + i] = weight(__ldcs(logw + n * ld + i), ws.lmax[n]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_mexp_vec(const float4* __restrict__ logw, int64_t ld4, int32_t N,
+                                                       int32_t P4, Ws ws, int64_t ldq4) {
+    const int64_t total = static_cast<int64_t>(N) * P4;
+    float4* w4 = reinterpret_cast<float4*>(ws.w);
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t n = g / P4, i = g - n * P4;
+        const float lm = ws.lmax[n];
+        const float4 v = __ldcs(logw + n * ld4 + i);
+        w4[n * ldq4 + i] = make_float4(weight(v.x, lm), weight(v.y, lm), weight(v.z, lm), weight(v.w, lm));
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_metro(int32_t N, int32_t P, Ws ws, int64_t ldq, Key key,
+                                                    uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc) {
+    const int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (g >= static_cast<int64_t>(N) * P) return;
+    const int n = static_cast<int>(g / P);
+    const int32_t i = static_cast<int32_t>(g - static_cast<int64_t>(n) * P);
+    int32_t* out = anc + static_cast<int64_t>(n) * ld_anc + i;
+    if (B == 0 || ws.fstatus[n] != 0) {
+        *out = i;
+        return;
+    }
+    const float* w = ws.w + static_cast<int64_t>(n) * ldq;
+    const uint32_t filt = filt0 + static_cast<uint32_t>(n);
+    int32_t k = i;
+    float wk = __ldg(w + i);
+    const float kU = __uint_as_float(0x33800000u);  // 2^-24
+    for (int32_t b = 0; b < B; b += 8) {
+        uint32_t j[8];
+        float u[8], wj[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>((b >> 1) + t), 4u, filt,
+                                     key.k0, key.k1);
+            j[2 * t] = __umulhi(r.x, static_cast<uint32_t>(P));
+            u[2 * t] = __fmul_rn(static_cast<float>(r.y >> 8), kU);
+            j[2 * t + 1] = __umulhi(r.z, static_cast<uint32_t>(P));
+            u[2 * t + 1] = __fmul_rn(static_cast<float>(r.w >> 8), kU);
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) wj[s] = (b + s < B) ? __ldg(w + j[s]) : 0.0f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            if (b + s < B && __fmul_rn(u[s], wk) < wj[s]) {
+                k = static_cast<int32_t>(j[s]);
+                wk = wj[s];
+            }
+        }
+    }
+    *out = k;
+}
+
+// ============================================================================ a12: normalised weights
+__global__ void __launch_bounds__(kThreads) k_normw(const float* __restrict__ logw, int64_t ld, int32_t N,
+                                                    int32_t P, Ws ws, float* normw) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t n = g / P, i = g - n * P;
+        float v = NAN;
+        if (ws.fstatus[n] == 0)
+            v = static_cast<float>(static_cast<double>(weight(logw[n * ld + i], ws.lmax[n])) / ws.S[n]);
+        normw[g] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_identity(int32_t N, int32_t P, int32_t* anc, int64_t ld_anc) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t n = g / P, i = g - n * P;
+        anc[n * ld_anc + i] = static_cast<int32_t>(i);
+    }
+}
+
+// ============================================================================ a8: offspring
+__global__ void __launch_bounds__(kThreads) k_hist(const int32_t* __restrict__ anc, int64_t ld_anc, int32_t N,
+                                                   int32_t P, int32_t* o, int64_t ld_o) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    const int64_t g0 = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    const int64_t rounds = cdiv(total, stride);
+    for (int64_t r = 0; r < rounds; ++r) {  // warp-uniform trip count for __match_any_sync
+        const int64_t g = g0 + r * stride;
+        int32_t* addr = nullptr;
+        if (g < total) {
+            const int64_t n = g / P, k = g - n * P;
+            const int32_t a = __ldcs(anc + n * ld_anc + k);
+            if (a >= 0 && a < P) addr = o + n * ld_o + a;
+        }
+        const unsigned peers = __match_any_sync(kFull, reinterpret_cast<unsigned long long>(addr));
+        if (addr && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(addr, __popc(peers));
+    }
+}
+
+// ============================================================================ a9: permutation scan
+// Packed pair per particle: bits [0,31) free flag (o_i == 0), bits [31,62)
+// extras e_i = max(o_i - 1, 0).  Exclusive free rank and inclusive extras
+// offsets come out of one u64 lookback scan (both halves < 2^31, no carry).
+__global__ void __launch_bounds__(kThreads) k_pscan(int32_t P, int T, Ws ws, int64_t ldq, int32_t* perm,
+                                                    int64_t ld_perm) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_wtot[kThreads / 32];
+    __shared__ uint64_t s_off[kThreads / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(ws.tile_ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int n = static_cast<int>(tile / T);
+    const int j = static_cast<int>(tile - static_cast<int64_t>(n) * T);
+    const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
+    const int32_t* orow = ws.o + static_cast<int64_t>(n) * ldq;
+    int32_t ov[16];
+    uint64_t v[16];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        if (i0 + 3 < P) {
+            const int4 t = __ldcg(reinterpret_cast<const int4*>(orow + i0));
+            ov[r * 4 + 0] = t.x; ov[r * 4 + 1] = t.y; ov[r * 4 + 2] = t.z; ov[r * 4 + 3] = t.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ov[r * 4 + c] = (i0 + c < P) ? __ldcg(orow + i0 + c) : 1;
+        }
+        uint64_t loc = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int32_t o = ov[r * 4 + c];
+            const uint64_t e = (o > 1) ? static_cast<uint64_t>(o - 1) : 0ull;
+            loc += (e << 31) | (o == 0 ? 1ull : 0ull);
+            v[r * 4 + c] = loc;
+        }
+        const uint64_t incl = warp_incl_scan_u64(loc, lane);
+        const uint64_t excl = incl - loc + carry;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[r * 4 + c] += excl;
+        carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) s_wtot[warp] = carry;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t wv = (lane < kThreads / 32) ? s_wtot[lane] : 0ull;
+        const uint64_t wi = warp_incl_scan_u64(wv, lane);
+        const uint64_t agg = __shfl_sync(kFull, wi, kThreads / 32 - 1);
+        uint64_t* st = ws.tstatus + static_cast<int64_t>(n) * T;
+        uint64_t prefix = 0;
+        if (j == 0) {
+            if (lane == 0) st_release(st, kFlagInc | agg);
+        } else {
+            if (lane == 0) st_release(st + j, kFlagAgg | agg);
+            prefix = lookback(st, j, lane);
+            if (lane == 0) st_release(st + j, kFlagInc | (prefix + agg));
+        }
+        if (lane < kThreads / 32) s_off[lane] = prefix + wi - wv;
+        if (j == T - 1 && lane == 0) ws.F[n] = static_cast<int32_t>((prefix + agg) & 0x7FFFFFFFull);
+    }
+    __syncthreads();
+    const uint64_t off = s_off[warp];
+    uint32_t* qe = ws.Qe + static_cast<int64_t>(n) * ldq;
+    int32_t* fs = ws.freeslot + static_cast<int64_t>(n) * ldq;
+    int32_t* pr = perm + static_cast<int64_t>(n) * ld_perm;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        uint32_t e4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t i = i0 + c;
+            const uint64_t incl = v[r * 4 + c] + off;
+            e4[c] = static_cast<uint32_t>(incl >> 31);
+            if (i < P) {
+                if (ov[r * 4 + c] > 0) {
+                    pr[i] = static_cast<int32_t>(i);
+                } else {
+                    const uint64_t rank_excl = (incl & 0x7FFFFFFFull) - 1;  // this item is free: its own flag is 1
+                    fs[rank_excl] = static_cast<int32_t>(i);
+                }
+            }
+        }
+        if (i0 + 3 < P) {
+            __stcg(reinterpret_cast<uint4*>(qe + i0), make_uint4(e4[0], e4[1], e4[2], e4[3]));
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (i0 + c < P) qe[i0 + c] = e4[c];
+        }
+    }
+}
+
+// ============================================================================ a10: gather
+template <int CH>  // chunk bytes: 16, 4 or 1
+struct Chunk;
+template <> struct Chunk<16> { using T = int4; };
+template <> struct Chunk<4> { using T = int32_t; };
+template <> struct Chunk<1> { using T = char; };
+
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_gather_inplace(char* X, int64_t ld_bytes, int64_t ld_filter_bytes,
+                                                             int32_t N, int32_t P, int64_t cpr,
+                                                             const int32_t* __restrict__ perm, int64_t ld_perm) {
+    using T = typename Chunk<CH>::T;
+    const int64_t total = static_cast<int64_t>(N) * P * cpr;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t row = g / cpr, c = g - row * cpr;
+        const int64_t n = row / P, i = row - n * P;
+        const int32_t p = __ldg(perm + n * ld_perm + i);
+        if (p == i) continue;
+        char* base = X + n * ld_filter_bytes;
+        const T v = *reinterpret_cast<const T*>(base + p * ld_bytes + c * CH);
+        *reinterpret_cast<T*>(base + i * ld_bytes + c * CH) = v;
+    }
+}
+
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_gather_out(const char* __restrict__ X, char* __restrict__ Y,
+                                                         int64_t ld_x, int64_t ld_y, int32_t P, int64_t cpr,
+                                                         const int32_t* __restrict__ anc) {
+    using T = typename Chunk<CH>::T;
+    const int64_t total = static_cast<int64_t>(P) * cpr;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t i = g / cpr, c = g - i * cpr;
+        const int32_t p = __ldg(anc + i);
+        *reinterpret_cast<T*>(Y + i * ld_y + c * CH) = __ldg(reinterpret_cast<const T*>(X + p * ld_x + c * CH));
+    }
+}
+
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+int64_t grid_for(int64_t work, int per_sm = 8) {
+    const int64_t cap = static_cast<int64_t>(sm_count()) * per_sm;
+    const int64_t need = cdiv(work, kThreads);
+    return std::max<int64_t>(1, std::min(cap, need));
+}
+
+}  // namespace
+
+// ============================================================================ host side
+Layout make_layout(int32_t N, int32_t P, unsigned need) {
+    Layout L{};
+    const int64_t target = static_cast<int64_t>(sm_count()) * 4;
+    int64_t cpf = cdiv(target, N);
+    cpf = std::min<int64_t>(cpf, cdiv(P, 2048));
+    L.cpf_max = static_cast<int>(std::max<int64_t>(1, cpf));
+    L.T = static_cast<int>(cdiv(P, kTile));
+    L.ldq = (P + 3) / 4 * 4;
+    const int64_t NT = static_cast<int64_t>(N) * L.T;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = align_up(off, 256);
+        const size_t at = off;
+        off += bytes;
+        return at;
+    };
+    L.lmax = take(sizeof(float) * N);
+    L.fstatus = take(sizeof(int32_t) * N);
+    L.max_part = take(sizeof(float) * N * L.cpf_max);
+    L.max_bad = take(sizeof(int32_t) * N * L.cpf_max);
+    L.zero_begin = take(0);
+    L.max_cnt = take(sizeof(uint32_t) * N);
+    L.tile_ctr = take(sizeof(uint32_t));
+    L.tstatus = take(sizeof(uint64_t) * NT);
+    L.zero_end = align_up(off, 256);
+    L.tsum = take(sizeof(double) * NT);
+    L.tsum2 = take(sizeof(double) * NT);
+    L.Qtot = take(sizeof(uint64_t) * N);
+    L.S = take(sizeof(double) * N);
+    L.F = take(sizeof(int32_t) * N);
+    const size_t rows = static_cast<size_t>(N) * L.ldq;
+    L.Q = (need & kNeedQ) ? take(sizeof(uint64_t) * rows) : 0;
+    L.w = (need & kNeedW) ? take(sizeof(float) * rows) : 0;
+    L.o = (need & kNeedPermute) ? take(sizeof(int32_t) * rows) : 0;
+    L.Qe = (need & kNeedPermute) ? take(sizeof(uint32_t) * rows) : 0;
+    L.freeslot = (need & kNeedPermute) ? take(sizeof(int32_t) * rows) : 0;
+    L.total = align_up(off, 256);
+    return L;
+}
+
+Ws carve(void* base, const Layout& L) {
+    char* b = static_cast<char*>(base);
+    Ws w{};
+    w.lmax = reinterpret_cast<float*>(b + L.lmax);
+    w.fstatus = reinterpret_cast<int32_t*>(b + L.fstatus);
+    w.max_part = reinterpret_cast<float*>(b + L.max_part);
+    w.max_bad = reinterpret_cast<int32_t*>(b + L.max_bad);
+    w.max_cnt = reinterpret_cast<uint32_t*>(b + L.max_cnt);
+    w.tile_ctr = reinterpret_cast<uint32_t*>(b + L.tile_ctr);
+    w.tstatus = reinterpret_cast<uint64_t*>(b + L.tstatus);
+    w.tsum = reinterpret_cast<double*>(b + L.tsum);
+    w.tsum2 = reinterpret_cast<double*>(b + L.tsum2);
+    w.Qtot = reinterpret_cast<uint64_t*>(b + L.Qtot);
+    w.S = reinterpret_cast<double*>(b + L.S);
+    w.F = reinterpret_cast<int32_t*>(b + L.F);
+    w.Q = L.Q ? reinterpret_cast<uint64_t*>(b + L.Q) : nullptr;
+    w.w = L.w ? reinterpret_cast<float*>(b + L.w) : nullptr;
+    w.o = L.o ? reinterpret_cast<int32_t*>(b + L.o) : nullptr;
+    w.Qe = L.Qe ? reinterpret_cast<uint32_t*>(b + L.Qe) : nullptr;
+    w.freeslot = L.freeslot ? reinterpret_cast<int32_t*>(b + L.freeslot) : nullptr;
+    return w;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+cudaError_t launch_max(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
+                       int32_t* status_out, cudaStream_t s, uint64_t* launches) {
+    const int cpf = L.cpf_max;
+    int64_t chunk = cdiv(P, cpf);
+    chunk = (chunk + 3) / 4 * 4;
+    const bool vec = aligned16(logw) && (ld % 4 == 0);
+    const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
+    if (vec) { ProfScope ps_("k_max", s); k_max<true><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out); }
+    else { ProfScope ps_("k_max", s); k_max<false><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
+                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches) {
+    const int kfx = 61 - ceil_log2(P);
+    const bool vec = aligned16(logw) && (ld % 4 == 0);
+    const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * L.T));
+    if (vec)
+        { ProfScope ps_("k_scan", s); k_scan<true><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
+    else
+        { ProfScope ps_("k_scan", s); k_scan<false><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+static uint64_t stratum_width(int32_t P) {
+    const int m = ceil_log2(P);
+    if ((P & (P - 1)) == 0) return uint64_t{1} << (64 - m);
+    return UINT64_MAX / static_cast<uint64_t>(P);
+}
+
+cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                          uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                          uint64_t* launches) {
+    const Key key = make_key(seed);
+    if (scheme == 1) {
+        const int cpf = static_cast<int>(cdiv(P, kTile));
+        { ProfScope ps_("k_bsearch", s); k_bsearch<<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(
+            P, cpf, ws, L.ldq, key, first_filter, anc, ld_anc); }
+    } else {
+        const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), kMergeItems));
+        const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
+        if (scheme == 2) {
+            ModeSorted<2> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
+            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<2>><<<grid, kThreads, 0, s>>>(md, cpf); }
+        } else {
+            ModeSorted<3> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
+            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<3>><<<grid, kThreads, 0, s>>>(md, cpf); }
+        }
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L,
+                              const Ws& ws, uint64_t seed, uint32_t first_filter, int32_t B, int32_t* anc,
+                              int64_t ld_anc, cudaStream_t s, uint64_t* launches) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    if (B > 0) {
+        if (aligned16(logw) && ld % 4 == 0 && P % 4 == 0) {
+            { ProfScope ps_("k_mexp_vec", s); k_mexp_vec<<<static_cast<unsigned>(grid_for(total / 4)), kThreads, 0, s>>>(
+                reinterpret_cast<const float4*>(logw), ld / 4, N, P / 4, ws, L.ldq / 4); }
+        } else {
+            { ProfScope ps_("k_mexp", s); k_mexp<<<static_cast<unsigned>(grid_for(total)), kThreads, 0, s>>>(logw, ld, N, P, ws, L.ldq); }
+        }
+        ++*launches;
+    }
+    { ProfScope ps_("k_metro", s); k_metro<<<static_cast<unsigned>(cdiv(total, kThreads)), kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed),
+                                                                              first_filter, B, anc, ld_anc); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_normw(const float* logw, int64_t ld, int32_t N, int32_t P, const Ws& ws, float* normw,
+                         cudaStream_t s, uint64_t* launches) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    { ProfScope ps_("k_normw", s); k_normw<<<static_cast<unsigned>(grid_for(total)), kThreads, 0, s>>>(logw, ld, N, P, ws, normw); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_identity(int32_t N, int32_t P, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                            uint64_t* launches) {
+    const int64_t total = static_cast<int64_t>(N) * P;
+    { ProfScope ps_("k_identity", s); k_identity<<<static_cast<unsigned>(grid_for(total)), kThreads, 0, s>>>(N, P, anc, ld_anc); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, int32_t* o, int64_t ld_o,
+                             cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = cudaMemset2DAsync(o, static_cast<size_t>(ld_o) * 4, 0, static_cast<size_t>(P) * 4,
+                                      static_cast<size_t>(N), s);
+    if (e != cudaSuccess) return e;
+    const int64_t total = static_cast<int64_t>(N) * P;
+    { ProfScope ps_("k_hist", s); k_hist<<<static_cast<unsigned>(grid_for(total, 16)), kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_permute(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, const Layout& L,
+                           const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = launch_offspring(anc, ld_anc, N, P, ws.o, L.ldq, s, launches);
+    if (e != cudaSuccess) return e;
+    { ProfScope ps_("k_pscan", s); k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, perm,
+                                                                                     ld_perm); }
+    ++*launches;
+    const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), kMergeItems));
+    ModePermute md{ws.Qe, ws.freeslot, ws.F, L.ldq, P, perm, ld_perm};
+    { ProfScope ps_("k_merge_perm", s); k_merge<ModePermute><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes, int32_t N,
+                                  int32_t P, const int32_t* perm, int64_t ld_perm, cudaStream_t s,
+                                  uint64_t* launches) {
+    char* x = static_cast<char*>(X);
+    const bool a16 = aligned16(x) && row_bytes % 16 == 0 && ld_bytes % 16 == 0 && ld_filter_bytes % 16 == 0;
+    const bool a4 = (reinterpret_cast<uintptr_t>(x) & 3) == 0 && row_bytes % 4 == 0 && ld_bytes % 4 == 0 &&
+                    ld_filter_bytes % 4 == 0;
+    const int ch = a16 ? 16 : (a4 ? 4 : 1);
+    const int64_t cpr = row_bytes / ch;
+    const int64_t total = static_cast<int64_t>(N) * P * cpr;
+    const unsigned grid = static_cast<unsigned>(grid_for(total, 16));
+    if (ch == 16) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    else if (ch == 4) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<4><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    else { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<1><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y, int32_t P,
+                              const int32_t* anc, cudaStream_t s, uint64_t* launches) {
+    const char* x = static_cast<const char*>(X);
+    char* y = static_cast<char*>(Y);
+    const bool a16 = aligned16(x) && aligned16(y) && row_bytes % 16 == 0 && ld_x % 16 == 0 && ld_y % 16 == 0;
+    const bool a4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 3) == 0 &&
+                    row_bytes % 4 == 0 && ld_x % 4 == 0 && ld_y % 4 == 0;
+    const int ch = a16 ? 16 : (a4 ? 4 : 1);
+    const int64_t cpr = row_bytes / ch;
+    const int64_t total = static_cast<int64_t>(P) * cpr;
+    const unsigned grid = static_cast<unsigned>(grid_for(total, 16));
+    if (ch == 16) { ProfScope ps_("k_gather_out", s); k_gather_out<16><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    else if (ch == 4) { ProfScope ps_("k_gather_out", s); k_gather_out<4><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    else { ProfScope ps_("k_gather_out", s); k_gather_out<1><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+}  // namespace pf

@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA path (through the C-ABI binding) against the CPU oracle on the
+same seeded inputs.  Bit-exact for ancestors / offspring / permutations / gathers;
+lse, ess and normalised weights within 1e-6 relative (BJ north_star, NS-13).
+
+Sizes span several 4096-particle tiles and ragged tails; the full BASELINE sizes
+are checked in the launch configuration bench.py times (batched 1024 x 2^16) on
+sampled filters, and single filters up to 2^24 in full.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import pfinputs
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["multinomial", "stratified", "systematic", "metropolis"]
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_1202_6163_b200 import _build
+
+    _build.build()
+    import paper_1202_6163_b200 as pf
+
+    return pf
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+
+    return torch.device("cuda:0")
+
+
+def _gpu(x, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def _run(pf, dev, scheme, x, seed, B=0, filt=0, side=False):
+    import torch
+
+    g = _gpu(x, dev)
+    P = len(x)
+    if side:
+        lse = torch.empty(1, dtype=torch.float64, device=dev)
+        ess = torch.empty(1, dtype=torch.float64, device=dev)
+        v = torch.empty(P, dtype=torch.float32, device=dev)
+        st = torch.empty(1, dtype=torch.int32, device=dev)
+        a = pf.pf_resample_ex(scheme, g, seed, B, filter_index=filt, lse_out=lse, ess_out=ess, normw_out=v,
+                              status_out=st)
+        torch.cuda.synchronize()
+        return a.cpu().numpy(), float(lse.item()), float(ess.item()), v.cpu().numpy(), int(st.item())
+    if filt == 0:
+        fn = getattr(pf, f"pf_resample_{scheme}")
+        a = fn(g, seed, B)
+    else:
+        a = pf.pf_resample_ex(scheme, g, seed, B, filter_index=filt)
+    torch.cuda.synchronize()
+    return a.cpu().numpy()
+
+
+PS = [1, 2, 3, 7, 8, 16, 31, 1000, 4096, 4097, 12289, 65536, 100003]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("var", [0.1, 1.0, 10.0])
+def test_single_filter_bit_exact(pf, dev, orc, scheme, var):
+    for P in PS:
+        x = pfinputs.gaussian_logw(P, var, seed=P * 7 + int(var * 10))
+        for seed in (1, pfinputs.seed_for(P)):
+            B = 32 if scheme == "metropolis" else 0
+            a = _run(pf, dev, scheme, x, seed, B)
+            _, want = orc.resample(scheme, x, seed, B=B)
+            assert np.array_equal(a, want), (scheme, var, P, seed, np.nonzero(a != want)[0][:5])
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_edge_cases_bit_exact(pf, dev, orc, scheme):
+    cases = {
+        "equal": pfinputs.equal_logw(4097, -2.0),
+        "equal_pow2": pfinputs.equal_logw(8192, 5.0),
+        "single_support": pfinputs.single_support_logw(9000, 8191),
+        "single_support_first": pfinputs.single_support_logw(5000, 0),
+        "single_support_last": pfinputs.single_support_logw(5000, 4999),
+        "neg_inf_runs": pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(20000, 1.0, seed=5), frac=0.6),
+        "huge_range": np.float32(pfinputs.gaussian_logw(10000, 1.0, seed=6) * 1e4),
+        "subnormal_diffs": np.float32([1e-39, 0.0, -1e-39, 2e-39] * 100),
+        "big_offset": pfinputs.gaussian_logw(3000, 1.0, seed=8) + np.float32(1e6),
+        "dirichlet_0.01": pfinputs.dirichlet_logw(6000, 0.01, seed=3),
+    }
+    for name, x in cases.items():
+        for B in ((0, 1, 7, 33) if scheme == "metropolis" else (0,)):
+            a = _run(pf, dev, scheme, x, 12345, B)
+            st, want = orc.resample(scheme, x, 12345, B=B)
+            assert st == 0
+            assert np.array_equal(a, want), (scheme, name, B)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_invalid_inputs(pf, dev, orc, scheme):
+    for x in (np.float32([0, np.nan, 1, 2]), np.float32([0, np.inf] * 3000), np.full(5000, -np.inf, np.float32)):
+        a, lse, ess, v, st = _run(pf, dev, scheme, x, 3, B=4, side=True)
+        assert st == 1
+        assert np.array_equal(a, np.arange(len(x)))
+        assert math.isnan(lse) and math.isnan(ess) and np.all(np.isnan(v))
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_side_outputs(pf, dev, orc, scheme):
+    """lse, ess and normalised weights within 1e-6 relative of the oracle (NS-13)."""
+    for P, var in ((1, 1.0), (16, 1.0), (4097, 10.0), (1 << 20, 1.0)):
+        x = pfinputs.gaussian_logw(P, var, seed=P)
+        a, lse, ess, v, st = _run(pf, dev, scheme, x, 9, B=8, side=True)
+        _, want, wlse, wv, wess = orc.resample(scheme, x, 9, B=8, side=True)
+        assert st == 0
+        assert np.array_equal(a, want)
+        assert abs(lse - wlse) <= 1e-6 * max(1.0, abs(wlse))
+        assert abs(ess - wess) <= 1e-6 * wess
+        assert np.all(np.abs(v - wv) <= 1e-6 * np.maximum(np.abs(wv), 1e-30))
+
+
+def test_filter_index_streams(pf, dev, orc):
+    x = pfinputs.gaussian_logw(5000, 1.0, seed=2)
+    for scheme in SCHEMES:
+        a = _run(pf, dev, scheme, x, 77, B=16, filt=123456)
+        _, want = orc.resample(scheme, x, 77, B=16, filter_index=123456)
+        assert np.array_equal(a, want)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_batched_bit_exact(pf, dev, orc, scheme):
+    import torch
+
+    for N, P, ld in ((3, 1, 1), (7, 1000, 1000), (5, 4097, 4100), (64, 4096, 4096), (9, 12289, 12300)):
+        base = pfinputs.gaussian_logw(ld, 1.0, seed=N * P, N=N)
+        x = pfinputs.with_neg_inf_runs(base)
+        x[N // 2, :] = -np.inf  # one invalid filter in the batch
+        g = _gpu(x, dev)[:, :P]
+        st = torch.empty(N, dtype=torch.int32, device=dev)
+        a = pf.pf_resample_batched(scheme, g, 4242, B=12, first_filter=17, status_out=st)
+        torch.cuda.synchronize()
+        a = a.cpu().numpy()
+        wst, want = orc.resample_batched(scheme, np.ascontiguousarray(x[:, :P]), 4242, B=12, first_filter=17)
+        assert np.array_equal(st.cpu().numpy(), wst)
+        assert np.array_equal(a, want), (scheme, N, P)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_bench_config_sampled(pf, dev, orc, scheme):
+    """BASELINE C3 at full size in the launch configuration bench.py times: 1024 filters x 2^16,
+    sigma^2 = 1; sampled filters (incl. first and last) compared to the oracle in full."""
+    import torch
+
+    N, P = 1024, 1 << 16
+    x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+    B = 32 if scheme == "metropolis" else 0
+    a = pf.pf_resample_batched(scheme, x, 0xC3, B=B, first_filter=0)
+    torch.cuda.synchronize()
+    for n in (0, 1, 511, 777, 1023):
+        xn = x[n].cpu().numpy()
+        _, want = orc.resample(scheme, xn, 0xC3, B=B, filter_index=n)
+        assert np.array_equal(a[n].cpu().numpy(), want), (scheme, n)
+
+
+@pytest.mark.parametrize("P", [1 << 20, (1 << 22) + 12345, 1 << 24])
+def test_large_single_filter(pf, dev, orc, P):
+    """C2 (2^20) and larger single filters in full, all prefix-sum schemes; Metropolis on sampled chains."""
+    import torch
+
+    x = pfinputs.gaussian_logw(P, 10.0 if P > (1 << 22) else 1.0, seed=P)
+    g = _gpu(x, dev)
+    for scheme in ("multinomial", "stratified", "systematic"):
+        a = getattr(pf, f"pf_resample_{scheme}")(g, 555).cpu().numpy()
+        _, want = orc.resample(scheme, x, 555)
+        assert np.array_equal(a, want), scheme
+    a = pf.pf_resample_metropolis(g, 556, 32).cpu().numpy()
+    st, w = orc.weights(x)
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([[0, P - 1], rng.integers(0, P, 3000)]))
+    for i in idx:
+        assert a[i] == orc.metropolis_chains(w, int(i), 1, 556, 32)[0]
+
+
+def test_offspring_permute_gather(pf, dev, orc):
+    import torch
+
+    rng = np.random.default_rng(1)
+    for P in (1, 2, 5, 1000, 4097, 65536, 100003):
+        for scheme in ("multinomial", "systematic", "metropolis"):
+            x = pfinputs.gaussian_logw(P, float(rng.choice([0.1, 1.0, 10.0])), seed=P)
+            _, anc = orc.resample(scheme, x, 5, B=3)
+            anc = rng.permutation(anc).astype(np.int32) if scheme == "multinomial" else anc
+            ga = _gpu(anc, dev)
+            o = pf.pf_ancestors_to_offspring(ga)
+            perm = pf.pf_permute(ga)
+            torch.cuda.synchronize()
+            assert np.array_equal(o.cpu().numpy(), orc.ancestors_to_offspring(anc))
+            want_perm = orc.permute(anc)
+            assert np.array_equal(perm.cpu().numpy(), want_perm), (P, scheme)
+            for D in (16, 3):
+                X = pfinputs.state_matrix(P, D, seed=P)
+                gX = _gpu(X, dev)
+                pf.pf_gather_state(gX, perm)
+                Y = pf.pf_gather_state_out(_gpu(X, dev), ga)
+                torch.cuda.synchronize()
+                assert np.array_equal(gX.cpu().numpy(), orc.gather_inplace(X, want_perm))
+                assert np.array_equal(Y.cpu().numpy(), orc.gather_out(X, anc))
+
+
+def test_batched_offspring_permute_gather(pf, dev, orc):
+    import torch
+
+    N, P, D = 33, 5000, 16
+    x = pfinputs.gaussian_logw(P, 1.0, seed=1, N=N)
+    _, A = orc.resample_batched("multinomial", x, 8)
+    gA = _gpu(A, dev)
+    O = pf.pf_ancestors_to_offspring(gA)
+    Pm = pf.pf_permute(gA)
+    X = np.stack([pfinputs.state_matrix(P, D, seed=n) for n in range(N)])
+    gX = _gpu(X, dev)
+    pf.pf_gather_state(gX, Pm)
+    torch.cuda.synchronize()
+    for n in range(N):
+        assert np.array_equal(O[n].cpu().numpy(), orc.ancestors_to_offspring(A[n]))
+        wp = orc.permute(A[n])
+        assert np.array_equal(Pm[n].cpu().numpy(), wp)
+        assert np.array_equal(gX[n].cpu().numpy(), orc.gather_inplace(X[n], wp))
+
+
+def test_repeatability_and_launch_count(pf, dev):
+    import torch
+
+    x = _gpu(pfinputs.gaussian_logw(1 << 18, 1.0, seed=3), dev)
+    c0 = pf.pf_launch_count()
+    a1 = pf.pf_resample_stratified(x, 11).clone()
+    a2 = pf.pf_resample_stratified(x, 11)
+    torch.cuda.synchronize()
+    assert torch.equal(a1, a2)
+    assert pf.pf_launch_count() - c0 == 6  # max, scan, merge per call
