@@ -132,6 +132,13 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Flag and value share one 64-bit word, so the lookback needs no acquire per
+// probe: a relaxed (L1-bypassing) load sees a consistent (flag, value) pair.
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Warp-cooperative decoupled lookback (Merrill & Garland 2016) over the
 // status words of tiles [0, tile) of one segment.  Returns the exclusive
@@ -141,12 +148,9 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* status, int64_t til
     int64_t pred = tile - 1;
     while (true) {
         const int64_t idx = pred - lane;
-        uint64_t s = (idx >= 0) ? ld_acquire(status + idx) : kFlagInc;
+        uint64_t s = (idx >= 0) ? ld_relaxed(status + idx) : kFlagInc;
         while (__any_sync(0xFFFFFFFFu, (s >> kFlagShift) == 0)) {
-            if ((s >> kFlagShift) == 0) {
-                __nanosleep(20);
-                s = ld_acquire(status + idx);
-            }
+            if ((s >> kFlagShift) == 0) s = ld_relaxed(status + idx);
         }
         const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (s >> kFlagShift) == 2);
         if (inc) {

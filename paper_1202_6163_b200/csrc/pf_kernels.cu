@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_max(const float* __restrict__ logw
 // Tiles are taken in order from an atomic counter (forward progress of the
 // lookback), never straddle filters, and publish (aggregate | inclusive) words.
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ logw, int64_t ld, int32_t P, int T,
+__global__ void __launch_bounds__(kThreads, 4) k_scan(const float* __restrict__ logw, int64_t ld, int32_t P, int T,
                                                    int kfx, Ws ws, int64_t ldq, int write_q, double* lse_out,
                                                    double* ess_out) {
     __shared__ uint32_t s_tile;
@@ -137,33 +137,37 @@ __global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ log
     const float* row = logw + static_cast<int64_t>(n) * ld;
     const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
 
-    uint64_t q[16];
-    double sw = 0.0, sw2 = 0.0;
-    uint64_t carry = 0;
+    // Pass 1: load all 16 log-weights first (4 x 16-byte loads in flight), then
+    // weights.  Registers hold only w (16 floats) and the per-row exclusive
+    // lane offsets (4 x u64); q is recomputed after the tile prefix arrives.
+    float w[16];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t i0 = base + r * 128 + lane * 4;
-        float v[4];
         if (VEC && i0 + 3 < P) {
             const float4 t = __ldcs(reinterpret_cast<const float4*>(row + i0));
-            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            w[r * 4 + 0] = t.x; w[r * 4 + 1] = t.y; w[r * 4 + 2] = t.z; w[r * 4 + 3] = t.w;
         } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) v[c] = (i0 + c < P) ? row[i0 + c] : -INFINITY;
+            for (int c = 0; c < 4; ++c) w[r * 4 + c] = (i0 + c < P) ? row[i0 + c] : -INFINITY;
         }
+    }
+    double sw = 0.0, sw2 = 0.0;
+    uint64_t excl[4];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
         uint64_t loc = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const float w = weight(v[c], lm);
-            sw += static_cast<double>(w);
-            sw2 += static_cast<double>(w) * static_cast<double>(w);
-            loc += quantise(w, kfx);
-            q[r * 4 + c] = loc;
+            const float wv = weight(w[r * 4 + c], lm);
+            w[r * 4 + c] = wv;
+            sw += static_cast<double>(wv);
+            sw2 += static_cast<double>(wv) * static_cast<double>(wv);
+            loc += quantise(wv, kfx);
         }
         const uint64_t incl = warp_incl_scan_u64(loc, lane);
-        const uint64_t excl = incl - loc + carry;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) q[r * 4 + c] += excl;
+        excl[r] = incl - loc + carry;
         carry += __shfl_sync(kFull, incl, 31);
     }
     sw = warp_sum_f64(sw);
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ log
         uint64_t* st = ws.tstatus + static_cast<int64_t>(n) * T;
         if (lane == 0) {
             double a = 0.0, b = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) { a += s_sw[w]; b += s_sw2[w]; }
+            for (int k = 0; k < kThreads / 32; ++k) { a += s_sw[k]; b += s_sw2[k]; }
             ws.tsum[tile] = a;
             ws.tsum2[tile] = b;
         }
@@ -214,14 +218,21 @@ __global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ log
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t i0 = base + r * 128 + lane * 4;
+        uint64_t run = off + excl[r];
+        uint64_t q4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            run += quantise(w[r * 4 + c], kfx);
+            q4[c] = run;
+        }
         if (i0 + 3 < P) {
             ulonglong2* dst = reinterpret_cast<ulonglong2*>(qrow + i0);
-            __stcg(dst, make_ulonglong2(q[r * 4 + 0] + off, q[r * 4 + 1] + off));
-            __stcg(dst + 1, make_ulonglong2(q[r * 4 + 2] + off, q[r * 4 + 3] + off));
+            __stcg(dst, make_ulonglong2(q4[0], q4[1]));
+            __stcg(dst + 1, make_ulonglong2(q4[2], q4[3]));
         } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-                if (i0 + c < P) qrow[i0 + c] = q[r * 4 + c] + off;
+                if (i0 + c < P) qrow[i0 + c] = q4[c];
         }
     }
 }
@@ -354,12 +365,20 @@ __device__ __forceinline__ int64_t merge_split(const Mode& md, const typename Mo
     return lo;
 }
 
+// Sliding-window merge: CTA cb owns the merged diagonals [cb*chunk, +chunk).
+// One warp-parallel global search finds the start split; afterwards every
+// window of kWin merged items starts where the previous one ended, so the
+// window only needs the next kWin items of each list (smem) and a per-thread
+// diagonal search in shared memory.
+constexpr int kWin = 2048;
+constexpr int kWinItems = kWin / kThreads;  // 8 merged items per thread
+
 template <class Mode>
-__global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf) {
-    __shared__ uint64_t s_keys[kMergeItems];
-    __shared__ __align__(16) int32_t s_out[kMergeItems];
-    // the two split points live in s_out[0..3] until the fill barrier (read before s_out is written)
-    int64_t* s_split = reinterpret_cast<int64_t*>(s_out);
+__global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf, int64_t chunk) {
+    __shared__ uint64_t sA[kWin];
+    __shared__ uint64_t sB[kWin];
+    __shared__ int32_t s_out[kWin];
+    __shared__ int64_t s_split[2];
     const int n = blockIdx.x / cpf;
     const int cb = blockIdx.x - n * cpf;
     if (!md.valid(n)) {
@@ -369,45 +388,60 @@ __global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf) {
     const typename Mode::Ctx c = md.ctx(n);
     const int64_t nA = md.nA(c), nB = md.P;
     const int64_t total = nA + nB;
-    const int64_t d0 = static_cast<int64_t>(cb) * kMergeItems;
+    const int64_t d0 = static_cast<int64_t>(cb) * chunk;
     if (d0 >= total) return;
-    const int64_t d1 = min(d0 + kMergeItems, total);
+    const int64_t d1 = min(d0 + chunk, total);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (warp < 2) {
-        const int64_t ka = merge_split(md, c, warp ? d1 : d0, nA, nB, lane);
-        if (lane == 0) s_split[warp] = ka;
+    if (warp == 0) {
+        const int64_t ka = merge_split(md, c, d0, nA, nB, lane);
+        if (lane == 0) { s_split[0] = ka; s_split[1] = d0 - ka; }
     }
     __syncthreads();
-    const int64_t ka0 = s_split[0], ka1 = s_split[1];
-    const int64_t ib0 = d0 - ka0;
-    const int na = static_cast<int>(ka1 - ka0);
-    const int nb = static_cast<int>((d1 - ka1) - ib0);
-    md.fill_a(c, ka0, na, s_keys);
-    for (int t = tid; t < nb; t += kThreads) s_keys[na + t] = md.b(c, ib0 + t);
-    __syncthreads();
-    const int cnt = na + nb;
-    const int dd = tid * kItems;
-    if (dd < cnt) {
-        int lo = max(0, dd - nb), hi = min(dd, na);
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_keys[mid] < s_keys[na + dd - 1 - mid]) lo = mid + 1;
-            else hi = mid;
-        }
-        int a = lo, b = dd - lo;
-        const int end = min(dd + kItems, cnt);
-        for (int it = dd; it < end; ++it) {
-            const bool take_b = (b < nb) && (a >= na || s_keys[na + b] <= s_keys[a]);
-            if (take_b) {
-                ++b;
-            } else {
-                s_out[a] = static_cast<int32_t>(ib0 + b);
-                ++a;
+    int64_t ka = s_split[0], ib = s_split[1];
+    for (int64_t d = d0; d < d1; d += kWin) {
+        const int wlen = static_cast<int>(min(static_cast<int64_t>(kWin), d1 - d));
+        const int na = static_cast<int>(min(static_cast<int64_t>(wlen), nA - ka));
+        const int nb = static_cast<int>(min(static_cast<int64_t>(wlen), nB - ib));
+        md.fill_a(c, ka, na, sA);
+        for (int t = tid; t < nb; t += kThreads) sB[t] = md.b(c, ib + t);
+        __syncthreads();
+        const int dd = tid * kWinItems;
+        if (dd < wlen) {
+            int lo = max(0, dd - nb), hi = min(dd, na);
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sA[mid] < sB[dd - 1 - mid]) lo = mid + 1;
+                else hi = mid;
             }
+            int a = lo, b = dd - lo;
+            const int end = min(dd + kWinItems, wlen);
+            uint64_t xa = (a < na) ? sA[a] : 0ull;
+            uint64_t xb = (b < nb) ? sB[b] : 0ull;
+            const int32_t ibase = static_cast<int32_t>(ib);
+#pragma unroll
+            for (int it = 0; it < kWinItems; ++it) {
+                if (dd + it < end) {
+                    const bool take_b = (b < nb) && (a >= na || xb <= xa);
+                    if (take_b) {
+                        ++b;
+                        xb = (b < nb) ? sB[b] : 0ull;
+                    } else {
+                        s_out[a] = ibase + b;
+                        ++a;
+                        xa = (a < na) ? sA[a] : 0ull;
+                    }
+                }
+            }
+            if (end == wlen && dd + kWinItems >= wlen) { s_split[0] = a; s_split[1] = b; }
         }
+        __syncthreads();
+        const int a_end = static_cast<int>(s_split[0]);
+        const int b_end = static_cast<int>(s_split[1]);
+        md.emit(c, ka, a_end, s_out);
+        ka += a_end;
+        ib += b_end;
+        __syncthreads();
     }
-    __syncthreads();
-    md.emit(c, ka0, na, s_out);
 }
 
 // ============================================================================ a4+a5: multinomial
@@ -568,11 +602,67 @@ __global__ void __launch_bounds__(kThreads) k_hist(const int32_t* __restrict__ a
     }
 }
 
+// Offspring histogram over one filter row with P % 4 == 0 and 16-byte aligned
+// rows: each warp takes 128 consecutive ancestors (one int4 per lane) and
+// issues one reduction per run of equal values (a run head adds the distance
+// to the next head), so sorted ancestors (stratified / systematic) cost one
+// atomic per surviving particle and unsorted ones one per slot.
+__global__ void __launch_bounds__(kThreads) k_hist_runs(const int32_t* __restrict__ anc, int64_t ld_anc,
+                                                        int32_t N, int32_t P, int32_t* o, int64_t ld_o) {
+    const int lane = threadIdx.x & 31;
+    const int64_t per_row = P / 128 + ((P % 128) ? 1 : 0);  // warp-blocks per filter
+    const int64_t nblk = static_cast<int64_t>(N) * per_row;
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    for (int64_t blk = blockIdx.x * static_cast<int64_t>(kThreads / 32) + (threadIdx.x >> 5); blk < nblk;
+         blk += wstride) {
+        const int64_t n = blk / per_row;
+        const int64_t k0 = (blk - n * per_row) * 128 + lane * 4;
+        int32_t v[4] = {-1, -1, -1, -1};
+        if (k0 < P) {  // P % 4 == 0: a lane's 4 items are all valid or all beyond P
+            const int4 t = __ldcs(reinterpret_cast<const int4*>(anc + n * ld_anc + k0));
+            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        }
+        const int32_t prev = __shfl_up_sync(kFull, v[3], 1);
+        // head bits of this lane's 4 items
+        unsigned h = 0;
+        h |= (lane == 0 || v[0] != prev) ? 1u : 0u;
+        h |= (v[1] != v[0]) ? 2u : 0u;
+        h |= (v[2] != v[1]) ? 4u : 0u;
+        h |= (v[3] != v[2]) ? 8u : 0u;
+        // position of the first head in later lanes (suffix min over lanes > lane)
+        int first = h ? (lane * 4 + __ffs(h) - 1) : 128;
+        int nxt = 128;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_down_sync(kFull, first, off);
+            if (lane + off < 32) first = min(first, t);
+        }
+        // first now = min over lanes >= lane; shift by one lane for "strictly later"
+        nxt = __shfl_down_sync(kFull, first, 1);
+        if (lane == 31) nxt = 128;
+        int32_t* row = o + n * ld_o;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (!(h & (1u << c)) || v[c] < 0 || v[c] >= P) continue;
+            // run end: next head inside this lane, else the first head of a later lane
+            int end = nxt;
+#pragma unroll
+            for (int d = 3; d > c; --d)
+                if (h & (1u << d)) end = lane * 4 + d;
+            int len = end - (lane * 4 + c);
+            // the window may end before P: clip to valid items
+            const int64_t lim = P - (k0 - lane * 4);
+            if (end > lim) len = static_cast<int>(lim) - (lane * 4 + c);
+            atomicAdd(row + v[c], len);
+        }
+    }
+}
+
 // ============================================================================ a9: permutation scan
 // Packed pair per particle: bits [0,31) free flag (o_i == 0), bits [31,62)
 // extras e_i = max(o_i - 1, 0).  Exclusive free rank and inclusive extras
 // offsets come out of one u64 lookback scan (both halves < 2^31, no carry).
-__global__ void __launch_bounds__(kThreads) k_pscan(int32_t P, int T, Ws ws, int64_t ldq, int32_t* perm,
+__global__ void __launch_bounds__(kThreads, 5) k_pscan(int32_t P, int T, Ws ws, int64_t ldq, int32_t* perm,
                                                     int64_t ld_perm) {
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_wtot[kThreads / 32];
@@ -586,8 +676,6 @@ __global__ void __launch_bounds__(kThreads) k_pscan(int32_t P, int T, Ws ws, int
     const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
     const int32_t* orow = ws.o + static_cast<int64_t>(n) * ldq;
     int32_t ov[16];
-    uint64_t v[16];
-    uint64_t carry = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t i0 = base + r * 128 + lane * 4;
@@ -598,18 +686,20 @@ __global__ void __launch_bounds__(kThreads) k_pscan(int32_t P, int T, Ws ws, int
 #pragma unroll
             for (int c = 0; c < 4; ++c) ov[r * 4 + c] = (i0 + c < P) ? __ldcg(orow + i0 + c) : 1;
         }
+    }
+    auto packed = [](int32_t o) -> uint64_t {
+        const uint64_t e = (o > 1) ? static_cast<uint64_t>(o - 1) : 0ull;
+        return (e << 31) | (o == 0 ? 1ull : 0ull);
+    };
+    uint64_t excl[4];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
         uint64_t loc = 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int32_t o = ov[r * 4 + c];
-            const uint64_t e = (o > 1) ? static_cast<uint64_t>(o - 1) : 0ull;
-            loc += (e << 31) | (o == 0 ? 1ull : 0ull);
-            v[r * 4 + c] = loc;
-        }
+        for (int c = 0; c < 4; ++c) loc += packed(ov[r * 4 + c]);
         const uint64_t incl = warp_incl_scan_u64(loc, lane);
-        const uint64_t excl = incl - loc + carry;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) v[r * 4 + c] += excl;
+        excl[r] = incl - loc + carry;
         carry += __shfl_sync(kFull, incl, 31);
     }
     if (lane == 0) s_wtot[warp] = carry;
@@ -638,17 +728,18 @@ __global__ void __launch_bounds__(kThreads) k_pscan(int32_t P, int T, Ws ws, int
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t i0 = base + r * 128 + lane * 4;
+        uint64_t run = off + excl[r];
         uint32_t e4[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int64_t i = i0 + c;
-            const uint64_t incl = v[r * 4 + c] + off;
-            e4[c] = static_cast<uint32_t>(incl >> 31);
+            run += packed(ov[r * 4 + c]);
+            e4[c] = static_cast<uint32_t>(run >> 31);
             if (i < P) {
                 if (ov[r * 4 + c] > 0) {
                     pr[i] = static_cast<int32_t>(i);
                 } else {
-                    const uint64_t rank_excl = (incl & 0x7FFFFFFFull) - 1;  // this item is free: its own flag is 1
+                    const uint64_t rank_excl = (run & 0x7FFFFFFFull) - 1;  // this item is free: its own flag is 1
                     fs[rank_excl] = static_cast<int32_t>(i);
                 }
             }
@@ -688,17 +779,121 @@ __global__ void __launch_bounds__(kThreads) k_gather_inplace(char* X, int64_t ld
     }
 }
 
+// In-place gather, 16-byte chunks, warp-cooperative: each warp takes 128
+// consecutive rows (one int4 of permutation entries per lane), compacts the
+// moved rows (perm[i] != i) into a per-warp list, then copies their chunks
+// with up to kGU 16-byte loads in flight per lane before any store.  Safe in
+// place: loads only touch survivor rows, stores only non-survivor rows.
+constexpr int kGU = 8;
+__global__ void __launch_bounds__(kThreads) k_gather_rows16(char* X, int64_t ld_bytes, int64_t ld_filter_bytes,
+                                                            int32_t N, int32_t P, int cpr,
+                                                            const int32_t* __restrict__ perm, int64_t ld_perm,
+                                                            int vec_perm) {
+    __shared__ int64_t s_dst[kThreads / 32][128];
+    __shared__ int64_t s_src[kThreads / 32][128];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t rows = static_cast<int64_t>(N) * P;
+    const int64_t nblk = cdiv(rows, 128);
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    for (int64_t blk = blockIdx.x * static_cast<int64_t>(kThreads / 32) + warp; blk < nblk; blk += wstride) {
+        const int64_t r0 = blk * 128 + lane * 4;
+        int32_t pv[4];
+        int64_t rr[4];
+        int moved = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rr[c] = r0 + c;
+        if (vec_perm && r0 + 3 < rows && (r0 / P) == ((r0 + 3) / P)) {
+            const int64_t n = r0 / P, i = r0 - n * P;
+            const int4 t = __ldg(reinterpret_cast<const int4*>(perm + n * ld_perm + i));
+            pv[0] = t.x; pv[1] = t.y; pv[2] = t.z; pv[3] = t.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                pv[c] = -1;
+                if (rr[c] < rows) {
+                    const int64_t n = rr[c] / P, i = rr[c] - n * P;
+                    pv[c] = __ldg(perm + n * ld_perm + i);
+                }
+            }
+        }
+        unsigned mbits = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (rr[c] < rows) {
+                const int64_t n = rr[c] / P, i = rr[c] - n * P;
+                if (pv[c] != i) { mbits |= 1u << c; ++moved; }
+            }
+        }
+        // warp exclusive scan of moved counts -> slots in the per-warp list
+        int incl = moved;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int nmoved = __shfl_sync(kFull, incl, 31);
+        int at = incl - moved;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (mbits & (1u << c)) {
+                const int64_t n = rr[c] / P, i = rr[c] - n * P;
+                char* base = X + n * ld_filter_bytes;
+                s_dst[warp][at] = reinterpret_cast<int64_t>(base + i * ld_bytes);
+                s_src[warp][at] = reinterpret_cast<int64_t>(base + static_cast<int64_t>(pv[c]) * ld_bytes);
+                ++at;
+            }
+        }
+        __syncwarp();
+        const int items = nmoved * cpr;
+        for (int it0 = 0; it0 < items; it0 += 32 * kGU) {
+            int4 v[kGU];
+#pragma unroll
+            for (int u = 0; u < kGU; ++u) {
+                const int it = it0 + u * 32 + lane;
+                if (it < items) {
+                    const int rw = it / cpr, ch = it - rw * cpr;
+                    v[u] = *(reinterpret_cast<const int4*>(s_src[warp][rw]) + ch);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kGU; ++u) {
+                const int it = it0 + u * 32 + lane;
+                if (it < items) {
+                    const int rw = it / cpr, ch = it - rw * cpr;
+                    __stcs(reinterpret_cast<int4*>(s_dst[warp][rw]) + ch, v[u]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <int CH>
 __global__ void __launch_bounds__(kThreads) k_gather_out(const char* __restrict__ X, char* __restrict__ Y,
                                                          int64_t ld_x, int64_t ld_y, int32_t P, int64_t cpr,
                                                          const int32_t* __restrict__ anc) {
     using T = typename Chunk<CH>::T;
     const int64_t total = static_cast<int64_t>(P) * cpr;
-    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
-         g += static_cast<int64_t>(gridDim.x) * kThreads) {
-        const int64_t i = g / cpr, c = g - i * cpr;
-        const int32_t p = __ldg(anc + i);
-        *reinterpret_cast<T*>(Y + i * ld_y + c * CH) = __ldg(reinterpret_cast<const T*>(X + p * ld_x + c * CH));
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int64_t g0 = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g0 < total; g0 += 4 * stride) {
+        T v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t g = g0 + u * stride;
+            if (g < total) {
+                const int64_t i = g / cpr, c = g - i * cpr;
+                const int32_t p = __ldg(anc + i);
+                v[u] = __ldg(reinterpret_cast<const T*>(X + p * ld_x + c * CH));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t g = g0 + u * stride;
+            if (g < total) {
+                const int64_t i = g / cpr, c = g - i * cpr;
+                *reinterpret_cast<T*>(Y + i * ld_y + c * CH) = v[u];
+            }
+        }
     }
 }
 
@@ -813,6 +1008,14 @@ cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, con
     return cudaPeekAtLastError();
 }
 
+// merged items per merge CTA: enough CTAs for ~10 per SM, at most 16 windows each
+static int64_t merge_chunk(int32_t N, int32_t P) {
+    const int64_t total = static_cast<int64_t>(N) * 2 * P;
+    int64_t ch = cdiv(total, static_cast<int64_t>(sm_count()) * 10);
+    ch = cdiv(ch, kWin) * kWin;
+    return std::max<int64_t>(kWin, std::min<int64_t>(ch, 16 * kWin));
+}
+
 static uint64_t stratum_width(int32_t P) {
     const int m = ceil_log2(P);
     if ((P & (P - 1)) == 0) return uint64_t{1} << (64 - m);
@@ -828,14 +1031,15 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
         { ProfScope ps_("k_bsearch", s); k_bsearch<<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(
             P, cpf, ws, L.ldq, key, first_filter, anc, ld_anc); }
     } else {
-        const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), kMergeItems));
+        const int64_t chunk = merge_chunk(N, P);
+        const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
         const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
         if (scheme == 2) {
             ModeSorted<2> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
-            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<2>><<<grid, kThreads, 0, s>>>(md, cpf); }
+            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<2>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
         } else {
             ModeSorted<3> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
-            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<3>><<<grid, kThreads, 0, s>>>(md, cpf); }
+            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<3>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
         }
     }
     ++*launches;
@@ -883,7 +1087,17 @@ cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int3
                                       static_cast<size_t>(N), s);
     if (e != cudaSuccess) return e;
     const int64_t total = static_cast<int64_t>(N) * P;
-    { ProfScope ps_("k_hist", s); k_hist<<<static_cast<unsigned>(grid_for(total, 16)), kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o); }
+    const bool runs = (P % 4 == 0) && ((reinterpret_cast<uintptr_t>(anc) & 15) == 0) && (ld_anc % 4 == 0);
+    if (runs) {
+        const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
+        const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
+                                                                                     sm_count() * 8)));
+        ProfScope ps_("k_hist", s);
+        k_hist_runs<<<g, kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o);
+    } else {
+        ProfScope ps_("k_hist", s);
+        k_hist<<<static_cast<unsigned>(grid_for(total, 16)), kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o);
+    }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -895,9 +1109,10 @@ cudaError_t launch_permute(const int32_t* anc, int64_t ld_anc, int32_t N, int32_
     { ProfScope ps_("k_pscan", s); k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, perm,
                                                                                      ld_perm); }
     ++*launches;
-    const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), kMergeItems));
+    const int64_t chunk = merge_chunk(N, P);
+    const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
     ModePermute md{ws.Qe, ws.freeslot, ws.F, L.ldq, P, perm, ld_perm};
-    { ProfScope ps_("k_merge_perm", s); k_merge<ModePermute><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf); }
+    { ProfScope ps_("k_merge_perm", s); k_merge<ModePermute><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf, chunk); }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -913,7 +1128,16 @@ cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, 
     const int64_t cpr = row_bytes / ch;
     const int64_t total = static_cast<int64_t>(N) * P * cpr;
     const unsigned grid = static_cast<unsigned>(grid_for(total, 16));
-    if (ch == 16) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    if (ch == 16 && cpr <= 64) {
+        const int vec_perm = ((reinterpret_cast<uintptr_t>(perm) & 15) == 0 && ld_perm % 4 == 0 && P % 4 == 0) ? 1 : 0;
+        const int64_t nblk = cdiv(static_cast<int64_t>(N) * P, 128);
+        const unsigned g2 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
+                                                                                      sm_count() * 8)));
+        ProfScope ps_("k_gather_inplace", s);
+        k_gather_rows16<<<g2, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, static_cast<int>(cpr), perm,
+                                                ld_perm, vec_perm);
+    }
+    else if (ch == 16) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
     else if (ch == 4) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<4><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
     else { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<1><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
     ++*launches;
