@@ -64,13 +64,20 @@ typedef enum {
 
 enum { PF_FILTER_OK = 0, PF_FILTER_INVALID_WEIGHTS = 1 };
 
+/* pf_opts.flags bits */
+enum {
+    /* diagnostics: force the multi-launch path (max -> lookback scan -> search)
+     * even where the one-launch cluster kernel applies.  Results are identical. */
+    PF_NO_FUSION = 1u << 1
+};
+
 /*
  * Optional outputs and controls of pf_resample_ex / pf_resample_batched.
  * All device pointers are nullable.  A zero-initialised struct means "none".
  */
 typedef struct {
     uint32_t filter_index; /* Philox c3 of a single-filter call (batched: first_filter+n) */
-    uint32_t flags;        /* reserved, must be 0 */
+    uint32_t flags;        /* PF_NO_FUSION or 0; other bits -> PF_ERR_UNSUPPORTED */
     double* lse_out;       /* [N] ln sum_i exp(logw_i)  (NS-13; 1e-6 rel. of oracle)       */
     float* normw_out;      /* [N][P] (row stride P) v_i = w_i / sum_j w_j  (NS-13)          */
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */

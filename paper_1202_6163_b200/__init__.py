@@ -20,6 +20,7 @@ from ._build import LIB as _LIB_PATH
 PF_MULTINOMIAL, PF_STRATIFIED, PF_SYSTEMATIC, PF_METROPOLIS = 1, 2, 3, 4
 SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
 PF_FILTER_OK, PF_FILTER_INVALID_WEIGHTS = 0, 1
+PF_NO_FUSION = 1 << 1  # pf_opts.flags: force the multi-launch path (diagnostics)
 
 
 class PfError(RuntimeError):
@@ -139,7 +140,7 @@ def _scheme(s):
 
 # ----------------------------------------------------------------------------- resamplers
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
-                   lse_out=None, normw_out=None, ess_out=None, status_out=None, stream=None):
+                   lse_out=None, normw_out=None, ess_out=None, status_out=None, flags: int = 0, stream=None):
     """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -149,7 +150,7 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
     if ancestors is None:
         ancestors = torch.empty(P, dtype=torch.int32, device=logw.device)
     _need_cuda(ancestors, torch.int32, "ancestors")
-    opts = _Opts(filter_index=filter_index)
+    opts = _Opts(filter_index=filter_index, flags=flags)
     if lse_out is not None:
         _need_cuda(lse_out, torch.float64, "lse_out"); opts.lse_out = lse_out.data_ptr()
     if ess_out is not None:
@@ -191,7 +192,7 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 
 
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
-                        lse_out=None, normw_out=None, ess_out=None, status_out=None, stream=None):
+                        lse_out=None, normw_out=None, ess_out=None, status_out=None, flags: int = 0, stream=None):
     """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P]."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -203,7 +204,7 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
         ancestors = torch.empty((N, P), dtype=torch.int32, device=logw.device)
     _need_cuda(ancestors, torch.int32, "ancestors")
     aptr, ald = _rows(ancestors, "ancestors")
-    opts = _Opts()
+    opts = _Opts(flags=flags)
     for name, t, dt in (("lse_out", lse_out, torch.float64), ("ess_out", ess_out, torch.float64),
                         ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32)):
         if t is not None:

@@ -99,12 +99,21 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     if (!logw || !anc) return PF_ERR_INVALID_ARG;
     if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
     if (N < 1 || P < 1 || B < 0 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
-    if (opts && opts->flags != 0) return PF_ERR_UNSUPPORTED;
+    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION)) != 0) return PF_ERR_UNSUPPORTED;
     double* lse = opts ? opts->lse_out : nullptr;
     double* ess = opts ? opts->ess_out : nullptr;
     float* normw = opts ? opts->normw_out : nullptr;
     int32_t* status_out = opts ? opts->status_out : nullptr;
 
+    const bool no_fusion = opts && (opts->flags & PF_NO_FUSION);
+    if (!no_fusion && pf::fused_supported(scheme, P)) {
+        // one launch per batch: cluster-per-filter kernel, no workspace (pf_fused.cu)
+        uint64_t nl = 0;
+        const cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
+                                                      ess, normw, status_out, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     const pf::Layout L = pf::make_layout(N, P, needs_for(scheme));
     void* base = nullptr;
     pf_status st = get_workspace(opts, L.total, s, &base);

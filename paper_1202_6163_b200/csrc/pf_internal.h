@@ -81,4 +81,11 @@ cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, 
 cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y, int32_t P,
                               const int32_t* anc, cudaStream_t s, uint64_t* launches);
 
+// One-launch cluster-per-filter resampler for stratified/systematic (pf_fused.cu).
+bool fused_supported(int scheme, int32_t P);
+cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                                uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
+                                double* ess_out, float* normw, int32_t* status_out, cudaStream_t s,
+                                uint64_t* launches);
+
 }  // namespace pf

@@ -47,18 +47,22 @@ def _gpu(x, dev):
     return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
 
 
-def _run(pf, dev, scheme, x, seed, B=0, filt=0, side=False):
+def _run(pf, dev, scheme, x, seed, B=0, filt=0, side=False, flags=0):
     import torch
 
     g = _gpu(x, dev)
     P = len(x)
+    if flags and not side:
+        a = pf.pf_resample_ex(scheme, g, seed, B, filter_index=filt, flags=flags)
+        torch.cuda.synchronize()
+        return a.cpu().numpy()
     if side:
         lse = torch.empty(1, dtype=torch.float64, device=dev)
         ess = torch.empty(1, dtype=torch.float64, device=dev)
         v = torch.empty(P, dtype=torch.float32, device=dev)
         st = torch.empty(1, dtype=torch.int32, device=dev)
         a = pf.pf_resample_ex(scheme, g, seed, B, filter_index=filt, lse_out=lse, ess_out=ess, normw_out=v,
-                              status_out=st)
+                              status_out=st, flags=flags)
         torch.cuda.synchronize()
         return a.cpu().numpy(), float(lse.item()), float(ess.item()), v.cpu().numpy(), int(st.item())
     if filt == 0:
@@ -83,6 +87,50 @@ def test_single_filter_bit_exact(pf, dev, orc, scheme, var):
             a = _run(pf, dev, scheme, x, seed, B)
             _, want = orc.resample(scheme, x, seed, B=B)
             assert np.array_equal(a, want), (scheme, var, P, seed, np.nonzero(a != want)[0][:5])
+
+
+@pytest.mark.parametrize("scheme", ["stratified", "systematic"])
+def test_multilaunch_path_bit_exact(pf, dev, orc, scheme):
+    """The multi-launch path (k_max -> k_scan -> k_merge), forced with PF_NO_FUSION at sizes where the
+    one-launch cluster kernel would otherwise run, is bit-exact too; side outputs included."""
+    for P in (1, 2, 7, 16, 1000, 4097, 65536, 100003, 131072):
+        for var in (0.1, 10.0):
+            x = pfinputs.gaussian_logw(P, var, seed=P + 3)
+            a = _run(pf, dev, scheme, x, 99, flags=pf.PF_NO_FUSION)
+            _, want = orc.resample(scheme, x, 99)
+            assert np.array_equal(a, want), (scheme, P, var)
+            a, lse, ess, v, st = _run(pf, dev, scheme, x, 98, side=True, flags=pf.PF_NO_FUSION)
+            _, want, wlse, wv, wess = orc.resample(scheme, x, 98, side=True)
+            assert np.array_equal(a, want)
+            assert abs(lse - wlse) <= 1e-6 * max(1.0, abs(wlse))
+
+
+@pytest.mark.parametrize("scheme", ["stratified", "systematic"])
+def test_cluster_path_sizes(pf, dev, orc, scheme):
+    """Cluster sizes 1..8 of the one-launch kernel (P up to 8 x 16384), ragged CTA ranges, skew."""
+    import torch
+
+    for P in (16383, 16384, 16385, 32768 + 5, 49152, 65536, 98304 + 7, 131072):
+        x = pfinputs.gaussian_logw(P, 10.0, seed=P)
+        a = _run(pf, dev, scheme, x, 31)
+        _, want = orc.resample(scheme, x, 31)
+        assert np.array_equal(a, want), (scheme, P)
+    # batched with more filters than resident clusters, ld > P, an invalid filter
+    N, P, ld = 300, 20000, 20004
+    x = pfinputs.gaussian_logw(ld, 1.0, seed=5, N=N)
+    x[7, 100] = np.nan
+    g = _gpu(x, dev)[:, :P]
+    st = torch.empty(N, dtype=torch.int32, device=dev)
+    lse = torch.empty(N, dtype=torch.float64, device=dev)
+    a = pf.pf_resample_batched(scheme, g, 4, first_filter=1000, status_out=st, lse_out=lse)
+    torch.cuda.synchronize()
+    wst, want = orc.resample_batched(scheme, np.ascontiguousarray(x[:, :P]), 4, first_filter=1000)
+    assert np.array_equal(st.cpu().numpy(), wst)
+    assert np.array_equal(a.cpu().numpy(), want)
+    for n in (0, 7, 299):
+        _, _, wl, _, _ = orc.resample(scheme, np.ascontiguousarray(x[n, :P]), 4, filter_index=1000 + n, side=True)
+        got = float(lse[n].item())
+        assert (np.isnan(wl) and np.isnan(got)) or abs(got - wl) <= 1e-6 * max(1.0, abs(wl))
 
 
 @pytest.mark.parametrize("scheme", SCHEMES)
@@ -247,4 +295,8 @@ def test_repeatability_and_launch_count(pf, dev):
     a2 = pf.pf_resample_stratified(x, 11)
     torch.cuda.synchronize()
     assert torch.equal(a1, a2)
-    assert pf.pf_launch_count() - c0 == 6  # max, scan, merge per call
+    assert pf.pf_launch_count() - c0 == 2  # one cluster kernel per call (P <= 8 x 16384)
+    c0 = pf.pf_launch_count()
+    pf.pf_resample_ex("stratified", x, 11, flags=pf.PF_NO_FUSION)
+    torch.cuda.synchronize()
+    assert pf.pf_launch_count() - c0 == 3  # max, scan, merge
