@@ -54,11 +54,16 @@ __device__ __forceinline__ uint64_t hi_word(const u32x4& v) {
 
 // ---------------------------------------------------------------- NS-4
 // Deterministic float32 exp of t <= 0; constants are the NS-4 bit patterns.
+// Written without branches (selects only); every value equals NS-4 step by
+// step: for n = -127 the scale bits are 0, so w = p * 0 = 0, which is what
+// step 6 returns.
 __device__ __forceinline__ float dexp(float t) {
-    if (!(t >= -88.0f)) return 0.0f;                        // step 1
-    if (fabsf(t) < __uint_as_float(0x00800000u)) t = 0.0f;  // step 2
-    const float n = rintf(__fmul_rn(t, __uint_as_float(0x3FB8AA3Bu)));  // step 3
-    float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), t);            // step 4
+    const float kTiny = __uint_as_float(0x00800000u);  // 2^-126
+    const bool kill = !(t >= -88.0f);                   // step 1 (also -inf)
+    float tt = kill ? 0.0f : t;
+    tt = (fabsf(tt) < kTiny) ? 0.0f : tt;               // step 2
+    const float n = rintf(__fmul_rn(tt, __uint_as_float(0x3FB8AA3Bu)));  // step 3
+    float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), tt);           // step 4
     r = __fmaf_rn(-n, __uint_as_float(0x35BFBE8Eu), r);
     float p = __uint_as_float(0x39500D01u);                               // step 5
     p = __fmaf_rn(p, r, __uint_as_float(0x3AB60B61u));
@@ -69,23 +74,24 @@ __device__ __forceinline__ float dexp(float t) {
     p = __fmaf_rn(p, r, 1.0f);
     p = __fmaf_rn(p, r, 1.0f);
     const int ni = static_cast<int>(n);                                   // step 6
-    if (ni < -126) return 0.0f;
-    float w = __fmul_rn(p, __uint_as_float(static_cast<uint32_t>(ni + 127) << 23));
-    if (w < __uint_as_float(0x00800000u)) return 0.0f;                   // step 7
+    const uint32_t sbits = (ni >= -126) ? (static_cast<uint32_t>(ni + 127) << 23) : 0u;
+    float w = __fmul_rn(p, __uint_as_float(sbits));
+    w = (kill || w < kTiny) ? 0.0f : w;                                   // step 7
     return fminf(w, 1.0f);
 }
 
 // ---------------------------------------------------------------- NS-5
-// q = trunc(w * 2^kfx) computed on the float's bit fields (exact).
+// q = trunc(w * 2^kfx) computed on the float's bit fields (exact), without
+// branches: w is 0 or a normal float in [2^-126, 1] (NS-4 flushes), so the
+// value is mant * 2^(e - 150 + kfx) with a left or right shift.
 __device__ __forceinline__ uint64_t quantise(float w, int kfx) {
     const uint32_t b = __float_as_uint(w);
-    const int e = static_cast<int>(b >> 23);
-    if (e == 0) return 0ull;  // zero (dexp never returns subnormals)
-    const uint64_t mant = (b & 0x7FFFFFu) | 0x800000u;
-    const int s = e - 150 + kfx;
-    if (s >= 0) return mant << s;
-    if (s <= -24) return 0ull;
-    return mant >> (-s);
+    const uint32_t e = b >> 23;
+    const uint64_t mant = (b & 0x7FFFFFu) | (e ? 0x800000u : 0u);
+    const int s = static_cast<int>(e) - 150 + kfx;
+    const uint64_t left = mant << (s > 0 ? s : 0);
+    const uint64_t right = mant >> min(-s, 63);
+    return (s >= 0) ? left : right;
 }
 
 // w_i = dexp(fl(logw_i - lmax)) (NS-3)

@@ -1,23 +1,24 @@
-// pf_fused.cu — one-launch resampler for batches of small/medium filters.
+// pf_fused.cu — one-launch resampler for batches of filters with P <= 8 x 8192
+// (stratified and systematic; SURVEY §8 rows a1-a5, a11, a12 in one kernel).
 //
-// One thread-block CLUSTER per filter (CL = ceil(P / 16384) CTAs, <= 8), a
-// persistent loop over filters.  CTA c of the cluster owns particles
-// [c*PP, (c+1)*PP) and keeps their inclusive fixed-point cumulative weights
-// Q_i (NS-5) in shared memory (PP <= 16384 -> <= 128 KiB).  Per filter:
-//   A  log-weights -> registers (float4, coalesced); local max; cluster max
-//      through DSMEM (a1, NS-1/NS-2)
-//   B  w = dexp, q = trunc(w 2^kfx) (a2, NS-3..NS-5); block scan in
-//      registers + shared memory; cluster exchange of the CTA totals gives
-//      the CTA's offset O_c and the filter total Q (a3, the "collective
-//      prefix-sum" of P:125-128, here inside one launch); lse / ESS /
-//      normalised weights fused (a12)
-//   C  slots whose positions fall in [O_c, O_c + T_c) form a contiguous range
-//      [k_lo, k_hi) (positions are sorted, NS-9/NS-10), found by a
-//      warp-parallel search over k; each thread takes 16 consecutive slots,
-//      generates their positions (Philox, NS-6) and finds a_k = min{i : Q_i >
-//      x_k} by a binary search for the first slot and a galloping search from
-//      the previous answer for the rest (a4+a5).
-// HBM traffic: 4 B/particle in (logw) + 4 B out (ancestors) (+4 B normw).
+// One thread-block CLUSTER per filter (CL = ceil(P / 8192) CTAs), persistent
+// over filters.  CTA c owns particles [c*PP, (c+1)*PP), 16 per thread.
+//   A  log-weights -> registers (float4, coalesced); CTA max; cluster max
+//      through distributed shared memory (a1, NS-1, NS-2).
+//   B  w = dexp, q = trunc(w 2^kfx) (a2, NS-3..5); block scan of q in
+//      registers + shared memory; a DSMEM exchange of the CTA totals gives the
+//      CTA offset O_c and the filter total Q (a3 — the paper's "collective
+//      prefix-sum", without a second launch); lse / ESS / v_i fused
+//      (a12, NS-13).
+//   C  positions are sorted (NS-9, NS-10), so the slots landing in particle i
+//      are [E_{i-1}, E_i) with E_i = c(Q_i) = #{k : x_k < Q_i}.  c() has a
+//      closed form: x_k < v  <=>  k*D + rho_k < v 2^64 / Q; a double-precision
+//      estimate of k* = (v 2^64/Q - rho)/D is within 2^-19 of the truth, so one
+//      exact integer position check decides the count (the boundary case takes
+//      a second check).  Particle i then marks heads[E_{i-1}] = i when E_i >
+//      E_{i-1}, and a max-scan over the slot window gives every ancestor
+//      a_k = max{i : E_{i-1} <= k} = min{i : Q_i > x_k} (a4+a5, NS-search).
+// HBM traffic: 4 B/particle in (logw) + 4 B out (ancestors).  No workspace.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -32,12 +33,14 @@ namespace pf {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kFT = 512;               // threads per CTA
-constexpr int kFW = kFT / 32;          // warps per CTA
-constexpr int kFI = 32;                // particles per thread
-constexpr int kFR = kFI / 4;           // float4 rows per thread
-constexpr int kPP = kFT * kFI;         // 16384 particles per CTA (max)
-constexpr int kSlotsPerThread = 16;
+constexpr int kFT = 512;           // threads per CTA (2 CTAs / SM)
+constexpr int kFW = kFT / 32;      // 16 warps
+constexpr int kFI = 16;            // particles per thread
+constexpr int kFR = kFI / 4;       // 4 float4 rows
+constexpr int kPP = kFT * kFI;     // 8192 particles per CTA (max)
+constexpr int kChunk = 256;        // slots per warp max-scan pass (8 per lane)
+constexpr int kTPL = kFR * kFW / 32;  // (row, warp) totals per lane in the phase-B scan
+static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32 (row, warp) totals");
 
 struct Exchange {
     float m;
@@ -54,57 +57,78 @@ struct FusedArgs {
     Key key;
     uint32_t filt0;
     int kfx;
-    int vec;  // logw rows 16-byte aligned and PP % 4 == 0
+    int vec;       // logw rows 16-byte aligned
+    int sums;      // lse / ess / normw requested
     int32_t* anc;
     int64_t ld_anc;
-    int anc_vec;  // ancestor rows 16-byte aligned
+    int anc_vec;   // ancestor rows 16-byte aligned
     double* lse_out;
     double* ess_out;
     float* normw;
     int32_t* status_out;
 };
 
+struct Pos {
+    uint64_t D, Qtot, rho;
+    Key key;
+    uint32_t filt;
+    int64_t P;
+    double A, Bc;  // k* = v * A - Bc
+};
+
 template <int SCHEME>
-__device__ __forceinline__ uint64_t position(const FusedArgs& a, uint32_t filt, uint64_t Qtot, uint64_t rho,
-                                             int64_t k) {
+__device__ __forceinline__ uint64_t xpos(const Pos& z, int64_t k) {
+    uint64_t rho = z.rho;
     if (SCHEME == 2) {
-        const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 2u, filt, a.key.k0, a.key.k1);
-        rho = mulhi64((k & 1) ? hi_word(r) : lo_word(r), a.D);
+        const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 2u, z.filt, z.key.k0, z.key.k1);
+        rho = mulhi64((k & 1) ? hi_word(r) : lo_word(r), z.D);
     }
-    return mulhi64(static_cast<uint64_t>(k) * a.D + rho, Qtot);
+    return mulhi64(static_cast<uint64_t>(k) * z.D + rho, z.Qtot);
 }
 
-// #{k in [0, P) : x_k < v} by a 32-ary warp search (x_k nondecreasing in k).
+// c(v) = #{k in [0, P) : x_k < v}
 template <int SCHEME>
-__device__ int64_t count_below(const FusedArgs& a, uint32_t filt, uint64_t Qtot, uint64_t rho, uint64_t v,
-                               int lane) {
-    int64_t lo = 0, hi = a.P;
-    while (hi > lo) {
-        const int64_t step = (hi - lo + 31) / 32;
-        const int64_t m = lo + lane * step;
-        const bool p = (m < hi) && (position<SCHEME>(a, filt, Qtot, rho, m) < v);
-        const int L = __popc(__ballot_sync(kFull, p));
-        const int64_t nlo = (L == 0) ? lo : lo + static_cast<int64_t>(L - 1) * step + 1;
-        const int64_t mL = lo + static_cast<int64_t>(L) * step;
-        hi = (mL < hi) ? mL : hi;
-        lo = nlo;
+__device__ __forceinline__ uint32_t count_below(const Pos& z, uint64_t v) {
+    const double kf = fma(static_cast<double>(v), z.A, -z.Bc);
+    const double fl = floor(kf);
+    const double fr = kf - fl;
+    int64_t c;
+    if (fr > 0x1p-12 && fr < 1.0 - 0x1p-12) {
+        const int64_t n = static_cast<int64_t>(fl);
+        if (SCHEME == 3) {
+            c = n + 1;  // k* in (n, n+1): exactly the k <= n count (clamped below)
+        } else {
+            // strata k < n lie below v, k > n above; stratum n decides itself
+            c = (n < 0) ? 0 : ((n >= z.P) ? z.P : n + (xpos<SCHEME>(z, n) < v ? 1 : 0));
+        }
+    } else {
+        const int64_t m0 = llrint(kf);
+        if (SCHEME == 3) {
+            c = m0 + ((m0 >= 0 && m0 < z.P && xpos<SCHEME>(z, m0) < v) ? 1 : 0);
+        } else {
+            const int64_t a = m0 - 1;
+            c = min(max(a, int64_t{0}), z.P);
+            if (a >= 0 && a < z.P && xpos<SCHEME>(z, a) < v) ++c;
+            if (m0 >= 0 && m0 < z.P && xpos<SCHEME>(z, m0) < v) ++c;
+        }
     }
-    return lo;
+    return static_cast<uint32_t>(min(max(c, int64_t{0}), z.P));
 }
 
-template <int SCHEME>
-__global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
-    extern __shared__ __align__(16) uint64_t sQ[];
+template <int SCHEME, bool SUMS>
+__global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
     __shared__ Exchange s_x;
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];
     __shared__ uint64_t s_wt[kFR][kFW];
+    __shared__ uint32_t s_lastE[kFR][kFW];
+    __shared__ __align__(16) int32_t s_buf[kFW][kChunk];
     __shared__ float s_lmax;
     __shared__ int s_bad;
     __shared__ uint64_t s_off, s_tot, s_Qtot;
     __shared__ double s_S, s_S2;
-    __shared__ int64_t s_k[2];
+    __shared__ uint32_t s_klo, s_khi;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int c = static_cast<int>(cluster.block_rank());
@@ -137,8 +161,8 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
         int bad = 0;
 #pragma unroll
         for (int t = 0; t < kFI; ++t) {
-            if (isnan(v[t]) || v[t] == INFINITY) bad = 1;
-            else m = fmaxf(m, v[t]);
+            bad |= (isnan(v[t]) || v[t] == INFINITY) ? 1 : 0;
+            m = fmaxf(m, v[t]);  // fmaxf ignores NaN; +inf makes the filter invalid anyway
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -147,22 +171,34 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
         }
         if (lane == 0) { s_f[warp] = m; s_i[warp] = bad; }
         __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < kFW; ++w) { m = fmaxf(m, s_f[w]); bad |= s_i[w]; }
-            s_x.m = m;
-            s_x.bad = bad;
+        if (warp == 0) {
+            float mm = (lane < kFW) ? s_f[lane] : -INFINITY;
+            int bb = (lane < kFW) ? s_i[lane] : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+                bb |= __shfl_xor_sync(kFull, bb, o);
+            }
+            if (lane == 0) { s_x.m = mm; s_x.bad = bb; }
         }
         cluster.sync();  // #1
-        if (tid == 0) {
+        if (warp == 0) {
             float gm = -INFINITY;
             int gb = 0;
-            for (int r = 0; r < CL; ++r) {
-                const Exchange* rx = cluster.map_shared_rank(&s_x, r);
-                gm = fmaxf(gm, rx->m);
-                gb |= rx->bad;
+            if (lane < CL) {
+                const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
+                gm = rx->m;
+                gb = rx->bad;
             }
-            s_lmax = gm;
-            s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
+                gb |= __shfl_xor_sync(kFull, gb, o);
+            }
+            if (lane == 0) {
+                s_lmax = gm;
+                s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+            }
         }
         __syncthreads();
         if (s_bad) {
@@ -176,14 +212,14 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
                 if (a.ess_out) a.ess_out[n] = NAN;
                 if (a.status_out) a.status_out[n] = 1;
             }
-            cluster.sync();  // readers of s_x.m are done before the next filter writes it
+            cluster.sync();  // remote readers of s_x are done before the next filter writes it
             continue;
         }
         const float lm = s_lmax;
 
         // ---------------- B: weights, quantise, block scan, cluster offsets
         double sw = 0.0, sw2 = 0.0;
-        uint64_t rs[kFR];
+        uint64_t ex[kFR];
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
             uint64_t loc = 0;
@@ -191,90 +227,99 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
             for (int q = 0; q < 4; ++q) {
                 const float w = weight(v[j * 4 + q], lm);
                 v[j * 4 + q] = w;
-                sw += static_cast<double>(w);
-                sw2 += static_cast<double>(w) * static_cast<double>(w);
+                if (SUMS) {
+                    sw += static_cast<double>(w);
+                    sw2 += static_cast<double>(w) * static_cast<double>(w);
+                }
                 loc += quantise(w, a.kfx);
             }
-            rs[j] = loc;
-        }
-        uint64_t ex[kFR];
-#pragma unroll
-        for (int j = 0; j < kFR; ++j) {
-            const uint64_t incl = warp_incl_scan_u64(rs[j], lane);
-            ex[j] = incl - rs[j];
+            const uint64_t incl = warp_incl_scan_u64(loc, lane);
+            ex[j] = incl - loc;
             const uint64_t wt = __shfl_sync(kFull, incl, 31);
             if (lane == 0) s_wt[j][warp] = wt;
         }
-        sw = warp_sum_f64(sw);
-        sw2 = warp_sum_f64(sw2);
-        if (lane == 0) { s_d[0][warp] = sw; s_d[1][warp] = sw2; }
+        if (SUMS) {
+            sw = warp_sum_f64(sw);
+            sw2 = warp_sum_f64(sw2);
+            if (lane == 0) { s_d[0][warp] = sw; s_d[1][warp] = sw2; }
+        }
         __syncthreads();
         if (warp == 0) {
-            // exclusive scan of the kFR x kFW warp totals in (row, warp) order: 4 per lane
-            uint64_t t4[4];
+            // exclusive scan of the (row, warp) totals in (row, warp) order: kTPL per lane
+            uint64_t t4[kTPL];
             uint64_t tsum = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int idx = lane * 4 + q;
+            for (int q = 0; q < kTPL; ++q) {
+                const int idx = lane * kTPL + q;
                 t4[q] = s_wt[idx / kFW][idx % kFW];
                 tsum += t4[q];
             }
             const uint64_t incl = warp_incl_scan_u64(tsum, lane);
             uint64_t run = incl - tsum;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int idx = lane * 4 + q;
+            for (int q = 0; q < kTPL; ++q) {
+                const int idx = lane * kTPL + q;
                 s_wt[idx / kFW][idx % kFW] = run;
                 run += t4[q];
             }
-            if (lane == 31) s_tot = incl;
+            double A = 0.0, Bv = 0.0;
+            if (SUMS) {
+                A = (lane < kFW) ? s_d[0][lane] : 0.0;  // fixed-order tree over the warp partials
+                Bv = (lane < kFW) ? s_d[1][lane] : 0.0;
+                A = warp_sum_f64(A);
+                Bv = warp_sum_f64(Bv);
+            }
+            if (lane == 31) {
+                s_x.tot = incl;
+                s_tot = incl;
+            }
             if (lane == 0) {
-                double A = 0.0, Bv = 0.0;
-                for (int w = 0; w < kFW; ++w) { A += s_d[0][w]; Bv += s_d[1][w]; }
                 s_x.sw = A;
                 s_x.sw2 = Bv;
             }
         }
-        __syncthreads();
-        if (tid == 0) s_x.tot = s_tot;
         cluster.sync();  // #2
-        if (tid == 0) {
-            uint64_t off = 0, tot = 0;
+        if (warp == 0) {
+            uint64_t tot = 0, off = 0;
             double S = 0.0, S2 = 0.0;
-            for (int r = 0; r < CL; ++r) {
-                const Exchange* rx = cluster.map_shared_rank(&s_x, r);
-                if (r < c) off += rx->tot;
-                tot += rx->tot;
-                S += rx->sw;
-                S2 += rx->sw2;
+            if (lane < CL) {
+                const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
+                tot = rx->tot;
+                off = (lane < c) ? tot : 0ull;
+                S = rx->sw;
+                S2 = rx->sw2;
             }
-            s_off = off;
-            s_Qtot = tot;
-            s_S = S;
-            s_S2 = S2;
+            // fixed rank order for the double sums (deterministic): serial over lanes
+            double Sr = 0.0, S2r = 0.0;
+            for (int r = 0; r < CL; ++r) {
+                Sr += __shfl_sync(kFull, S, r);
+                S2r += __shfl_sync(kFull, S2, r);
+            }
+            tot = warp_sum_u64(tot);
+            off = warp_sum_u64(off);
+            if (lane == 0) {
+                s_off = off;
+                s_Qtot = tot;
+                s_S = Sr;
+                s_S2 = S2r;
+            }
         }
         __syncthreads();
         const uint64_t O = s_off;
-        const uint64_t Qtot = s_Qtot;
-        // inclusive Q into shared memory (natural order)
-#pragma unroll
-        for (int j = 0; j < kFR; ++j) {
-            const int i0 = j * (kFT * 4) + tid * 4;
-            uint64_t run = O + s_wt[j][warp] + ex[j];
-            uint64_t q4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                run += quantise(v[j * 4 + q], a.kfx);
-                q4[q] = run;
-            }
-            if (i0 + 3 < np) {
-                reinterpret_cast<ulonglong2*>(sQ + i0)[0] = make_ulonglong2(q4[0], q4[1]);
-                reinterpret_cast<ulonglong2*>(sQ + i0)[1] = make_ulonglong2(q4[2], q4[3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (i0 + q < np) sQ[i0 + q] = q4[q];
-            }
+        Pos z;
+        z.D = a.D;
+        z.Qtot = s_Qtot;
+        z.key = a.key;
+        z.filt = filt;
+        z.P = a.P;
+        z.rho = (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+        // A = 2^64 / (D Q), Bc = rho / D  (the double estimate of k*)
+        z.A = 0x1p64 / (static_cast<double>(z.D) * static_cast<double>(z.Qtot));
+        z.Bc = (SCHEME == 3) ? static_cast<double>(z.rho) / static_cast<double>(z.D) : 0.0;
+        if (c == 0 && tid == 0) {
+            if (a.lse_out) a.lse_out[n] = static_cast<double>(lm) + log(s_S);
+            if (a.ess_out) a.ess_out[n] = s_S * s_S / s_S2;
+            if (a.status_out) a.status_out[n] = 0;
         }
         if (a.normw) {
             const double S = s_S;
@@ -287,91 +332,93 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
                     if (i0 + q < np) nrow[i0 + q] = static_cast<float>(static_cast<double>(v[j * 4 + q]) / S);
             }
         }
-        if (c == 0 && tid == 0) {
-            if (a.lse_out) a.lse_out[n] = static_cast<double>(lm) + log(s_S);
-            if (a.ess_out) a.ess_out[n] = s_S * s_S / s_S2;
-            if (a.status_out) a.status_out[n] = 0;
-        }
-
-        // ---------------- C: slots of this CTA and their ancestors
-        uint64_t rho = 0;
-        if (SCHEME == 3) rho = mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D);
         if (a.P == 1) {
             if (tid == 0) a.anc[static_cast<int64_t>(n) * a.ld_anc] = 0;
-        } else if (np > 0) {
-            if (warp < 2) {
-                int64_t k;
-                if (warp == 0) k = (c == 0) ? 0 : count_below<SCHEME>(a, filt, Qtot, rho, O, lane);
-                else k = (c == CL - 1 || p1 == a.P) ? a.P : count_below<SCHEME>(a, filt, Qtot, rho, O + s_tot, lane);
-                if (lane == 0) s_k[warp] = k;
-            }
             __syncthreads();
-            const int64_t k_lo = s_k[0], k_hi = s_k[1];
-            int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
-            const int64_t b_first = k_lo / kSlotsPerThread;
-            const int64_t b_last = (k_hi + kSlotsPerThread - 1) / kSlotsPerThread;  // exclusive
-            for (int64_t b = b_first + tid; b < b_last; b += kFT) {
-                const int64_t kb = b * kSlotsPerThread;
-                uint64_t x[kSlotsPerThread];
-                if (SCHEME == 2) {
+            continue;
+        }
+
+        // ---------------- C: E_i = c(Q_i), heads, max-scan
+        uint32_t E[kFI];
 #pragma unroll
-                    for (int t = 0; t < kSlotsPerThread; t += 2) {
-                        const u32x4 r = philox10(static_cast<uint32_t>((kb + t) >> 1), 0u, 2u, filt, a.key.k0,
-                                                 a.key.k1);
-                        x[t] = mulhi64(static_cast<uint64_t>(kb + t) * a.D + mulhi64(lo_word(r), a.D), Qtot);
-                        x[t + 1] = mulhi64(static_cast<uint64_t>(kb + t + 1) * a.D + mulhi64(hi_word(r), a.D), Qtot);
-                    }
+        for (int j = 0; j < kFR; ++j) {
+            uint64_t run = O + s_wt[j][warp] + ex[j];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                run += quantise(v[j * 4 + q], a.kfx);
+                E[j * 4 + q] = count_below<SCHEME>(z, run);
+            }
+            if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
+        }
+        if (tid == 0) {
+            s_klo = count_below<SCHEME>(z, O);
+            s_khi = count_below<SCHEME>(z, O + s_tot);
+        }
+        __syncthreads();
+        const uint32_t k_lo = s_klo, k_hi = s_khi;
+        // E_{i-1} of the first particle of each 4-chunk (natural order: row j, warp, lane, q);
+        // the other three predecessors are the chunk's own E values.
+        uint32_t first[kFR];
+#pragma unroll
+        for (int j = 0; j < kFR; ++j) {
+            const uint32_t up = __shfl_up_sync(kFull, E[j * 4 + 3], 1);
+            if (lane > 0) first[j] = up;
+            else if (warp > 0) first[j] = s_lastE[j][warp - 1];
+            else if (j > 0) first[j] = s_lastE[j - 1][kFW - 1];
+            else first[j] = k_lo;
+        }
+        int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
+        const int32_t idbase = static_cast<int32_t>(p0) + tid * 4;
+        int4* b4 = reinterpret_cast<int4*>(s_buf[warp]);
+        // Each (row, warp) owns the contiguous slot range [S0, S1) of its 128 particles.
+        // Per 256-slot chunk: heads[E_{i-1}] = i, then a warp max-scan gives
+        // a_k = max{i : E_{i-1} <= k}; 8 slots per lane, vector stores.
+#pragma unroll
+        for (int j = 0; j < kFR; ++j) {
+            const uint32_t S0 = __shfl_sync(kFull, first[j], 0);
+            const uint32_t S1 = __shfl_sync(kFull, E[j * 4 + 3], 31);
+            int32_t carry = -1;
+            for (uint32_t c0 = S0 & ~3u; c0 < S1; c0 += kChunk) {
+                b4[2 * lane] = make_int4(-1, -1, -1, -1);
+                b4[2 * lane + 1] = make_int4(-1, -1, -1, -1);
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                    const uint32_t rel = pe - c0;  // wraps when pe < c0
+                    if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kChunk))
+                        s_buf[warp][rel] = idbase + j * (kFT * 4) + q;
+                }
+                __syncwarp();
+                const int4 lo = b4[2 * lane], hi = b4[2 * lane + 1];
+                int32_t h[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+                for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
+                int32_t incl = h[7];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t u = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl = max(incl, u);
+                }
+                int32_t pre = __shfl_up_sync(kFull, incl, 1);
+                pre = max(carry, (lane == 0) ? -1 : pre);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
+                carry = max(carry, __shfl_sync(kFull, incl, 31));
+                const uint32_t k0 = c0 + 8 * lane;
+                if (a.anc_vec && k0 >= S0 && k0 + 8 <= S1) {
+                    int4* dst = reinterpret_cast<int4*>(arow + k0);
+                    __stcs(dst, make_int4(h[0], h[1], h[2], h[3]));
+                    __stcs(dst + 1, make_int4(h[4], h[5], h[6], h[7]));
                 } else {
 #pragma unroll
-                    for (int t = 0; t < kSlotsPerThread; ++t)
-                        x[t] = mulhi64(static_cast<uint64_t>(kb + t) * a.D + rho, Qtot);
+                    for (int t = 0; t < 8; ++t)
+                        if (k0 + t >= S0 && k0 + t < S1) arow[k0 + t] = h[t];
                 }
-                int32_t out[kSlotsPerThread];
-                int cur = -1;  // local index of the previous answer
-#pragma unroll
-                for (int t = 0; t < kSlotsPerThread; ++t) {
-                    const int64_t k = kb + t;
-                    out[t] = 0;
-                    if (k < k_lo || k >= k_hi) continue;
-                    const uint64_t xv = x[t];
-                    int lo, hi;
-                    if (cur < 0) {
-                        lo = 0;
-                        hi = np - 1;
-                    } else if (sQ[cur] > xv) {
-                        lo = hi = cur;
-                    } else {
-                        // gallop: find hi with sQ[hi] > xv
-                        int step = 1;
-                        lo = cur + 1;
-                        hi = min(cur + step, np - 1);
-                        while (hi < np - 1 && sQ[hi] <= xv) {
-                            lo = hi + 1;
-                            step <<= 1;
-                            hi = min(cur + step, np - 1);
-                        }
-                    }
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (sQ[mid] > xv) hi = mid;
-                        else lo = mid + 1;
-                    }
-                    cur = lo;
-                    out[t] = static_cast<int32_t>(p0 + lo);
-                }
-                if (a.anc_vec && kb >= k_lo && kb + kSlotsPerThread <= k_hi) {
-                    int4* dst = reinterpret_cast<int4*>(arow + kb);
-#pragma unroll
-                    for (int t = 0; t < kSlotsPerThread; t += 4)
-                        __stcs(dst + t / 4, make_int4(out[t], out[t + 1], out[t + 2], out[t + 3]));
-                } else {
-#pragma unroll
-                    for (int t = 0; t < kSlotsPerThread; ++t)
-                        if (kb + t >= k_lo && kb + t < k_hi) arow[kb + t] = out[t];
-                }
+                __syncwarp();
             }
         }
-        __syncthreads();  // sQ and s_k are reused by the next filter
+        __syncthreads();
     }
     cluster.sync();  // keep this CTA's shared memory alive for remote readers
 }
@@ -387,16 +434,10 @@ int device_sms() {
     return sms;
 }
 
-template <int SCHEME>
+template <int SCHEME, bool SUMS>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(a.PP) * sizeof(uint64_t);
-    auto kern = k_fused_sorted<SCHEME>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPP * static_cast<int>(sizeof(uint64_t)));
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-        attr_set = true;
-    }
+    const size_t smem = 0;
+    auto kern = k_fused_sorted<SCHEME, SUMS>;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -444,6 +485,7 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.filt0 = first_filter;
     a.kfx = 61 - m;
     a.vec = ((reinterpret_cast<uintptr_t>(logw) & 15) == 0 && ld % 4 == 0) ? 1 : 0;
+    a.sums = (lse_out || ess_out || normw) ? 1 : 0;
     a.anc = anc;
     a.ld_anc = ld_anc;
     a.anc_vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0) ? 1 : 0;
@@ -452,7 +494,9 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.normw = normw;
     a.status_out = status_out;
     ProfScope ps_("k_fused_sorted", s);
-    cudaError_t e = (scheme == 2) ? launch_fused_t<2>(a, s) : launch_fused_t<3>(a, s);
+    cudaError_t e;
+    if (scheme == 2) e = a.sums ? launch_fused_t<2, true>(a, s) : launch_fused_t<2, false>(a, s);
+    else e = a.sums ? launch_fused_t<3, true>(a, s) : launch_fused_t<3, false>(a, s);
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

@@ -780,51 +780,28 @@ __global__ void __launch_bounds__(kThreads) k_gather_inplace(char* X, int64_t ld
 }
 
 // In-place gather, 16-byte chunks, warp-cooperative: each warp takes 128
-// consecutive rows (one int4 of permutation entries per lane), compacts the
-// moved rows (perm[i] != i) into a per-warp list, then copies their chunks
-// with up to kGU 16-byte loads in flight per lane before any store.  Safe in
-// place: loads only touch survivor rows, stores only non-survivor rows.
-constexpr int kGU = 8;
-__global__ void __launch_bounds__(kThreads) k_gather_rows16(char* X, int64_t ld_bytes, int64_t ld_filter_bytes,
-                                                            int32_t N, int32_t P, int cpr,
-                                                            const int32_t* __restrict__ perm, int64_t ld_perm,
-                                                            int vec_perm) {
-    __shared__ int64_t s_dst[kThreads / 32][128];
-    __shared__ int64_t s_src[kThreads / 32][128];
+// consecutive rows of one filter (one int4 of permutation entries per lane),
+// compacts the moved rows (perm[i] != i) into a per-warp (dst, src) list, then
+// copies their chunks with kGU 16-byte loads in flight per lane before the
+// stores.  Safe in place: loads only touch survivor rows, stores only
+// non-survivor rows.  Requires P % 4 == 0 and 16-byte aligned rows.
+constexpr int kGU = 4;
+__global__ void __launch_bounds__(kThreads, 8) k_gather_rows16(char* X, int64_t ld_bytes, int64_t ld_filter_bytes,
+                                                               int32_t N, int32_t P, int cpr,
+                                                               const int32_t* __restrict__ perm, int64_t ld_perm) {
+    __shared__ int2 s_ds[kThreads / 32][128];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t rows = static_cast<int64_t>(N) * P;
-    const int64_t nblk = cdiv(rows, 128);
+    const int per_filter = (P + 127) / 128;
+    const int64_t nblk = static_cast<int64_t>(N) * per_filter;
     const int64_t wstride = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
     for (int64_t blk = blockIdx.x * static_cast<int64_t>(kThreads / 32) + warp; blk < nblk; blk += wstride) {
-        const int64_t r0 = blk * 128 + lane * 4;
-        int32_t pv[4];
-        int64_t rr[4];
-        int moved = 0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) rr[c] = r0 + c;
-        if (vec_perm && r0 + 3 < rows && (r0 / P) == ((r0 + 3) / P)) {
-            const int64_t n = r0 / P, i = r0 - n * P;
-            const int4 t = __ldg(reinterpret_cast<const int4*>(perm + n * ld_perm + i));
-            pv[0] = t.x; pv[1] = t.y; pv[2] = t.z; pv[3] = t.w;
-        } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                pv[c] = -1;
-                if (rr[c] < rows) {
-                    const int64_t n = rr[c] / P, i = rr[c] - n * P;
-                    pv[c] = __ldg(perm + n * ld_perm + i);
-                }
-            }
-        }
-        unsigned mbits = 0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (rr[c] < rows) {
-                const int64_t n = rr[c] / P, i = rr[c] - n * P;
-                if (pv[c] != i) { mbits |= 1u << c; ++moved; }
-            }
-        }
-        // warp exclusive scan of moved counts -> slots in the per-warp list
+        const int n = static_cast<int>(blk / per_filter);
+        const int i0 = static_cast<int>(blk - static_cast<int64_t>(n) * per_filter) * 128 + lane * 4;
+        int4 pv = make_int4(0, 1, 2, 3);  // identity for rows past P (not moved)
+        if (i0 < P) pv = __ldg(reinterpret_cast<const int4*>(perm + n * ld_perm + i0));
+        else pv = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+        const int m0 = (pv.x != i0), m1 = (pv.y != i0 + 1), m2 = (pv.z != i0 + 2), m3 = (pv.w != i0 + 3);
+        const int moved = m0 + m1 + m2 + m3;
         int incl = moved;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -833,17 +810,12 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows16(char* X, int64_t ld_
         }
         const int nmoved = __shfl_sync(kFull, incl, 31);
         int at = incl - moved;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (mbits & (1u << c)) {
-                const int64_t n = rr[c] / P, i = rr[c] - n * P;
-                char* base = X + n * ld_filter_bytes;
-                s_dst[warp][at] = reinterpret_cast<int64_t>(base + i * ld_bytes);
-                s_src[warp][at] = reinterpret_cast<int64_t>(base + static_cast<int64_t>(pv[c]) * ld_bytes);
-                ++at;
-            }
-        }
+        if (m0) s_ds[warp][at++] = make_int2(i0, pv.x);
+        if (m1) s_ds[warp][at++] = make_int2(i0 + 1, pv.y);
+        if (m2) s_ds[warp][at++] = make_int2(i0 + 2, pv.z);
+        if (m3) s_ds[warp][at++] = make_int2(i0 + 3, pv.w);
         __syncwarp();
+        char* base = X + n * ld_filter_bytes;
         const int items = nmoved * cpr;
         for (int it0 = 0; it0 < items; it0 += 32 * kGU) {
             int4 v[kGU];
@@ -852,7 +824,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows16(char* X, int64_t ld_
                 const int it = it0 + u * 32 + lane;
                 if (it < items) {
                     const int rw = it / cpr, ch = it - rw * cpr;
-                    v[u] = *(reinterpret_cast<const int4*>(s_src[warp][rw]) + ch);
+                    v[u] = *reinterpret_cast<const int4*>(base + static_cast<int64_t>(s_ds[warp][rw].y) * ld_bytes + ch * 16);
                 }
             }
 #pragma unroll
@@ -860,7 +832,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows16(char* X, int64_t ld_
                 const int it = it0 + u * 32 + lane;
                 if (it < items) {
                     const int rw = it / cpr, ch = it - rw * cpr;
-                    __stcs(reinterpret_cast<int4*>(s_dst[warp][rw]) + ch, v[u]);
+                    __stcs(reinterpret_cast<int4*>(base + static_cast<int64_t>(s_ds[warp][rw].x) * ld_bytes + ch * 16), v[u]);
                 }
             }
         }
@@ -1128,14 +1100,14 @@ cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, 
     const int64_t cpr = row_bytes / ch;
     const int64_t total = static_cast<int64_t>(N) * P * cpr;
     const unsigned grid = static_cast<unsigned>(grid_for(total, 16));
-    if (ch == 16 && cpr <= 64) {
-        const int vec_perm = ((reinterpret_cast<uintptr_t>(perm) & 15) == 0 && ld_perm % 4 == 0 && P % 4 == 0) ? 1 : 0;
-        const int64_t nblk = cdiv(static_cast<int64_t>(N) * P, 128);
+    const bool vec_perm = ((reinterpret_cast<uintptr_t>(perm) & 15) == 0 && ld_perm % 4 == 0 && P % 4 == 0);
+    if (ch == 16 && cpr <= 64 && vec_perm) {
+        const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
         const unsigned g2 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
                                                                                       sm_count() * 8)));
         ProfScope ps_("k_gather_inplace", s);
         k_gather_rows16<<<g2, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, static_cast<int>(cpr), perm,
-                                                ld_perm, vec_perm);
+                                                ld_perm);
     }
     else if (ch == 16) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
     else if (ch == 4) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<4><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }

@@ -289,7 +289,7 @@ def test_batched_offspring_permute_gather(pf, dev, orc):
 def test_repeatability_and_launch_count(pf, dev):
     import torch
 
-    x = _gpu(pfinputs.gaussian_logw(1 << 18, 1.0, seed=3), dev)
+    x = _gpu(pfinputs.gaussian_logw(1 << 16, 1.0, seed=3), dev)
     c0 = pf.pf_launch_count()
     a1 = pf.pf_resample_stratified(x, 11).clone()
     a2 = pf.pf_resample_stratified(x, 11)
