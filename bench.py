@@ -3,9 +3,12 @@
 
 One step = one pass of the whole hot path over a batch of synthetic filters
 (BASELINE.json configs[2], "batched PMCMC: 1024 independent filters x 2^16"):
-  pf_resample_batched (log-weight max, dexp + u64 lookback scan, ancestor search)
-  -> pf_permute_batched (offspring histogram + canonical permutation)
-  -> pf_gather_state_batched (in-place gather of a D=16 float32 state).
+  pf_resample_batched (a1-a5: max, dexp + u64 scan, ancestor search; a8:
+      offspring counts as a side output)
+  -> pf_permute_offspring_batched (a9: canonical in-place permutation)
+  -> pf_gather_state_batched (a10: in-place gather of a D=16 float32 state).
+The generic chain through pf_permute(ancestors) (histogram path) is timed
+as an extra (`extras.step_via_pf_permute_of_ancestors`).
 Metric: resampled particles/s (whole job, all ranks).  Multi-GPU: one process
 per GPU (torchrun); rank g owns filters [g*N, (g+1)*N) (global Philox filter
 indices), no data-path collective -> weak scaling; --strong splits a fixed N.
@@ -162,11 +165,14 @@ def run_ours(args):
     X = torch.randn((N, P, args.D), generator=torch.Generator(device=dev).manual_seed(first + 1), device=dev,
                     dtype=torch.float32)
     anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+    off = torch.empty((N, P), dtype=torch.int32, device=dev)
     perm = torch.empty((N, P), dtype=torch.int32, device=dev)
 
     def step():
-        pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
-        pf.pf_permute(anc, permuted=perm, stream=stream)
+        # a1-a5 (+a8: offspring as a side output of the resampler), a9, a10
+        pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
+                               stream=stream)
+        pf.pf_permute_offspring(off, permuted=perm, stream=stream)
         pf.pf_gather_state(X, perm, stream=stream)
 
     sampler = ClockSampler(local)
@@ -223,7 +229,8 @@ def run_ours(args):
         "k_metro": 8 * NP,
         "k_hist": 8 * NP,
         "k_pscan": 12 * NP,
-        "k_merge_perm": 4 * NP + 8 * free,
+        "k_push": 8 * NP + 8 * free,
+        "k_fused_sorted": 8 * NP + 4 * NP,
         "k_gather_inplace": 4 * NP + 2 * row * free,
     }
     hbm, peak_src = peaks()
@@ -269,6 +276,23 @@ def run_ours(args):
                 "ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
         extras["resample_only"] = per_scheme
 
+        # ---------------- generic chain: permutation from arbitrary ancestors (histogram path)
+        def step_generic():
+            pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
+            pf.pf_permute(anc, permuted=perm, stream=stream)
+            pf.pf_gather_state(X, perm, stream=stream)
+
+        step_generic()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(max(3, min(args.steps, 10))):
+            step_generic()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gms = g0.elapsed_time(g1) / max(3, min(args.steps, 10))
+        extras["step_via_pf_permute_of_ancestors"] = {"ms": round(gms, 4), "particles_per_s": N * P / (gms / 1e3)}
+
         # ---------------- end to end through the public API with host buffers
         h_logw = logw.cpu().pin_memory()
         h_out = torch.empty((N, P), dtype=torch.int32).pin_memory()
@@ -276,8 +300,9 @@ def run_ours(args):
 
         def e2e_step():
             d_logw.copy_(h_logw, non_blocking=True)
-            pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
-            pf.pf_permute(anc, permuted=perm, stream=stream)
+            pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
+                                   stream=stream)
+            pf.pf_permute_offspring(off, permuted=perm, stream=stream)
             pf.pf_gather_state(X, perm, stream=stream)
             h_out.copy_(perm, non_blocking=True)
 

@@ -82,6 +82,9 @@ typedef struct {
     float* normw_out;      /* [N][P] (row stride P) v_i = w_i / sum_j w_j  (NS-13)          */
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */
     int32_t* status_out;   /* [N] PF_FILTER_* per filter                                    */
+    int32_t* offspring_out; /* [N][P] (row stride = ancestors' ld) o_i = #{k : a_k = i} (NS-14);
+                              the one-launch stratified/systematic kernel derives it from its
+                              slot counts at no extra pass; other paths run the histogram   */
     void* workspace;       /* device, nullable -> library pool                              */
     size_t workspace_bytes;
 } pf_opts;
@@ -146,6 +149,16 @@ pf_status pf_permute_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int3
                              int32_t* permuted, int64_t ld_perm, pf_stream_t stream);
 
 /*
+ * Canonical permutation from offspring counts (NS-15): identical result to
+ * pf_permute(anc) for any ancestors with these offspring.  offspring[i] >= 0
+ * and sum_i offspring[i] == P are required (not checked).  Use with
+ * pf_opts.offspring_out to skip the ancestor histogram.
+ */
+pf_status pf_permute_offspring(const int32_t* offspring, int32_t P, int32_t* permuted, pf_stream_t stream);
+pf_status pf_permute_offspring_batched(const int32_t* offspring, int64_t ld_off, int32_t N, int32_t P,
+                                       int32_t* permuted, int64_t ld_perm, pf_stream_t stream);
+
+/*
  * State gather in place (NS-16): for each i with permuted[i] != i,
  * row i of X (row_bytes bytes at X + i*ld_bytes) <- row permuted[i].  Safe in
  * place ONLY for a pf_permute output (reads touch survivors, writes touch
@@ -190,6 +203,14 @@ typedef struct {
 } pf_kernel_time;
 void pf_profile_enable(int32_t on);
 int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries);
+
+/*
+ * Diagnostics: pf_set_fusion(0) makes every entry point use its multi-launch
+ * path (lookback scans, merge-path searches) even where a one-launch cluster
+ * kernel applies; pf_set_fusion(1) (default) re-enables them.  Results are
+ * identical either way; only speed differs.  Process-wide.
+ */
+void pf_set_fusion(int32_t on);
 
 /* Library version string. */
 const char* pf_version(void);

@@ -35,6 +35,7 @@ class _Opts(ctypes.Structure):
         ("normw_out", ctypes.c_void_p),
         ("ess_out", ctypes.c_void_p),
         ("status_out", ctypes.c_void_p),
+        ("offspring_out", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
     ]
@@ -57,6 +58,8 @@ _SIGS = {
     "pf_ancestors_to_offspring_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
     "pf_permute": ([_V, _I32, _V, _V], ctypes.c_int),
     "pf_permute_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
+    "pf_permute_offspring": ([_V, _I32, _V, _V], ctypes.c_int),
+    "pf_permute_offspring_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
     "pf_gather_state": ([_V, _I64, _I64, _I32, _V, _V], ctypes.c_int),
     "pf_gather_state_batched": ([_V, _I64, _I64, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
     "pf_gather_state_out": ([_V, _V, _I64, _I64, _I64, _I32, _V, _V], ctypes.c_int),
@@ -64,6 +67,7 @@ _SIGS = {
     "pf_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "pf_launch_count": ([], _U64),
     "pf_profile_enable": ([_I32], None),
+    "pf_set_fusion": ([_I32], None),
     "pf_profile_collect": ([_V, _I32], _I32),
     "pf_version": ([], ctypes.c_char_p),
     "pf_release": ([], None),
@@ -140,7 +144,8 @@ def _scheme(s):
 
 # ----------------------------------------------------------------------------- resamplers
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
-                   lse_out=None, normw_out=None, ess_out=None, status_out=None, flags: int = 0, stream=None):
+                   lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
+                   flags: int = 0, stream=None):
     """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -159,6 +164,8 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
         _need_cuda(normw_out, torch.float32, "normw_out"); opts.normw_out = normw_out.data_ptr()
     if status_out is not None:
         _need_cuda(status_out, torch.int32, "status_out"); opts.status_out = status_out.data_ptr()
+    if offspring_out is not None:
+        _need_cuda(offspring_out, torch.int32, "offspring_out"); opts.offspring_out = offspring_out.data_ptr()
     rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
                               ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_ex")
@@ -192,7 +199,8 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 
 
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
-                        lse_out=None, normw_out=None, ess_out=None, status_out=None, flags: int = 0, stream=None):
+                        lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
+                        flags: int = 0, stream=None):
     """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P]."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -206,7 +214,8 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
     aptr, ald = _rows(ancestors, "ancestors")
     opts = _Opts(flags=flags)
     for name, t, dt in (("lse_out", lse_out, torch.float64), ("ess_out", ess_out, torch.float64),
-                        ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32)):
+                        ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32),
+                        ("offspring_out", offspring_out, torch.int32)):
         if t is not None:
             _need_cuda(t, dt, name)
             setattr(opts, name, t.data_ptr())
@@ -254,6 +263,25 @@ def pf_permute(anc, permuted=None, stream=None):
         pp, pld = _rows(permuted, "permuted")
         rc = lib().pf_permute_batched(ap, ald, N, P, pp, pld, _stream(anc, stream))
     _check(rc, "pf_permute")
+    return permuted
+
+
+def pf_permute_offspring(offspring, permuted=None, stream=None):
+    """Canonical permutation (NS-15) from int32 offspring counts [P] or [N, P] (sum P per row)."""
+    torch = _torch()
+    _need_cuda(offspring, torch.int32, "offspring")
+    if permuted is None:
+        permuted = torch.empty_like(offspring)
+    _need_cuda(permuted, torch.int32, "permuted")
+    if offspring.dim() == 1:
+        rc = lib().pf_permute_offspring(offspring.data_ptr(), offspring.shape[0], permuted.data_ptr(),
+                                        _stream(offspring, stream))
+    else:
+        N, P = offspring.shape
+        op, old = _rows(offspring, "offspring")
+        pp, pld = _rows(permuted, "permuted")
+        rc = lib().pf_permute_offspring_batched(op, old, N, P, pp, pld, _stream(offspring, stream))
+    _check(rc, "pf_permute_offspring")
     return permuted
 
 
@@ -322,6 +350,11 @@ def pf_profile_collect() -> dict:
     if n < 0:
         raise PfError("pf_profile_collect: CUDA error")
     return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(n, 64))}
+
+
+def pf_set_fusion(on: bool = True) -> None:
+    """Diagnostics: False forces the multi-launch paths everywhere (identical results)."""
+    lib().pf_set_fusion(1 if on else 0)
 
 
 def pf_version() -> str:

@@ -17,6 +17,7 @@
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<bool> g_no_fusion{false};  // pf_set_fusion(0): diagnostics, multi-launch paths everywhere
 
 struct PoolBlock {
     void* ptr = nullptr;
@@ -104,13 +105,14 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     double* ess = opts ? opts->ess_out : nullptr;
     float* normw = opts ? opts->normw_out : nullptr;
     int32_t* status_out = opts ? opts->status_out : nullptr;
+    int32_t* offspring_out = opts ? opts->offspring_out : nullptr;
 
-    const bool no_fusion = opts && (opts->flags & PF_NO_FUSION);
+    const bool no_fusion = (opts && (opts->flags & PF_NO_FUSION)) || g_no_fusion.load();
     if (!no_fusion && pf::fused_supported(scheme, P)) {
         // one launch per batch: cluster-per-filter kernel, no workspace (pf_fused.cu)
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
-                                                      ess, normw, status_out, s, &nl);
+                                                      ess, normw, status_out, offspring_out, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }
@@ -135,6 +137,7 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
             e = pf::launch_metropolis(logw, ld, N, P, L, ws, seed, first_filter, B, anc, ld_anc, s, &nl);
     }
     if (normw && e == cudaSuccess) e = pf::launch_normw(logw, ld, N, P, ws, normw, s, &nl);
+    if (offspring_out && e == cudaSuccess) e = pf::launch_offspring(anc, ld_anc, N, P, offspring_out, ld_anc, s, &nl);
     g_launches += nl;
     return cuda_status(e);
 }
@@ -160,6 +163,8 @@ ProfScope::~ProfScope() {
 extern "C" {
 
 void pf_profile_enable(int32_t on) { g_prof_on.store(on != 0); }
+
+void pf_set_fusion(int32_t on) { g_no_fusion.store(on == 0); }
 
 int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -259,6 +264,27 @@ pf_status pf_permute_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int3
     if (e == cudaSuccess) e = pf::launch_permute(anc, ld_anc, N, P, L, ws, permuted, ld_perm, s, &nl);
     g_launches += nl;
     return cuda_status(e);
+}
+
+pf_status pf_permute_offspring_batched(const int32_t* offspring, int64_t ld_off, int32_t N, int32_t P,
+                                       int32_t* permuted, int64_t ld_perm, pf_stream_t stream) {
+    if (!offspring || !permuted || N < 1 || P < 1 || ld_off < P || ld_perm < P) return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const pf::Layout L = pf::make_layout(N, P, pf::kNeedPermute);
+    void* base = nullptr;
+    pf_status st = pool_get(L.total, s, &base);
+    if (st != PF_OK) return st;
+    const pf::Ws ws = pf::carve(base, L);
+    uint64_t nl = 0;
+    cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e == cudaSuccess)
+        e = pf::launch_permute_from_offspring(offspring, ld_off, N, P, L, ws, permuted, ld_perm, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_permute_offspring(const int32_t* offspring, int32_t P, int32_t* permuted, pf_stream_t stream) {
+    return pf_permute_offspring_batched(offspring, P, 1, P, permuted, P, stream);
 }
 
 pf_status pf_permute(const int32_t* anc, int32_t P, int32_t* permuted, pf_stream_t stream) {

@@ -66,6 +66,7 @@ struct FusedArgs {
     double* ess_out;
     float* normw;
     int32_t* status_out;
+    int32_t* off;   // offspring out (row stride ld_anc), nullable
 };
 
 struct Pos {
@@ -205,6 +206,8 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
             // NS-1: invalid filter -> identity ancestors, NaN side outputs
             int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
             for (int64_t k = p0 + tid; k < p1; k += kFT) arow[k] = static_cast<int32_t>(k);
+            if (a.off)
+                for (int64_t k = p0 + tid; k < p1; k += kFT) a.off[static_cast<int64_t>(n) * a.ld_anc + k] = 1;
             if (a.normw)
                 for (int64_t k = p0 + tid; k < p1; k += kFT) a.normw[static_cast<int64_t>(n) * a.P + k] = NAN;
             if (c == 0 && tid == 0) {
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
         }
         if (a.P == 1) {
             if (tid == 0) a.anc[static_cast<int64_t>(n) * a.ld_anc] = 0;
+            if (tid == 0 && a.off) a.off[static_cast<int64_t>(n) * a.ld_anc] = 1;
             __syncthreads();
             continue;
         }
@@ -366,6 +370,26 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
             else if (warp > 0) first[j] = s_lastE[j][warp - 1];
             else if (j > 0) first[j] = s_lastE[j - 1][kFW - 1];
             else first[j] = k_lo;
+        }
+        if (a.off) {
+            // a8 fused: o_i = E_i - E_{i-1}
+            int32_t* orow = a.off + static_cast<int64_t>(n) * a.ld_anc + p0;
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                const int32_t o0 = static_cast<int32_t>(E[j * 4 + 0] - first[j]);
+                const int32_t o1 = static_cast<int32_t>(E[j * 4 + 1] - E[j * 4 + 0]);
+                const int32_t o2 = static_cast<int32_t>(E[j * 4 + 2] - E[j * 4 + 1]);
+                const int32_t o3 = static_cast<int32_t>(E[j * 4 + 3] - E[j * 4 + 2]);
+                if (a.anc_vec && (p0 & 3) == 0 && i0 + 3 < np) {
+                    __stcs(reinterpret_cast<int4*>(orow + i0), make_int4(o0, o1, o2, o3));
+                } else {
+                    if (i0 + 0 < np) orow[i0 + 0] = o0;
+                    if (i0 + 1 < np) orow[i0 + 1] = o1;
+                    if (i0 + 2 < np) orow[i0 + 2] = o2;
+                    if (i0 + 3 < np) orow[i0 + 3] = o3;
+                }
+            }
         }
         int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
         const int32_t idbase = static_cast<int32_t>(p0) + tid * 4;
@@ -468,8 +492,8 @@ bool fused_supported(int scheme, int32_t P) {
 
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
-                                double* ess_out, float* normw, int32_t* status_out, cudaStream_t s,
-                                uint64_t* launches) {
+                                double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
+                                cudaStream_t s, uint64_t* launches) {
     FusedArgs a{};
     a.logw = logw;
     a.ld = ld;
@@ -493,6 +517,7 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.ess_out = ess_out;
     a.normw = normw;
     a.status_out = status_out;
+    a.off = offspring;
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
     if (scheme == 2) e = a.sums ? launch_fused_t<2, true>(a, s) : launch_fused_t<2, false>(a, s);

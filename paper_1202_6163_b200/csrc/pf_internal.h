@@ -75,6 +75,9 @@ cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int3
                              cudaStream_t s, uint64_t* launches);
 cudaError_t launch_permute(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, const Layout& L,
                            const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_permute_from_offspring(const int32_t* o, int64_t ld_o, int32_t N, int32_t P, const Layout& L,
+                                         const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s,
+                                         uint64_t* launches);
 cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes, int32_t N,
                                   int32_t P, const int32_t* perm, int64_t ld_perm, cudaStream_t s,
                                   uint64_t* launches);
@@ -85,7 +88,7 @@ cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t
 bool fused_supported(int scheme, int32_t P);
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
-                                double* ess_out, float* normw, int32_t* status_out, cudaStream_t s,
-                                uint64_t* launches);
+                                double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
+                                cudaStream_t s, uint64_t* launches);
 
 }  // namespace pf

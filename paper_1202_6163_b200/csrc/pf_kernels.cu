@@ -312,41 +312,6 @@ struct ModeSorted {
     }
 };
 
-struct PermCtx {
-    int n;
-    int64_t F;
-    const uint32_t* Qe;
-};
-
-// Canonical permutation (NS-15): free rank r -> survivor min{j : Qe_j > r}.
-struct ModePermute {
-    const uint32_t* Qe;
-    const int32_t* freeslot;
-    const int32_t* F;
-    int64_t ldq;
-    int32_t P;
-    int32_t* perm;
-    int64_t ld_perm;
-
-    using Ctx = PermCtx;
-    __device__ Ctx ctx(int n) const {
-        return {n, static_cast<int64_t>(F[n]), Qe + static_cast<int64_t>(n) * ldq};
-    }
-    __device__ bool valid(int) const { return true; }
-    __device__ int64_t nA(const Ctx& c) const { return c.F; }
-    __device__ uint64_t x(const Ctx&, int64_t r) const { return static_cast<uint64_t>(r); }
-    __device__ uint64_t b(const Ctx& c, int64_t i) const { return c.Qe[i]; }
-    __device__ void fill_a(const Ctx&, int64_t ka0, int na, uint64_t* s) const {
-        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = static_cast<uint64_t>(ka0 + t);
-    }
-    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
-        const int32_t* fs = freeslot + static_cast<int64_t>(c.n) * ldq + ka0;
-        int32_t* dst = perm + static_cast<int64_t>(c.n) * ld_perm;
-        for (int t = threadIdx.x; t < na; t += kThreads) dst[fs[t]] = s_out[t];
-    }
-    __device__ void identity(int, int, int) const {}
-};
-
 template <class Mode>
 __device__ __forceinline__ int64_t merge_split(const Mode& md, const typename Mode::Ctx& c, int64_t d, int64_t nA,
                                                int64_t nB, int lane) {
@@ -662,8 +627,8 @@ __global__ void __launch_bounds__(kThreads) k_hist_runs(const int32_t* __restric
 // Packed pair per particle: bits [0,31) free flag (o_i == 0), bits [31,62)
 // extras e_i = max(o_i - 1, 0).  Exclusive free rank and inclusive extras
 // offsets come out of one u64 lookback scan (both halves < 2^31, no carry).
-__global__ void __launch_bounds__(kThreads, 5) k_pscan(int32_t P, int T, Ws ws, int64_t ldq, int32_t* perm,
-                                                    int64_t ld_perm) {
+__global__ void __launch_bounds__(kThreads, 5) k_pscan(int32_t P, int T, Ws ws, int64_t ldq, const int32_t* o_in,
+                                                       int64_t ld_o, int o_vec, int32_t* perm, int64_t ld_perm) {
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_wtot[kThreads / 32];
     __shared__ uint64_t s_off[kThreads / 32];
@@ -674,12 +639,12 @@ __global__ void __launch_bounds__(kThreads, 5) k_pscan(int32_t P, int T, Ws ws, 
     const int n = static_cast<int>(tile / T);
     const int j = static_cast<int>(tile - static_cast<int64_t>(n) * T);
     const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
-    const int32_t* orow = ws.o + static_cast<int64_t>(n) * ldq;
+    const int32_t* orow = o_in + static_cast<int64_t>(n) * ld_o;
     int32_t ov[16];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t i0 = base + r * 128 + lane * 4;
-        if (i0 + 3 < P) {
+        if (o_vec && i0 + 3 < P) {
             const int4 t = __ldcg(reinterpret_cast<const int4*>(orow + i0));
             ov[r * 4 + 0] = t.x; ov[r * 4 + 1] = t.y; ov[r * 4 + 2] = t.z; ov[r * 4 + 3] = t.w;
         } else {
@@ -750,6 +715,92 @@ __global__ void __launch_bounds__(kThreads, 5) k_pscan(int32_t P, int T, Ws ws, 
 #pragma unroll
             for (int c = 0; c < 4; ++c)
                 if (i0 + c < P) qe[i0 + c] = e4[c];
+        }
+    }
+}
+
+// ============================================================================ a9: push
+// Completes the canonical permutation: the extras of a block of 128
+// consecutive particles occupy the contiguous free ranks [R0, R0 + S)
+// (R0 = exclusive extras prefix of the block's first particle).  Each warp
+// expands its block's extras list in 256-rank chunks with a head-mark +
+// max-scan in shared memory (owner of rank r = max{j : off_j <= r}) and writes
+// perm[freeslot[R0 + r]] = owner with coalesced free-slot reads.
+constexpr int kPushChunk = 256;
+__global__ void __launch_bounds__(kThreads) k_push(int32_t N, int32_t P, Ws ws, int64_t ldq, const int32_t* o_in,
+                                                   int64_t ld_o, int o_vec, int32_t* perm, int64_t ld_perm) {
+    __shared__ __align__(16) int32_t s_buf[kThreads / 32][kPushChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t per_filter = cdiv(P, 128);
+    const int64_t nblk = static_cast<int64_t>(N) * per_filter;
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    int4* b4 = reinterpret_cast<int4*>(s_buf[warp]);
+    for (int64_t blk = blockIdx.x * static_cast<int64_t>(kThreads / 32) + warp; blk < nblk; blk += wstride) {
+        const int64_t n = blk / per_filter;
+        const int64_t i0 = (blk - n * per_filter) * 128 + lane * 4;
+        const int32_t* orow = o_in + n * ld_o;
+        int32_t ov[4] = {1, 1, 1, 1};
+        if (o_vec && i0 + 3 < P) {
+            const int4 t = __ldcs(reinterpret_cast<const int4*>(orow + i0));
+            ov[0] = t.x; ov[1] = t.y; ov[2] = t.z; ov[3] = t.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (i0 + c < P) ov[c] = orow[i0 + c];
+        }
+        uint32_t e[4], loc = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            e[c] = ov[c] > 1 ? static_cast<uint32_t>(ov[c] - 1) : 0u;
+            loc += e[c];
+        }
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t S = __shfl_sync(kFull, incl, 31);
+        if (S == 0) continue;
+        const uint32_t lane_off = incl - loc;  // block-relative offset of this lane's first extra
+        // R0: exclusive extras prefix of the block's first particle (from the inclusive Qe of lane 0's first)
+        uint32_t R0 = 0;
+        if (lane == 0) R0 = __ldcg(ws.Qe + n * ldq + i0) - e[0];
+        R0 = __shfl_sync(kFull, R0, 0);
+        const int32_t* fs = ws.freeslot + n * ldq + R0;
+        int32_t* prow = perm + n * ld_perm;
+        int32_t carry = -1;
+        for (uint32_t c0 = 0; c0 < S; c0 += kPushChunk) {
+            b4[2 * lane] = make_int4(-1, -1, -1, -1);
+            b4[2 * lane + 1] = make_int4(-1, -1, -1, -1);
+            __syncwarp();
+            uint32_t off = lane_off;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t rel = off - c0;
+                if (e[c] > 0 && rel < static_cast<uint32_t>(kPushChunk)) s_buf[warp][rel] = static_cast<int32_t>(i0 + c);
+                off += e[c];
+            }
+            __syncwarp();
+            const int4 lo = b4[2 * lane], hi = b4[2 * lane + 1];
+            int32_t h[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
+            int32_t run = h[7];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t u = __shfl_up_sync(kFull, run, o);
+                if (lane >= o) run = max(run, u);
+            }
+            int32_t pre = __shfl_up_sync(kFull, run, 1);
+            pre = max(carry, lane == 0 ? -1 : pre);
+            carry = max(carry, __shfl_sync(kFull, run, 31));
+            const uint32_t r0 = c0 + 8 * lane;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (r0 + t < S) prow[__ldcg(fs + r0 + t)] = max(h[t], pre);
+            }
+            __syncwarp();
         }
     }
 }
@@ -1074,19 +1125,29 @@ cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int3
     return cudaPeekAtLastError();
 }
 
+cudaError_t launch_permute_from_offspring(const int32_t* o, int64_t ld_o, int32_t N, int32_t P, const Layout& L,
+                                         const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s,
+                                         uint64_t* launches) {
+    const int o_vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0 && ld_o % 4 == 0) ? 1 : 0;
+    { ProfScope ps_("k_pscan", s); k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, o, ld_o, o_vec, perm,
+                                                                                     ld_perm); }
+    ++*launches;
+    {
+        ProfScope ps_("k_push", s);
+        const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
+        const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
+                                                                                     sm_count() * 8)));
+        k_push<<<g, kThreads, 0, s>>>(N, P, ws, L.ldq, o, ld_o, o_vec, perm, ld_perm);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
 cudaError_t launch_permute(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, const Layout& L,
                            const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s, uint64_t* launches) {
     cudaError_t e = launch_offspring(anc, ld_anc, N, P, ws.o, L.ldq, s, launches);
     if (e != cudaSuccess) return e;
-    { ProfScope ps_("k_pscan", s); k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, perm,
-                                                                                     ld_perm); }
-    ++*launches;
-    const int64_t chunk = merge_chunk(N, P);
-    const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
-    ModePermute md{ws.Qe, ws.freeslot, ws.F, L.ldq, P, perm, ld_perm};
-    { ProfScope ps_("k_merge_perm", s); k_merge<ModePermute><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf, chunk); }
-    ++*launches;
-    return cudaPeekAtLastError();
+    return launch_permute_from_offspring(ws.o, L.ldq, N, P, L, ws, perm, ld_perm, s, launches);
 }
 
 cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, int64_t ld_filter_bytes, int32_t N,

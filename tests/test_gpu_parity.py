@@ -266,6 +266,71 @@ def test_offspring_permute_gather(pf, dev, orc):
                 assert np.array_equal(Y.cpu().numpy(), orc.gather_out(X, anc))
 
 
+@pytest.mark.parametrize("fusion", [True, False])
+def test_permute_paths(pf, dev, orc, fusion):
+    """Both permutation paths (cluster kernel, and the multi-launch hist -> lookback scan -> merge path
+    forced with pf_set_fusion(False)) against the oracle: sorted and unsorted ancestors, heavy
+    particles (sigma^2 = 10), ragged sizes, batched with ld > P."""
+    import torch
+
+    pf.pf_set_fusion(fusion)
+    try:
+        rng = np.random.default_rng(2)
+        for P in (1, 3, 8, 4096, 8191, 8193, 30000, 65536):
+            for scheme, var in (("systematic", 10.0), ("multinomial", 1.0), ("stratified", 0.1)):
+                x = pfinputs.gaussian_logw(P, var, seed=P + 1)
+                _, anc = orc.resample(scheme, x, 17)
+                if scheme == "multinomial":
+                    anc = rng.permutation(anc).astype(np.int32)
+                perm = pf.pf_permute(_gpu(anc, dev))
+                torch.cuda.synchronize()
+                assert np.array_equal(perm.cpu().numpy(), orc.permute(anc)), (fusion, P, scheme)
+        N, P, ld = 21, 12000, 12004
+        x = pfinputs.gaussian_logw(P, 1.0, seed=4, N=N)
+        _, A = orc.resample_batched("systematic", x, 5)
+        Ag = torch.zeros((N, ld), dtype=torch.int32, device=dev)
+        Ag[:, :P] = _gpu(A, dev)
+        out = torch.full((N, ld), -7, dtype=torch.int32, device=dev)
+        pf.pf_permute(Ag[:, :P], permuted=out[:, :P])
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        for n in range(N):
+            assert np.array_equal(o[n, :P], orc.permute(A[n]))
+        assert np.all(o[:, P:] == -7)
+    finally:
+        pf.pf_set_fusion(True)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("fusion", [True, False])
+def test_offspring_out_and_permute_offspring(pf, dev, orc, scheme, fusion):
+    """pf_opts.offspring_out (fused: derived from slot counts; otherwise the histogram) equals the
+    oracle's offspring, and pf_permute_offspring equals the oracle's canonical permutation."""
+    import torch
+
+    pf.pf_set_fusion(fusion)
+    try:
+        for N, P, var in ((1, 1, 1.0), (1, 7, 1.0), (3, 4097, 10.0), (16, 65536, 1.0), (2, 100003, 0.1)):
+            x = pfinputs.gaussian_logw(P, var, seed=P, N=N)
+            if N > 2:
+                x[1, :] = -np.inf  # an invalid filter: identity ancestors, offspring 1
+            g = _gpu(x, dev)
+            off = torch.empty((N, P), dtype=torch.int32, device=dev)
+            B = 9 if scheme == "metropolis" else 0
+            a = pf.pf_resample_batched(scheme, g, 71, B=B, offspring_out=off)
+            perm = pf.pf_permute_offspring(off)
+            torch.cuda.synchronize()
+            _, want = orc.resample_batched(scheme, x, 71, B=B)
+            assert np.array_equal(a.cpu().numpy(), want)
+            O = off.cpu().numpy()
+            Pm = perm.cpu().numpy()
+            for n in range(N):
+                assert np.array_equal(O[n], orc.ancestors_to_offspring(want[n])), (scheme, N, P, n)
+                assert np.array_equal(Pm[n], orc.permute(want[n])), (scheme, N, P, n)
+    finally:
+        pf.pf_set_fusion(True)
+
+
 def test_batched_offspring_permute_gather(pf, dev, orc):
     import torch
 
