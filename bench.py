@@ -38,6 +38,8 @@ WORKLOADS = {
     "c3": (1024, 1 << 16, "C3 batched PMCMC: 1024 filters x 2^16 particles per GPU"),
     "c2": (1, 1 << 20, "C2 single filter P=2^20"),
     "p24": (1, 1 << 24, "single filter P=2^24"),
+    # C5: one giant filter, 2^25 particles per GPU (weak), sharded with NCCL exchanges
+    "c5": (1, 1 << 25, "C5 giant filter sharded over GPUs: 2^25 particles per GPU"),
 }
 
 
@@ -134,6 +136,72 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def run_c5(args):
+    """Giant filter: P_global = 2^25 x world, contiguous shards, NCCL all_reduce / all_gather
+    between the shard stages (paper_1202_6163_b200.shard)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1202_6163_b200 as pf
+    import pfinputs
+    from paper_1202_6163_b200.shard import SingleComm, TorchComm, resample_sharded, shard_range
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = TorchComm() if world > 1 else SingleComm()
+    _, Pper, desc = WORKLOADS["c5"]
+    P_global = Pper * world
+    p0, Pl = shard_range(P_global, world, rank)
+    logw = pfinputs.gaussian_logw_torch(Pl, args.var, pfinputs.BASE_SEED + rank, 1, dev)[0].contiguous()
+    scheme = args.scheme
+    B = args.B if scheme == "metropolis" else 0
+    seed = pfinputs.seed_for(0)
+
+    def step():
+        return resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    l0 = pf.pf_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    launches = pf.pf_launch_count() - l0
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    clocks = sampler.stop()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": P_global * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 log-weights / u64 fixed-point scan / int32 indices",
+            "data": "synthetic",
+            "config": {"workload": desc + f", P_global={P_global}, sigma^2={args.var}, scheme={scheme}"
+                                  + (f", B={B}" if scheme == "metropolis" else ""),
+                       "parallelism": f"particle-sharded x{world}: all_reduce(MAX) + all_gather(totals)"
+                                      + (" + all_gather(weights)" if scheme == "metropolis" else ""),
+                       "l2": "inputs larger than L2 (logw 128 MiB/GPU, Q 256 MiB/GPU)"},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks,
+        }))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -457,6 +525,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

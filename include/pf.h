@@ -176,6 +176,54 @@ pf_status pf_gather_state_out(const void* X, void* Y, int64_t row_bytes, int64_t
                               int32_t P, const int32_t* anc, pf_stream_t stream);
 
 /*
+ * Giant-filter sharding.  One filter of P_global
+ * particles is split into contiguous shards; shard g owns particles
+ * [p0, p0 + Pl).  The stages below run on the shard's GPU; the caller issues
+ * the collectives between them (torch.distributed / NCCL):
+ *   1 pf_shard_max          -> all_reduce(MAX) of lmax, all_reduce(MAX) of bad
+ *   2 pf_shard_scan         -> all_gather of the 8-byte local totals (and sums)
+ *   3 pf_shard_search       (stratified / systematic / multinomial)
+ *   Metropolis: pf_shard_weights -> all_gather of the weights ->
+ *               pf_metropolis_from_weights on any slot range.
+ * Every stage evaluates the single-filter numeric spec (NS-2..NS-11) with the
+ * GLOBAL max and k_fx(P_global), so the assembled ancestors are bit-identical
+ * to pf_resample_ex on the whole filter (filter_index, seed as given).
+ */
+/* d_lmax[0] = max of the shard's log-weights (-inf if none); d_bad[0] = 1 if
+ * any NaN or +inf (else 0).  Device outputs. */
+pf_status pf_shard_max(const float* logw, int32_t Pl, float* d_lmax, int32_t* d_bad, pf_stream_t stream);
+/* d_Q[Pl] (u64, device, caller-owned) = inclusive fixed-point scan of the shard
+ * with the global max *d_gmax and k_fx = 61 - ceil(log2 P_global) (NS-5);
+ * d_total[0] = Q of the shard's last particle; d_wsum[0] = sum of the shard's
+ * w_i in double (lse = gmax + ln sum over shards, NS-13).  d_wsum nullable. */
+pf_status pf_shard_scan(const float* logw, int32_t Pl, int64_t P_global, const float* d_gmax, uint64_t* d_Q,
+                        uint64_t* d_total, double* d_wsum, pf_stream_t stream);
+/* Ancestors of the slots whose positions fall in this shard's range of the
+ * cumulative weights.  d_totals[nshards] = every shard's d_total (all-gathered,
+ * device).  d_gmax / d_gbad = all-reduced max and bad flag (device).  Writes
+ * anc_out[k] = global ancestor index for each slot k of this shard (anc_out has
+ * P_global entries; other entries untouched) and d_slot_range[0..1] = [k_lo,
+ * k_hi).  Stratified/systematic: positions are sorted, the slot range is found
+ * by search and merged with d_Q (work ~ Pl + slots).  Multinomial: every shard
+ * regenerates all P_global positions and keeps its own (replicated position
+ * generation; exact, not work-optimal).  An invalid global filter (bad or all
+ * -inf) writes the identity for slots [p0, p0 + Pl).  P_global <= 2^31 - 1. */
+pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                          const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
+                          const int32_t* d_gbad, uint64_t seed, uint32_t filter_index, int32_t* anc_out,
+                          int64_t* d_slot_range, pf_stream_t stream);
+/* Metropolis weights of the shard: w_out[Pl] = dexp(logw - *d_gmax) (NS-4). */
+pf_status pf_shard_weights(const float* logw, int32_t Pl, const float* d_gmax, float* w_out, pf_stream_t stream);
+/* Metropolis chains (NS-11) for slots [slot0, slot0 + nslots) of a filter whose
+ * full weight vector w_full[P_global] is on this device; anc[s] = final state of
+ * chain slot0 + s.  Bit-identical to the same chains of pf_resample_metropolis.
+ * d_gmax / d_gbad (nullable, device): the all-reduced max and bad flag; an
+ * invalid filter (bad, or max = -inf) gives the identity (NS-1). */
+pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int64_t slot0, int32_t nslots,
+                                     uint64_t seed, int32_t B, uint32_t filter_index, const float* d_gmax,
+                                     const int32_t* d_gbad, int32_t* anc, pf_stream_t stream);
+
+/*
  * Host helper: minimum B with lambda^B <= eps (alpha+beta)/max(alpha,beta)
  * (Eq. (4)-(5)), alpha = (1 - w_max)/(P w_max) (Eq. (2)), beta = 1/P.  Returns 0 if
  * B = 0 already satisfies Eq. (4), -1 on invalid arguments.  Host-only, no GPU.

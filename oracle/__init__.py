@@ -56,6 +56,8 @@ def lib():
         L.pfo_lmax.argtypes = [P, i32, P]
         L.pfo_weights.argtypes = [P, i32, P]
         L.pfo_kfx.argtypes = [i32]
+        L.pfo_weights_with.argtypes = [P, i32, f32, P]
+        L.pfo_cumulative_with.argtypes = [P, i32, f32, ctypes.c_int, P]
         L.pfo_cumulative.argtypes = [P, i32, P]
         L.pfo_position.argtypes = [ctypes.c_int, i32, u64, u64, u32, i64]
         L.pfo_position.restype = u64
@@ -113,6 +115,20 @@ def weights(logw: np.ndarray):
     w = np.zeros(len(logw), dtype=np.float32)
     st = lib().pfo_weights(_p(logw), len(logw), _p(w))
     return st, w
+
+
+def weights_with(logw: np.ndarray, lmax: float) -> np.ndarray:
+    logw = np.ascontiguousarray(logw, dtype=np.float32)
+    w = np.zeros(len(logw), dtype=np.float32)
+    lib().pfo_weights_with(_p(logw), len(logw), float(lmax), _p(w))
+    return w
+
+
+def cumulative_with(logw: np.ndarray, lmax: float, kfx_bits: int) -> np.ndarray:
+    logw = np.ascontiguousarray(logw, dtype=np.float32)
+    Q = np.zeros(len(logw), dtype=np.uint64)
+    lib().pfo_cumulative_with(_p(logw), len(logw), float(lmax), int(kfx_bits), _p(Q))
+    return Q
 
 
 def kfx(P: int) -> int:

@@ -132,16 +132,22 @@ int pfo_lmax(const float* logw, int32_t P, float* lmax)
     return PFO_FILTER_OK;
 }
 
+/* NS-3 / NS-4 with a given maximum (used for a shard of a larger filter) */
+void pfo_weights_with(const float* logw, int32_t P, float lmax, float* w)
+{
+    for (int32_t i = 0; i < P; ++i) {
+        float t = logw[i] - lmax; /* one binary32 subtraction, RN */
+        w[i] = pfo_dexp(t);
+    }
+}
+
 /* NS-3 / NS-4 */
 int pfo_weights(const float* logw, int32_t P, float* w)
 {
     float lmax;
     int st = pfo_lmax(logw, P, &lmax);
     if (st != PFO_FILTER_OK) return st;
-    for (int32_t i = 0; i < P; ++i) {
-        float t = logw[i] - lmax; /* one binary32 subtraction, RN */
-        w[i] = pfo_dexp(t);
-    }
+    pfo_weights_with(logw, P, lmax, w);
     return PFO_FILTER_OK;
 }
 
@@ -155,21 +161,27 @@ static int ceil_log2(int64_t P)
 
 int pfo_kfx(int32_t P) { return 61 - ceil_log2(P); }
 
-int pfo_cumulative(const float* logw, int32_t P, uint64_t* Q)
+/* NS-5 with a given maximum and fraction bits: inclusive scan of q_i */
+void pfo_cumulative_with(const float* logw, int32_t P, float lmax, int kfx, uint64_t* Q)
 {
-    float* w = (float*)malloc(sizeof(float) * (size_t)P);
-    int st = pfo_weights(logw, P, w);
-    if (st == PFO_FILTER_OK) {
-        double scale = ldexp(1.0, pfo_kfx(P)); /* 2^k_fx */
-        uint64_t acc = 0;
-        for (int32_t i = 0; i < P; ++i) {
-            /* exact: a 24-bit mantissa times a power of two, then truncate */
-            uint64_t q = (uint64_t)((double)w[i] * scale);
-            acc += q;
-            Q[i] = acc;
-        }
+    float* w = (float*)malloc(sizeof(float) * (size_t)(P > 0 ? P : 1));
+    pfo_weights_with(logw, P, lmax, w);
+    double scale = ldexp(1.0, kfx); /* 2^k_fx */
+    uint64_t acc = 0;
+    for (int32_t i = 0; i < P; ++i) {
+        /* exact: a 24-bit mantissa times a power of two, then truncate */
+        uint64_t q = (uint64_t)((double)w[i] * scale);
+        acc += q;
+        Q[i] = acc;
     }
     free(w);
+}
+
+int pfo_cumulative(const float* logw, int32_t P, uint64_t* Q)
+{
+    float lmax;
+    int st = pfo_lmax(logw, P, &lmax);
+    if (st == PFO_FILTER_OK) pfo_cumulative_with(logw, P, lmax, pfo_kfx(P), Q);
     return st;
 }
 

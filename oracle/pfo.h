@@ -33,6 +33,12 @@ int pfo_lmax(const float* logw, int32_t P, float* lmax);
 /* NS-3/NS-4: w_i = dexp(fl(logw_i - lmax)); returns filter status. */
 int pfo_weights(const float* logw, int32_t P, float* w);
 
+/* NS-3/NS-4 with an explicit (e.g. global) maximum: w_i = dexp(fl(logw_i - lmax)). */
+void pfo_weights_with(const float* logw, int32_t P, float lmax, float* w);
+
+/* NS-5 with explicit maximum and fraction bits (a shard of a larger filter). */
+void pfo_cumulative_with(const float* logw, int32_t P, float lmax, int kfx, uint64_t* Q);
+
 /* NS-5: fixed-point fraction bits k_fx = 61 - ceil(log2 P). */
 int pfo_kfx(int32_t P);
 

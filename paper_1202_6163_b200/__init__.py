@@ -63,6 +63,12 @@ _SIGS = {
     "pf_gather_state": ([_V, _I64, _I64, _I32, _V, _V], ctypes.c_int),
     "pf_gather_state_batched": ([_V, _I64, _I64, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
     "pf_gather_state_out": ([_V, _V, _I64, _I64, _I64, _I32, _V, _V], ctypes.c_int),
+    "pf_shard_max": ([_V, _I32, _V, _V, _V], ctypes.c_int),
+    "pf_shard_scan": ([_V, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_search": ([ctypes.c_int, _V, _I32, _I64, _I64, _V, _I32, _I32, _V, _V, _U64, _U32, _V, _V, _V],
+                        ctypes.c_int),
+    "pf_shard_weights": ([_V, _I32, _V, _V, _V], ctypes.c_int),
+    "pf_metropolis_from_weights": ([_V, _I64, _I64, _I32, _U64, _I32, _U32, _V, _V, _V, _V], ctypes.c_int),
     "pf_metropolis_required_B": ([_I64, _F64, _F64], _I32),
     "pf_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "pf_launch_count": ([], _U64),
@@ -322,6 +328,69 @@ def pf_gather_state_out(X, anc, Y=None, stream=None):
                                    anc.data_ptr(), _stream(X, stream))
     _check(rc, "pf_gather_state_out")
     return Y
+
+
+# ----------------------------------------------------------------------------- giant-filter shards
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def pf_shard_max(logw_local, stream=None):
+    """Stage 1 of a sharded filter: (lmax[1] f32, bad[1] i32) of this shard (device tensors)."""
+    torch = _torch()
+    _need_cuda(logw_local, torch.float32, "logw")
+    lmax = torch.empty(1, dtype=torch.float32, device=logw_local.device)
+    bad = torch.empty(1, dtype=torch.int32, device=logw_local.device)
+    _check(lib().pf_shard_max(logw_local.data_ptr(), logw_local.shape[0], lmax.data_ptr(), bad.data_ptr(),
+                              _stream(logw_local, stream)), "pf_shard_max")
+    return lmax, bad
+
+
+def pf_shard_scan(logw_local, P_global: int, gmax, stream=None):
+    """Stage 2: (Q[Pl] u64 as int64 tensor, total[1], wsum[1] f64) with the global max and k_fx(P_global)."""
+    torch = _torch()
+    _need_cuda(logw_local, torch.float32, "logw")
+    Pl = logw_local.shape[0]
+    Q = torch.empty(Pl, dtype=torch.int64, device=logw_local.device)
+    total = torch.empty(1, dtype=torch.int64, device=logw_local.device)
+    wsum = torch.empty(1, dtype=torch.float64, device=logw_local.device)
+    _check(lib().pf_shard_scan(logw_local.data_ptr(), Pl, P_global, gmax.data_ptr(), Q.data_ptr(),
+                               total.data_ptr(), wsum.data_ptr(), _stream(logw_local, stream)), "pf_shard_scan")
+    return Q, total, wsum
+
+
+def pf_shard_search(scheme, Q, p0: int, P_global: int, totals, shard: int, gmax, gbad, seed: int,
+                    filter_index: int, anc_out, stream=None):
+    """Stage 3: writes anc_out[k] (int32 [P_global]) for this shard's slots; returns slot_range[2] (int64)."""
+    torch = _torch()
+    rng = torch.empty(2, dtype=torch.int64, device=Q.device)
+    _check(lib().pf_shard_search(_scheme(scheme), Q.data_ptr(), Q.shape[0], p0, P_global, totals.data_ptr(),
+                                 totals.shape[0], shard, gmax.data_ptr(), gbad.data_ptr(), seed & (2 ** 64 - 1),
+                                 filter_index, anc_out.data_ptr(), rng.data_ptr(), _stream(Q, stream)),
+           "pf_shard_search")
+    return rng
+
+
+def pf_shard_weights(logw_local, gmax, w_out=None, stream=None):
+    torch = _torch()
+    _need_cuda(logw_local, torch.float32, "logw")
+    if w_out is None:
+        w_out = torch.empty_like(logw_local)
+    _check(lib().pf_shard_weights(logw_local.data_ptr(), logw_local.shape[0], gmax.data_ptr(), w_out.data_ptr(),
+                                  _stream(logw_local, stream)), "pf_shard_weights")
+    return w_out
+
+
+def pf_metropolis_from_weights(w_full, slot0: int, nslots: int, seed: int, B: int, filter_index: int = 0,
+                               gmax=None, gbad=None, anc=None, stream=None):
+    torch = _torch()
+    _need_cuda(w_full, torch.float32, "w_full")
+    if anc is None:
+        anc = torch.empty(nslots, dtype=torch.int32, device=w_full.device)
+    _check(lib().pf_metropolis_from_weights(w_full.data_ptr(), w_full.shape[0], slot0, nslots,
+                                            seed & (2 ** 64 - 1), B, filter_index, _ptr(gmax), _ptr(gbad),
+                                            anc.data_ptr(), _stream(w_full, stream)), "pf_metropolis_from_weights")
+    return anc
 
 
 # ----------------------------------------------------------------------------- host helpers

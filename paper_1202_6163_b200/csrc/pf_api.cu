@@ -319,6 +319,88 @@ pf_status pf_gather_state_out(const void* X, void* Y, int64_t row_bytes, int64_t
     return cuda_status(e);
 }
 
+// ---------------------------------------------------------------- giant-filter shards
+pf_status pf_shard_max(const float* logw, int32_t Pl, float* d_lmax, int32_t* d_bad, pf_stream_t stream) {
+    if (!logw || !d_lmax || !d_bad || Pl < 1) return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const pf::Layout L = pf::make_layout(1, Pl, 0u);
+    void* base = nullptr;
+    pf_status st = pool_get(L.total, s, &base);
+    if (st != PF_OK) return st;
+    const pf::Ws ws = pf::carve(base, L);
+    uint64_t nl = 0;
+    cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e == cudaSuccess) e = pf::launch_max(logw, Pl, 1, Pl, L, ws, nullptr, s, &nl, d_lmax, d_bad);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_scan(const float* logw, int32_t Pl, int64_t P_global, const float* d_gmax, uint64_t* d_Q,
+                        uint64_t* d_total, double* d_wsum, pf_stream_t stream) {
+    if (!logw || !d_gmax || !d_Q || !d_total || Pl < 1 || P_global < Pl || P_global > INT32_MAX)
+        return PF_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(d_Q) & 15) != 0) return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const pf::Layout L = pf::make_layout(1, Pl, 0u);
+    void* base = nullptr;
+    pf_status st = pool_get(L.total, s, &base);
+    if (st != PF_OK) return st;
+    pf::Ws ws = pf::carve(base, L);
+    ws.Q = d_Q;
+    uint64_t nl = 0;
+    cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws.fstatus, 0, sizeof(int32_t), s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ws.lmax, d_gmax, sizeof(float), cudaMemcpyDeviceToDevice, s);
+    const int kfx = 61 - pf::ceil_log2(P_global);
+    if (e == cudaSuccess) e = pf::launch_scan(logw, Pl, 1, Pl, L, ws, true, nullptr, nullptr, s, &nl, kfx);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_total, ws.Qtot, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && d_wsum) e = cudaMemcpyAsync(d_wsum, ws.S, sizeof(double), cudaMemcpyDeviceToDevice, s);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                          const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
+                          const int32_t* d_gbad, uint64_t seed, uint32_t filter_index, int32_t* anc_out,
+                          int64_t* d_slot_range, pf_stream_t stream) {
+    if (!d_Q || !d_totals || !d_gmax || !d_gbad || !anc_out || !d_slot_range) return PF_ERR_INVALID_ARG;
+    if (scheme < PF_MULTINOMIAL || scheme > PF_SYSTEMATIC) return PF_ERR_UNSUPPORTED;
+    if (Pl < 1 || p0 < 0 || P_global < p0 + Pl || P_global > INT32_MAX || nshards < 1 || shard < 0 ||
+        shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* ctx = nullptr;
+    pf_status st = pool_get(pf::shard_ctx_bytes(), s, &ctx);
+    if (st != PF_OK) return st;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_shard_search(scheme, d_Q, Pl, p0, P_global, d_totals, nshards, shard, d_gmax,
+                                                  d_gbad, seed, filter_index, anc_out, d_slot_range, ctx, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_weights(const float* logw, int32_t Pl, const float* d_gmax, float* w_out, pf_stream_t stream) {
+    if (!logw || !d_gmax || !w_out || Pl < 1) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_shard_weights(logw, Pl, d_gmax, w_out, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int64_t slot0, int32_t nslots,
+                                     uint64_t seed, int32_t B, uint32_t filter_index, const float* d_gmax,
+                                     const int32_t* d_gbad, int32_t* anc, pf_stream_t stream) {
+    if (!w_full || !anc || P_global < 1 || P_global > INT32_MAX || slot0 < 0 || nslots < 0 ||
+        slot0 + nslots > P_global || B < 0)
+        return PF_ERR_INVALID_ARG;
+    if (nslots == 0) return PF_OK;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_metro_slots(w_full, P_global, slot0, nslots, seed, B, filter_index, d_gmax,
+                                                 d_gbad, anc, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
 int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps) {
     if (P < 1 || !(w_max > 0.0) || w_max > 1.0 || !(eps > 0.0)) return -1;
     const double beta = 1.0 / static_cast<double>(P);

@@ -58,9 +58,11 @@ Ws carve(void* base, const Layout& L);
 // Launchers: enqueue on `s`; return cudaPeekAtLastError().  `launches` is
 // incremented by the number of kernels enqueued.
 cudaError_t launch_max(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
-                       int32_t* status_out, cudaStream_t s, uint64_t* launches);
+                       int32_t* status_out, cudaStream_t s, uint64_t* launches, float* lmax_out = nullptr,
+                       int32_t* bad_out = nullptr);
 cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
-                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches);
+                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches,
+                        int kfx_override = -1);
 cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
                           uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
                           uint64_t* launches);
@@ -83,6 +85,18 @@ cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, 
                                   uint64_t* launches);
 cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int64_t ld_y, int32_t P,
                               const int32_t* anc, cudaStream_t s, uint64_t* launches);
+
+// Giant-filter shard stages (C5).
+cudaError_t launch_shard_search(int scheme, const uint64_t* Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                const uint64_t* totals, int nshards, int shard, const float* gmax,
+                                const int32_t* gbad, uint64_t seed, uint32_t filt, int32_t* anc,
+                                int64_t* range_out, void* ctx_mem, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_shard_weights(const float* logw, int32_t Pl, const float* gmax, float* w, cudaStream_t s,
+                                 uint64_t* launches);
+cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, int32_t nslots, uint64_t seed,
+                               int32_t B, uint32_t filt, const float* gmax, const int32_t* gbad, int32_t* anc,
+                               cudaStream_t s, uint64_t* launches);
+size_t shard_ctx_bytes();
 
 // One-launch cluster-per-filter resampler for stratified/systematic (pf_fused.cu).
 bool fused_supported(int scheme, int32_t P);

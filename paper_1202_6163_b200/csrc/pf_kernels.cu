@@ -31,7 +31,8 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // ============================================================================ a1: max
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_max(const float* __restrict__ logw, int64_t ld, int32_t P,
-                                                  int cpf, int64_t chunk, Ws ws, int32_t* status_out) {
+                                                  int cpf, int64_t chunk, Ws ws, int32_t* status_out,
+                                                  float* lmax_out, int32_t* bad_out) {
     __shared__ float s_m[kThreads / 32];
     __shared__ int s_b[kThreads / 32];
     __shared__ int s_last;
@@ -104,6 +105,8 @@ __global__ void __launch_bounds__(kThreads) k_max(const float* __restrict__ logw
         ws.lmax[n] = m;
         ws.fstatus[n] = st;
         if (status_out) status_out[n] = st;
+        if (lmax_out) lmax_out[n] = m;
+        if (bad_out) bad_out[n] = bad;
     }
 }
 
@@ -920,6 +923,203 @@ __global__ void __launch_bounds__(kThreads) k_gather_out(const char* __restrict_
     }
 }
 
+// ============================================================================ shards (C5)
+struct ShardCtxDev {
+    int64_t k_lo, k_hi;
+    uint64_t off, Qtot, T;
+    int32_t invalid;
+};
+
+template <int SCHEME>
+__device__ __forceinline__ uint64_t shard_position(int64_t k, uint64_t D, uint64_t rho, uint64_t Qtot, Key key,
+                                                   uint32_t filt) {
+    if (SCHEME == 2) {
+        const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 2u, filt, key.k0, key.k1);
+        rho = mulhi64((k & 1) ? hi_word(r) : lo_word(r), D);
+    }
+    return mulhi64(static_cast<uint64_t>(k) * D + rho, Qtot);
+}
+
+// One warp: offsets from the all-gathered totals, validity, and the slot range
+// [k_lo, k_hi) = [#{k : x_k < off}, #{k : x_k < off + T}) by 32-ary searches.
+template <int SCHEME>
+__global__ void k_shard_range(const uint64_t* totals, int nshards, int shard, const float* gmax,
+                              const int32_t* gbad, int64_t P_global, uint64_t D, Key key, uint32_t filt,
+                              ShardCtxDev* ctx, int64_t* range_out) {
+    const int lane = threadIdx.x & 31;
+    uint64_t off = 0, tot = 0;
+    for (int h = 0; h < nshards; ++h) {
+        const uint64_t t = totals[h];
+        if (h < shard) off += t;
+        tot += t;
+    }
+    const uint64_t T = totals[shard];
+    const int invalid = (*gbad != 0 || *gmax == -INFINITY) ? 1 : 0;
+    uint64_t rho = 0;
+    if (SCHEME == 3) rho = mulhi64(lo_word(philox10(0u, 0u, 3u, filt, key.k0, key.k1)), D);
+    int64_t kk[2];
+    for (int w = 0; w < 2; ++w) {
+        const uint64_t v = w ? off + T : off;
+        int64_t lo = 0, hi = P_global;
+        while (hi > lo) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t m = lo + lane * step;
+            const bool p = (m < hi) && (shard_position<SCHEME>(m, D, rho, tot, key, filt) < v);
+            const int L = __popc(__ballot_sync(kFull, p));
+            const int64_t nlo = (L == 0) ? lo : lo + static_cast<int64_t>(L - 1) * step + 1;
+            const int64_t mL = lo + static_cast<int64_t>(L) * step;
+            hi = (mL < hi) ? mL : hi;
+            lo = nlo;
+        }
+        kk[w] = lo;
+    }
+    if (lane == 0) {
+        ctx->k_lo = invalid ? 0 : kk[0];
+        ctx->k_hi = invalid ? 0 : kk[1];
+        ctx->off = off;
+        ctx->Qtot = tot;
+        ctx->T = T;
+        ctx->invalid = invalid;
+        range_out[0] = ctx->k_lo;
+        range_out[1] = ctx->k_hi;
+    }
+}
+
+struct ShardCtx {
+    int n;
+    int64_t k_lo, nA;
+    uint64_t off, Qtot, D, rho;
+    uint32_t filt;
+};
+
+template <int SCHEME>
+struct ModeShard {
+    const uint64_t* Q;
+    const ShardCtxDev* dctx;
+    uint64_t D;
+    Key key;
+    uint32_t filt;
+    int32_t P;  // particles of this shard (the B list)
+    int64_t p0;
+    int32_t* anc;
+
+    using Ctx = ShardCtx;
+    __device__ Ctx ctx(int) const {
+        Ctx c;
+        c.n = 0;
+        c.k_lo = dctx->k_lo;
+        c.nA = dctx->k_hi - dctx->k_lo;
+        c.off = dctx->off;
+        c.Qtot = dctx->Qtot;
+        c.D = D;
+        c.filt = filt;
+        c.rho = 0;
+        if (SCHEME == 3) c.rho = mulhi64(lo_word(philox10(0u, 0u, 3u, filt, key.k0, key.k1)), D);
+        return c;
+    }
+    __device__ bool valid(int) const { return dctx->invalid == 0; }
+    __device__ int64_t nA(const Ctx& c) const { return c.nA; }
+    __device__ uint64_t x(const Ctx& c, int64_t m) const {
+        return shard_position<SCHEME>(c.k_lo + m, c.D, c.rho, c.Qtot, key, c.filt);
+    }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return c.off + __ldg(Q + i); }
+    __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
+        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        int32_t* dst = anc + c.k_lo + ka0;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[t] = static_cast<int32_t>(p0 + s_out[t]);
+    }
+    __device__ void identity(int, int cb, int cpf) const {
+        const int64_t per = cdiv(P, cpf);
+        const int64_t b0 = cb * per, b1 = min(static_cast<int64_t>(P), b0 + per);
+        for (int64_t k = b0 + threadIdx.x; k < b1; k += kThreads) anc[p0 + k] = static_cast<int32_t>(p0 + k);
+    }
+};
+
+// Multinomial shard: every shard regenerates all positions (NS-8) and keeps
+// those in its cumulative-weight range [off, off + T); binary search in d_Q.
+__global__ void __launch_bounds__(kThreads) k_shard_multinomial(const uint64_t* __restrict__ Q, int32_t Pl,
+                                                                int64_t p0, int64_t P_global,
+                                                                const ShardCtxDev* dctx, Key key, uint32_t filt,
+                                                                int32_t* anc) {
+    const ShardCtxDev c = *dctx;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    const int64_t g0 = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (c.invalid) {
+        for (int64_t k = g0; k < Pl; k += stride) anc[p0 + k] = static_cast<int32_t>(p0 + k);
+        return;
+    }
+    const int64_t npairs = (P_global + 1) / 2;
+    for (int64_t pr = g0; pr < npairs; pr += stride) {
+        const u32x4 r = philox10(static_cast<uint32_t>(pr), 0u, 1u, filt, key.k0, key.k1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t k = 2 * pr + h;
+            if (k >= P_global) break;
+            const uint64_t x = mulhi64(h ? hi_word(r) : lo_word(r), c.Qtot);
+            if (x < c.off || x - c.off >= c.T) continue;
+            const uint64_t xl = x - c.off;  // local position; local Q is relative to the shard
+            int64_t lo = 0, hi = Pl - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(Q + mid) > xl) hi = mid;
+                else lo = mid + 1;
+            }
+            anc[k] = static_cast<int32_t>(p0 + lo);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_shard_weights(const float* __restrict__ logw, int32_t Pl,
+                                                            const float* gmax, float* w) {
+    const float lm = *gmax;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < Pl;
+         i += static_cast<int64_t>(gridDim.x) * kThreads)
+        w[i] = weight(__ldcs(logw + i), lm);
+}
+
+// Metropolis chains slot0 .. slot0 + nslots - 1 over the full weight vector (NS-11).
+__global__ void __launch_bounds__(kThreads) k_metro_slots(const float* __restrict__ w, int64_t P_global,
+                                                          int64_t slot0, int32_t nslots, Key key, uint32_t filt,
+                                                          int32_t B, const float* gmax, const int32_t* gbad,
+                                                          int32_t* anc) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (s >= nslots) return;
+    const int64_t i = slot0 + s;
+    const bool invalid = (gbad && *gbad != 0) || (gmax && *gmax == -INFINITY);
+    if (invalid || B == 0) {
+        anc[s] = static_cast<int32_t>(i);
+        return;
+    }
+    int64_t k = i;
+    float wk = __ldg(w + i);
+    const float kU = __uint_as_float(0x33800000u);
+    for (int32_t b = 0; b < B; b += 8) {
+        uint32_t j[8];
+        float u[8], wj[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>((b >> 1) + t), 4u, filt, key.k0,
+                                     key.k1);
+            j[2 * t] = static_cast<uint32_t>((static_cast<uint64_t>(r.x) * static_cast<uint64_t>(P_global)) >> 32);
+            u[2 * t] = __fmul_rn(static_cast<float>(r.y >> 8), kU);
+            j[2 * t + 1] = static_cast<uint32_t>((static_cast<uint64_t>(r.z) * static_cast<uint64_t>(P_global)) >> 32);
+            u[2 * t + 1] = __fmul_rn(static_cast<float>(r.w >> 8), kU);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) wj[t] = (b + t < B) ? __ldg(w + j[t]) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (b + t < B && __fmul_rn(u[t], wk) < wj[t]) {
+                k = j[t];
+                wk = wj[t];
+            }
+        }
+    }
+    anc[s] = static_cast<int32_t>(k);
+}
+
 int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -1006,21 +1206,22 @@ Ws carve(void* base, const Layout& L) {
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 cudaError_t launch_max(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
-                       int32_t* status_out, cudaStream_t s, uint64_t* launches) {
+                       int32_t* status_out, cudaStream_t s, uint64_t* launches, float* lmax_out, int32_t* bad_out) {
     const int cpf = L.cpf_max;
     int64_t chunk = cdiv(P, cpf);
     chunk = (chunk + 3) / 4 * 4;
     const bool vec = aligned16(logw) && (ld % 4 == 0);
     const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
-    if (vec) { ProfScope ps_("k_max", s); k_max<true><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out); }
-    else { ProfScope ps_("k_max", s); k_max<false><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out); }
+    if (vec) { ProfScope ps_("k_max", s); k_max<true><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
+    else { ProfScope ps_("k_max", s); k_max<false><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
     ++*launches;
     return cudaPeekAtLastError();
 }
 
 cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L, const Ws& ws,
-                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches) {
-    const int kfx = 61 - ceil_log2(P);
+                        bool write_q, double* lse_out, double* ess_out, cudaStream_t s, uint64_t* launches,
+                        int kfx_override) {
+    const int kfx = (kfx_override >= 0) ? kfx_override : 61 - ceil_log2(P);
     const bool vec = aligned16(logw) && (ld % 4 == 0);
     const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * L.T));
     if (vec)
@@ -1194,5 +1395,63 @@ cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t
     ++*launches;
     return cudaPeekAtLastError();
 }
+
+// ---------------------------------------------------------------- shard launchers
+cudaError_t launch_shard_search(int scheme, const uint64_t* Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                const uint64_t* totals, int nshards, int shard, const float* gmax,
+                                const int32_t* gbad, uint64_t seed, uint32_t filt, int32_t* anc,
+                                int64_t* range_out, void* ctx_mem, cudaStream_t s, uint64_t* launches) {
+    const Key key = make_key(seed);
+    ShardCtxDev* dctx = static_cast<ShardCtxDev*>(ctx_mem);
+    const uint64_t D = (P_global <= 1) ? 0 : stratum_width(static_cast<int32_t>(P_global));
+    // the range kernel evaluates sorted positions; multinomial only needs the offsets from it
+    {
+        ProfScope ps_("k_shard_range", s);
+        if (scheme == 2) k_shard_range<2><<<1, 32, 0, s>>>(totals, nshards, shard, gmax, gbad, P_global, D, key, filt, dctx, range_out);
+        else k_shard_range<3><<<1, 32, 0, s>>>(totals, nshards, shard, gmax, gbad, P_global, D, key, filt, dctx, range_out);
+    }
+    ++*launches;
+    if (scheme == 1) {
+        ProfScope ps_("k_shard_multinomial", s);
+        k_shard_multinomial<<<static_cast<unsigned>(grid_for((P_global + 1) / 2, 8)), kThreads, 0, s>>>(
+            Q, Pl, p0, P_global, dctx, key, filt, anc);
+        ++*launches;
+        return cudaPeekAtLastError();
+    }
+    const int64_t chunk = merge_chunk(1, static_cast<int32_t>(std::min<int64_t>(P_global, INT32_MAX / 2)));
+    const int cpf = static_cast<int>(cdiv(P_global + Pl, chunk));
+    if (scheme == 2) {
+        ModeShard<2> md{Q, dctx, D, key, filt, Pl, p0, anc};
+        ProfScope ps_("k_merge", s);
+        k_merge<ModeShard<2>><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
+    } else {
+        ModeShard<3> md{Q, dctx, D, key, filt, Pl, p0, anc};
+        ProfScope ps_("k_merge", s);
+        k_merge<ModeShard<3>><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_shard_weights(const float* logw, int32_t Pl, const float* gmax, float* w, cudaStream_t s,
+                                 uint64_t* launches) {
+    ProfScope ps_("k_shard_weights", s);
+    k_shard_weights<<<static_cast<unsigned>(grid_for(Pl)), kThreads, 0, s>>>(logw, Pl, gmax, w);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, int32_t nslots, uint64_t seed,
+                               int32_t B, uint32_t filt, const float* gmax, const int32_t* gbad, int32_t* anc,
+                               cudaStream_t s, uint64_t* launches) {
+    ProfScope ps_("k_metro_slots", s);
+    k_metro_slots<<<static_cast<unsigned>(cdiv(nslots, kThreads)), kThreads, 0, s>>>(w, P_global, slot0, nslots,
+                                                                                     make_key(seed), filt, B, gmax,
+                                                                                     gbad, anc);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+size_t shard_ctx_bytes() { return sizeof(ShardCtxDev); }
 
 }  // namespace pf

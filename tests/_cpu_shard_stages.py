@@ -1,0 +1,54 @@
+"""CPU stand-ins for the shard stages of paper_1202_6163_b200.shard, built on the
+oracle (TEST INFRASTRUCTURE).  They let the multi-rank decomposition logic
+(offsets from all-gathered totals, slot ranges, assembly) run under
+torch.distributed with gloo on CPU; the GPU kernels of the same stages are
+checked against the oracle in tests/test_gpu_parity.py (fake-shard mode)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+
+
+class CpuOracleStages:
+    def max(self, logw):
+        x = logw.numpy()
+        bad = bool(np.isnan(x).any() or np.isposinf(x).any())
+        ok = x[~np.isnan(x) & ~np.isposinf(x)]
+        m = np.float32(ok.max()) if ok.size else np.float32(-np.inf)
+        return torch.tensor([m], dtype=torch.float32), torch.tensor([int(bad)], dtype=torch.int32)
+
+    def scan(self, logw, P_global, gmax):
+        x = logw.numpy()
+        g = float(gmax.item())
+        Q = oracle.cumulative_with(x, g, oracle.kfx(P_global))
+        w = oracle.weights_with(x, g)
+        return (torch.from_numpy(Q.view(np.int64).copy()), torch.tensor([int(Q[-1])], dtype=torch.int64),
+                torch.tensor([float(np.sum(w.astype(np.float64)))], dtype=torch.float64))
+
+    def search(self, scheme, Q, p0, P_global, totals, shard, gmax, gbad, seed, filter_index, anc_out):
+        Ql = Q.numpy().view(np.uint64)
+        Pl = len(Ql)
+        if int(gbad.item()) or float(gmax.item()) == -np.inf:
+            anc_out[p0:p0 + Pl] = torch.arange(p0, p0 + Pl, dtype=torch.int32)
+            return torch.tensor([0, 0], dtype=torch.int64)
+        tot = [int(v) for v in totals.numpy().view(np.uint64)]
+        off, Qtot, T = sum(tot[:shard]), sum(tot), tot[shard]
+        ks = []
+        for k in range(P_global):
+            x = oracle.position(scheme, P_global, Qtot, seed, filter_index, k)
+            if off <= x < off + T:
+                anc_out[k] = p0 + int(np.searchsorted(Ql, np.uint64(x - off), side="right"))
+                ks.append(k)
+        rng = (min(ks), max(ks) + 1) if ks else (0, 0)
+        return torch.tensor(rng, dtype=torch.int64)
+
+    def weights(self, logw, gmax):
+        return torch.from_numpy(oracle.weights_with(logw.numpy(), float(gmax.item())))
+
+    def metropolis(self, w_full, slot0, nslots, seed, B, filter_index, gmax, gbad):
+        if int(gbad.item()) or float(gmax.item()) == -np.inf:
+            return torch.arange(slot0, slot0 + nslots, dtype=torch.int32)
+        a = oracle.metropolis_chains(w_full.numpy(), slot0, nslots, seed, B, filter_index)
+        return torch.from_numpy(a)

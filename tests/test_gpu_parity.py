@@ -365,3 +365,29 @@ def test_repeatability_and_launch_count(pf, dev):
     pf.pf_resample_ex("stratified", x, 11, flags=pf.PF_NO_FUSION)
     torch.cuda.synchronize()
     assert pf.pf_launch_count() - c0 == 3  # max, scan, merge
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_giant_filter_fake_shards(pf, dev, orc, scheme):
+    """C5 decomposition on one GPU (fake-shard mode): the shard kernels (pf_shard_max / scan / search,
+    pf_shard_weights, pf_metropolis_from_weights) with host-side exchanges reproduce the single-filter
+    result bit-exactly, for several shard counts, a shard without weight, and an invalid filter."""
+    import torch
+
+    from paper_1202_6163_b200.shard import resample_sharded_local, shard_range
+
+    B = 16 if scheme == "metropolis" else 0
+    cases = [(1000, 2, 1.0, ""), (4097, 3, 10.0, ""), (65536, 8, 1.0, ""), (100003, 5, 0.1, ""),
+             (1 << 20, 8, 1.0, ""), (9000, 4, 1.0, "neg_inf_shard"), (5000, 2, 1.0, "invalid")]
+    for P, G, var, kind in cases:
+        x = pfinputs.gaussian_logw(P, var, seed=P + G)
+        if kind == "neg_inf_shard":
+            p0, Pl = shard_range(P, G, 2)
+            x[p0:p0 + Pl] = -np.inf
+        if kind == "invalid":
+            x[17] = np.inf
+        g = _gpu(x, dev)
+        a = resample_sharded_local(scheme, g, G, 4321, B=B, filter_index=3)
+        torch.cuda.synchronize()
+        _, want = orc.resample(scheme, x, 4321, B=B, filter_index=3)
+        assert np.array_equal(a.cpu().numpy(), want), (scheme, P, G, kind)

@@ -1,0 +1,100 @@
+"""World-size-2 multi-process tests of the N>1 paths on CPU (gloo, 127.0.0.1).
+
+* Giant filter sharded over ranks (config C5's decomposition):
+  paper_1202_6163_b200.shard.resample_sharded with real torch.distributed
+  collectives (all_reduce MAX, all_gather of totals / weights) and CPU stand-in
+  stages (oracle-based), assembled ancestors == the oracle's single-filter run.
+* Batched filters sharded over ranks (config C3, bench.py): rank g owns filters
+  [g N, (g+1) N) with first_filter = g N; the union equals a single-rank batch.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir, cases):
+    sys.path.insert(0, ROOT)
+    import oracle
+    import pfinputs
+    from paper_1202_6163_b200.shard import TorchComm, resample_sharded, shard_range
+    from tests._cpu_shard_stages import CpuOracleStages
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = TorchComm()
+    stages = CpuOracleStages()
+    for ci, (scheme, P, var, seed, B, kind) in enumerate(cases):
+        x = pfinputs.gaussian_logw(P, var, seed=P)
+        if kind == "neg_inf_shard":
+            p0, Pl = shard_range(P, world, 1)
+            x[p0:p0 + Pl] = -np.inf  # rank 1 holds no weight at all
+        if kind == "invalid":
+            x[3] = np.nan
+        p0, Pl = shard_range(P, world, rank)
+        anc, info = resample_sharded(scheme, torch.from_numpy(x[p0:p0 + Pl].copy()), P, seed, B=B,
+                                     filter_index=5, comm=comm, stages=stages)
+        if rank == 0:
+            np.save(os.path.join(outdir, f"shard_{ci}.npy"), anc.numpy())
+    # batched filters: rank g owns filters [g N, (g+1) N)
+    N, P = 3, 500
+    xs = pfinputs.gaussian_logw(P, 1.0, seed=11, N=N * world)
+    mine = xs[rank * N:(rank + 1) * N]
+    st, A = oracle.resample_batched("stratified", mine, 99, first_filter=rank * N)
+    parts = [torch.zeros((N, P), dtype=torch.int32) for _ in range(world)]
+    dist.all_gather(parts, torch.from_numpy(A))
+    if rank == 0:
+        np.save(os.path.join(outdir, "batched.npy"), torch.cat(parts).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+CASES = [
+    ("systematic", 1000, 1.0, 7, 0, ""),
+    ("stratified", 999, 10.0, 8, 0, ""),
+    ("multinomial", 777, 1.0, 9, 0, ""),
+    ("metropolis", 1001, 1.0, 10, 12, ""),
+    ("systematic", 1024, 1.0, 11, 0, "neg_inf_shard"),
+    ("metropolis", 600, 0.1, 12, 7, "neg_inf_shard"),
+    ("stratified", 500, 1.0, 13, 0, "invalid"),
+    ("metropolis", 500, 1.0, 14, 3, "invalid"),
+]
+
+
+def test_two_rank_giant_filter_and_batches(tmp_path):
+    import oracle
+    import pfinputs
+    from paper_1202_6163_b200.shard import shard_range
+
+    oracle.build()
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), CASES), nprocs=world, join=True)
+    for ci, (scheme, P, var, seed, B, kind) in enumerate(CASES):
+        x = pfinputs.gaussian_logw(P, var, seed=P)
+        if kind == "neg_inf_shard":
+            p0, Pl = shard_range(P, world, 1)
+            x[p0:p0 + Pl] = -np.inf
+        if kind == "invalid":
+            x[3] = np.nan
+        _, want = oracle.resample(scheme, x, seed, B=B, filter_index=5)
+        got = np.load(os.path.join(tmp_path, f"shard_{ci}.npy"))
+        assert np.array_equal(got, want), (scheme, P, kind)
+    xs = pfinputs.gaussian_logw(500, 1.0, seed=11, N=3 * world)
+    _, want = oracle.resample_batched("stratified", xs, 99, first_filter=0)
+    assert np.array_equal(np.load(os.path.join(tmp_path, "batched.npy")), want)
