@@ -413,6 +413,9 @@ __global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf, int64_t ch
 }
 
 // ============================================================================ a4+a5: multinomial
+// 8 slots per thread searched in lockstep: every step of the smem and global
+// binary searches issues 8 independent loads (fixed trip counts, no divergence).
+constexpr int kBS = 8;
 __global__ void __launch_bounds__(kThreads) k_bsearch(int32_t P, int cpf, Ws ws, int64_t ldq, Key key,
                                                       uint32_t filt0, int32_t* anc, int64_t ld_anc) {
     __shared__ uint64_t spl[kSplitters];
@@ -432,32 +435,49 @@ __global__ void __launch_bounds__(kThreads) k_bsearch(int32_t P, int cpf, Ws ws,
     for (int s = threadIdx.x; s < nspl; s += kThreads) spl[s] = __ldg(Q + min((s + 1) * chunk, int64_t{P}) - 1);
     __syncthreads();
     const uint32_t filt = filt0 + static_cast<uint32_t>(n);
-    auto search = [&](uint64_t R) -> int32_t {
-        const uint64_t pos = mulhi64(R, Qtot);
-        int lo = 0, hi = nspl - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (spl[mid] > pos) hi = mid;
-            else lo = mid + 1;
+    const bool vec = ((reinterpret_cast<uintptr_t>(arow) & 15) == 0);
+    for (int64_t kb = k0 + kBS * threadIdx.x; kb < k1; kb += kBS * kThreads) {
+        uint64_t pos[kBS];
+#pragma unroll
+        for (int t = 0; t < kBS; t += 2) {
+            const u32x4 r = philox10(static_cast<uint32_t>((kb + t) >> 1), 0u, 1u, filt, key.k0, key.k1);
+            pos[t] = mulhi64(lo_word(r), Qtot);
+            pos[t + 1] = mulhi64(hi_word(r), Qtot);
         }
-        int64_t alo = lo * chunk, ahi = min((lo + 1) * chunk, int64_t{P}) - 1;
-        while (alo < ahi) {
-            const int64_t mid = (alo + ahi) >> 1;
-            if (__ldg(Q + mid) > pos) ahi = mid;
-            else alo = mid + 1;
+        // splitter level: first s with spl[s] > pos (spl[nspl-1] = Qtot > pos)
+        int lo[kBS];
+#pragma unroll
+        for (int t = 0; t < kBS; ++t) lo[t] = 0;
+        for (int len = nspl; len > 1;) {
+            const int half = len >> 1;
+#pragma unroll
+            for (int t = 0; t < kBS; ++t) lo[t] += (spl[lo[t] + half - 1] <= pos[t]) ? half : 0;
+            len -= half;
         }
-        return static_cast<int32_t>(alo);
-    };
-    const bool vec = ((reinterpret_cast<uintptr_t>(arow) & 7) == 0);
-    for (int64_t k = k0 + 2 * threadIdx.x; k < k1; k += 2 * kThreads) {
-        const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, 1u, filt, key.k0, key.k1);
-        const int32_t a0 = search(lo_word(r));
-        if (k + 1 < k1) {
-            const int32_t a1 = search(hi_word(r));
-            if (vec) *reinterpret_cast<int2*>(arow + k) = make_int2(a0, a1);
-            else { arow[k] = a0; arow[k + 1] = a1; }
+        // global level inside [lo*chunk, lo*chunk + chunk), entries >= P act as +inf
+        int64_t g[kBS];
+#pragma unroll
+        for (int t = 0; t < kBS; ++t) g[t] = static_cast<int64_t>(lo[t]) * chunk;
+        for (int64_t len = chunk; len > 1;) {
+            const int64_t half = len >> 1;
+#pragma unroll
+            for (int t = 0; t < kBS; ++t) {
+                const int64_t idx = g[t] + half - 1;
+                const bool le = (idx < P) && (__ldg(Q + min(idx, static_cast<int64_t>(P) - 1)) <= pos[t]);
+                g[t] += le ? half : 0;
+            }
+            len -= half;
+        }
+        if (vec && kb + kBS <= k1) {
+            int4* dst = reinterpret_cast<int4*>(arow + kb);
+            dst[0] = make_int4(static_cast<int32_t>(g[0]), static_cast<int32_t>(g[1]), static_cast<int32_t>(g[2]),
+                               static_cast<int32_t>(g[3]));
+            dst[1] = make_int4(static_cast<int32_t>(g[4]), static_cast<int32_t>(g[5]), static_cast<int32_t>(g[6]),
+                               static_cast<int32_t>(g[7]));
         } else {
-            arow[k] = a0;
+#pragma unroll
+            for (int t = 0; t < kBS; ++t)
+                if (kb + t < k1) arow[kb + t] = static_cast<int32_t>(g[t]);
         }
     }
 }
