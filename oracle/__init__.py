@@ -72,6 +72,12 @@ def lib():
         L.pfo_permute.argtypes = [P, i32, P]
         L.pfo_gather_inplace.argtypes = [P, i64, i64, i32, P]
         L.pfo_gather_out.argtypes = [P, P, i64, i64, i64, i32, P]
+        L.pfo_dlog.argtypes = [f64]
+        L.pfo_dlog.restype = f64
+        L.pfo_spacing.argtypes = [u64, u32, i64]
+        L.pfo_spacing.restype = u64
+        L.pfo_spacings.argtypes = [i32, u64, u32, P]
+        L.pfo_resample_sorted_multinomial.argtypes = [P, i32, u64, u32, P]
         L.pfo_metropolis_required_B.argtypes = [i64, f64, f64]
         L.pfo_metropolis_required_B.restype = i32
         _lib = L
@@ -188,6 +194,23 @@ def resample_batched(scheme, logw: np.ndarray, seed: int, B: int = 0, first_filt
     a = np.zeros((N, P), dtype=np.int32)
     st = np.zeros(N, dtype=np.int32)
     lib().pfo_resample_batched(_scheme(scheme), _p(logw), P, N, P, seed, first_filter, B, _p(a), P, _p(st))
+    return st, a
+
+
+def dlog(x: float) -> float:
+    return float(lib().pfo_dlog(float(x)))
+
+
+def spacings(P: int, seed: int, filter_index: int = 0) -> np.ndarray:
+    G = np.zeros(P + 1, dtype=np.uint64)
+    lib().pfo_spacings(P, seed, filter_index, _p(G))
+    return G
+
+
+def resample_sorted_multinomial(logw: np.ndarray, seed: int, filter_index: int = 0):
+    logw = np.ascontiguousarray(logw, dtype=np.float32)
+    a = np.zeros(len(logw), dtype=np.int32)
+    st = lib().pfo_resample_sorted_multinomial(_p(logw), len(logw), seed, filter_index, _p(a))
     return st, a
 
 

@@ -343,6 +343,97 @@ void pfo_resample_batched(int scheme, const float* logw, int64_t ld_logw, int32_
 }
 
 /* ------------------------------------------------------------------------ */
+/* NS-12  sorted-uniform multinomial (variant a6): exponential spacings.     */
+/* The P order statistics of P i.i.d. uniforms are G_k / G_P, k < P, where   */
+/* G_k = e_0 + ... + e_k and e_j are i.i.d. exponentials; here fixed point.  */
+/* ------------------------------------------------------------------------ */
+static double f64_from_bits(uint64_t b)
+{
+    double d;
+    memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+/* deterministic natural log of x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt 2),
+ * log m = 2 atanh(s), s = (m - 1)/(m + 1), series to s^19; every operation is
+ * one IEEE binary64 operation (NS-12) */
+double pfo_dlog(double x)
+{
+    uint64_t bits;
+    memcpy(&bits, &x, sizeof bits);
+    int e = (int)((bits >> 52) & 0x7FF) - 1023;
+    double m = f64_from_bits((bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull); /* [1, 2) */
+    if (m > f64_from_bits(0x3FF6A09E667F3BCDull)) { /* sqrt 2 */
+        m = m * 0.5;
+        e = e + 1;
+    }
+    double f = m - 1.0;
+    double s = f / (m + 1.0);
+    double z = s * s;
+    double p = f64_from_bits(0x3faaf286bca1af28ull);            /* 1/19 */
+    p = fma(p, z, f64_from_bits(0x3fae1e1e1e1e1e1eull));       /* 1/17 */
+    p = fma(p, z, f64_from_bits(0x3fb1111111111111ull));       /* 1/15 */
+    p = fma(p, z, f64_from_bits(0x3fb3b13b13b13b14ull));       /* 1/13 */
+    p = fma(p, z, f64_from_bits(0x3fb745d1745d1746ull));       /* 1/11 */
+    p = fma(p, z, f64_from_bits(0x3fbc71c71c71c71cull));       /* 1/9  */
+    p = fma(p, z, f64_from_bits(0x3fc2492492492492ull));       /* 1/7  */
+    p = fma(p, z, f64_from_bits(0x3fc999999999999aull));       /* 1/5  */
+    p = fma(p, z, f64_from_bits(0x3fd5555555555555ull));       /* 1/3  */
+    double t = 2.0 * s;
+    double r = t * z;
+    double logm = fma(r, p, t);
+    double de = (double)e;
+    double lo = de * f64_from_bits(0x3DEA39EF35793C76ull);     /* e ln2_lo */
+    double b = lo + logm;
+    double hi = de * f64_from_bits(0x3FE62E42FEE00000ull);     /* e ln2_hi (exact) */
+    return hi + b;
+}
+
+/* e_k = trunc(-dlog(U_k) 2^24) + 1, U_k = (r_k + 1/2) 2^-32, r_k = word (k & 3) of
+ * Philox(k >> 2, 0, tag 5, filter) */
+uint64_t pfo_spacing(uint64_t seed, uint32_t filter_index, int64_t k)
+{
+    uint32_t x[4];
+    philox_draw(seed, (uint32_t)(k >> 2), 0u, 5u, filter_index, x);
+    double U = ((double)x[k & 3] + 0.5) * f64_from_bits(0x3DF0000000000000ull); /* 2^-32 */
+    double E = -pfo_dlog(U);
+    return (uint64_t)(E * 16777216.0) + 1u;
+}
+
+/* G_k = e_0 + ... + e_k for k = 0..P (P + 1 values) */
+void pfo_spacings(int32_t P, uint64_t seed, uint32_t filter_index, uint64_t* G)
+{
+    uint64_t acc = 0;
+    for (int64_t k = 0; k <= P; ++k) {
+        acc += pfo_spacing(seed, filter_index, k);
+        G[k] = acc;
+    }
+}
+
+/* slot k < P: position x_k = floor(G_k Q / G_P); a_k = min{i : Q_i > x_k} */
+int pfo_resample_sorted_multinomial(const float* logw, int32_t P, uint64_t seed, uint32_t filter_index,
+                                    int32_t* anc)
+{
+    uint64_t* Q = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)P);
+    int st = pfo_cumulative(logw, P, Q);
+    if (st != PFO_FILTER_OK) {
+        for (int32_t i = 0; i < P; ++i) anc[i] = i;
+        free(Q);
+        return st;
+    }
+    uint64_t* G = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)P + 1));
+    pfo_spacings(P, seed, filter_index, G);
+    uint64_t Qtot = Q[P - 1], GP = G[P];
+    for (int32_t k = 0; k < P; ++k) {
+        uint64_t x = (uint64_t)(((unsigned __int128)G[k] * (unsigned __int128)Qtot) / (unsigned __int128)GP);
+        anc[k] = pfo_upper_bound(Q, P, x);
+    }
+    free(G);
+    free(Q);
+    return PFO_FILTER_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* NS-14 conversions ("Converting between the two is straightforward"). */
 /* ------------------------------------------------------------------------ */
 void pfo_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* o)

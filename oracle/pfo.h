@@ -71,6 +71,13 @@ void pfo_resample_batched(int scheme, const float* logw, int64_t ld_logw, int32_
                           uint64_t seed, uint32_t first_filter, int32_t B,
                           int32_t* anc, int64_t ld_anc, int32_t* status);
 
+/* NS-12 sorted-uniform multinomial (variant a6). */
+double pfo_dlog(double x);
+uint64_t pfo_spacing(uint64_t seed, uint32_t filter_index, int64_t k);
+void pfo_spacings(int32_t P, uint64_t seed, uint32_t filter_index, uint64_t* G);
+int pfo_resample_sorted_multinomial(const float* logw, int32_t P, uint64_t seed, uint32_t filter_index,
+                                    int32_t* anc);
+
 /* NS-14 / SPEC S:60-77 conversions. */
 void pfo_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* o);
 void pfo_offspring_to_ancestors(const int32_t* o, int32_t P, int32_t* anc);

@@ -590,3 +590,67 @@ def test_batched_matches_single(orc):
         # different filters draw different streams
         if s != "metropolis":
             assert not all(np.array_equal(A[0], A[n]) for n in range(1, N)) or s == "systematic"
+
+
+# --------------------------------------------------------------------------- NS-12 (a6)
+def test_dlog_accuracy(orc):
+    """NS-12: the deterministic double log is within 2 ulp of math.log on (0, 1] (catches a wrong
+    series coefficient, a dropped ln2 term or a wrong sqrt(2) reduction)."""
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([(rng.integers(0, 2 ** 32, 50000) + 0.5) / 2 ** 32,
+                         [2 ** -33, 0.5, 0.7071067811865476, 0.7071067811865475, 1 - 2 ** -33, 0.999999]])
+    for x in xs:
+        d, e = orc.dlog(float(x)), math.log(float(x))
+        assert abs(d - e) <= 2 * math.ulp(e), x
+    assert orc.dlog(1.0) == 0.0
+
+
+def test_spacings_are_uniform_order_statistics(orc):
+    """NS-12: e_k >= 1 with mean 2^24 (Exp(1) in 2^-24 units), G strictly increasing, and
+    E[G_k / G_P] = (k+1)/(P+1) (the k-th of P uniform order statistics)."""
+    P, R = 9, 3000
+    ratios = np.zeros((R, P))
+    e_all = []
+    for r in range(R):
+        G = orc.spacings(P, pfinputs.seed_for(r), filter_index=r % 7).astype(np.float64)
+        assert np.all(np.diff(G) >= 1) and G[0] >= 1
+        e_all.append(np.diff(np.concatenate([[0.0], G])))
+        ratios[r] = G[:P] / G[P]
+    e_all = np.concatenate(e_all) / 2.0 ** 24
+    assert abs(e_all.mean() - 1.0) < 5 * 1.0 / math.sqrt(len(e_all))
+    k = np.arange(P)
+    mean = (k + 1) / (P + 1)
+    var = mean * (1 - mean) / (P + 2)  # Beta(k+1, P-k) variance
+    z = (ratios.mean(axis=0) - mean) / np.sqrt(var / R)
+    assert np.all(np.abs(z) < 5), z
+
+
+def test_sorted_multinomial_search_and_invariants(orc):
+    """a6: big-int recomputation of x_k = floor(G_k Q / G_P) and linear-scan search equal the oracle;
+    ancestors nondecreasing; zero weights never chosen."""
+    for P in (1, 2, 5, 64, 1000):
+        x = pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(P, 1.0, seed=P))
+        for seed in (3, 0xABCDEF0123456789):
+            st, a = orc.resample_sorted_multinomial(x, seed, filter_index=2)
+            _, Q = orc.cumulative(x)
+            Q = [int(v) for v in Q]
+            G = [int(v) for v in orc.spacings(P, seed, 2)]
+            want = [next(i for i in range(P) if Q[i] > G[k] * Q[-1] // G[P]) for k in range(P)]
+            assert list(a) == want
+            assert np.all(np.diff(a) >= 0) and np.all(np.isfinite(x[a]))
+
+
+def test_sorted_multinomial_offspring_law(orc):
+    """a6 has the multinomial law (Fig. 1(a)): exact multinomial pmf of the offspring
+    vector at P <= 5 vs oracle frequencies (chi-square)."""
+    from collections import Counter
+
+    n = 6000
+    for P, seed in ((3, 1), (4, 2), (5, 3)):
+        x = pfinputs.gaussian_logw(P, 1.0, seed=seed)
+        pmf = _pmf_multinomial(_probs(orc, x), P)
+        c = Counter()
+        for s in range(n):
+            _, a = orc.resample_sorted_multinomial(x, pfinputs.seed_for(s))
+            c[tuple(orc.ancestors_to_offspring(a))] += 1
+        assert _gof(c, pmf, n) > 1e-4, P
