@@ -342,6 +342,20 @@ def run_ours(args):
             sms = a0.elapsed_time(a1) / reps
             per_scheme[sch if sch != "metropolis" else f"metropolis_B{b}"] = {
                 "ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
+        # a6: sorted-uniform multinomial (PF_SORTED)
+        for _ in range(2):
+            pf.pf_resample_batched("multinomial", logw, seed, first_filter=first, ancestors=anc, flags=pf.PF_SORTED,
+                                   stream=stream)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(reps):
+            pf.pf_resample_batched("multinomial", logw, seed, first_filter=first, ancestors=anc, flags=pf.PF_SORTED,
+                                   stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        sms = a0.elapsed_time(a1) / reps
+        per_scheme["multinomial_sorted_a6"] = {"ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
         extras["resample_only"] = per_scheme
 
         # ---------------- generic chain: permutation from arbitrary ancestors (histogram path)

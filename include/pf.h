@@ -66,6 +66,12 @@ enum { PF_FILTER_OK = 0, PF_FILTER_INVALID_WEIGHTS = 1 };
 
 /* pf_opts.flags bits */
 enum {
+    /* with PF_MULTINOMIAL: the sorted-uniform multinomial (NS-12):
+     * positions are the uniform order statistics G_k / G_P of exponential
+     * spacings (Philox tag 5, deterministic double log), so the ancestors come
+     * out nondecreasing and the search is a merge instead of per-slot binary
+     * searches.  Same law as PF_MULTINOMIAL (Fig. 1(a)), different random stream. */
+    PF_SORTED = 1u << 0,
     /* diagnostics: force the multi-launch path (max -> lookback scan -> search)
      * even where the one-launch cluster kernel applies.  Results are identical. */
     PF_NO_FUSION = 1u << 1
@@ -77,7 +83,7 @@ enum {
  */
 typedef struct {
     uint32_t filter_index; /* Philox c3 of a single-filter call (batched: first_filter+n) */
-    uint32_t flags;        /* PF_NO_FUSION or 0; other bits -> PF_ERR_UNSUPPORTED */
+    uint32_t flags;        /* PF_SORTED (multinomial only) | PF_NO_FUSION; other bits -> PF_ERR_UNSUPPORTED */
     double* lse_out;       /* [N] ln sum_i exp(logw_i)  (NS-13; 1e-6 rel. of oracle)       */
     float* normw_out;      /* [N][P] (row stride P) v_i = w_i / sum_j w_j  (NS-13)          */
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */

@@ -20,6 +20,7 @@ from ._build import LIB as _LIB_PATH
 PF_MULTINOMIAL, PF_STRATIFIED, PF_SYSTEMATIC, PF_METROPOLIS = 1, 2, 3, 4
 SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
 PF_FILTER_OK, PF_FILTER_INVALID_WEIGHTS = 0, 1
+PF_SORTED = 1 << 0  # pf_opts.flags with multinomial: sorted-uniform variant (a6, NS-12)
 PF_NO_FUSION = 1 << 1  # pf_opts.flags: force the multi-launch path (diagnostics)
 
 

@@ -100,7 +100,9 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     if (!logw || !anc) return PF_ERR_INVALID_ARG;
     if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
     if (N < 1 || P < 1 || B < 0 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
-    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION)) != 0) return PF_ERR_UNSUPPORTED;
+    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORTED)) != 0) return PF_ERR_UNSUPPORTED;
+    const bool sorted_multi = opts && (opts->flags & PF_SORTED);
+    if (sorted_multi && scheme != PF_MULTINOMIAL) return PF_ERR_UNSUPPORTED;
     double* lse = opts ? opts->lse_out : nullptr;
     double* ess = opts ? opts->ess_out : nullptr;
     float* normw = opts ? opts->normw_out : nullptr;
@@ -116,19 +118,23 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
-    const pf::Layout L = pf::make_layout(N, P, needs_for(scheme));
+    const pf::Layout L = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u));
     void* base = nullptr;
     pf_status st = get_workspace(opts, L.total, s, &base);
     if (st != PF_OK) return st;
     const pf::Ws ws = pf::carve(base, L);
     uint64_t nl = 0;
     cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (sorted_multi && e == cudaSuccess)  // spacings do not depend on the weights: first
+        e = pf::launch_sorted_multinomial(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl, true);
     if (e == cudaSuccess) e = pf::launch_max(logw, ld, N, P, L, ws, status_out, s, &nl);
     const bool side = lse || ess || normw;
     if (scheme != PF_METROPOLIS) {
         if (e == cudaSuccess) e = pf::launch_scan(logw, ld, N, P, L, ws, P > 1, lse, ess, s, &nl);
         if (e == cudaSuccess) {
             if (P == 1) e = pf::launch_identity(N, P, anc, ld_anc, s, &nl);
+            else if (sorted_multi)
+                e = pf::launch_sorted_multinomial(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl, false);
             else e = pf::launch_search(scheme, N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl);
         }
     } else {

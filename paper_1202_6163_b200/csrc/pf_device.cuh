@@ -170,6 +170,73 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* status, int64_t til
     }
 }
 
+// ---------------------------------------------------------------- NS-12 (a6)
+// Deterministic binary64 log of x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt 2),
+// log m = 2 atanh(s), s = (m - 1)/(m + 1), series to s^19 (NS-12 constants).
+__device__ __forceinline__ double ddlog(double x) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(x));
+    int e = static_cast<int>((bits >> 52) & 0x7FF) - 1023;
+    double m = __longlong_as_double(static_cast<long long>((bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    if (m > __longlong_as_double(0x3FF6A09E667F3BCDll)) {
+        m = __dmul_rn(m, 0.5);
+        e = e + 1;
+    }
+    const double f = __dsub_rn(m, 1.0);
+    const double s = __ddiv_rn(f, __dadd_rn(m, 1.0));
+    const double z = __dmul_rn(s, s);
+    double p = __longlong_as_double(0x3faaf286bca1af28ll);
+    p = __fma_rn(p, z, __longlong_as_double(0x3fae1e1e1e1e1e1ell));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fb1111111111111ll));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fb3b13b13b13b14ll));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fb745d1745d1746ll));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fbc71c71c71c71cll));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fc2492492492492ll));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fc999999999999all));
+    p = __fma_rn(p, z, __longlong_as_double(0x3fd5555555555555ll));
+    const double t = __dmul_rn(2.0, s);
+    const double r = __dmul_rn(t, z);
+    const double logm = __fma_rn(r, p, t);
+    const double de = static_cast<double>(e);
+    const double lo = __dmul_rn(de, __longlong_as_double(0x3DEA39EF35793C76ll));
+    const double b = __dadd_rn(lo, logm);
+    const double hi = __dmul_rn(de, __longlong_as_double(0x3FE62E42FEE00000ll));
+    return __dadd_rn(hi, b);
+}
+
+// e = trunc(-ddlog(U) 2^24) + 1 for the 32-bit draw r, U = (r + 1/2) 2^-32
+__device__ __forceinline__ uint64_t spacing_from_word(uint32_t r) {
+    const double U = __dmul_rn(__dadd_rn(static_cast<double>(r), 0.5), __longlong_as_double(0x3DF0000000000000ll));
+    const double E = -ddlog(U);
+    return static_cast<uint64_t>(__dmul_rn(E, 16777216.0)) + 1ull;
+}
+
+// floor(a * b / d) for a < d (so the quotient is < b), exact: double estimate,
+// then two exact 128-bit corrections.
+__device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t b, uint64_t d) {
+    const uint64_t plo = a * b, phi = __umul64hi(a, b);
+    uint64_t q = static_cast<uint64_t>(__dmul_rn(static_cast<double>(a), __ddiv_rn(static_cast<double>(b),
+                                                                                 static_cast<double>(d))));
+    for (int it = 0; it < 2; ++it) {
+        // r = p - q d as signed 128-bit; coarse correction by r / d in double
+        const uint64_t tlo = q * d, thi = __umul64hi(q, d);
+        const uint64_t rlo = plo - tlo;
+        const int64_t rhi = static_cast<int64_t>(phi - thi - (plo < tlo ? 1ull : 0ull));
+        const double rd = __dadd_rn(__dmul_rn(static_cast<double>(rhi), 18446744073709551616.0),
+                                    static_cast<double>(rlo));
+        const double dq = floor(__ddiv_rn(rd, static_cast<double>(d)));
+        q = static_cast<uint64_t>(static_cast<int64_t>(q) + static_cast<int64_t>(dq));
+    }
+    // final exact fix-up: ensure q d <= p < (q + 1) d
+    for (int it = 0; it < 3; ++it) {
+        const uint64_t tlo = q * d, thi = __umul64hi(q, d);
+        if (thi > phi || (thi == phi && tlo > plo)) { --q; continue; }
+        const uint64_t ulo = tlo + d, uhi = thi + (ulo < tlo ? 1ull : 0ull);
+        if (uhi < phi || (uhi == phi && ulo <= plo)) { ++q; continue; }
+        break;
+    }
+    return q;
+}
+
 // Host/device shared integer helpers (no method arithmetic beyond NS-5/NS-7 sizes).
 __host__ __device__ __forceinline__ int ceil_log2(int64_t P) {
     int m = 0;

@@ -40,17 +40,23 @@ struct Ws {
     uint32_t* Qe;        // [N*ldq]   permute: inclusive extras count
     int32_t* freeslot;   // [N*ldq]   permute: r-th free slot
     int32_t* F;          // [N]       permute: number of free slots
+    uint32_t* tile_ctr2; // [1]       zeroed per call (spacings scan)
+    uint64_t* tstatus2;  // [N*T2]    zeroed per call
+    uint64_t* G;         // [N*ldg]   a6: inclusive spacings sums G_0..G_P
+    uint64_t* Gtot;      // [N]       a6: G_P
 };
 
 struct Layout {
     size_t lmax, fstatus, max_part, max_bad, zero_begin, max_cnt, tile_ctr, tstatus, zero_end;
-    size_t tsum, tsum2, Q, Qtot, S, w, o, Qe, freeslot, F, total;
+    size_t tsum, tsum2, Q, Qtot, S, w, o, Qe, freeslot, F, tile_ctr2, tstatus2, G, Gtot, total;
     int cpf_max;  // CTAs per filter of k_max
     int T;        // scan tiles per filter
+    int T2;       // spacings-scan tiles per filter (P + 1 values)
     int64_t ldq;  // padded row length (multiple of 4)
+    int64_t ldg;  // padded spacings row length (P + 1 rounded to 4)
 };
 
-enum Need : unsigned { kNeedQ = 1u, kNeedW = 2u, kNeedPermute = 4u };
+enum Need : unsigned { kNeedQ = 1u, kNeedW = 2u, kNeedPermute = 4u, kNeedG = 8u };
 
 Layout make_layout(int32_t N, int32_t P, unsigned need);
 Ws carve(void* base, const Layout& L);
@@ -66,6 +72,9 @@ cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, con
 cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
                           uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
                           uint64_t* launches);
+cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                                      uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                                      uint64_t* launches, bool spacings_only);
 cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t P, const Layout& L,
                               const Ws& ws, uint64_t seed, uint32_t first_filter, int32_t B, int32_t* anc,
                               int64_t ld_anc, cudaStream_t s, uint64_t* launches);

@@ -482,6 +482,123 @@ __global__ void __launch_bounds__(kThreads) k_bsearch(int32_t P, int cpf, Ws ws,
     }
 }
 
+// ============================================================================ a6: spacings
+// Inclusive scan of the exponential spacings e_0..e_P (NS-12) of each filter,
+// same tile / lookback structure as k_scan; the values come from Philox
+// (tag 5, one call per 4 consecutive k) and the deterministic double log.
+__global__ void __launch_bounds__(kThreads, 4) k_gscan(int32_t P, int T2, Ws ws, int64_t ldg, Key key,
+                                                       uint32_t filt0) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_wtot[kThreads / 32];
+    __shared__ uint64_t s_off[kThreads / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(ws.tile_ctr2, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int n = static_cast<int>(tile / T2);
+    const int j = static_cast<int>(tile - static_cast<int64_t>(n) * T2);
+    const int64_t base = static_cast<int64_t>(j) * kTile + warp * 512;
+    const uint32_t filt = filt0 + static_cast<uint32_t>(n);
+    uint64_t v[16];
+    uint64_t excl[4];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        uint64_t loc = 0;
+        if (i0 <= P) {
+            const u32x4 x = philox10(static_cast<uint32_t>(i0 >> 2), 0u, 5u, filt, key.k0, key.k1);
+            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                v[r * 4 + c] = (i0 + c <= P) ? spacing_from_word(w4[c]) : 0ull;
+                loc += v[r * 4 + c];
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[r * 4 + c] = 0ull;
+        }
+        const uint64_t incl = warp_incl_scan_u64(loc, lane);
+        excl[r] = incl - loc + carry;
+        carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) s_wtot[warp] = carry;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t wv = (lane < kThreads / 32) ? s_wtot[lane] : 0ull;
+        const uint64_t wi = warp_incl_scan_u64(wv, lane);
+        const uint64_t agg = __shfl_sync(kFull, wi, kThreads / 32 - 1);
+        uint64_t* st = ws.tstatus2 + static_cast<int64_t>(n) * T2;
+        uint64_t prefix = 0;
+        if (j == 0) {
+            if (lane == 0) st_release(st, kFlagInc | agg);
+        } else {
+            if (lane == 0) st_release(st + j, kFlagAgg | agg);
+            prefix = lookback(st, j, lane);
+            if (lane == 0) st_release(st + j, kFlagInc | (prefix + agg));
+        }
+        if (lane < kThreads / 32) s_off[lane] = prefix + wi - wv;
+    }
+    __syncthreads();
+    const uint64_t off = s_off[warp];
+    uint64_t* grow = ws.G + static_cast<int64_t>(n) * ldg;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i0 = base + r * 128 + lane * 4;
+        uint64_t run = off + excl[r];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            run += v[r * 4 + c];
+            if (i0 + c <= P) grow[i0 + c] = run;
+            if (i0 + c == P) ws.Gtot[n] = run;
+        }
+    }
+}
+
+struct SpacCtx {
+    int n;
+    uint64_t Qtot, GP;
+    const uint64_t* Q;
+    const uint64_t* G;
+};
+
+// a6 merge: slot k's position is x_k = floor(G_k Q / G_P) (exact 128/64 division);
+// a_k = min{i : Q_i > x_k} as for the other sorted schemes.
+struct ModeSpacings {
+    const uint64_t* Q;
+    int64_t ldq;
+    const uint64_t* Qtot;
+    const int32_t* fstatus;
+    const uint64_t* G;
+    int64_t ldg;
+    const uint64_t* Gtot;
+    int32_t P;
+    int32_t* anc;
+    int64_t ld_anc;
+
+    using Ctx = SpacCtx;
+    __device__ Ctx ctx(int n) const {
+        return {n, Qtot[n], Gtot[n], Q + static_cast<int64_t>(n) * ldq, G + static_cast<int64_t>(n) * ldg};
+    }
+    __device__ bool valid(int n) const { return fstatus[n] == 0; }
+    __device__ int64_t nA(const Ctx&) const { return P; }
+    __device__ uint64_t x(const Ctx& c, int64_t k) const { return muldiv_floor(__ldg(c.G + k), c.Qtot, c.GP); }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return __ldg(c.Q + i); }
+    __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
+        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        int32_t* dst = anc + static_cast<int64_t>(c.n) * ld_anc + ka0;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[t] = s_out[t];
+    }
+    __device__ void identity(int n, int cb, int cpf) const {
+        const int64_t per = cdiv(P, cpf);
+        const int64_t b0 = cb * per, b1 = min(static_cast<int64_t>(P), b0 + per);
+        int32_t* dst = anc + static_cast<int64_t>(n) * ld_anc;
+        for (int64_t k = b0 + threadIdx.x; k < b1; k += kThreads) dst[k] = static_cast<int32_t>(k);
+    }
+};
+
 // ============================================================================ a7: Metropolis
 __global__ void __launch_bounds__(kThreads) k_mexp(const float* __restrict__ logw, int64_t ld, int32_t N,
                                                    int32_t P, Ws ws, int64_t ldq) {
@@ -1184,6 +1301,10 @@ Layout make_layout(int32_t N, int32_t P, unsigned need) {
     L.max_cnt = take(sizeof(uint32_t) * N);
     L.tile_ctr = take(sizeof(uint32_t));
     L.tstatus = take(sizeof(uint64_t) * NT);
+    L.T2 = static_cast<int>(cdiv(static_cast<int64_t>(P) + 1, kTile));
+    L.ldg = (static_cast<int64_t>(P) + 1 + 3) / 4 * 4;
+    L.tile_ctr2 = (need & kNeedG) ? take(sizeof(uint32_t)) : 0;
+    L.tstatus2 = (need & kNeedG) ? take(sizeof(uint64_t) * static_cast<int64_t>(N) * L.T2) : 0;
     L.zero_end = align_up(off, 256);
     L.tsum = take(sizeof(double) * NT);
     L.tsum2 = take(sizeof(double) * NT);
@@ -1196,6 +1317,8 @@ Layout make_layout(int32_t N, int32_t P, unsigned need) {
     L.o = (need & kNeedPermute) ? take(sizeof(int32_t) * rows) : 0;
     L.Qe = (need & kNeedPermute) ? take(sizeof(uint32_t) * rows) : 0;
     L.freeslot = (need & kNeedPermute) ? take(sizeof(int32_t) * rows) : 0;
+    L.G = (need & kNeedG) ? take(sizeof(uint64_t) * static_cast<size_t>(N) * L.ldg) : 0;
+    L.Gtot = (need & kNeedG) ? take(sizeof(uint64_t) * N) : 0;
     L.total = align_up(off, 256);
     return L;
 }
@@ -1220,6 +1343,10 @@ Ws carve(void* base, const Layout& L) {
     w.o = L.o ? reinterpret_cast<int32_t*>(b + L.o) : nullptr;
     w.Qe = L.Qe ? reinterpret_cast<uint32_t*>(b + L.Qe) : nullptr;
     w.freeslot = L.freeslot ? reinterpret_cast<int32_t*>(b + L.freeslot) : nullptr;
+    w.tile_ctr2 = L.tile_ctr2 ? reinterpret_cast<uint32_t*>(b + L.tile_ctr2) : nullptr;
+    w.tstatus2 = L.tstatus2 ? reinterpret_cast<uint64_t*>(b + L.tstatus2) : nullptr;
+    w.G = L.G ? reinterpret_cast<uint64_t*>(b + L.G) : nullptr;
+    w.Gtot = L.Gtot ? reinterpret_cast<uint64_t*>(b + L.Gtot) : nullptr;
     return w;
 }
 
@@ -1473,5 +1600,28 @@ cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, 
 }
 
 size_t shard_ctx_bytes() { return sizeof(ShardCtxDev); }
+
+cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                                      uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                                      uint64_t* launches, bool spacings_only) {
+    const Key key = make_key(seed);
+    if (spacings_only) {
+        ProfScope ps_("k_gscan", s);
+        k_gscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T2), kThreads, 0, s>>>(P, L.T2, ws, L.ldg, key,
+                                                                                          first_filter);
+        ++*launches;
+        return cudaPeekAtLastError();
+    }
+    const int64_t chunk = merge_chunk(N, P);
+    const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
+    ModeSpacings md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, ws.G, L.ldg, ws.Gtot, P, anc, ld_anc};
+    {
+        ProfScope ps_("k_merge_spacings", s);
+        k_merge<ModeSpacings><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf,
+                                                                                                     chunk);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
 
 }  // namespace pf

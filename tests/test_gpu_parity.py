@@ -391,3 +391,29 @@ def test_giant_filter_fake_shards(pf, dev, orc, scheme):
         torch.cuda.synchronize()
         _, want = orc.resample(scheme, x, 4321, B=B, filter_index=3)
         assert np.array_equal(a.cpu().numpy(), want), (scheme, P, G, kind)
+
+
+def test_sorted_multinomial_a6(pf, dev, orc):
+    """a6 (PF_SORTED with the multinomial): spacings scan + exact 128/64 positions + merge,
+    bit-exact against the oracle; batched with ld > P and an invalid filter; ragged sizes."""
+    import torch
+
+    for P in (1, 2, 3, 7, 16, 1000, 4095, 4096, 4097, 65536, 100003, 1 << 20):
+        for var in ((1.0, 10.0) if P < (1 << 20) else (1.0,)):
+            x = pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(P, var, seed=P + 9))
+            a = pf.pf_resample_ex("multinomial", _gpu(x, dev), 2718, filter_index=6, flags=pf.PF_SORTED)
+            torch.cuda.synchronize()
+            _, want = orc.resample_sorted_multinomial(x, 2718, filter_index=6)
+            assert np.array_equal(a.cpu().numpy(), want), (P, var)
+    N, P, ld = 9, 5000, 5003
+    x = pfinputs.gaussian_logw(ld, 1.0, seed=2, N=N)
+    x[4, 10] = np.nan
+    g = _gpu(x, dev)[:, :P]
+    st = torch.empty(N, dtype=torch.int32, device=dev)
+    A = pf.pf_resample_batched("multinomial", g, 31, first_filter=100, flags=pf.PF_SORTED, status_out=st)
+    torch.cuda.synchronize()
+    A = A.cpu().numpy()
+    for n in range(N):
+        s_, want = orc.resample_sorted_multinomial(np.ascontiguousarray(x[n, :P]), 31, filter_index=100 + n)
+        assert int(st[n].item()) == s_
+        assert np.array_equal(A[n], want), n
