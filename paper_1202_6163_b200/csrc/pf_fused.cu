@@ -474,10 +474,16 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(a.CL, 1, 1);
-    int max_clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
-        cudaGetLastError();
-        max_clusters = std::max(1, device_sms() / a.CL);
+    // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us)
+    static int cached[2][2][17] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][a.CL];
+    if (max_clusters == 0) {
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+            cudaGetLastError();
+            max_clusters = std::max(1, device_sms() / a.CL);
+        }
     }
     const int clusters = std::max(1, std::min(a.N, max_clusters));
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * a.CL), 1, 1);
