@@ -298,7 +298,8 @@ def run_ours(args):
         "k_hist": 8 * NP,
         "k_pscan": 12 * NP,
         "k_push": 8 * NP + 8 * free,
-        "k_fused_sorted": 8 * NP + 4 * NP,
+        "k_fused_sorted": 12 * NP,  # logw in, ancestors + offspring out
+        "k_coop_sorted": 12 * NP,
         "k_gather_inplace": 4 * NP + 2 * row * free,
     }
     hbm, peak_src = peaks()

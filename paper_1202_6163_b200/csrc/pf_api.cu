@@ -118,6 +118,17 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
+    if (!no_fusion && !normw && pf::coop_supported(scheme, P)) {
+        // one cooperative launch for large filters (pf_fused.cu); tiny scratch from the pool
+        void* sc = nullptr;
+        pf_status st2 = pool_get(pf::coop_scratch_bytes(), s, &sc);
+        if (st2 != PF_OK) return st2;
+        uint64_t nl = 0;
+        const cudaError_t e = pf::launch_coop_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
+                                                     ess, status_out, offspring_out, sc, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     const pf::Layout L = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u));
     void* base = nullptr;
     pf_status st = get_workspace(opts, L.total, s, &base);

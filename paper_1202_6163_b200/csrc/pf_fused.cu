@@ -447,6 +447,342 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
     cluster.sync();  // keep this CTA's shared memory alive for remote readers
 }
 
+// ============================================================================ cooperative
+// One-launch resampler for LARGE filters (P > 8 x 8192): a cooperative grid of
+// G co-resident CTAs, CTA c owning the contiguous chunk [c*CH, (c+1)*CH) of
+// every filter, processed in 8192-particle sub-tiles.
+//   A  chunk max -> global array -> grid sync -> every CTA reduces the G maxima
+//   B  chunk sum of q (log-weights re-read, L2-resident up to ~2^24 particles)
+//      -> grid sync -> chunk offset O_c = sum of earlier chunk totals
+//   C  sub-tiles in order with a running carry: dexp, quantise, block scan,
+//      E_i = c(Q_i), per-warp head-mark + max-scan expansion of the runs
+//      [E_{i-1}, E_i) straight into the ancestors (no Q array in HBM).
+// HBM: 4 B/particle in (+2 L2 re-reads) + 4 B out.  Two grid syncs per filter.
+struct CoopArgs {
+    const float* logw;
+    int64_t ld;
+    int32_t N, P;
+    int64_t CH;  // particles per CTA chunk (multiple of kPP)
+    uint64_t D;
+    Key key;
+    uint32_t filt0;
+    int kfx;
+    int vec;
+    int32_t* anc;
+    int64_t ld_anc;
+    int anc_vec;
+    double* lse_out;
+    double* ess_out;
+    int32_t* status_out;
+    int32_t* off;  // offspring out (row stride ld_anc), nullable
+    // scratch (device): [G] per-CTA values
+    float* g_max;
+    int32_t* g_bad;
+    uint64_t* g_tot;
+    double* g_sw;
+    double* g_sw2;
+};
+
+template <int SCHEME, bool SUMS>
+__global__ void __launch_bounds__(kFT, 2) k_coop_sorted(CoopArgs a) {
+    __shared__ float s_f[kFW];
+    __shared__ int s_i[kFW];
+    __shared__ double s_d[2][kFW];
+    __shared__ uint64_t s_wt[kFR][kFW];
+    __shared__ uint32_t s_lastE[kFR][kFW];
+    __shared__ __align__(16) int32_t s_buf[kFW][kChunk];
+    __shared__ float s_lmax;
+    __shared__ int s_bad;
+    __shared__ uint64_t s_u64[4];
+    __shared__ double s_S, s_S2;
+    __shared__ uint32_t s_prevE;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = gridDim.x, c = blockIdx.x;
+    for (int n = 0; n < a.N; ++n) {
+        const float* frow = a.logw + static_cast<int64_t>(n) * a.ld;
+        const int64_t c0 = static_cast<int64_t>(c) * a.CH;
+        const int64_t c1 = min(static_cast<int64_t>(a.P), c0 + a.CH);
+        const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+        // ---------------- A: chunk max
+        float m = -INFINITY;
+        int bad = 0;
+        for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+                float v4[4];
+                if (a.vec && i0 + 3 < c1) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(frow + i0));
+                    v4[0] = t.x; v4[1] = t.y; v4[2] = t.z; v4[3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v4[q] = (i0 + q < c1) ? __ldg(frow + i0 + q) : -INFINITY;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    bad |= (isnan(v4[q]) || v4[q] == INFINITY) ? 1 : 0;
+                    m = fmaxf(m, v4[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+            bad |= __shfl_xor_sync(kFull, bad, o);
+        }
+        if (lane == 0) { s_f[warp] = m; s_i[warp] = bad; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < kFW; ++w) { m = fmaxf(m, s_f[w]); bad |= s_i[w]; }
+            a.g_max[c] = m;
+            a.g_bad[c] = bad;
+        }
+        grid.sync();
+        if (warp == 0) {
+            float gm = -INFINITY;
+            int gb = 0;
+            for (int r = lane; r < G; r += 32) { gm = fmaxf(gm, __ldcg(a.g_max + r)); gb |= __ldcg(a.g_bad + r); }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
+                gb |= __shfl_xor_sync(kFull, gb, o);
+            }
+            if (lane == 0) { s_lmax = gm; s_bad = (gb || gm == -INFINITY) ? 1 : 0; }
+        }
+        __syncthreads();
+        const float lm = s_lmax;
+        int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
+        if (s_bad) {
+            for (int64_t k = c0 + tid; k < c1; k += kFT) arow[k] = static_cast<int32_t>(k);
+            if (a.off)
+                for (int64_t k = c0 + tid; k < c1; k += kFT) a.off[static_cast<int64_t>(n) * a.ld_anc + k] = 1;
+            if (c == 0 && tid == 0) {
+                if (a.lse_out) a.lse_out[n] = NAN;
+                if (a.ess_out) a.ess_out[n] = NAN;
+                if (a.status_out) a.status_out[n] = 1;
+            }
+            grid.sync();  // g_max/g_bad are rewritten by the next filter
+            continue;
+        }
+        // ---------------- B: chunk totals
+        uint64_t tot = 0;
+        double sw = 0.0, sw2 = 0.0;
+        for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+                float v4[4];
+                if (a.vec && i0 + 3 < c1) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(frow + i0));
+                    v4[0] = t.x; v4[1] = t.y; v4[2] = t.z; v4[3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v4[q] = (i0 + q < c1) ? __ldg(frow + i0 + q) : -INFINITY;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float w = weight(v4[q], lm);
+                    tot += quantise(w, a.kfx);
+                    if (SUMS) {
+                        sw += static_cast<double>(w);
+                        sw2 += static_cast<double>(w) * static_cast<double>(w);
+                    }
+                }
+            }
+        }
+        tot = warp_sum_u64(tot);
+        if (SUMS) { sw = warp_sum_f64(sw); sw2 = warp_sum_f64(sw2); }
+        if (lane == 0) { s_wt[0][warp] = tot; s_d[0][warp] = sw; s_d[1][warp] = sw2; }
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t t = 0;
+            double A = 0.0, Bv = 0.0;
+            for (int w = 0; w < kFW; ++w) { t += s_wt[0][w]; A += s_d[0][w]; Bv += s_d[1][w]; }
+            a.g_tot[c] = t;
+            a.g_sw[c] = A;
+            a.g_sw2[c] = Bv;
+        }
+        grid.sync();
+        if (warp == 0) {
+            uint64_t off = 0, all = 0;
+            for (int r = lane; r < G; r += 32) {
+                const uint64_t t = __ldcg(a.g_tot + r);
+                all += t;
+                if (r < c) off += t;
+            }
+            off = warp_sum_u64(off);
+            all = warp_sum_u64(all);
+            if (lane == 0) {
+                s_u64[0] = off;
+                s_u64[1] = all;
+                if (SUMS && c == 0) {
+                    double S = 0.0, S2 = 0.0;
+                    for (int r = 0; r < G; ++r) { S += __ldcg(a.g_sw + r); S2 += __ldcg(a.g_sw2 + r); }
+                    if (a.lse_out) a.lse_out[n] = static_cast<double>(lm) + log(S);
+                    if (a.ess_out) a.ess_out[n] = S * S / S2;
+                }
+                if (c == 0 && a.status_out) a.status_out[n] = 0;
+            }
+        }
+        __syncthreads();
+        Pos z;
+        z.D = a.D;
+        z.Qtot = s_u64[1];
+        z.key = a.key;
+        z.filt = filt;
+        z.P = a.P;
+        z.rho = (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+        z.A = 0x1p64 / (static_cast<double>(z.D) * static_cast<double>(z.Qtot));
+        z.Bc = (SCHEME == 3) ? static_cast<double>(z.rho) / static_cast<double>(z.D) : 0.0;
+        uint64_t carry = s_u64[0];
+        if (tid == 0) s_prevE = count_below<SCHEME>(z, carry);
+        // ---------------- C: sub-tiles in order
+        for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+            float v[kFI];
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+                if (a.vec && i0 + 3 < c1) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(frow + i0));
+                    v[j * 4 + 0] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[j * 4 + q] = (i0 + q < c1) ? __ldg(frow + i0 + q) : -INFINITY;
+                }
+            }
+            uint64_t ex[kFR];
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                uint64_t loc = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float w = weight(v[j * 4 + q], lm);
+                    v[j * 4 + q] = w;
+                    loc += quantise(w, a.kfx);
+                }
+                const uint64_t incl = warp_incl_scan_u64(loc, lane);
+                ex[j] = incl - loc;
+                const uint64_t wt = __shfl_sync(kFull, incl, 31);
+                if (lane == 0) s_wt[j][warp] = wt;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                uint64_t t4[kTPL];
+                uint64_t tsum = 0;
+#pragma unroll
+                for (int q = 0; q < kTPL; ++q) {
+                    const int idx = lane * kTPL + q;
+                    t4[q] = s_wt[idx / kFW][idx % kFW];
+                    tsum += t4[q];
+                }
+                const uint64_t incl = warp_incl_scan_u64(tsum, lane);
+                uint64_t run = incl - tsum;
+#pragma unroll
+                for (int q = 0; q < kTPL; ++q) {
+                    const int idx = lane * kTPL + q;
+                    s_wt[idx / kFW][idx % kFW] = run;
+                    run += t4[q];
+                }
+                if (lane == 31) s_u64[2] = incl;  // sub-tile total
+            }
+            __syncthreads();
+            uint32_t E[kFI];
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                uint64_t run = carry + s_wt[j][warp] + ex[j];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    run += quantise(v[j * 4 + q], a.kfx);
+                    E[j * 4 + q] = count_below<SCHEME>(z, run);
+                }
+                if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
+            }
+            __syncthreads();
+            uint32_t first[kFR];
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const uint32_t up = __shfl_up_sync(kFull, E[j * 4 + 3], 1);
+                if (lane > 0) first[j] = up;
+                else if (warp > 0) first[j] = s_lastE[j][warp - 1];
+                else if (j > 0) first[j] = s_lastE[j - 1][kFW - 1];
+                else first[j] = s_prevE;
+            }
+            const int32_t idbase = static_cast<int32_t>(t0) + tid * 4;
+            if (a.off) {
+                int32_t* orow = a.off + static_cast<int64_t>(n) * a.ld_anc;
+#pragma unroll
+                for (int j = 0; j < kFR; ++j) {
+                    const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+                    const int32_t o0 = static_cast<int32_t>(E[j * 4 + 0] - first[j]);
+                    const int32_t o1 = static_cast<int32_t>(E[j * 4 + 1] - E[j * 4 + 0]);
+                    const int32_t o2 = static_cast<int32_t>(E[j * 4 + 2] - E[j * 4 + 1]);
+                    const int32_t o3 = static_cast<int32_t>(E[j * 4 + 3] - E[j * 4 + 2]);
+                    if (a.anc_vec && i0 + 3 < c1) {
+                        __stcs(reinterpret_cast<int4*>(orow + i0), make_int4(o0, o1, o2, o3));
+                    } else {
+                        if (i0 + 0 < c1) orow[i0 + 0] = o0;
+                        if (i0 + 1 < c1) orow[i0 + 1] = o1;
+                        if (i0 + 2 < c1) orow[i0 + 2] = o2;
+                        if (i0 + 3 < c1) orow[i0 + 3] = o3;
+                    }
+                }
+            }
+            int4* b4 = reinterpret_cast<int4*>(s_buf[warp]);
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const uint32_t S0 = __shfl_sync(kFull, first[j], 0);
+                const uint32_t S1 = __shfl_sync(kFull, E[j * 4 + 3], 31);
+                int32_t cy = -1;
+                for (uint32_t q0 = S0 & ~3u; q0 < S1; q0 += kChunk) {
+                    b4[2 * lane] = make_int4(-1, -1, -1, -1);
+                    b4[2 * lane + 1] = make_int4(-1, -1, -1, -1);
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                        const uint32_t rel = pe - q0;
+                        if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kChunk))
+                            s_buf[warp][rel] = idbase + j * (kFT * 4) + q;
+                    }
+                    __syncwarp();
+                    const int4 lo = b4[2 * lane], hi = b4[2 * lane + 1];
+                    int32_t h[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+                    for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
+                    int32_t incl = h[7];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int32_t u = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl = max(incl, u);
+                    }
+                    int32_t pre = __shfl_up_sync(kFull, incl, 1);
+                    pre = max(cy, (lane == 0) ? -1 : pre);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
+                    cy = max(cy, __shfl_sync(kFull, incl, 31));
+                    const uint32_t k0 = q0 + 8 * lane;
+                    if (a.anc_vec && k0 >= S0 && k0 + 8 <= S1) {
+                        int4* dst = reinterpret_cast<int4*>(arow + k0);
+                        __stcs(dst, make_int4(h[0], h[1], h[2], h[3]));
+                        __stcs(dst + 1, make_int4(h[4], h[5], h[6], h[7]));
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (k0 + t >= S0 && k0 + t < S1) arow[k0 + t] = h[t];
+                    }
+                    __syncwarp();
+                }
+            }
+            carry += s_u64[2];
+            __syncthreads();
+            if (tid == 0) s_prevE = s_lastE[kFR - 1][kFW - 1];
+            __syncthreads();
+        }
+        grid.sync();  // scratch arrays are rewritten by the next filter
+    }
+}
+
 int device_sms() {
     static int sms = 0;
     if (!sms) {
@@ -491,6 +827,64 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool coop_supported(int scheme, int32_t P) { return (scheme == 2 || scheme == 3) && P > 8 * kPP; }
+
+size_t coop_scratch_bytes() { return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8); }
+
+cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                               uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
+                               double* ess_out, int32_t* status_out, int32_t* offspring, void* scratch,
+                               cudaStream_t s, uint64_t* launches) {
+    CoopArgs a{};
+    const bool sums = lse_out || ess_out;
+    void* kern = (scheme == 2) ? (sums ? (void*)k_coop_sorted<2, true> : (void*)k_coop_sorted<2, false>)
+                               : (sums ? (void*)k_coop_sorted<3, true> : (void*)k_coop_sorted<3, false>);
+    static int per_sm[2][2] = {};
+    int& occ = per_sm[scheme - 2][sums ? 1 : 0];
+    if (occ == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, 0) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            occ = 1;
+        }
+    }
+    int G = std::min(device_sms() * occ, 4096);
+    // chunks are whole 8192-particle sub-tiles; never more CTAs than sub-tiles
+    const int64_t tiles = (static_cast<int64_t>(P) + kPP - 1) / kPP;
+    G = static_cast<int>(std::min<int64_t>(G, tiles));
+    const int64_t per = (tiles + G - 1) / G;
+    a.CH = per * kPP;
+    G = static_cast<int>((static_cast<int64_t>(P) + a.CH - 1) / a.CH);
+    a.logw = logw;
+    a.ld = ld;
+    a.N = N;
+    a.P = P;
+    const int m = ceil_log2(P);
+    a.D = ((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P));
+    a.key = make_key(seed);
+    a.filt0 = first_filter;
+    a.kfx = 61 - m;
+    a.vec = ((reinterpret_cast<uintptr_t>(logw) & 15) == 0 && ld % 4 == 0) ? 1 : 0;
+    a.anc = anc;
+    a.ld_anc = ld_anc;
+    a.anc_vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0) ? 1 : 0;
+    a.lse_out = lse_out;
+    a.ess_out = ess_out;
+    a.status_out = status_out;
+    a.off = offspring;
+    char* sc = static_cast<char*>(scratch);
+    a.g_max = reinterpret_cast<float*>(sc);
+    a.g_bad = reinterpret_cast<int32_t*>(sc + 4096 * 4);
+    a.g_tot = reinterpret_cast<uint64_t*>(sc + 4096 * 8);
+    a.g_sw = reinterpret_cast<double*>(sc + 4096 * 16);
+    a.g_sw2 = reinterpret_cast<double*>(sc + 4096 * 24);
+    void* args[] = {&a};
+    ProfScope ps_("k_coop_sorted", s);
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kFT), args, 0, s);
+    ++*launches;
+    if (e != cudaSuccess) return e;
+    return cudaPeekAtLastError();
+}
 
 bool fused_supported(int scheme, int32_t P) {
     return (scheme == 2 || scheme == 3) && P >= 1 && P <= 8 * kPP;
