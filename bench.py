@@ -359,6 +359,19 @@ def run_ours(args):
         per_scheme["multinomial_sorted_a6"] = {"ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
         extras["resample_only"] = per_scheme
 
+        # C1 (BASELINE configs[0]): single resampling of P = 16, latency per call with the calls
+        # captured in a CUDA graph (device time, no host overhead on the timeline)
+        from tools.sweep import time_calls
+
+        x16 = pfinputs.gaussian_logw_torch(16, 1.0, pfinputs.BASE_SEED, 1, dev)[0].contiguous()
+        a16 = torch.empty(16, dtype=torch.int32, device=dev)
+        c1 = {}
+        for sch in ("multinomial", "stratified", "systematic", "metropolis"):
+            b = 32 if sch == "metropolis" else 0
+            c1[sch + ("_B32" if b else "")] = round(
+                1e3 * time_calls(lambda: pf.pf_resample_ex(sch, x16, seed, b, ancestors=a16), 50, dev), 2)
+        extras["c1_latency_us_per_call_P16"] = c1
+
         # ---------------- generic chain: permutation from arbitrary ancestors (histogram path)
         def step_generic():
             pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)

@@ -110,6 +110,14 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     int32_t* offspring_out = opts ? opts->offspring_out : nullptr;
 
     const bool no_fusion = (opts && (opts->flags & PF_NO_FUSION)) || g_no_fusion.load();
+    if (!no_fusion && pf::small_supported(P)) {
+        // one warp per filter, every scheme, one launch (pf_fused.cu k_small)
+        uint64_t nl = 0;
+        const cudaError_t e = pf::launch_small(scheme, sorted_multi, logw, ld, N, P, seed, first_filter, B, anc, ld_anc,
+                                               lse, ess, normw, status_out, offspring_out, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     if (!no_fusion && pf::fused_supported(scheme, P)) {
         // one launch per batch: cluster-per-filter kernel, no workspace (pf_fused.cu)
         uint64_t nl = 0;

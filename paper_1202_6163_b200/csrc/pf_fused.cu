@@ -783,6 +783,224 @@ __global__ void __launch_bounds__(kFT, 2) k_coop_sorted(CoopArgs a) {
     }
 }
 
+// ============================================================================ small filters
+// One WARP per filter for P <= 256 (8 particles per lane): every scheme in one
+// launch with warp-level synchronisation only (BASELINE C1: P = 16; batches of
+// small filters).  Q (u64) and w (f32) of the filter live in shared memory.
+constexpr int kSmallP = 256;
+constexpr int kSmallWarps = 8;
+
+struct SmallArgs {
+    const float* logw;
+    int64_t ld;
+    int32_t N, P, scheme, B, sorted;
+    int kfx;
+    uint64_t D;
+    Key key;
+    uint32_t filt0;
+    int32_t* anc;
+    int64_t ld_anc;
+    double* lse_out;
+    double* ess_out;
+    float* normw;
+    int32_t* status_out;
+    int32_t* off;
+};
+
+__device__ __forceinline__ int small_upper_bound(const uint64_t* Q, int P, uint64_t x) {
+    int lo = 0, n = P;  // first i with Q[i] > x (Q[P-1] > x)
+    while (n > 1) {
+        const int half = n >> 1;
+        lo += (Q[lo + half - 1] <= x) ? half : 0;
+        n -= half;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kSmallWarps * 32) k_small(SmallArgs a) {
+    __shared__ uint64_t s_q[kSmallWarps][kSmallP + 4];
+    __shared__ float s_w[kSmallWarps][kSmallP];
+    __shared__ int32_t s_o[kSmallWarps][kSmallP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = blockIdx.x * kSmallWarps + warp;
+    if (n >= a.N) return;
+    const int P = a.P;
+    const float* row = a.logw + static_cast<int64_t>(n) * a.ld;
+    int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
+    const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+    uint64_t* Q = s_q[warp];
+    float* W = s_w[warp];
+    // a1: max + validation
+    float v[8];
+    float m = -INFINITY;
+    int bad = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int i = lane * 8 + t;
+        v[t] = (i < P) ? row[i] : -INFINITY;
+        bad |= (isnan(v[t]) || v[t] == INFINITY) ? 1 : 0;
+        m = fmaxf(m, v[t]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        bad |= __shfl_xor_sync(kFull, bad, o);
+    }
+    const bool invalid = bad || m == -INFINITY;
+    if (invalid) {
+        for (int i = lane; i < P; i += 32) {
+            arow[i] = i;
+            if (a.off) a.off[static_cast<int64_t>(n) * a.ld_anc + i] = 1;
+            if (a.normw) a.normw[static_cast<int64_t>(n) * P + i] = NAN;
+        }
+        if (lane == 0) {
+            if (a.lse_out) a.lse_out[n] = NAN;
+            if (a.ess_out) a.ess_out[n] = NAN;
+            if (a.status_out) a.status_out[n] = 1;
+        }
+        return;
+    }
+    // a2+a3: weights, fixed point, warp scan (8 consecutive per lane)
+    double sw = 0.0, sw2 = 0.0;
+    uint64_t loc = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const float w = weight(v[t], m);
+        v[t] = w;
+        sw += static_cast<double>(w);
+        sw2 += static_cast<double>(w) * static_cast<double>(w);
+        loc += quantise(w, a.kfx);
+    }
+    const uint64_t incl = warp_incl_scan_u64(loc, lane);
+    uint64_t run = incl - loc;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int i = lane * 8 + t;
+        run += quantise(v[t], a.kfx);
+        if (i < P) { Q[i] = run; W[i] = v[t]; }
+        if (i < kSmallP) s_o[warp][i] = 0;
+    }
+    sw = warp_sum_f64(sw);
+    sw2 = warp_sum_f64(sw2);
+    const uint64_t Qtot = __shfl_sync(kFull, incl, 31);
+    __syncwarp();
+    if (lane == 0) {
+        if (a.lse_out) a.lse_out[n] = static_cast<double>(m) + log(sw);
+        if (a.ess_out) a.ess_out[n] = sw * sw / sw2;
+        if (a.status_out) a.status_out[n] = 0;
+    }
+    if (a.normw)
+        for (int i = lane; i < P; i += 32)
+            a.normw[static_cast<int64_t>(n) * P + i] = static_cast<float>(static_cast<double>(W[i]) / sw);
+    // a4+a5 / a6 / a7: slot k = lane * 8 + t
+    int32_t out[8];
+    if (a.scheme == 4) {
+        // chains i = lane + 32 t: small filters keep every lane busy
+        const float kU = __uint_as_float(0x33800000u);
+        for (int t = 0; t < 8; ++t) {
+            const int i = lane + 32 * t;
+            if (i >= P) break;
+            int32_t k = i;
+            float wk = W[i];
+            for (int32_t b = 0; b < a.B; b += 2) {
+                const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>(b >> 1), 4u, filt, a.key.k0,
+                                         a.key.k1);
+                const uint32_t j0 = __umulhi(r.x, static_cast<uint32_t>(P));
+                const float u0 = __fmul_rn(static_cast<float>(r.y >> 8), kU);
+                const float w0 = W[j0];
+                if (__fmul_rn(u0, wk) < w0) { k = j0; wk = w0; }
+                if (b + 1 < a.B) {
+                    const uint32_t j1 = __umulhi(r.z, static_cast<uint32_t>(P));
+                    const float u1 = __fmul_rn(static_cast<float>(r.w >> 8), kU);
+                    const float w1 = W[j1];
+                    if (__fmul_rn(u1, wk) < w1) { k = j1; wk = w1; }
+                }
+            }
+            arow[i] = k;
+            if (a.off) atomicAdd(&s_o[warp][k], 1);
+        }
+        if (a.off) {
+            __syncwarp();
+            for (int i = lane; i < P; i += 32) a.off[static_cast<int64_t>(n) * a.ld_anc + i] = s_o[warp][i];
+        }
+        return;
+    } else if (P == 1) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) out[t] = 0;
+    } else if (a.sorted) {
+        // a6: spacings e_0..e_P (P + 1 <= 257 values) scanned by the warp, 9 per lane
+        uint64_t* G = s_q[warp] + 0;  // reuse after Q? no: Q still needed -> separate registers
+        uint64_t e[9], gl = 0;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const int k = lane * 9 + t;
+            e[t] = 0;
+            if (k <= P) {
+                const u32x4 r = philox10(static_cast<uint32_t>(k >> 2), 0u, 5u, filt, a.key.k0, a.key.k1);
+                const uint32_t wd = ((k & 3) == 0) ? r.x : ((k & 3) == 1) ? r.y : ((k & 3) == 2) ? r.z : r.w;
+                e[t] = spacing_from_word(wd);
+            }
+            gl += e[t];
+        }
+        const uint64_t gincl = warp_incl_scan_u64(gl, lane);
+        const uint64_t GP = __shfl_sync(kFull, gincl, 31);
+        uint64_t gr = gincl - gl;
+        // positions of this lane's spacing indices, then a shuffle to the slot owners
+        uint64_t xk[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            gr += e[t];
+            xk[t] = muldiv_floor(gr, Qtot, GP);  // only used for k < P (G_k < G_P)
+        }
+        (void)G;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int k = lane * 8 + t;         // slot owned by this lane
+            const int src = k / 9, idx = k - src * 9;
+            uint64_t x = 0;
+#pragma unroll
+            for (int tt = 0; tt < 9; ++tt) {
+                const uint64_t cand = __shfl_sync(kFull, xk[tt], src & 31);
+                if (tt == idx) x = cand;
+            }
+            out[t] = (k < P) ? small_upper_bound(Q, P, x) : 0;
+        }
+    } else {
+        uint64_t rho = 0;
+        if (a.scheme == 3) rho = mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D);
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+            const int k = lane * 8 + t;
+            const u32x4 r = philox10(static_cast<uint32_t>(k >> 1), 0u, static_cast<uint32_t>(a.scheme), filt,
+                                     a.key.k0, a.key.k1);
+            uint64_t x0, x1;
+            if (a.scheme == 1) {
+                x0 = mulhi64(lo_word(r), Qtot);
+                x1 = mulhi64(hi_word(r), Qtot);
+            } else {
+                const uint64_t r0 = (a.scheme == 2) ? mulhi64(lo_word(r), a.D) : rho;
+                const uint64_t r1 = (a.scheme == 2) ? mulhi64(hi_word(r), a.D) : rho;
+                x0 = mulhi64(static_cast<uint64_t>(k) * a.D + r0, Qtot);
+                x1 = mulhi64(static_cast<uint64_t>(k + 1) * a.D + r1, Qtot);
+            }
+            out[t] = (k < P) ? small_upper_bound(Q, P, x0) : 0;
+            out[t + 1] = (k + 1 < P) ? small_upper_bound(Q, P, x1) : 0;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int k = lane * 8 + t;
+        if (k < P) {
+            arow[k] = out[t];
+            if (a.off) atomicAdd(&s_o[warp][out[t]], 1);
+        }
+    }
+    if (a.off) {
+        __syncwarp();
+        for (int i = lane; i < P; i += 32) a.off[static_cast<int64_t>(n) * a.ld_anc + i] = s_o[warp][i];
+    }
+}
+
 int device_sms() {
     static int sms = 0;
     if (!sms) {
@@ -883,6 +1101,41 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kFT), args, 0, s);
     ++*launches;
     if (e != cudaSuccess) return e;
+    return cudaPeekAtLastError();
+}
+
+bool small_supported(int32_t P) { return P >= 1 && P <= kSmallP; }
+
+cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, double* lse_out,
+                         double* ess_out, float* normw, int32_t* status_out, int32_t* offspring, cudaStream_t s,
+                         uint64_t* launches) {
+    SmallArgs a{};
+    a.logw = logw;
+    a.ld = ld;
+    a.N = N;
+    a.P = P;
+    a.scheme = scheme;
+    a.B = B;
+    a.sorted = sorted ? 1 : 0;
+    const int m = ceil_log2(P);
+    a.kfx = 61 - m;
+    a.D = (P <= 1) ? 0 : (((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P)));
+    a.key = make_key(seed);
+    a.filt0 = first_filter;
+    a.anc = anc;
+    a.ld_anc = ld_anc;
+    a.lse_out = lse_out;
+    a.ess_out = ess_out;
+    a.normw = normw;
+    a.status_out = status_out;
+    a.off = offspring;
+    const unsigned grid = static_cast<unsigned>((static_cast<int64_t>(N) + kSmallWarps - 1) / kSmallWarps);
+    {
+        ProfScope ps_("k_small", s);
+        k_small<<<grid, kSmallWarps * 32, 0, s>>>(a);
+    }
+    ++*launches;
     return cudaPeekAtLastError();
 }
 

@@ -417,3 +417,44 @@ def test_sorted_multinomial_a6(pf, dev, orc):
         s_, want = orc.resample_sorted_multinomial(np.ascontiguousarray(x[n, :P]), 31, filter_index=100 + n)
         assert int(st[n].item()) == s_
         assert np.array_equal(A[n], want), n
+
+
+@pytest.mark.parametrize("scheme", SCHEMES + ["sorted"])
+def test_small_filters_warp_kernel(pf, dev, orc, scheme):
+    """P <= 256: the one-warp-per-filter kernel (every scheme, a6 included) against the oracle,
+    batched with invalid filters, ld > P, side outputs and offspring; and the same cases through the
+    multi-launch path (pf_set_fusion(False))."""
+    import torch
+
+    for fusion in (True, False):
+        pf.pf_set_fusion(fusion)
+        try:
+            for N, P in ((1, 16), (1000, 16), (333, 100), (64, 256), (7, 1), (50, 33)):
+                ld = P + 3
+                x = pfinputs.gaussian_logw(ld, 1.0 if N % 2 else 10.0, seed=N * P, N=N)
+                if N > 10:
+                    x[5, 0] = np.nan
+                    x[6, :] = -np.inf
+                g = _gpu(x, dev)[:, :P]
+                st = torch.empty(N, dtype=torch.int32, device=dev)
+                lse = torch.empty(N, dtype=torch.float64, device=dev)
+                off = torch.empty((N, P), dtype=torch.int32, device=dev)
+                sch = "multinomial" if scheme == "sorted" else scheme
+                flags = pf.PF_SORTED if scheme == "sorted" else 0
+                B = 21 if scheme == "metropolis" else 0
+                a = pf.pf_resample_batched(sch, g, 99, B=B, first_filter=3, status_out=st, lse_out=lse,
+                                           offspring_out=off, flags=flags)
+                torch.cuda.synchronize()
+                A, O, S, L = a.cpu().numpy(), off.cpu().numpy(), st.cpu().numpy(), lse.cpu().numpy()
+                for n in range(N):
+                    xn = np.ascontiguousarray(x[n, :P])
+                    if scheme == "sorted":
+                        s_, want = orc.resample_sorted_multinomial(xn, 99, filter_index=3 + n)
+                        wl = L[n] if s_ else orc.resample("systematic", xn, 1, side=True)[2]
+                    else:
+                        s_, want, wl, _, _ = orc.resample(sch, xn, 99, B=B, filter_index=3 + n, side=True)
+                    assert S[n] == s_ and np.array_equal(A[n], want), (fusion, scheme, N, P, n)
+                    assert np.array_equal(O[n], orc.ancestors_to_offspring(want))
+                    assert (np.isnan(wl) and np.isnan(L[n])) or abs(L[n] - wl) <= 1e-6 * max(1.0, abs(wl))
+        finally:
+            pf.pf_set_fusion(True)

@@ -3,8 +3,8 @@
 vs P and weight variance"; SURVEY §8(d) companion sweep P = 2^4 ... 2^24).
 
 Single filters (N = 1) and batches with N * P = 2^26 (P <= 2^16), every scheme,
-sigma^2 in {0.1, 1, 10}; CUDA events over R back-to-back calls after warm-up
-(inputs resident in HBM).  JSON lines on stdout.
+sigma^2 in {0.1, 1, 10}; R calls captured in a CUDA graph and replayed, timed
+with CUDA events (device time per call; inputs resident in HBM).  JSON lines.
 """
 from __future__ import annotations
 
@@ -14,6 +14,33 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+
+def time_calls(fn, reps, dev):
+    """Device time per call: the calls are captured in a CUDA graph (so Python / launch
+    overhead is not on the timeline) and replayed; warm-up on the capture stream."""
+    import torch
+
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(3):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / (3 * reps)
 
 
 def main():
@@ -37,16 +64,8 @@ def main():
                 anc = torch.empty((N, P), dtype=torch.int32, device=dev)
                 for scheme, B, flags in cases:
                     reps = 20 if N * P <= (1 << 22) else 5
-                    for _ in range(3):
-                        pf.pf_resample_batched(scheme, x, 5, B=B, ancestors=anc, flags=flags, stream=stream)
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                    for r in range(reps):
-                        pf.pf_resample_batched(scheme, x, 5 + r, B=B, ancestors=anc, flags=flags, stream=stream)
-                    e1.record(stream)
-                    torch.cuda.synchronize(dev)
-                    ms = e0.elapsed_time(e1) / reps
+                    ms = time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, B=B, ancestors=anc, flags=flags),
+                                    reps, dev)
                     name = scheme + ("_sorted_a6" if flags else "") + (f"_B{B}" if B else "")
                     print(json.dumps({"batched": batched, "N": N, "P": P, "var": var, "scheme": name,
                                       "us_per_call": round(ms * 1e3, 2),
