@@ -40,6 +40,8 @@ WORKLOADS = {
     "p24": (1, 1 << 24, "single filter P=2^24"),
     # C5: one giant filter, 2^25 particles per GPU (weak), sharded with NCCL exchanges
     "c5": (1, 1 << 25, "C5 giant filter sharded over GPUs: 2^25 particles per GPU"),
+    # C4: bootstrap particle filter step on the 16-dim linear-Gaussian model
+    "c4": (1, 1 << 18, "C4 bootstrap PF step, linear-Gaussian model, P=2^18, D=16"),
 }
 
 
@@ -200,6 +202,57 @@ def run_c5(args):
         }))
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_c4(args):
+    """C4: one step = one bootstrap-PF time step (propagate + weight, resample with lse and
+    offspring, log-likelihood accumulation, permute, in-place gather of the D=16 state); K steps
+    captured in a CUDA graph (the filter loop is launch-bound at P = 2^18) and replayed."""
+    import torch
+
+    import paper_1202_6163_b200 as pf
+    import pfinputs
+    from paper_1202_6163_b200.pf_demo import LinearGaussianPF
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _, P, desc = WORKLOADS["c4"]
+    ys = pfinputs.lg_observations(args.steps + args.warmup, seed=pfinputs.BASE_SEED + rank)
+    f = LinearGaussianPF(P=P, D=args.D, scheme=args.scheme, B=args.B if args.scheme == "metropolis" else 0,
+                         seed=pfinputs.seed_for(rank), device=dev)
+    s = torch.cuda.Stream(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    with torch.cuda.stream(s):
+        for t in range(args.warmup):
+            f.step(float(ys[t]))
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    l0 = pf.pf_launch_count()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(args.steps):
+            f.step(float(ys[args.warmup + t]))
+    launches = pf.pf_launch_count() - l0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": P * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 state / f32 log-weights / u64 scan / int32 indices",
+            "data": "synthetic (observations simulated from the model)",
+            "config": {"workload": desc + f", scheme={args.scheme}", "P": P, "D": args.D,
+                       "pf_steps_per_s": args.steps / (ms / 1e3), "timing": "K steps captured in one CUDA graph"},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks,
+        }))
 
 
 def run_ours(args):
@@ -555,6 +608,8 @@ def main():
         run_reference(args)
     elif args.workload == "c5":
         run_c5(args)
+    elif args.workload == "c4":
+        run_c4(args)
     else:
         run_ours(args)
 

@@ -230,6 +230,26 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
                                      const int32_t* d_gbad, int32_t* anc, pf_stream_t stream);
 
 /*
+ * Bootstrap particle filter demo model (BASELINE config C4; P:43-68 steps 1-3;
+ * DESIGN.md R-20): a diagonal AR(1) state in D dimensions, x_t = phi x_{t-1} +
+ * sigma_x eps_t, observed through y_t = x_t[0] + sigma_y eta_t.  X is float32
+ * [P][ld] row-major (ld >= D, device).  Noise: Philox4x32-10 (tag 6 for the
+ * transition, 7 for the initial draw; counter (particle, step * ceil(D/4) + block,
+ * tag, 0)) -> Box-Muller normals (float32 intrinsics; not part of the bit-exact
+ * resampling contract).
+ */
+/* x_0 ~ N(0, sigma_x^2 / (1 - phi^2)) in every dimension (stationary start). */
+pf_status pf_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, uint64_t seed,
+                     pf_stream_t stream);
+/* Propagate (step 2) and weight (step 3): x <- phi x + sigma_x eps, then
+ * logw_i = -(y - x_i[0])^2 / (2 sigma_y^2).  t = time index (1-based). */
+pf_status pf_lg_propagate_weight(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x,
+                                 float sigma_y, float y, uint64_t seed, int32_t t, float* logw, pf_stream_t stream);
+/* loglik[0] += lse[0] - ln P - ln(2 pi sigma_y^2) / 2: the log of the bootstrap
+ * likelihood increment p(y_t | y_1:t-1) (lse from pf_resample_ex lse_out). */
+pf_status pf_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* loglik, pf_stream_t stream);
+
+/*
  * Host helper: minimum B with lambda^B <= eps (alpha+beta)/max(alpha,beta)
  * (Eq. (4)-(5)), alpha = (1 - w_max)/(P w_max) (Eq. (2)), beta = 1/P.  Returns 0 if
  * B = 0 already satisfies Eq. (4), -1 on invalid arguments.  Host-only, no GPU.

@@ -70,6 +70,10 @@ _SIGS = {
                         ctypes.c_int),
     "pf_shard_weights": ([_V, _I32, _V, _V, _V], ctypes.c_int),
     "pf_metropolis_from_weights": ([_V, _I64, _I64, _I32, _U64, _I32, _U32, _V, _V, _V, _V], ctypes.c_int),
+    "pf_lg_init": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, _U64, _V], ctypes.c_int),
+    "pf_lg_propagate_weight": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                ctypes.c_float, _U64, _I32, _V, _V], ctypes.c_int),
+    "pf_lg_accumulate": ([_V, _I32, ctypes.c_float, _V, _V], ctypes.c_int),
     "pf_metropolis_required_B": ([_I64, _F64, _F64], _I32),
     "pf_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "pf_launch_count": ([], _U64),
@@ -392,6 +396,33 @@ def pf_metropolis_from_weights(w_full, slot0: int, nslots: int, seed: int, B: in
                                             seed & (2 ** 64 - 1), B, filter_index, _ptr(gmax), _ptr(gbad),
                                             anc.data_ptr(), _stream(w_full, stream)), "pf_metropolis_from_weights")
     return anc
+
+
+# ----------------------------------------------------------------------------- C4 demo model
+def pf_lg_init(X, phi: float, sigma_x: float, seed: int, stream=None):
+    torch = _torch()
+    _need_cuda(X, torch.float32, "X")
+    _check(lib().pf_lg_init(X.data_ptr(), X.stride(0), X.shape[0], X.shape[1], phi, sigma_x, seed & (2 ** 64 - 1),
+                            _stream(X, stream)), "pf_lg_init")
+    return X
+
+
+def pf_lg_propagate_weight(X, phi: float, sigma_x: float, sigma_y: float, y: float, seed: int, t: int, logw=None,
+                           stream=None):
+    torch = _torch()
+    _need_cuda(X, torch.float32, "X")
+    if logw is None:
+        logw = torch.empty(X.shape[0], dtype=torch.float32, device=X.device)
+    _check(lib().pf_lg_propagate_weight(X.data_ptr(), X.stride(0), X.shape[0], X.shape[1], phi, sigma_x, sigma_y,
+                                        float(y), seed & (2 ** 64 - 1), t, logw.data_ptr(), _stream(X, stream)),
+           "pf_lg_propagate_weight")
+    return logw
+
+
+def pf_lg_accumulate(lse, P: int, sigma_y: float, loglik, stream=None):
+    _check(lib().pf_lg_accumulate(lse.data_ptr(), P, sigma_y, loglik.data_ptr(), _stream(lse, stream)),
+           "pf_lg_accumulate")
+    return loglik
 
 
 # ----------------------------------------------------------------------------- host helpers

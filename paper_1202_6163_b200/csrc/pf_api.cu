@@ -426,6 +426,34 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
     return cuda_status(e);
 }
 
+// ---------------------------------------------------------------- C4 demo model
+pf_status pf_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, uint64_t seed,
+                     pf_stream_t stream) {
+    if (!X || P < 1 || D < 1 || ld < D || !(phi * phi < 1.0f) || !(sigma_x >= 0.0f)) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_lg_init(X, ld, P, D, phi, sigma_x, seed, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_lg_propagate_weight(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x,
+                                 float sigma_y, float y, uint64_t seed, int32_t t, float* logw, pf_stream_t stream) {
+    if (!X || !logw || P < 1 || D < 1 || ld < D || !(sigma_y > 0.0f) || t < 0) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_lg_step(X, ld, P, D, phi, sigma_x, sigma_y, y, seed, t, logw,
+                                             static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* loglik, pf_stream_t stream) {
+    if (!lse || !loglik || P < 1 || !(sigma_y > 0.0f)) return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_lg_accumulate(lse, P, sigma_y, loglik, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
 int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps) {
     if (P < 1 || !(w_max > 0.0) || w_max > 1.0 || !(eps > 0.0)) return -1;
     const double beta = 1.0 / static_cast<double>(P);

@@ -107,6 +107,14 @@ cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, 
                                cudaStream_t s, uint64_t* launches);
 size_t shard_ctx_bytes();
 
+// C4 demo model (linear-Gaussian bootstrap filter).
+cudaError_t launch_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, uint64_t seed,
+                           cudaStream_t s, uint64_t* launches);
+cudaError_t launch_lg_step(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, float sigma_y,
+                           float y, uint64_t seed, int32_t t, float* logw, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* loglik, cudaStream_t s,
+                                 uint64_t* launches);
+
 // One-launch cluster-per-filter resampler for stratified/systematic (pf_fused.cu).
 bool fused_supported(int scheme, int32_t P);
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,

@@ -1257,6 +1257,71 @@ __global__ void __launch_bounds__(kThreads) k_metro_slots(const float* __restric
     anc[s] = static_cast<int32_t>(k);
 }
 
+// ============================================================================ C4 demo model
+__device__ __forceinline__ void box_muller4(const u32x4& r, float z[4]) {
+    const float k = 2.3283064365386963e-10f;  // 2^-32
+    const float u1 = (static_cast<float>(r.x) + 0.5f) * k, u2 = (static_cast<float>(r.y) + 0.5f) * k;
+    const float u3 = (static_cast<float>(r.z) + 0.5f) * k, u4 = (static_cast<float>(r.w) + 0.5f) * k;
+    const float a = sqrtf(-2.0f * logf(u1)), b = sqrtf(-2.0f * logf(u3));
+    float s1, c1, s2, c2;
+    sincospif(2.0f * u2, &s1, &c1);
+    sincospif(2.0f * u4, &s2, &c2);
+    z[0] = a * c1; z[1] = a * s1; z[2] = b * c2; z[3] = b * s2;
+}
+
+__global__ void __launch_bounds__(kThreads) k_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float sd,
+                                                      Key key) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (i >= P) return;
+    float* row = X + i * ld;
+    const int nb = (D + 3) / 4;
+    for (int b = 0; b < nb; ++b) {
+        float z[4];
+        box_muller4(philox10(static_cast<uint32_t>(i), static_cast<uint32_t>(b), 7u, 0u, key.k0, key.k1), z);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (4 * b + q < D) row[4 * b + q] = sd * z[q];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_lg_step(float* X, int64_t ld, int32_t P, int32_t D, float phi,
+                                                      float sx, float inv2vy, float y, Key key, int32_t t,
+                                                      float* logw, int vec) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (i >= P) return;
+    float* row = X + i * ld;
+    const int nb = (D + 3) / 4;
+    float x0 = 0.0f;
+    for (int b = 0; b < nb; ++b) {
+        float z[4];
+        box_muller4(philox10(static_cast<uint32_t>(i), static_cast<uint32_t>(t * nb + b), 6u, 0u, key.k0, key.k1), z);
+        if (vec && 4 * b + 3 < D) {
+            float4 v = reinterpret_cast<float4*>(row)[b];
+            v.x = phi * v.x + sx * z[0];
+            v.y = phi * v.y + sx * z[1];
+            v.z = phi * v.z + sx * z[2];
+            v.w = phi * v.w + sx * z[3];
+            reinterpret_cast<float4*>(row)[b] = v;
+            if (b == 0) x0 = v.x;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (4 * b + q < D) {
+                    const float nv = phi * row[4 * b + q] + sx * z[q];
+                    row[4 * b + q] = nv;
+                    if (b == 0 && q == 0) x0 = nv;
+                }
+            }
+        }
+    }
+    const float d = y - x0;
+    logw[i] = -d * d * inv2vy;
+}
+
+__global__ void k_lg_accumulate(const double* lse, double c, double* loglik) {
+    if (threadIdx.x == 0) loglik[0] += lse[0] - c;
+}
+
 int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -1620,6 +1685,35 @@ cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, con
         k_merge<ModeSpacings><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf,
                                                                                                      chunk);
     }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, uint64_t seed,
+                           cudaStream_t s, uint64_t* launches) {
+    const float sd = sigma_x / sqrtf(1.0f - phi * phi);
+    ProfScope ps_("k_lg_init", s);
+    k_lg_init<<<static_cast<unsigned>(cdiv(P, kThreads)), kThreads, 0, s>>>(X, ld, P, D, sd, make_key(seed));
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_lg_step(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, float sigma_y,
+                           float y, uint64_t seed, int32_t t, float* logw, cudaStream_t s, uint64_t* launches) {
+    const int vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 4 == 0) ? 1 : 0;
+    ProfScope ps_("k_lg_step", s);
+    k_lg_step<<<static_cast<unsigned>(cdiv(P, kThreads)), kThreads, 0, s>>>(
+        X, ld, P, D, phi, sigma_x, 0.5f / (sigma_y * sigma_y), y, make_key(seed), t, logw, vec);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* loglik, cudaStream_t s,
+                                 uint64_t* launches) {
+    const double c = std::log(static_cast<double>(P)) +
+                     0.5 * std::log(2.0 * 3.14159265358979323846 * static_cast<double>(sigma_y) * sigma_y);
+    ProfScope ps_("k_lg_accumulate", s);
+    k_lg_accumulate<<<1, 32, 0, s>>>(lse, c, loglik);
     ++*launches;
     return cudaPeekAtLastError();
 }

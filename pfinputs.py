@@ -88,3 +88,15 @@ def with_neg_inf_runs(logw: np.ndarray, frac: float = 0.3, seed: int = 7) -> np.
 def state_matrix(P: int, D: int, seed: int = BASE_SEED) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed ^ 0x5A5A))
     return rng.standard_normal(size=(P, D), dtype=np.float32)
+
+
+def lg_observations(T: int, phi: float = 0.9, sigma_x: float = 1.0, sigma_y: float = 1.0, D: int = 16,
+                    seed: int = BASE_SEED) -> np.ndarray:
+    """Observation sequence y_1..y_T simulated from the C4 model (R-20)."""
+    rng = np.random.Generator(np.random.PCG64(seed ^ 0xC4))
+    x = rng.standard_normal(D) * sigma_x / np.sqrt(1 - phi * phi)
+    ys = np.zeros(T)
+    for t in range(T):
+        x = phi * x + sigma_x * rng.standard_normal(D)
+        ys[t] = x[0] + sigma_y * rng.standard_normal()
+    return ys

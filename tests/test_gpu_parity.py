@@ -458,3 +458,24 @@ def test_small_filters_warp_kernel(pf, dev, orc, scheme):
                     assert (np.isnan(wl) and np.isnan(L[n])) or abs(L[n] - wl) <= 1e-6 * max(1.0, abs(wl))
         finally:
             pf.pf_set_fusion(True)
+
+
+def test_pf_linear_gaussian_c4(pf, dev, orc):
+    """C4: bootstrap PF (propagate + weight kernels, resample, permute, gather) on the 16-dim
+    linear-Gaussian model: log-likelihood within Monte Carlo error of the Kalman filter, and every
+    checked step's resampling bit-exact against the oracle fed the GPU's log-weights."""
+    from oracle.kalman import kalman_loglik
+    from paper_1202_6163_b200.pf_demo import LinearGaussianPF
+
+    T = 40
+    ys = pfinputs.lg_observations(T, seed=5)
+    want, _ = kalman_loglik(ys)
+    lls = [LinearGaussianPF(P=1 << 16, seed=100 + r).run(ys) for r in range(6)]
+    mean, sd = float(np.mean(lls)), float(np.std(lls, ddof=1))
+    assert abs(mean - want) < 5 * sd / math.sqrt(len(lls)) + 0.05, (mean, want, sd)
+    for scheme in ("systematic", "stratified", "multinomial", "metropolis"):
+        f = LinearGaussianPF(P=5000, seed=9, scheme=scheme, B=16 if scheme == "metropolis" else 0)
+        for y in ys[:4]:
+            logw, anc, s = f.step(float(y), check=True)
+            _, wanted = orc.resample(scheme, logw, s, B=f.B)
+            assert np.array_equal(anc, wanted), scheme

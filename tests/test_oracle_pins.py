@@ -654,3 +654,20 @@ def test_sorted_multinomial_offspring_law(orc):
             _, a = orc.resample_sorted_multinomial(x, pfinputs.seed_for(s))
             c[tuple(orc.ancestors_to_offspring(a))] += 1
         assert _gof(c, pmf, n) > 1e-4, P
+
+
+def test_kalman_oracle_against_joint_gaussian():
+    """C4 oracle (R-20): the Kalman log-likelihood equals the exact joint Gaussian log-density of
+    y_1:T (stationary AR(1) covariance phi^|s-t| sigma_x^2/(1-phi^2) + sigma_y^2 delta_st)."""
+    from scipy.stats import multivariate_normal
+
+    from oracle.kalman import kalman_loglik
+
+    for phi, sx, sy, T in ((0.9, 1.0, 1.0, 30), (0.5, 0.7, 2.0, 12)):
+        ys = pfinputs.lg_observations(T, phi, sx, sy, seed=T)
+        ll, _ = kalman_loglik(ys, phi, sx, sy)
+        s0 = sx * sx / (1 - phi * phi)
+        idx = np.arange(T)
+        C = s0 * phi ** np.abs(idx[:, None] - idx[None, :]) + sy * sy * np.eye(T)
+        want = multivariate_normal(mean=np.zeros(T), cov=C).logpdf(ys)
+        assert abs(ll - want) < 1e-9 * max(1.0, abs(want)), (ll, want)
