@@ -4,8 +4,8 @@
 One step = one pass of the whole hot path over a batch of synthetic filters
 (BASELINE.json configs[2], "batched PMCMC: 1024 independent filters x 2^16"):
   pf_resample_batched (a1-a5: max, dexp + u64 scan, ancestor search; a8:
-      offspring counts as a side output)
-  -> pf_permute_offspring_batched (a9: canonical in-place permutation)
+      offspring counts and a9: the canonical in-place permutation as side
+      outputs, all in the one-launch cluster kernel)
   -> pf_gather_state_batched (a10: in-place gather of a D=16 float32 state).
 The generic chain through pf_permute(ancestors) (histogram path) is timed
 as an extra (`extras.step_via_pf_permute_of_ancestors`).
@@ -290,10 +290,10 @@ def run_ours(args):
     perm = torch.empty((N, P), dtype=torch.int32, device=dev)
 
     def step():
-        # a1-a5 (+a8: offspring as a side output of the resampler), a9, a10
+        # a1-a5, a8 (offspring) and a9 (canonical permutation) as side outputs of the resampler
+        # (fused into the cluster kernel for P <= 65536), then a10 (in-place gather)
         pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
-                               stream=stream)
-        pf.pf_permute_offspring(off, permuted=perm, stream=stream)
+                               permuted_out=perm, stream=stream)
         pf.pf_gather_state(X, perm, stream=stream)
 
     sampler = ClockSampler(local)
@@ -351,7 +351,7 @@ def run_ours(args):
         "k_hist": 8 * NP,
         "k_pscan": 12 * NP,
         "k_push": 8 * NP + 8 * free,
-        "k_fused_sorted": 12 * NP,  # logw in, ancestors + offspring out
+        "k_fused_sorted": 16 * NP,  # logw in; ancestors, offspring, permutation out
         "k_coop_sorted": 12 * NP,
         "k_gather_inplace": 4 * NP + 2 * row * free,
     }
@@ -450,8 +450,7 @@ def run_ours(args):
         def e2e_step():
             d_logw.copy_(h_logw, non_blocking=True)
             pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
-                                   stream=stream)
-            pf.pf_permute_offspring(off, permuted=perm, stream=stream)
+                                   permuted_out=perm, stream=stream)
             pf.pf_gather_state(X, perm, stream=stream)
             h_out.copy_(perm, non_blocking=True)
 

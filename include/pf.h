@@ -91,6 +91,10 @@ typedef struct {
     int32_t* offspring_out; /* [N][P] (row stride = ancestors' ld) o_i = #{k : a_k = i} (NS-14);
                               the one-launch stratified/systematic kernel derives it from its
                               slot counts at no extra pass; other paths run the histogram   */
+    int32_t* permuted_out;  /* [N][P] (row stride = ancestors' ld) the canonical in-place
+                              permutation of the ancestors (NS-15, = pf_permute(ancestors));
+                              fused into the cluster kernel (P <= 65536), otherwise computed
+                              from the offspring after the search                           */
     void* workspace;       /* device, nullable -> library pool                              */
     size_t workspace_bytes;
 } pf_opts;

@@ -37,6 +37,7 @@ class _Opts(ctypes.Structure):
         ("ess_out", ctypes.c_void_p),
         ("status_out", ctypes.c_void_p),
         ("offspring_out", ctypes.c_void_p),
+        ("permuted_out", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
     ]
@@ -156,7 +157,7 @@ def _scheme(s):
 # ----------------------------------------------------------------------------- resamplers
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
                    lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                   flags: int = 0, stream=None):
+                   permuted_out=None, flags: int = 0, stream=None):
     """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -177,6 +178,8 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
         _need_cuda(status_out, torch.int32, "status_out"); opts.status_out = status_out.data_ptr()
     if offspring_out is not None:
         _need_cuda(offspring_out, torch.int32, "offspring_out"); opts.offspring_out = offspring_out.data_ptr()
+    if permuted_out is not None:
+        _need_cuda(permuted_out, torch.int32, "permuted_out"); opts.permuted_out = permuted_out.data_ptr()
     rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
                               ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_ex")
@@ -211,7 +214,7 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
                         lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                        flags: int = 0, stream=None):
+                        permuted_out=None, flags: int = 0, stream=None):
     """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P]."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -226,7 +229,7 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
     opts = _Opts(flags=flags)
     for name, t, dt in (("lse_out", lse_out, torch.float64), ("ess_out", ess_out, torch.float64),
                         ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32),
-                        ("offspring_out", offspring_out, torch.int32)):
+                        ("offspring_out", offspring_out, torch.int32), ("permuted_out", permuted_out, torch.int32)):
         if t is not None:
             _need_cuda(t, dt, name)
             setattr(opts, name, t.data_ptr())

@@ -108,9 +108,10 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     float* normw = opts ? opts->normw_out : nullptr;
     int32_t* status_out = opts ? opts->status_out : nullptr;
     int32_t* offspring_out = opts ? opts->offspring_out : nullptr;
+    int32_t* permuted_out = opts ? opts->permuted_out : nullptr;
 
     const bool no_fusion = (opts && (opts->flags & PF_NO_FUSION)) || g_no_fusion.load();
-    if (!no_fusion && pf::small_supported(P)) {
+    if (!no_fusion && pf::small_supported(P) && !permuted_out) {
         // one warp per filter, every scheme, one launch (pf_fused.cu k_small)
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_small(scheme, sorted_multi, logw, ld, N, P, seed, first_filter, B, anc, ld_anc,
@@ -122,14 +123,42 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         // one launch per batch: cluster-per-filter kernel, no workspace (pf_fused.cu)
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
-                                                      ess, normw, status_out, offspring_out, s, &nl);
+                                                      ess, normw, status_out, offspring_out, permuted_out, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
+    if (permuted_out) {
+        // not fused for this size/scheme: resample (offspring as a side output), then the
+        // canonical permutation from the offspring (k_pscan + k_push).  One pool block holds
+        // [permutation scratch | offspring (if the caller gave none) | resample workspace].
+        if (opts && opts->workspace) return PF_ERR_UNSUPPORTED;
+        const pf::Layout LP = pf::make_layout(N, P, pf::kNeedPermute);
+        const pf::Layout LR = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u));
+        const size_t off_bytes = offspring_out ? 0 : static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4;
+        const size_t o1 = (LP.total + 255) / 256 * 256;
+        const size_t o2b = (o1 + off_bytes + 255) / 256 * 256;
+        void* big = nullptr;
+        pf_status st0 = pool_get(o2b + LR.total, s, &big);
+        if (st0 != PF_OK) return st0;
+        const pf::Ws wp = pf::carve(big, LP);
+        int32_t* off = offspring_out ? offspring_out : reinterpret_cast<int32_t*>(static_cast<char*>(big) + o1);
+        pf_opts o2 = opts ? *opts : pf_opts{};
+        o2.permuted_out = nullptr;
+        o2.offspring_out = off;
+        o2.workspace = static_cast<char*>(big) + o2b;
+        o2.workspace_bytes = LR.total;
+        pf_status st2 = resample_impl(scheme, logw, ld, N, P, seed, first_filter, B, anc, ld_anc, &o2, s);
+        if (st2 != PF_OK) return st2;
+        uint64_t nl = 0;
+        cudaError_t e = cudaMemsetAsync(static_cast<char*>(big) + LP.zero_begin, 0, LP.zero_end - LP.zero_begin, s);
+        if (e == cudaSuccess) e = pf::launch_permute_from_offspring(off, ld_anc, N, P, LP, wp, permuted_out, ld_anc, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }
     if (!no_fusion && !normw && pf::coop_supported(scheme, P)) {
         // one cooperative launch for large filters (pf_fused.cu); tiny scratch from the pool
         void* sc = nullptr;
-        pf_status st2 = pool_get(pf::coop_scratch_bytes(), s, &sc);
+        pf_status st2 = get_workspace(opts, pf::coop_scratch_bytes(), s, &sc);
         if (st2 != PF_OK) return st2;
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_coop_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,

@@ -47,6 +47,7 @@ struct Exchange {
     int bad;
     uint64_t tot;
     double sw, sw2;
+    uint64_t ptot;  // packed (extras << 31 | free) total of the CTA (phase D)
 };
 
 struct FusedArgs {
@@ -67,6 +68,7 @@ struct FusedArgs {
     float* normw;
     int32_t* status_out;
     int32_t* off;   // offspring out (row stride ld_anc), nullable
+    int32_t* perm;  // canonical permutation out (row stride ld_anc), nullable (PERM)
 };
 
 struct Pos {
@@ -116,9 +118,12 @@ __device__ __forceinline__ uint32_t count_below(const Pos& z, uint64_t v) {
     return static_cast<uint32_t>(min(max(c, int64_t{0}), z.P));
 }
 
-template <int SCHEME, bool SUMS>
+template <int SCHEME, bool SUMS, bool PERM>
 __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
+    extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
     __shared__ Exchange s_x;
+    __shared__ uint32_t s_rf[9];
+    __shared__ uint64_t s_poff;
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];
@@ -208,6 +213,8 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
             for (int64_t k = p0 + tid; k < p1; k += kFT) arow[k] = static_cast<int32_t>(k);
             if (a.off)
                 for (int64_t k = p0 + tid; k < p1; k += kFT) a.off[static_cast<int64_t>(n) * a.ld_anc + k] = 1;
+            if (PERM)
+                for (int64_t k = p0 + tid; k < p1; k += kFT) a.perm[static_cast<int64_t>(n) * a.ld_anc + k] = static_cast<int32_t>(k);
             if (a.normw)
                 for (int64_t k = p0 + tid; k < p1; k += kFT) a.normw[static_cast<int64_t>(n) * a.P + k] = NAN;
             if (c == 0 && tid == 0) {
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
         if (a.P == 1) {
             if (tid == 0) a.anc[static_cast<int64_t>(n) * a.ld_anc] = 0;
             if (tid == 0 && a.off) a.off[static_cast<int64_t>(n) * a.ld_anc] = 1;
+            if (PERM && tid == 0) a.perm[static_cast<int64_t>(n) * a.ld_anc] = 0;
             __syncthreads();
             continue;
         }
@@ -440,6 +448,138 @@ __global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
                         if (k0 + t >= S0 && k0 + t < S1) arow[k0 + t] = h[t];
                 }
                 __syncwarp();
+            }
+        }
+        if (PERM) {
+            // ---------------- D: canonical permutation (NS-15) from o_i = E_i - E_{i-1}
+            // packed value per particle: (extras << 31) | free; padding particles are neither
+            uint64_t pex[kFR];
+            __syncthreads();  // s_wt is reused
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                uint64_t loc = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                    const uint32_t o = E[j * 4 + q] - pe;
+                    const bool real = (j * (kFT * 4) + tid * 4 + q) < np;
+                    loc += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && real) ? 1ull : 0ull);
+                }
+                const uint64_t incl = warp_incl_scan_u64(loc, lane);
+                pex[j] = incl - loc;
+                const uint64_t wt = __shfl_sync(kFull, incl, 31);
+                if (lane == 0) s_wt[j][warp] = wt;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                uint64_t t4[kTPL];
+                uint64_t tsum = 0;
+#pragma unroll
+                for (int q = 0; q < kTPL; ++q) {
+                    const int idx = lane * kTPL + q;
+                    t4[q] = s_wt[idx / kFW][idx % kFW];
+                    tsum += t4[q];
+                }
+                const uint64_t incl = warp_incl_scan_u64(tsum, lane);
+                uint64_t run = incl - tsum;
+#pragma unroll
+                for (int q = 0; q < kTPL; ++q) {
+                    const int idx = lane * kTPL + q;
+                    s_wt[idx / kFW][idx % kFW] = run;
+                    run += t4[q];
+                }
+                if (lane == 31) s_x.ptot = incl;
+            }
+            cluster.sync();  // #3 packed CTA totals published
+            if (warp == 0) {
+                uint64_t pt = 0;
+                if (lane < CL) pt = cluster.map_shared_rank(&s_x, lane)->ptot;
+                // free-rank prefix of every CTA (for the owner lookup) and this CTA's packed offset
+                uint64_t incl = pt;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint64_t u = __shfl_up_sync(kFull, incl, o2);
+                    if (lane >= o2) incl += u;
+                }
+                const uint64_t excl = incl - pt;
+                if (lane <= CL && lane < 9) s_rf[lane] = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
+                if (lane == c) s_poff = excl;
+            }
+            __syncthreads();
+            const uint64_t poff = s_poff;
+            const uint32_t rf_c = s_rf[c];
+            int32_t* prow = a.perm + static_cast<int64_t>(n) * a.ld_anc;
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                uint64_t run = poff + s_wt[j][warp] + pex[j];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = j * (kFT * 4) + tid * 4 + q;
+                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                    const uint32_t o = E[j * 4 + q] - pe;
+                    if (i < np) {
+                        if (o > 0) prow[p0 + i] = static_cast<int32_t>(p0 + i);
+                        else s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull) - rf_c] = static_cast<int32_t>(p0 + i);
+                    }
+                    run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
+                }
+            }
+            cluster.sync();  // #4 every CTA's free-slot list complete
+            // survivors' extra copies: per (row, warp) the extras ranks are contiguous
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const uint64_t base = poff + s_wt[j][warp] + pex[j];
+                uint32_t eloc = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                    const uint32_t o = E[j * 4 + q] - pe;
+                    eloc += o > 1 ? o - 1 : 0;
+                }
+                const uint32_t my_x0 = static_cast<uint32_t>(base >> 31);  // this lane's first extras rank
+                const uint32_t X0 = __shfl_sync(kFull, my_x0, 0);
+                uint32_t xincl = eloc;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const uint32_t u = __shfl_up_sync(kFull, xincl, o2);
+                    if (lane >= o2) xincl += u;
+                }
+                const uint32_t XW = __shfl_sync(kFull, xincl, 31);
+                // 32 ranks per pass, one per lane: head-mark in 32 smem slots, shuffle max-scan
+                int32_t carry = -1;
+                int32_t* hb = s_buf[warp];
+                for (uint32_t c0 = 0; c0 < XW; c0 += 32) {
+                    hb[lane] = -1;
+                    __syncwarp();
+                    uint32_t rel0 = my_x0 - X0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                        const uint32_t o = E[j * 4 + q] - pe;
+                        const uint32_t e = o > 1 ? o - 1 : 0;
+                        const uint32_t rel = rel0 - c0;
+                        if (e > 0 && rel < 32u) hb[rel] = idbase + j * (kFT * 4) + q;
+                        rel0 += e;
+                    }
+                    __syncwarp();
+                    int32_t h = hb[lane];
+#pragma unroll
+                    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                        const int32_t u = __shfl_up_sync(kFull, h, o2);
+                        if (lane >= o2) h = max(h, u);
+                    }
+                    h = max(h, carry);
+                    carry = __shfl_sync(kFull, h, 31);
+                    const uint32_t rl = c0 + lane;
+                    if (rl < XW) {
+                        const uint32_t r = X0 + rl;  // global free rank
+                        int cc = 0;
+                        for (int q2 = 1; q2 < CL; ++q2) cc += (s_rf[q2] <= r) ? 1 : 0;
+                        const int32_t* rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
+                        prow[rfs[r - s_rf[cc]]] = h;
+                    }
+                    __syncwarp();
+                }
             }
         }
         __syncthreads();
@@ -1012,10 +1152,15 @@ int device_sms() {
     return sms;
 }
 
-template <int SCHEME, bool SUMS>
+template <int SCHEME, bool SUMS, bool PERM>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    const size_t smem = 0;
-    auto kern = k_fused_sorted<SCHEME, SUMS>;
+    const size_t smem = PERM ? static_cast<size_t>(kPP) * sizeof(int32_t) : 0;
+    auto kern = k_fused_sorted<SCHEME, SUMS, PERM>;
+    static bool smem_attr_set = false;
+    if (PERM && !smem_attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        smem_attr_set = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1029,10 +1174,8 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(a.CL, 1, 1);
     // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us)
-    static int cached[2][2][17] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][a.CL];
+    static int cached[2][2][2][17] = {};
+    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][PERM ? 1 : 0][a.CL];
     if (max_clusters == 0) {
         if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
             cudaGetLastError();
@@ -1146,7 +1289,7 @@ bool fused_supported(int scheme, int32_t P) {
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
-                                cudaStream_t s, uint64_t* launches) {
+                                int32_t* permuted, cudaStream_t s, uint64_t* launches) {
     FusedArgs a{};
     a.logw = logw;
     a.ld = ld;
@@ -1171,10 +1314,17 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.normw = normw;
     a.status_out = status_out;
     a.off = offspring;
+    a.perm = permuted;
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
-    if (scheme == 2) e = a.sums ? launch_fused_t<2, true>(a, s) : launch_fused_t<2, false>(a, s);
-    else e = a.sums ? launch_fused_t<3, true>(a, s) : launch_fused_t<3, false>(a, s);
+    const bool pm = a.perm != nullptr;
+    if (scheme == 2) {
+        if (pm) e = a.sums ? launch_fused_t<2, true, true>(a, s) : launch_fused_t<2, false, true>(a, s);
+        else e = a.sums ? launch_fused_t<2, true, false>(a, s) : launch_fused_t<2, false, false>(a, s);
+    } else {
+        if (pm) e = a.sums ? launch_fused_t<3, true, true>(a, s) : launch_fused_t<3, false, true>(a, s);
+        else e = a.sums ? launch_fused_t<3, true, false>(a, s) : launch_fused_t<3, false, false>(a, s);
+    }
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

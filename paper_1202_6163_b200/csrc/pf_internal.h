@@ -120,7 +120,7 @@ bool fused_supported(int scheme, int32_t P);
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
-                                cudaStream_t s, uint64_t* launches);
+                                int32_t* permuted, cudaStream_t s, uint64_t* launches);
 
 // One-warp-per-filter kernel for P <= 256, every scheme (pf_fused.cu).
 bool small_supported(int32_t P);

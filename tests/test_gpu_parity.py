@@ -479,3 +479,40 @@ def test_pf_linear_gaussian_c4(pf, dev, orc):
             logw, anc, s = f.step(float(y), check=True)
             _, wanted = orc.resample(scheme, logw, s, B=f.B)
             assert np.array_equal(anc, wanted), scheme
+
+
+@pytest.mark.parametrize("scheme", SCHEMES + ["sorted"])
+def test_permuted_out(pf, dev, orc, scheme):
+    """pf_opts.permuted_out (fused into the cluster kernel for stratified/systematic, P <= 65536;
+    resample + permutation from offspring otherwise) equals the oracle's canonical permutation of the
+    oracle's ancestors; batched, ragged, with an invalid filter; with and without offspring_out."""
+    import torch
+
+    sch = "multinomial" if scheme == "sorted" else scheme
+    flags = pf.PF_SORTED if scheme == "sorted" else 0
+    B = 13 if scheme == "metropolis" else 0
+    for N, P, var in ((1, 100, 1.0), (5, 8192, 10.0), (3, 8193, 1.0), (12, 30000, 1.0), (2, 65536, 10.0),
+                      (1, 100003, 1.0)):
+        ld = P + 4
+        x = pfinputs.gaussian_logw(ld, var, seed=N + P, N=N)
+        if N > 3:
+            x[2, :] = -np.inf
+        g = _gpu(x, dev)[:, :P]
+        for with_off in (False, True):
+            perm = torch.full((N, ld), -5, dtype=torch.int32, device=dev)[:, :P]
+            off = torch.empty((N, ld), dtype=torch.int32, device=dev)[:, :P] if with_off else None
+            anc = torch.empty((N, ld), dtype=torch.int32, device=dev)[:, :P]
+            pf.pf_resample_batched(sch, g, 8, B=B, first_filter=2, ancestors=anc, offspring_out=off,
+                                   permuted_out=perm, flags=flags)
+            torch.cuda.synchronize()
+            A, Pm = anc.cpu().numpy(), perm.cpu().numpy()
+            for n in range(N):
+                xn = np.ascontiguousarray(x[n, :P])
+                if scheme == "sorted":
+                    _, want = orc.resample_sorted_multinomial(xn, 8, filter_index=2 + n)
+                else:
+                    _, want = orc.resample(sch, xn, 8, B=B, filter_index=2 + n)
+                assert np.array_equal(A[n], want), (scheme, N, P, n)
+                assert np.array_equal(Pm[n], orc.permute(want)), (scheme, N, P, n, with_off)
+                if with_off:
+                    assert np.array_equal(off.cpu().numpy()[n], orc.ancestors_to_offspring(want))
