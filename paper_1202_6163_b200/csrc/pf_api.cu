@@ -92,7 +92,11 @@ cudaEvent_t prof_event() {
 
 pf_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
 
-unsigned needs_for(int scheme) { return scheme == PF_METROPOLIS ? pf::kNeedW : pf::kNeedQ; }
+unsigned needs_for(int scheme) {
+    if (scheme == PF_METROPOLIS) return pf::kNeedW;
+    if (scheme == PF_MULTINOMIAL) return pf::kNeedQ | pf::kNeedBuckets;
+    return pf::kNeedQ;
+}
 
 pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,

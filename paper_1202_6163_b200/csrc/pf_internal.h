@@ -44,11 +44,13 @@ struct Ws {
     uint64_t* tstatus2;  // [N*T2]    zeroed per call
     uint64_t* G;         // [N*ldg]   a6: inclusive spacings sums G_0..G_P
     uint64_t* Gtot;      // [N]       a6: G_P
+    int32_t* bidx;       // [N*ldb]   multinomial bucket index idx[b] = min{i : Q_i > floor(b Q / NB)}
 };
 
 struct Layout {
     size_t lmax, fstatus, max_part, max_bad, zero_begin, max_cnt, tile_ctr, tstatus, zero_end;
-    size_t tsum, tsum2, Q, Qtot, S, w, o, Qe, freeslot, F, tile_ctr2, tstatus2, G, Gtot, total;
+    size_t tsum, tsum2, Q, Qtot, S, w, o, Qe, freeslot, F, tile_ctr2, tstatus2, G, Gtot, bidx, total;
+    int64_t ldb;  // bucket-index row length NB = 2^ceil(log2 P)
     int cpf_max;  // CTAs per filter of k_max
     int T;        // scan tiles per filter
     int T2;       // spacings-scan tiles per filter (P + 1 values)
@@ -56,7 +58,7 @@ struct Layout {
     int64_t ldg;  // padded spacings row length (P + 1 rounded to 4)
 };
 
-enum Need : unsigned { kNeedQ = 1u, kNeedW = 2u, kNeedPermute = 4u, kNeedG = 8u };
+enum Need : unsigned { kNeedQ = 1u, kNeedW = 2u, kNeedPermute = 4u, kNeedG = 8u, kNeedBuckets = 16u };
 
 Layout make_layout(int32_t N, int32_t P, unsigned need);
 Ws carve(void* base, const Layout& L);

@@ -599,6 +599,109 @@ struct ModeSpacings {
     }
 };
 
+// ============================================================================ a4+a5: multinomial (bucketed)
+// Bucket index of the multinomial search: NB = 2^ceil(log2 P) equal buckets of
+// the 64-bit uniform R; bucket b covers positions [floor(b Q / NB), floor((b+1) Q / NB)]
+// (x = mulhi64(R, Q) is monotone in R), so idx[b] = min{i : Q_i > floor(b Q / NB)}
+// bounds the ancestor of every slot whose R falls in bucket b:
+// idx[b] <= a_k <= idx[b+1].  The index is the merge of those NB sorted values
+// with Q (k_merge<ModeBuckets>).
+struct BucketCtx {
+    int n;
+    uint64_t Qtot;
+    const uint64_t* Q;
+};
+
+struct ModeBuckets {
+    const uint64_t* Q;
+    int64_t ldq;
+    const uint64_t* Qtot;
+    const int32_t* fstatus;
+    int lgNB;
+    int32_t NB;
+    int32_t P;  // particles (the B list)
+    int32_t* idx;
+    int64_t ldb;
+
+    using Ctx = BucketCtx;
+    __device__ Ctx ctx(int n) const { return {n, Qtot[n], Q + static_cast<int64_t>(n) * ldq}; }
+    __device__ bool valid(int n) const { return fstatus[n] == 0; }
+    __device__ int64_t nA(const Ctx&) const { return NB; }
+    __device__ uint64_t x(const Ctx& c, int64_t b) const {
+        return lgNB == 0 ? 0ull : mulhi64(static_cast<uint64_t>(b) << (64 - lgNB), c.Qtot);
+    }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return __ldg(c.Q + i); }
+    __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
+        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        int32_t* dst = idx + static_cast<int64_t>(c.n) * ldb + ka0;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[t] = s_out[t];
+    }
+    __device__ void identity(int, int, int) const {}
+};
+
+// per slot: bucket from the top bits of R_k, then a binary search in the
+// (usually 1-3 particle) range [idx[b], idx[b+1]]; 8 slots per thread.
+__global__ void __launch_bounds__(kThreads) k_bsearch_buckets(int32_t N, int32_t P, Ws ws, int64_t ldq, int64_t ldb,
+                                                              int lgNB, Key key, uint32_t filt0, int32_t* anc,
+                                                              int64_t ld_anc) {
+    const int64_t per_row = cdiv(P, 8);
+    const int64_t total = static_cast<int64_t>(N) * per_row;
+    for (int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < total;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t n = g / per_row;
+        const int64_t kb = (g - n * per_row) * 8;
+        int32_t* arow = anc + n * ld_anc;
+        if (ws.fstatus[n] != 0) {
+            for (int t = 0; t < 8; ++t)
+                if (kb + t < P) arow[kb + t] = static_cast<int32_t>(kb + t);
+            continue;
+        }
+        const uint64_t* Q = ws.Q + n * ldq;
+        const int32_t* bi = ws.bidx + n * ldb;
+        const uint64_t Qtot = ws.Qtot[n];
+        const uint32_t filt = filt0 + static_cast<uint32_t>(n);
+        uint64_t pos[8];
+        int32_t lo[8], hi[8];
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+            const u32x4 r = philox10(static_cast<uint32_t>((kb + t) >> 1), 0u, 1u, filt, key.k0, key.k1);
+            const uint64_t R0 = lo_word(r), R1 = hi_word(r);
+            pos[t] = mulhi64(R0, Qtot);
+            pos[t + 1] = mulhi64(R1, Qtot);
+            const int64_t b0 = lgNB ? static_cast<int64_t>(R0 >> (64 - lgNB)) : 0;
+            const int64_t b1 = lgNB ? static_cast<int64_t>(R1 >> (64 - lgNB)) : 0;
+            lo[t] = __ldg(bi + b0);
+            hi[t] = (b0 + 1 < (int64_t{1} << lgNB)) ? min(__ldg(bi + b0 + 1), P - 1) : P - 1;
+            lo[t + 1] = __ldg(bi + b1);
+            hi[t + 1] = (b1 + 1 < (int64_t{1} << lgNB)) ? min(__ldg(bi + b1 + 1), P - 1) : P - 1;
+        }
+        bool more = true;
+        while (more) {
+            more = false;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (lo[t] < hi[t]) {
+                    const int32_t mid = (lo[t] + hi[t]) >> 1;
+                    if (__ldg(Q + mid) > pos[t]) hi[t] = mid;
+                    else lo[t] = mid + 1;
+                    more |= lo[t] < hi[t];
+                }
+            }
+        }
+        if (kb + 8 <= P && ((reinterpret_cast<uintptr_t>(arow + kb) & 15) == 0)) {
+            int4* dst = reinterpret_cast<int4*>(arow + kb);
+            dst[0] = make_int4(lo[0], lo[1], lo[2], lo[3]);
+            dst[1] = make_int4(lo[4], lo[5], lo[6], lo[7]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (kb + t < P) arow[kb + t] = lo[t];
+        }
+    }
+}
+
 // ============================================================================ a7: Metropolis
 __global__ void __launch_bounds__(kThreads) k_mexp(const float* __restrict__ logw, int64_t ld, int32_t N,
                                                    int32_t P, Ws ws, int64_t ldq) {
@@ -1383,6 +1486,8 @@ Layout make_layout(int32_t N, int32_t P, unsigned need) {
     L.Qe = (need & kNeedPermute) ? take(sizeof(uint32_t) * rows) : 0;
     L.freeslot = (need & kNeedPermute) ? take(sizeof(int32_t) * rows) : 0;
     L.G = (need & kNeedG) ? take(sizeof(uint64_t) * static_cast<size_t>(N) * L.ldg) : 0;
+    L.ldb = int64_t{1} << ceil_log2(P);
+    L.bidx = (need & kNeedBuckets) ? take(sizeof(int32_t) * static_cast<size_t>(N) * L.ldb) : 0;
     L.Gtot = (need & kNeedG) ? take(sizeof(uint64_t) * N) : 0;
     L.total = align_up(off, 256);
     return L;
@@ -1412,6 +1517,7 @@ Ws carve(void* base, const Layout& L) {
     w.tstatus2 = L.tstatus2 ? reinterpret_cast<uint64_t*>(b + L.tstatus2) : nullptr;
     w.G = L.G ? reinterpret_cast<uint64_t*>(b + L.G) : nullptr;
     w.Gtot = L.Gtot ? reinterpret_cast<uint64_t*>(b + L.Gtot) : nullptr;
+    w.bidx = L.bidx ? reinterpret_cast<int32_t*>(b + L.bidx) : nullptr;
     return w;
 }
 
@@ -1462,7 +1568,24 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
                           uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
                           uint64_t* launches) {
     const Key key = make_key(seed);
-    if (scheme == 1) {
+    if (scheme == 1 && ws.bidx) {
+        const int lgNB = ceil_log2(P);
+        const int32_t NB = 1 << lgNB;
+        const int64_t chunk = merge_chunk(N, P);
+        const int cpf = static_cast<int>(cdiv(static_cast<int64_t>(NB) + P, chunk));
+        ModeBuckets md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, lgNB, NB, P, ws.bidx, L.ldb};
+        {
+            ProfScope ps_("k_merge_buckets", s);
+            k_merge<ModeBuckets><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf,
+                                                                                                        chunk);
+        }
+        ++*launches;
+        {
+            ProfScope ps_("k_bsearch", s);
+            k_bsearch_buckets<<<static_cast<unsigned>(grid_for(static_cast<int64_t>(N) * cdiv(P, 8), 8)), kThreads, 0,
+                                s>>>(N, P, ws, L.ldq, L.ldb, lgNB, key, first_filter, anc, ld_anc);
+        }
+    } else if (scheme == 1) {
         const int cpf = static_cast<int>(cdiv(P, kTile));
         { ProfScope ps_("k_bsearch", s); k_bsearch<<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(
             P, cpf, ws, L.ldq, key, first_filter, anc, ld_anc); }
