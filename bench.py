@@ -365,16 +365,44 @@ def run_ours(args):
             ent["gbs"] = alg[name] / (per / 1e3) / 1e9
             ent["frac_hbm"] = ent["gbs"] / hbm
         kernels[name] = ent
+    # committed ncu evidence (DRAM traffic and warp instructions per launch) for this workload
+    evidence = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_kernel_evidence.json")) as f:
+            evidence = json.load(f).get(f"{args.workload}/{scheme}", {})
+    except Exception:
+        evidence = {}
+    # issue roofline: 148 SMs x 4 schedulers x 1 warp-instruction / cycle at the max SM clock
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    issue_peak = sm_count * 4 * 1.965e9 / 1e9  # G warp-instructions / s
+    for name, ent in kernels.items():
+        ev = evidence.get(name)
+        if ev:
+            ent["dram_traffic_bytes_ncu"] = ev["dram_bytes"]
+            ent["warp_inst_ncu"] = ev["warp_inst"]
+            ent["issue_ginst_s"] = ev["warp_inst"] / (ent["avg_ms"] / 1e3) / 1e9
+            ent["frac_issue"] = ent["issue_ginst_s"] / issue_peak
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
     step_kernel_ms = sum(v["avg_ms"] * v["launches_per_step"] for v in kernels.values())
     roofline = None
     if dom:
         d = kernels[dom]
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(d.get("gbs", 0.0), 1), "peak": hbm,
-                    "unit": "GB/s", "frac": round(d.get("frac_hbm", 0.0), 4), "traffic": None,
-                    "alg_bytes_per_launch": d.get("alg_bytes"), "avg_ms": round(d["avg_ms"], 5),
-                    "share_of_step": round(d["avg_ms"] * d["launches_per_step"] / max(step_kernel_ms, 1e-9), 3),
-                    "peak_source": peak_src}
+        share = round(d["avg_ms"] * d["launches_per_step"] / max(step_kernel_ms, 1e-9), 3)
+        if d.get("frac_issue", 0.0) > d.get("frac_hbm", 0.0):
+            # the kernel is bound by instruction issue, not by HBM
+            roofline = {"bound": "alu", "kernel": dom, "achieved": round(d["issue_ginst_s"], 1), "peak": round(issue_peak, 1),
+                        "unit": "G warp-inst/s", "frac": round(d["frac_issue"], 4),
+                        "traffic": d.get("dram_traffic_bytes_ncu"),
+                        "hbm_frac_of_alg_bytes": round(d.get("frac_hbm", 0.0), 4),
+                        "alg_bytes_per_launch": d.get("alg_bytes"), "avg_ms": round(d["avg_ms"], 5),
+                        "share_of_step": share,
+                        "peak_source": f"{sm_count} SMs x 4 schedulers x 1.965 GHz (sm_max_mhz); HBM peak {peak_src}"}
+        else:
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": round(d.get("gbs", 0.0), 1), "peak": hbm,
+                        "unit": "GB/s", "frac": round(d.get("frac_hbm", 0.0), 4),
+                        "traffic": d.get("dram_traffic_bytes_ncu"),
+                        "alg_bytes_per_launch": d.get("alg_bytes"), "avg_ms": round(d["avg_ms"], 5),
+                        "share_of_step": share, "peak_source": peak_src}
 
     extras = {}
     e2e = None
