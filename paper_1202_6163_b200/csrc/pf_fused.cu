@@ -33,11 +33,11 @@ namespace pf {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kFT = 512;           // threads per CTA (2 CTAs / SM)
-constexpr int kFW = kFT / 32;      // 16 warps
+constexpr int kFT = 1024;          // threads per CTA (1 CTA / SM)
+constexpr int kFW = kFT / 32;      // 32 warps
 constexpr int kFI = 16;            // particles per thread
 constexpr int kFR = kFI / 4;       // 4 float4 rows
-constexpr int kPP = kFT * kFI;     // 8192 particles per CTA (max)
+constexpr int kPP = kFT * kFI;     // 16384 particles per CTA (max)
 constexpr int kChunk = 256;        // slots per warp max-scan pass (8 per lane)
 constexpr int kTPL = kFR * kFW / 32;  // (row, warp) totals per lane in the phase-B scan
 static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32 (row, warp) totals");
@@ -119,7 +119,7 @@ __device__ __forceinline__ uint32_t count_below(const Pos& z, uint64_t v) {
 }
 
 template <int SCHEME, bool SUMS, bool PERM>
-__global__ void __launch_bounds__(kFT, 2) k_fused_sorted(FusedArgs a) {
+__global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
     extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
     __shared__ Exchange s_x;
     __shared__ uint32_t s_rf[9];
@@ -624,7 +624,7 @@ struct CoopArgs {
 };
 
 template <int SCHEME, bool SUMS>
-__global__ void __launch_bounds__(kFT, 2) k_coop_sorted(CoopArgs a) {
+__global__ void __launch_bounds__(kFT, 1) k_coop_sorted(CoopArgs a) {
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];
