@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--var", type=float, default=1.0, help="log-weight variance sigma^2")
     ap.add_argument("--D", type=int, default=16, help="state dimension (float32) for the gather")
     ap.add_argument("--strong", action="store_true", help="split a fixed N over ranks (strong scaling)")
+    ap.add_argument("--sorted", action="store_true",
+                    help="c5 with --scheme multinomial: the sorted-uniform multinomial (a6, PF_SORTED)")
     ap.add_argument("--no-extras", action="store_true", help="skip per-scheme / e2e / cpu_baseline extras")
     return ap.parse_args()
 
@@ -162,8 +164,10 @@ def run_c5(args):
     B = args.B if scheme == "metropolis" else 0
     seed = pfinputs.seed_for(0)
 
+    flags = 1 if (args.sorted and scheme == "multinomial") else 0
+
     def step():
-        return resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False)
+        return resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False, flags=flags)
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -194,9 +198,11 @@ def run_c5(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 log-weights / u64 fixed-point scan / int32 indices",
             "data": "synthetic",
             "config": {"workload": desc + f", P_global={P_global}, sigma^2={args.var}, scheme={scheme}"
+                                  + (" (sorted-uniform, a6)" if flags else "")
                                   + (f", B={B}" if scheme == "metropolis" else ""),
                        "parallelism": f"particle-sharded x{world}: all_reduce(MAX) + all_gather(totals)"
-                                      + (" + all_gather(weights)" if scheme == "metropolis" else ""),
+                                      + (" + all_gather(weights)" if scheme == "metropolis" else "")
+                                      + (" + all_gather(spacing totals)" if flags else ""),
                        "l2": "inputs larger than L2 (logw 128 MiB/GPU, Q 256 MiB/GPU)"},
             "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks,
         }))

@@ -95,7 +95,7 @@ typedef struct {
                               permutation of the ancestors (NS-15, = pf_permute(ancestors));
                               fused into the cluster kernel (P <= 65536), otherwise computed
                               from the offspring after the search                           */
-    void* workspace;       /* device, nullable -> library pool                              */
+    void* workspace;       /* device, 256-byte aligned, nullable -> library pool            */
     size_t workspace_bytes;
 } pf_opts;
 
@@ -222,6 +222,36 @@ pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int
                           const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
                           const int32_t* d_gbad, uint64_t seed, uint32_t filter_index, int32_t* anc_out,
                           int64_t* d_slot_range, pf_stream_t stream);
+/*
+ * Sorted-uniform multinomial (a6, NS-12) over shards: work-optimal.
+ * The P_global + 1 spacings e_0..e_P are split into nshards contiguous SPACING
+ * shards [s_h, s_{h+1}), s_h = min(P+1, h * ceil((P+1)/nshards)) (independent of
+ * the particle shards' sizes).  Stages after pf_shard_scan:
+ *   2b pf_shard_spacings_total -> all_gather of the 8-byte spacing totals
+ *   3  pf_shard_search_sorted
+ * Bit-identical to pf_resample_ex(PF_MULTINOMIAL, flags = PF_SORTED) on the whole filter.
+ */
+/* d_etotal[0] (device) = e_{s_h} + ... + e_{s_{h+1}-1} for h = shard (NS-12 e_k from
+ * Philox tag 5 of filter_index and seed).  0 <= shard < nshards. */
+pf_status pf_shard_spacings_total(int64_t P_global, int32_t nshards, int32_t shard, uint64_t seed,
+                                  uint32_t filter_index, uint64_t* d_etotal, pf_stream_t stream);
+/* Bytes of device workspace pf_shard_search_sorted needs (8 (P_global + P_global / 4096) + 1 KiB:
+ * the scanned G range is at most P_global slots, e.g. when one shard holds all the weight). */
+size_t pf_shard_search_sorted_workspace_bytes(int64_t P_global);
+/* Sorted multinomial ancestors of the slots whose positions x_k = floor(G_k Q / G_P)
+ * fall in this particle shard's range [off, off + T) of the cumulative weights.
+ * d_totals[nshards] / d_etotals[nshards]: all-gathered pf_shard_scan totals and
+ * pf_shard_spacings_total values (device).  The shard regenerates and scans only the
+ * spacing shards containing its slots (the plan is computed on the device), then
+ * merges the positions with d_Q.  anc_out (P_global entries, device) receives the
+ * global ancestor of each of its slots; d_slot_range[0..1] = [k_lo, k_hi).
+ * workspace: device, 256-byte aligned, >= pf_shard_search_sorted_workspace_bytes, or NULL for the
+ * library pool.  Invalid global filter: identity for slots [p0, p0 + Pl). */
+pf_status pf_shard_search_sorted(const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                 const uint64_t* d_totals, const uint64_t* d_etotals, int32_t nshards, int32_t shard,
+                                 const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                                 int32_t* anc_out, int64_t* d_slot_range, void* workspace, size_t workspace_bytes,
+                                 pf_stream_t stream);
 /* Metropolis weights of the shard: w_out[Pl] = dexp(logw - *d_gmax) (NS-4). */
 pf_status pf_shard_weights(const float* logw, int32_t Pl, const float* d_gmax, float* w_out, pf_stream_t stream);
 /* Metropolis chains (NS-11) for slots [slot0, slot0 + nslots) of a filter whose

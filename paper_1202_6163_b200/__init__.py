@@ -69,6 +69,10 @@ _SIGS = {
     "pf_shard_scan": ([_V, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
     "pf_shard_search": ([ctypes.c_int, _V, _I32, _I64, _I64, _V, _I32, _I32, _V, _V, _U64, _U32, _V, _V, _V],
                         ctypes.c_int),
+    "pf_shard_spacings_total": ([_I64, _I32, _I32, _U64, _U32, _V, _V], ctypes.c_int),
+    "pf_shard_search_sorted_workspace_bytes": ([_I64], _SZ),
+    "pf_shard_search_sorted": ([_V, _I32, _I64, _I64, _V, _V, _I32, _I32, _V, _V, _U64, _U32, _V, _V, _V, _SZ, _V],
+                               ctypes.c_int),
     "pf_shard_weights": ([_V, _I32, _V, _V, _V], ctypes.c_int),
     "pf_metropolis_from_weights": ([_V, _I64, _I64, _I32, _U64, _I32, _U32, _V, _V, _V, _V], ctypes.c_int),
     "pf_lg_init": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, _U64, _V], ctypes.c_int),
@@ -376,6 +380,35 @@ def pf_shard_search(scheme, Q, p0: int, P_global: int, totals, shard: int, gmax,
                                  totals.shape[0], shard, gmax.data_ptr(), gbad.data_ptr(), seed & (2 ** 64 - 1),
                                  filter_index, anc_out.data_ptr(), rng.data_ptr(), _stream(Q, stream)),
            "pf_shard_search")
+    return rng
+
+
+def pf_shard_spacings_total(P_global: int, nshards: int, shard: int, seed: int, filter_index: int, device,
+                            stream=None):
+    """Stage 2b (sorted multinomial, NS-12): etotal[1] (u64 as int64) = sum of the spacings
+    e_k over spacing shard ``shard`` of ``nshards`` (include/pf.h)."""
+    torch = _torch()
+    et = torch.empty(1, dtype=torch.int64, device=device)
+    _check(lib().pf_shard_spacings_total(P_global, nshards, shard, seed & (2 ** 64 - 1), filter_index,
+                                         et.data_ptr(), _stream(et, stream)), "pf_shard_spacings_total")
+    return et
+
+
+def pf_shard_search_sorted_workspace_bytes(P_global: int) -> int:
+    return int(lib().pf_shard_search_sorted_workspace_bytes(P_global))
+
+
+def pf_shard_search_sorted(Q, p0: int, P_global: int, totals, etotals, shard: int, gmax, gbad, seed: int,
+                           filter_index: int, anc_out, workspace=None, stream=None):
+    """Stage 3 of the sharded sorted multinomial: writes anc_out[k] (int32 [P_global]) for this
+    shard's slots; returns slot_range[2] (int64).  workspace: optional uint8 device tensor."""
+    torch = _torch()
+    rng = torch.zeros(2, dtype=torch.int64, device=Q.device)
+    wp, wb = (workspace.data_ptr(), workspace.numel() * workspace.element_size()) if workspace is not None else (None, 0)
+    _check(lib().pf_shard_search_sorted(Q.data_ptr(), Q.shape[0], p0, P_global, totals.data_ptr(),
+                                        etotals.data_ptr(), totals.shape[0], shard, gmax.data_ptr(), gbad.data_ptr(),
+                                        seed & (2 ** 64 - 1), filter_index, anc_out.data_ptr(), rng.data_ptr(), wp,
+                                        wb, _stream(Q, stream)), "pf_shard_search_sorted")
     return rng
 
 

@@ -56,7 +56,8 @@ pf_status pool_get(size_t bytes, cudaStream_t s, void** out) {
 
 pf_status get_workspace(const pf_opts* opts, size_t bytes, cudaStream_t s, void** out) {
     if (opts && opts->workspace) {
-        if (opts->workspace_bytes < bytes) return PF_ERR_WORKSPACE;
+        if (opts->workspace_bytes < bytes || (reinterpret_cast<uintptr_t>(opts->workspace) & 255) != 0)
+            return PF_ERR_WORKSPACE;
         *out = opts->workspace;
         return PF_OK;
     }
@@ -433,6 +434,49 @@ pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int
     uint64_t nl = 0;
     const cudaError_t e = pf::launch_shard_search(scheme, d_Q, Pl, p0, P_global, d_totals, nshards, shard, d_gmax,
                                                   d_gbad, seed, filter_index, anc_out, d_slot_range, ctx, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_spacings_total(int64_t P_global, int32_t nshards, int32_t shard, uint64_t seed,
+                                  uint32_t filter_index, uint64_t* d_etotal, pf_stream_t stream) {
+    if (!d_etotal || P_global < 1 || P_global > INT32_MAX || nshards < 1 || shard < 0 || shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_spacings_total(P_global, nshards, shard, seed, filter_index, d_etotal,
+                                                    static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+size_t pf_shard_search_sorted_workspace_bytes(int64_t P_global) {
+    if (P_global < 1 || P_global > INT32_MAX) return 0;
+    return pf::spac_shard_workspace_bytes(P_global);
+}
+
+pf_status pf_shard_search_sorted(const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                 const uint64_t* d_totals, const uint64_t* d_etotals, int32_t nshards, int32_t shard,
+                                 const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                                 int32_t* anc_out, int64_t* d_slot_range, void* workspace, size_t workspace_bytes,
+                                 pf_stream_t stream) {
+    if (!d_Q || !d_totals || !d_etotals || !d_gmax || !d_gbad || !anc_out || !d_slot_range)
+        return PF_ERR_INVALID_ARG;
+    if (Pl < 1 || p0 < 0 || P_global < p0 + Pl || P_global > INT32_MAX || nshards < 1 || shard < 0 ||
+        shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t need = pf::spac_shard_workspace_bytes(P_global);
+    void* ws = workspace;
+    if (ws) {
+        if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255) != 0) return PF_ERR_WORKSPACE;
+    } else {
+        const pf_status st = pool_get(need, s, &ws);
+        if (st != PF_OK) return st;
+    }
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_shard_search_sorted(d_Q, Pl, p0, P_global, d_totals, d_etotals, nshards, shard,
+                                                         d_gmax, d_gbad, seed, filter_index, anc_out, d_slot_range,
+                                                         ws, s, &nl);
     g_launches += nl;
     return cuda_status(e);
 }

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
     __shared__ int s_bad;
     __shared__ uint64_t s_off, s_tot, s_Qtot;
     __shared__ double s_S, s_S2;
-    __shared__ uint32_t s_klo, s_khi;
+    __shared__ uint32_t s_klo;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int c = static_cast<int>(cluster.block_rank());
@@ -362,12 +362,9 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
             }
             if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
         }
-        if (tid == 0) {
-            s_klo = count_below<SCHEME>(z, O);
-            s_khi = count_below<SCHEME>(z, O + s_tot);
-        }
+        if (tid == 0) s_klo = count_below<SCHEME>(z, O);
         __syncthreads();
-        const uint32_t k_lo = s_klo, k_hi = s_khi;
+        const uint32_t k_lo = s_klo;
         // E_{i-1} of the first particle of each 4-chunk (natural order: row j, warp, lane, q);
         // the other three predecessors are the chunk's own E values.
         uint32_t first[kFR];
@@ -634,7 +631,6 @@ __global__ void __launch_bounds__(kFT, 1) k_coop_sorted(CoopArgs a) {
     __shared__ float s_lmax;
     __shared__ int s_bad;
     __shared__ uint64_t s_u64[4];
-    __shared__ double s_S, s_S2;
     __shared__ uint32_t s_prevE;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1069,7 +1065,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(SmallArgs a) {
         for (int t = 0; t < 8; ++t) out[t] = 0;
     } else if (a.sorted) {
         // a6: spacings e_0..e_P (P + 1 <= 257 values) scanned by the warp, 9 per lane
-        uint64_t* G = s_q[warp] + 0;  // reuse after Q? no: Q still needed -> separate registers
         uint64_t e[9], gl = 0;
 #pragma unroll
         for (int t = 0; t < 9; ++t) {
@@ -1092,7 +1087,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(SmallArgs a) {
             gr += e[t];
             xk[t] = muldiv_floor(gr, Qtot, GP);  // only used for k < P (G_k < G_P)
         }
-        (void)G;
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
             const int k = lane * 8 + t;         // slot owned by this lane

@@ -10,8 +10,6 @@ namespace pf {
 constexpr int kThreads = 256;           // every kernel: 8 warps
 constexpr int kItems = 16;              // items per thread in scan / merge tiles
 constexpr int kTile = kThreads * kItems;  // 4096 particles per scan tile
-constexpr int kMergeItems = kTile;      // merged (slot + particle) items per merge CTA
-constexpr int kSplitters = 4096;        // smem splitters of the multinomial search
 
 // Per-kernel event tracing (pf_profile_enable); a no-op unless enabled.
 struct ProfScope {
@@ -108,6 +106,15 @@ cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, 
                                int32_t B, uint32_t filt, const float* gmax, const int32_t* gbad, int32_t* anc,
                                cudaStream_t s, uint64_t* launches);
 size_t shard_ctx_bytes();
+// a6 (sorted multinomial) shards.
+cudaError_t launch_spacings_total(int64_t P_global, int nshards, int shard, uint64_t seed, uint32_t filt,
+                                  uint64_t* etot, cudaStream_t s, uint64_t* launches);
+size_t spac_shard_workspace_bytes(int64_t P_global);
+cudaError_t launch_shard_search_sorted(const uint64_t* Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                       const uint64_t* totals, const uint64_t* etotals, int nshards, int shard,
+                                       const float* gmax, const int32_t* gbad, uint64_t seed, uint32_t filt,
+                                       int32_t* anc, int64_t* range_out, void* ws, cudaStream_t s,
+                                       uint64_t* launches);
 
 // C4 demo model (linear-Gaussian bootstrap filter).
 cudaError_t launch_lg_init(float* X, int64_t ld, int32_t P, int32_t D, float phi, float sigma_x, uint64_t seed,

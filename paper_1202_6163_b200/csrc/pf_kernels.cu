@@ -6,7 +6,7 @@
 //                                                                    HBM 4 B in + 8 B out
 //   k_merge     a4+a5   merge-path search of sorted positions (stratified / systematic)
 //                                                                    HBM 8 B in + 4 B out
-//   k_bsearch   a4+a5   per-slot search of i.i.d. positions (multinomial)
+//   k_merge<ModeBuckets> + k_bsearch_buckets  a4+a5  multinomial (bucket index + short per-slot searches)
 //   k_mexp/k_metro a7   Metropolis: weights once, then B-step chains (no collective)
 //   k_hist      a8      ancestors -> offspring (warp-aggregated atomics)
 //   k_pscan+k_merge a9  canonical in-place permutation
@@ -409,76 +409,6 @@ __global__ void __launch_bounds__(kThreads) k_merge(Mode md, int cpf, int64_t ch
         ka += a_end;
         ib += b_end;
         __syncthreads();
-    }
-}
-
-// ============================================================================ a4+a5: multinomial
-// 8 slots per thread searched in lockstep: every step of the smem and global
-// binary searches issues 8 independent loads (fixed trip counts, no divergence).
-constexpr int kBS = 8;
-__global__ void __launch_bounds__(kThreads) k_bsearch(int32_t P, int cpf, Ws ws, int64_t ldq, Key key,
-                                                      uint32_t filt0, int32_t* anc, int64_t ld_anc) {
-    __shared__ uint64_t spl[kSplitters];
-    const int n = blockIdx.x / cpf;
-    const int cb = blockIdx.x - n * cpf;
-    const int64_t k0 = static_cast<int64_t>(cb) * kTile;
-    const int64_t k1 = min(static_cast<int64_t>(P), k0 + kTile);
-    int32_t* arow = anc + static_cast<int64_t>(n) * ld_anc;
-    if (ws.fstatus[n] != 0) {
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) arow[k] = static_cast<int32_t>(k);
-        return;
-    }
-    const uint64_t* Q = ws.Q + static_cast<int64_t>(n) * ldq;
-    const uint64_t Qtot = ws.Qtot[n];
-    const int64_t chunk = cdiv(P, kSplitters);
-    const int nspl = static_cast<int>(cdiv(P, chunk));
-    for (int s = threadIdx.x; s < nspl; s += kThreads) spl[s] = __ldg(Q + min((s + 1) * chunk, int64_t{P}) - 1);
-    __syncthreads();
-    const uint32_t filt = filt0 + static_cast<uint32_t>(n);
-    const bool vec = ((reinterpret_cast<uintptr_t>(arow) & 15) == 0);
-    for (int64_t kb = k0 + kBS * threadIdx.x; kb < k1; kb += kBS * kThreads) {
-        uint64_t pos[kBS];
-#pragma unroll
-        for (int t = 0; t < kBS; t += 2) {
-            const u32x4 r = philox10(static_cast<uint32_t>((kb + t) >> 1), 0u, 1u, filt, key.k0, key.k1);
-            pos[t] = mulhi64(lo_word(r), Qtot);
-            pos[t + 1] = mulhi64(hi_word(r), Qtot);
-        }
-        // splitter level: first s with spl[s] > pos (spl[nspl-1] = Qtot > pos)
-        int lo[kBS];
-#pragma unroll
-        for (int t = 0; t < kBS; ++t) lo[t] = 0;
-        for (int len = nspl; len > 1;) {
-            const int half = len >> 1;
-#pragma unroll
-            for (int t = 0; t < kBS; ++t) lo[t] += (spl[lo[t] + half - 1] <= pos[t]) ? half : 0;
-            len -= half;
-        }
-        // global level inside [lo*chunk, lo*chunk + chunk), entries >= P act as +inf
-        int64_t g[kBS];
-#pragma unroll
-        for (int t = 0; t < kBS; ++t) g[t] = static_cast<int64_t>(lo[t]) * chunk;
-        for (int64_t len = chunk; len > 1;) {
-            const int64_t half = len >> 1;
-#pragma unroll
-            for (int t = 0; t < kBS; ++t) {
-                const int64_t idx = g[t] + half - 1;
-                const bool le = (idx < P) && (__ldg(Q + min(idx, static_cast<int64_t>(P) - 1)) <= pos[t]);
-                g[t] += le ? half : 0;
-            }
-            len -= half;
-        }
-        if (vec && kb + kBS <= k1) {
-            int4* dst = reinterpret_cast<int4*>(arow + kb);
-            dst[0] = make_int4(static_cast<int32_t>(g[0]), static_cast<int32_t>(g[1]), static_cast<int32_t>(g[2]),
-                               static_cast<int32_t>(g[3]));
-            dst[1] = make_int4(static_cast<int32_t>(g[4]), static_cast<int32_t>(g[5]), static_cast<int32_t>(g[6]),
-                               static_cast<int32_t>(g[7]));
-        } else {
-#pragma unroll
-            for (int t = 0; t < kBS; ++t)
-                if (kb + t < k1) arow[kb + t] = static_cast<int32_t>(g[t]);
-        }
     }
 }
 
@@ -1360,6 +1290,256 @@ __global__ void __launch_bounds__(kThreads) k_metro_slots(const float* __restric
     anc[s] = static_cast<int32_t>(k);
 }
 
+// ============================================================================ a6 shards (C5 sorted multinomial)
+// SURVEY §8(e) "Giant filter: sorted multinomial": the P + 1 spacings e_0..e_P
+// (NS-12) are split into nshards contiguous spacing shards [s_h, s_{h+1}),
+// s_h = min(P + 1, h * ceil((P + 1) / nshards)); rank h contributes the total of
+// its spacing shard, the totals are all-gathered, so every rank knows
+// G_{s_h - 1} = sum_{h' < h} etot_h' and G_P = sum of all.  Rank g's slots are
+// those with x_k = floor(G_k Q / G_P) in [off_g, off_g + T_g); it regenerates
+// and scans only the spacing shards that contain them.
+__device__ __forceinline__ uint64_t spacing_at(int64_t k, uint32_t filt, Key key) {
+    const u32x4 r = philox10(static_cast<uint32_t>(k >> 2), 0u, 5u, filt, key.k0, key.k1);
+    const int c = static_cast<int>(k & 3);
+    return spacing_from_word(c == 0 ? r.x : c == 1 ? r.y : c == 2 ? r.z : r.w);
+}
+
+__host__ __device__ __forceinline__ int64_t spacing_shard_begin(int64_t P, int nshards, int h) {
+    const int64_t per = (P + 1 + nshards - 1) / nshards;
+    return min(P + 1, static_cast<int64_t>(h) * per);
+}
+
+// sum of e_k over k in [k0, k1) into *etot (zeroed by the caller; integer atomics: order-free)
+__global__ void __launch_bounds__(kThreads) k_spacings_total(int64_t k0, int64_t k1, Key key, uint32_t filt,
+                                                             unsigned long long* etot) {
+    __shared__ uint64_t s_w[kThreads / 32];
+    uint64_t sum = 0;
+    const int64_t g0 = k0 >> 2, g1 = (k1 + 3) >> 2;  // groups of 4 spacings (one Philox call)
+    for (int64_t g = g0 + blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; g < g1;
+         g += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const u32x4 r = philox10(static_cast<uint32_t>(g), 0u, 5u, filt, key.k0, key.k1);
+        const uint32_t w4[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t k = 4 * g + c;
+            if (k >= k0 && k < k1) sum += spacing_from_word(w4[c]);
+        }
+    }
+    sum = warp_sum_u64(sum);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) s_w[warp] = sum;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t v = (lane < kThreads / 32) ? s_w[lane] : 0ull;
+        v = warp_sum_u64(v);
+        if (lane == 0 && v) atomicAdd(etot, static_cast<unsigned long long>(v));
+    }
+}
+
+struct SpacShardDev {
+    int64_t sa, sb;       // scanned slot range [sa, sb): G_ws[k - sa] = G_k
+    int64_t hlo[2];       // spacing shard holding the crossing of off and off + T
+    int64_t k_lo, k_hi;   // this rank's slots
+    uint64_t off, Qtot, T, GP, Gbase;
+    uint64_t ntiles;
+    int32_t invalid;
+};
+
+// a * b < c * d for u64 operands (exact 128-bit products)
+__device__ __forceinline__ bool lt128(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    const uint64_t h1 = __umul64hi(a, b), h2 = __umul64hi(c, d);
+    return h1 < h2 || (h1 == h2 && a * b < c * d);
+}
+
+// One warp: offsets, G at the spacing-shard boundaries, and the range of spacing
+// shards to scan.  crossing shard of v: h(v) = max{h : h == 0 or G_{s_h - 1} Q < v G_P}
+// (every slot before s_h has x < v; the first slot with x >= v lies in [s_h, s_{h+1}]).
+__global__ void k_spac_shard_plan(const uint64_t* totals, const uint64_t* etotals, int nshards, int shard,
+                                  const float* gmax, const int32_t* gbad, int64_t P, SpacShardDev* ctx) {
+    if (threadIdx.x != 0) return;
+    uint64_t off = 0, Qt = 0, GP = 0;
+    for (int h = 0; h < nshards; ++h) {
+        if (h < shard) off += totals[h];
+        Qt += totals[h];
+        GP += etotals[h];
+    }
+    const uint64_t T = totals[shard];
+    const int invalid = (*gbad != 0 || *gmax == -INFINITY) ? 1 : 0;
+    int64_t hv[2];
+    for (int w = 0; w < 2; ++w) {
+        const uint64_t v = w ? off + T : off;
+        int hb = 0;
+        uint64_t Gb = 0;  // G_{s_h - 1}
+        for (int h = 1; h < nshards; ++h) {
+            Gb += etotals[h - 1];
+            if (spacing_shard_begin(P, nshards, h) < P && lt128(Gb, Qt, v, GP)) hb = h;
+        }
+        hv[w] = hb;
+    }
+    uint64_t Gbase = 0;
+    for (int h = 0; h < hv[0]; ++h) Gbase += etotals[h];
+    const int64_t sa = spacing_shard_begin(P, nshards, static_cast<int>(hv[0]));
+    const int64_t sb = min(P, spacing_shard_begin(P, nshards, static_cast<int>(hv[1]) + 1));
+    ctx->sa = sa;
+    ctx->sb = (invalid || T == 0) ? sa : max(sa, sb);
+    ctx->hlo[0] = hv[0];
+    ctx->hlo[1] = hv[1];
+    ctx->off = off;
+    ctx->Qtot = Qt;
+    ctx->T = T;
+    ctx->GP = GP;
+    ctx->Gbase = Gbase;
+    ctx->ntiles = static_cast<uint64_t>(cdiv(ctx->sb - ctx->sa, kTile));
+    ctx->invalid = invalid;
+    ctx->k_lo = ctx->k_hi = 0;
+}
+
+// Persistent decoupled-lookback scan of e_k over [sa, sb) (the plan's range, read on
+// the device): G_ws[k - sa] = Gbase + e_sa + ... + e_k.  Tiles are taken in order from a
+// global counter, so a CTA only ever waits on tiles held by running CTAs.
+__global__ void __launch_bounds__(kThreads, 4) k_gscan_range(const SpacShardDev* ctx, Key key, uint32_t filt,
+                                                             uint32_t* tile_ctr, uint64_t* status, uint64_t* G) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_wtot[kThreads / 32];
+    __shared__ uint64_t s_off[kThreads / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t sa = ctx->sa, len = ctx->sb - ctx->sa;
+    const uint64_t ntiles = ctx->ntiles, Gbase = ctx->Gbase;
+    for (;;) {
+        if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (static_cast<uint64_t>(tile) >= ntiles) break;
+        const int64_t base = tile * kTile + warp * 512;  // relative to sa
+        uint64_t v[16];
+        uint64_t excl[4];
+        uint64_t carry = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i0 = base + r * 128 + lane * 4;
+            uint64_t loc = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                v[r * 4 + c] = (i0 + c < len) ? spacing_at(sa + i0 + c, filt, key) : 0ull;
+                loc += v[r * 4 + c];
+            }
+            const uint64_t incl = warp_incl_scan_u64(loc, lane);
+            excl[r] = incl - loc + carry;
+            carry += __shfl_sync(kFull, incl, 31);
+        }
+        if (lane == 0) s_wtot[warp] = carry;
+        __syncthreads();
+        if (warp == 0) {
+            const uint64_t wv = (lane < kThreads / 32) ? s_wtot[lane] : 0ull;
+            const uint64_t wi = warp_incl_scan_u64(wv, lane);
+            const uint64_t agg = __shfl_sync(kFull, wi, kThreads / 32 - 1);
+            uint64_t prefix = 0;
+            if (tile == 0) {
+                if (lane == 0) st_release(status, kFlagInc | agg);
+            } else {
+                if (lane == 0) st_release(status + tile, kFlagAgg | agg);
+                prefix = lookback(status, tile, lane);
+                if (lane == 0) st_release(status + tile, kFlagInc | (prefix + agg));
+            }
+            if (lane < kThreads / 32) s_off[lane] = prefix + wi - wv;
+        }
+        __syncthreads();
+        const uint64_t off = Gbase + s_off[warp];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i0 = base + r * 128 + lane * 4;
+            uint64_t run = off + excl[r];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                run += v[r * 4 + c];
+                if (i0 + c < len) G[i0 + c] = run;
+            }
+        }
+    }
+}
+
+// One warp: k(v) = #{k < P : G_k Q < v G_P} for v = off, off + T, searching the scanned
+// crossing shard (32-ary search over G_ws).
+__global__ void k_spac_shard_range(SpacShardDev* ctx, const uint64_t* G, int64_t P, int nshards,
+                                   int64_t* range_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sa = ctx->sa, sb = ctx->sb;
+    const uint64_t Qt = ctx->Qtot, GP = ctx->GP;
+    int64_t kk[2];
+    for (int w = 0; w < 2; ++w) {
+        const uint64_t v = w ? ctx->off + ctx->T : ctx->off;
+        const int h = static_cast<int>(ctx->hlo[w]);
+        // every k < s_h is below v; the crossing is in [s_h, min(s_{h+1}, P)]
+        int64_t lo = max(sa, spacing_shard_begin(P, nshards, h));
+        int64_t hi = min(sb, spacing_shard_begin(P, nshards, h + 1));
+        hi = max(lo, hi);
+        while (hi > lo) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t m = lo + lane * step;
+            const bool p = (m < hi) && lt128(G[m - sa], Qt, v, GP);
+            const int L = __popc(__ballot_sync(kFull, p));
+            const int64_t nlo = (L == 0) ? lo : lo + static_cast<int64_t>(L - 1) * step + 1;
+            const int64_t mL = lo + static_cast<int64_t>(L) * step;
+            hi = (mL < hi) ? mL : hi;
+            lo = nlo;
+        }
+        kk[w] = lo;
+    }
+    if (lane == 0) {
+        const bool empty = ctx->invalid || ctx->T == 0;
+        ctx->k_lo = empty ? 0 : kk[0];
+        ctx->k_hi = empty ? 0 : kk[1];
+        range_out[0] = ctx->k_lo;
+        range_out[1] = ctx->k_hi;
+    }
+}
+
+struct SpacShardCtx {
+    int n;
+    int64_t k_lo, nA, sa;
+    uint64_t off, Qtot, GP;
+};
+
+struct ModeShardSpacings {
+    const uint64_t* Q;
+    const SpacShardDev* dctx;
+    const uint64_t* G;
+    int32_t P;  // particles of this shard (the B list)
+    int64_t p0;
+    int32_t* anc;
+
+    using Ctx = SpacShardCtx;
+    __device__ Ctx ctx(int) const {
+        Ctx c;
+        c.n = 0;
+        c.k_lo = dctx->k_lo;
+        c.nA = dctx->k_hi - dctx->k_lo;
+        c.sa = dctx->sa;
+        c.off = dctx->off;
+        c.Qtot = dctx->Qtot;
+        c.GP = dctx->GP;
+        return c;
+    }
+    __device__ bool valid(int) const { return dctx->invalid == 0; }
+    __device__ int64_t nA(const Ctx& c) const { return c.nA; }
+    __device__ uint64_t x(const Ctx& c, int64_t m) const {
+        return muldiv_floor(__ldg(G + (c.k_lo + m - c.sa)), c.Qtot, c.GP);
+    }
+    __device__ uint64_t b(const Ctx& c, int64_t i) const { return c.off + __ldg(Q + i); }
+    __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
+        for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
+    }
+    __device__ void emit(const Ctx& c, int64_t ka0, int na, const int32_t* s_out) const {
+        int32_t* dst = anc + c.k_lo + ka0;
+        for (int t = threadIdx.x; t < na; t += kThreads) dst[t] = static_cast<int32_t>(p0 + s_out[t]);
+    }
+    __device__ void identity(int, int cb, int cpf) const {
+        const int64_t per = cdiv(P, cpf);
+        const int64_t b0 = cb * per, b1 = min(static_cast<int64_t>(P), b0 + per);
+        for (int64_t k = b0 + threadIdx.x; k < b1; k += kThreads) anc[p0 + k] = static_cast<int32_t>(p0 + k);
+    }
+};
+
 // ============================================================================ C4 demo model
 __device__ __forceinline__ void box_muller4(const u32x4& r, float z[4]) {
     const float k = 2.3283064365386963e-10f;  // 2^-32
@@ -1568,7 +1748,7 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
                           uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
                           uint64_t* launches) {
     const Key key = make_key(seed);
-    if (scheme == 1 && ws.bidx) {
+    if (scheme == 1) {
         const int lgNB = ceil_log2(P);
         const int32_t NB = 1 << lgNB;
         const int64_t chunk = merge_chunk(N, P);
@@ -1585,10 +1765,6 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
             k_bsearch_buckets<<<static_cast<unsigned>(grid_for(static_cast<int64_t>(N) * cdiv(P, 8), 8)), kThreads, 0,
                                 s>>>(N, P, ws, L.ldq, L.ldb, lgNB, key, first_filter, anc, ld_anc);
         }
-    } else if (scheme == 1) {
-        const int cpf = static_cast<int>(cdiv(P, kTile));
-        { ProfScope ps_("k_bsearch", s); k_bsearch<<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(
-            P, cpf, ws, L.ldq, key, first_filter, anc, ld_anc); }
     } else {
         const int64_t chunk = merge_chunk(N, P);
         const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
@@ -1788,6 +1964,82 @@ cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, 
 }
 
 size_t shard_ctx_bytes() { return sizeof(ShardCtxDev); }
+
+// ---------------------------------------------------------------- a6 shard launchers
+cudaError_t launch_spacings_total(int64_t P_global, int nshards, int shard, uint64_t seed, uint32_t filt,
+                                  uint64_t* etot, cudaStream_t s, uint64_t* launches) {
+    const int64_t k0 = spacing_shard_begin(P_global, nshards, shard);
+    const int64_t k1 = spacing_shard_begin(P_global, nshards, shard + 1);
+    cudaError_t e = cudaMemsetAsync(etot, 0, sizeof(uint64_t), s);
+    if (e != cudaSuccess || k1 <= k0) return e;
+    const int64_t groups = ((k1 + 3) >> 2) - (k0 >> 2);
+    {
+        ProfScope ps_("k_spacings_total", s);
+        k_spacings_total<<<static_cast<unsigned>(grid_for(groups, 8)), kThreads, 0, s>>>(
+            k0, k1, make_key(seed), filt, reinterpret_cast<unsigned long long*>(etot));
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+struct SpacShardLayout {
+    size_t ctx, ctr, status, G, zero_begin, zero_end, total;
+};
+
+static SpacShardLayout spac_shard_layout(int64_t P_global) {
+    SpacShardLayout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    L.ctx = take(sizeof(SpacShardDev));
+    L.zero_begin = off;
+    L.ctr = take(sizeof(uint32_t));
+    L.status = take(sizeof(uint64_t) * static_cast<size_t>(cdiv(P_global, kTile)));
+    L.zero_end = off;
+    L.G = take(sizeof(uint64_t) * static_cast<size_t>(P_global));
+    L.total = off;
+    return L;
+}
+
+size_t spac_shard_workspace_bytes(int64_t P_global) { return spac_shard_layout(P_global).total; }
+
+cudaError_t launch_shard_search_sorted(const uint64_t* Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                       const uint64_t* totals, const uint64_t* etotals, int nshards, int shard,
+                                       const float* gmax, const int32_t* gbad, uint64_t seed, uint32_t filt,
+                                       int32_t* anc, int64_t* range_out, void* ws, cudaStream_t s,
+                                       uint64_t* launches) {
+    const SpacShardLayout L = spac_shard_layout(P_global);
+    char* b = static_cast<char*>(ws);
+    SpacShardDev* dctx = reinterpret_cast<SpacShardDev*>(b + L.ctx);
+    uint64_t* G = reinterpret_cast<uint64_t*>(b + L.G);
+    const Key key = make_key(seed);
+    cudaError_t e = cudaMemsetAsync(b + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
+    if (e != cudaSuccess) return e;
+    { ProfScope ps_("k_spac_shard_plan", s); k_spac_shard_plan<<<1, 32, 0, s>>>(totals, etotals, nshards, shard, gmax, gbad, P_global, dctx); }
+    ++*launches;
+    {
+        ProfScope ps_("k_gscan_range", s);
+        const int64_t grid = std::min<int64_t>(static_cast<int64_t>(sm_count()) * 4, std::max<int64_t>(1, cdiv(P_global, kTile)));
+        k_gscan_range<<<static_cast<unsigned>(grid), kThreads, 0, s>>>(dctx, key, filt,
+                                                                      reinterpret_cast<uint32_t*>(b + L.ctr),
+                                                                      reinterpret_cast<uint64_t*>(b + L.status), G);
+    }
+    ++*launches;
+    { ProfScope ps_("k_spac_shard_range", s); k_spac_shard_range<<<1, 32, 0, s>>>(dctx, G, P_global, nshards, range_out); }
+    ++*launches;
+    const int64_t chunk = merge_chunk(1, static_cast<int32_t>(std::min<int64_t>(P_global, INT32_MAX / 2)));
+    const int cpf = static_cast<int>(cdiv(P_global + Pl, chunk));
+    ModeShardSpacings md{Q, dctx, G, Pl, p0, anc};
+    {
+        ProfScope ps_("k_merge", s);
+        k_merge<ModeShardSpacings><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
 
 cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
                                       uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,

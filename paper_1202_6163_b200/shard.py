@@ -10,6 +10,10 @@ into a per-GPU scan plus an 8-byte-per-rank exchange):
                        search: every rank computes its own slot range from the
                        totals (positions are functions of the slot index) and
                        writes the ancestors of those slots.
+  sorted multinomial   (a6, ``flags=PF_SORTED``) additionally all-gathers the
+                       8-byte totals of the exponential spacings of each
+                       spacing shard; each rank then regenerates
+                       only the spacing shards that hold its slots.
   Metropolis:          max  -> all_reduce(MAX); weights -> all_gather of the
                        weight vector; chains for the rank's own slots
                        (no collective inside the resampler).
@@ -26,6 +30,7 @@ from __future__ import annotations
 import math
 
 SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
+PF_SORTED = 1
 
 
 def shard_range(P_global: int, world: int, rank: int):
@@ -88,6 +93,13 @@ class GpuStages:
         return self.pf.pf_shard_search(scheme, Q, p0, P_global, totals, shard, gmax, gbad, seed, filter_index,
                                        anc_out)
 
+    def spacings_total(self, P_global, nshards, shard, seed, filter_index, device):
+        return self.pf.pf_shard_spacings_total(P_global, nshards, shard, seed, filter_index, device)
+
+    def search_sorted(self, Q, p0, P_global, totals, etotals, shard, gmax, gbad, seed, filter_index, anc_out):
+        return self.pf.pf_shard_search_sorted(Q, p0, P_global, totals, etotals, shard, gmax, gbad, seed,
+                                              filter_index, anc_out)
+
     def weights(self, logw, gmax):
         return self.pf.pf_shard_weights(logw, gmax)
 
@@ -96,7 +108,7 @@ class GpuStages:
 
 
 def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, filter_index: int = 0,
-                     comm=None, stages=None, assemble: bool = True):
+                     comm=None, stages=None, assemble: bool = True, flags: int = 0):
     """Resample one filter sharded over the ranks of ``comm``.
 
     logw_local: this rank's contiguous shard (``shard_range(P_global, world, rank)``).
@@ -110,6 +122,7 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     comm = comm or TorchComm()
     stages = stages or GpuStages()
     scheme_id = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+    is_sorted = _sorted(scheme_id, flags)
     world, rank = comm.world, comm.rank
     p0, Pl = shard_range(P_global, world, rank)
     if logw_local.shape[0] != Pl:
@@ -138,7 +151,12 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     totals = comm.all_gather_cat(total)
     wsums = comm.all_gather_cat(wsum)
     anc = torch.full((P_global,), -1, dtype=torch.int32, device=logw_local.device)
-    rng = stages.search(scheme_id, Q, p0, P_global, totals, rank, gmax, gbad, seed, filter_index, anc)
+    if is_sorted:
+        etot = stages.spacings_total(P_global, world, rank, seed, filter_index, logw_local.device)
+        etotals = comm.all_gather_cat(etot)
+        rng = stages.search_sorted(Q, p0, P_global, totals, etotals, rank, gmax, gbad, seed, filter_index, anc)
+    else:
+        rng = stages.search(scheme_id, Q, p0, P_global, totals, rank, gmax, gbad, seed, filter_index, anc)
     info["slot_range_dev"] = rng
     info["lse"] = (gmax, wsums)  # lse = gmax + ln(sum wsums) (NS-13), left on the device
     if not assemble:
@@ -146,14 +164,23 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     return comm.all_reduce_max(anc), info
 
 
+def _sorted(scheme_id: int, flags: int) -> bool:
+    if flags & ~PF_SORTED:
+        raise ValueError(f"unsupported flags {flags:#x}")
+    if flags & PF_SORTED and scheme_id != 1:
+        raise ValueError("PF_SORTED applies to the multinomial scheme only")
+    return bool(flags & PF_SORTED)
+
+
 def resample_sharded_local(scheme, logw_full, nshards: int, seed: int, B: int = 0, filter_index: int = 0,
-                           stages=None):
+                           stages=None, flags: int = 0):
     """Fake-shard mode: all shards on one device, exchanges done on the host.
     Exercises exactly the shard kernels and the offset logic of ``resample_sharded``."""
     import torch
 
     stages = stages or GpuStages()
     scheme_id = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+    is_sorted = _sorted(scheme_id, flags)
     P_global = logw_full.shape[0]
     parts = [shard_range(P_global, nshards, g) for g in range(nshards)]
     pieces = [logw_full[p0:p0 + Pl] for p0, Pl in parts]
@@ -166,6 +193,12 @@ def resample_sharded_local(scheme, logw_full, nshards: int, seed: int, B: int = 
     scans = [stages.scan(x, P_global, gmax) for x in pieces]
     totals = torch.cat([t for _, t, _ in scans])
     anc = torch.full((P_global,), -1, dtype=torch.int32, device=logw_full.device)
+    if is_sorted:
+        etotals = torch.cat([stages.spacings_total(P_global, nshards, g, seed, filter_index, logw_full.device)
+                             for g in range(nshards)])
+        for g, ((p0, Pl), (Q, _, _)) in enumerate(zip(parts, scans)):
+            stages.search_sorted(Q, p0, P_global, totals, etotals, g, gmax, gbad, seed, filter_index, anc)
+        return anc
     for g, ((p0, Pl), (Q, _, _)) in enumerate(zip(parts, scans)):
         stages.search(scheme_id, Q, p0, P_global, totals, g, gmax, gbad, seed, filter_index, anc)
     return anc

@@ -44,6 +44,39 @@ class CpuOracleStages:
         rng = (min(ks), max(ks) + 1) if ks else (0, 0)
         return torch.tensor(rng, dtype=torch.int64)
 
+    # a6 sorted multinomial (NS-12): spacing totals per spacing shard, positions
+    # x_k = floor(G_k Q / G_P) in exact Python integers from the oracle's G.
+    @staticmethod
+    def _spacing_range(P_global, nshards, h):
+        per = -(-(P_global + 1) // nshards)
+        return min(P_global + 1, h * per), min(P_global + 1, (h + 1) * per)
+
+    def spacings_total(self, P_global, nshards, shard, seed, filter_index, device=None):
+        G = [int(v) for v in oracle.spacings(P_global, seed, filter_index)]
+        k0, k1 = self._spacing_range(P_global, nshards, shard)
+        tot = (G[k1 - 1] - (G[k0 - 1] if k0 > 0 else 0)) if k1 > k0 else 0
+        return torch.tensor([tot], dtype=torch.int64)
+
+    def search_sorted(self, Q, p0, P_global, totals, etotals, shard, gmax, gbad, seed, filter_index, anc_out):
+        Ql = Q.numpy().view(np.uint64)
+        Pl = len(Ql)
+        if int(gbad.item()) or float(gmax.item()) == -np.inf:
+            anc_out[p0:p0 + Pl] = torch.arange(p0, p0 + Pl, dtype=torch.int32)
+            return torch.tensor([0, 0], dtype=torch.int64)
+        tot = [int(v) for v in totals.numpy().view(np.uint64)]
+        off, Qtot, T = sum(tot[:shard]), sum(tot), tot[shard]
+        GP = sum(int(v) for v in etotals.numpy().view(np.uint64))
+        G = [int(v) for v in oracle.spacings(P_global, seed, filter_index)]
+        assert G[P_global] == GP
+        ks = []
+        for k in range(P_global):
+            x = G[k] * Qtot // GP
+            if off <= x < off + T:
+                anc_out[k] = p0 + int(np.searchsorted(Ql, np.uint64(x - off), side="right"))
+                ks.append(k)
+        rng = (min(ks), max(ks) + 1) if ks else (0, 0)
+        return torch.tensor(rng, dtype=torch.int64)
+
     def weights(self, logw, gmax):
         return torch.from_numpy(oracle.weights_with(logw.numpy(), float(gmax.item())))
 

@@ -393,6 +393,36 @@ def test_giant_filter_fake_shards(pf, dev, orc, scheme):
         assert np.array_equal(a.cpu().numpy(), want), (scheme, P, G, kind)
 
 
+def test_giant_filter_fake_shards_sorted_multinomial(pf, dev, orc):
+    """C5 decomposition of the sorted multinomial (a6) on one GPU: spacing totals per
+    spacing shard, device-side plan, range scan of the spacings, merge.  Bit-exact against the
+    oracle's single-filter run for several shard counts, weight-skewed shards (one shard holding
+    almost all weight, so its slot range spans many spacing shards), a shard without weight and
+    an invalid filter."""
+    import torch
+
+    from paper_1202_6163_b200.shard import PF_SORTED, resample_sharded_local, shard_range
+
+    cases = [(1000, 2, 1.0, ""), (4097, 3, 10.0, ""), (65536, 8, 1.0, ""), (100003, 5, 0.1, ""),
+             (1 << 20, 8, 1.0, ""), (9000, 4, 1.0, "neg_inf_shard"), (5000, 2, 1.0, "invalid"),
+             (200000, 8, 1.0, "skew"), (7, 3, 1.0, ""), (1, 1, 1.0, ""), (3, 2, 1.0, "")]
+    for P, G, var, kind in cases:
+        x = pfinputs.gaussian_logw(P, var, seed=P + G + 1)
+        if kind == "neg_inf_shard":
+            p0, Pl = shard_range(P, G, 2)
+            x[p0:p0 + Pl] = -np.inf
+        if kind == "invalid":
+            x[17] = np.inf
+        if kind == "skew":
+            p0, Pl = shard_range(P, G, 5)
+            x[p0:p0 + Pl] += 12.0  # shard 5 holds nearly all the weight
+        g = _gpu(x, dev)
+        a = resample_sharded_local("multinomial", g, G, 1234, filter_index=4, flags=PF_SORTED)
+        torch.cuda.synchronize()
+        _, want = orc.resample_sorted_multinomial(x, 1234, filter_index=4)
+        assert np.array_equal(a.cpu().numpy(), want), (P, G, kind)
+
+
 def test_sorted_multinomial_a6(pf, dev, orc):
     """a6 (PF_SORTED with the multinomial): spacings scan + exact 128/64 positions + merge,
     bit-exact against the oracle; batched with ld > P and an invalid filter; ragged sizes."""

@@ -4,6 +4,8 @@
   paper_1202_6163_b200.shard.resample_sharded with real torch.distributed
   collectives (all_reduce MAX, all_gather of totals / weights) and CPU stand-in
   stages (oracle-based), assembled ancestors == the oracle's single-filter run.
+  Includes the sorted multinomial (a6), whose ranks also all-gather the totals of
+  their spacing shards.
 * Batched filters sharded over ranks (config C3, bench.py): rank g owns filters
   [g N, (g+1) N) with first_filter = g N; the union equals a single-rank batch.
 """
@@ -48,8 +50,9 @@ def _worker(rank, world, port, outdir, cases):
         if kind == "invalid":
             x[3] = np.nan
         p0, Pl = shard_range(P, world, rank)
+        flags = 1 if kind == "sorted" else 0
         anc, info = resample_sharded(scheme, torch.from_numpy(x[p0:p0 + Pl].copy()), P, seed, B=B,
-                                     filter_index=5, comm=comm, stages=stages)
+                                     filter_index=5, comm=comm, stages=stages, flags=flags)
         if rank == 0:
             np.save(os.path.join(outdir, f"shard_{ci}.npy"), anc.numpy())
     # batched filters: rank g owns filters [g N, (g+1) N)
@@ -74,6 +77,8 @@ CASES = [
     ("metropolis", 600, 0.1, 12, 7, "neg_inf_shard"),
     ("stratified", 500, 1.0, 13, 0, "invalid"),
     ("metropolis", 500, 1.0, 14, 3, "invalid"),
+    ("multinomial", 1000, 1.0, 15, 0, "sorted"),
+    ("multinomial", 777, 10.0, 16, 0, "sorted"),
 ]
 
 
@@ -92,7 +97,10 @@ def test_two_rank_giant_filter_and_batches(tmp_path):
             x[p0:p0 + Pl] = -np.inf
         if kind == "invalid":
             x[3] = np.nan
-        _, want = oracle.resample(scheme, x, seed, B=B, filter_index=5)
+        if kind == "sorted":
+            _, want = oracle.resample_sorted_multinomial(x, seed, filter_index=5)
+        else:
+            _, want = oracle.resample(scheme, x, seed, B=B, filter_index=5)
         got = np.load(os.path.join(tmp_path, f"shard_{ci}.npy"))
         assert np.array_equal(got, want), (scheme, P, kind)
     xs = pfinputs.gaussian_logw(500, 1.0, seed=11, N=3 * world)
