@@ -33,13 +33,19 @@ namespace pf {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kFT = 1024;          // threads per CTA (1 CTA / SM)
-constexpr int kFW = kFT / 32;      // 32 warps
+#ifndef PF_FUSED_THREADS
+#define PF_FUSED_THREADS 1024
+#endif
+constexpr int kFT = PF_FUSED_THREADS;  // threads per CTA (1024: 1 CTA / SM)
+constexpr int kFW = kFT / 32;      // warps per CTA
 constexpr int kFI = 16;            // particles per thread
 constexpr int kFR = kFI / 4;       // 4 float4 rows
 constexpr int kPP = kFT * kFI;     // 16384 particles per CTA (max)
 constexpr int kChunk = 256;        // slots per warp max-scan pass (8 per lane)
 constexpr int kTPL = kFR * kFW / 32;  // (row, warp) totals per lane in the phase-B scan
+constexpr int kXS = kFW * kChunk;   // slots (ranks) per CTA-wide expansion chunk: 8 per thread
+static_assert(kXS == 8 * kFT, "CTA-wide expansion assumes 8 slots per thread");
+static_assert(kFW <= 32, "the cross-warp max-scan reads one warp total per lane");
 static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32 (row, warp) totals");
 
 struct Exchange {
@@ -118,8 +124,48 @@ __device__ __forceinline__ uint32_t count_below(const Pos& z, uint64_t v) {
     return static_cast<uint32_t>(min(max(c, int64_t{0}), z.P));
 }
 
+__device__ __forceinline__ void cta_clear8(int32_t* s_head, int tid) {
+    int4* h4 = reinterpret_cast<int4*>(s_head);
+    h4[2 * tid] = make_int4(-1, -1, -1, -1);
+    h4[2 * tid + 1] = make_int4(-1, -1, -1, -1);
+}
+
+// CTA-wide inclusive max-scan of the kXS marks in s_head, 8 consecutive per thread (the
+// caller has synchronised after marking): h[t] = max(carry, marks [0, 8 tid + t]); carry
+// (block-uniform) becomes the chunk maximum.  One barrier.
+__device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_wmax, int32_t h[8], int32_t& carry,
+                                              int tid, int warp, int lane) {
+    const int4* h4 = reinterpret_cast<const int4*>(s_head);
+    const int4 lo = h4[2 * tid], hi = h4[2 * tid + 1];
+    h[0] = lo.x; h[1] = lo.y; h[2] = lo.z; h[3] = lo.w; h[4] = hi.x; h[5] = hi.y; h[6] = hi.z; h[7] = hi.w;
+#pragma unroll
+    for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
+    int32_t incl = h[7];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl = max(incl, u);
+    }
+    if (lane == 31) s_wmax[warp] = incl;
+    __syncthreads();
+    int32_t w = (lane < kFW) ? s_wmax[lane] : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w = max(w, u);
+    }
+    const int32_t wpre = __shfl_sync(kFull, w, (warp + 31) & 31);  // inclusive of warp - 1
+    const int32_t tot = __shfl_sync(kFull, w, 31);
+    int32_t pre = __shfl_up_sync(kFull, incl, 1);
+    pre = (lane == 0) ? -1 : pre;
+    pre = max(max(pre, carry), (warp == 0) ? -1 : wpre);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
+    carry = max(carry, tot);
+}
+
 template <int SCHEME, bool SUMS, bool PERM>
-__global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
+__global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
     extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
     __shared__ Exchange s_x;
     __shared__ uint32_t s_rf[9];
@@ -130,6 +176,7 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
     __shared__ uint64_t s_wt[kFR][kFW];
     __shared__ uint32_t s_lastE[kFR][kFW];
     __shared__ __align__(16) int32_t s_buf[kFW][kChunk];
+    __shared__ int32_t s_wmax[kFW];
     __shared__ float s_lmax;
     __shared__ int s_bad;
     __shared__ uint64_t s_off, s_tot, s_Qtot;
@@ -398,53 +445,39 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
         }
         int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
         const int32_t idbase = static_cast<int32_t>(p0) + tid * 4;
-        int4* b4 = reinterpret_cast<int4*>(s_buf[warp]);
-        // Each (row, warp) owns the contiguous slot range [S0, S1) of its 128 particles.
-        // Per 256-slot chunk: heads[E_{i-1}] = i, then a warp max-scan gives
-        // a_k = max{i : E_{i-1} <= k}; 8 slots per lane, vector stores.
-#pragma unroll
-        for (int j = 0; j < kFR; ++j) {
-            const uint32_t S0 = __shfl_sync(kFull, first[j], 0);
-            const uint32_t S1 = __shfl_sync(kFull, E[j * 4 + 3], 31);
+        int32_t* s_head = &s_buf[0][0];
+        // The CTA's slots are [k_lo, K1).  Per 8192-slot chunk (8 per thread): heads[E_{i-1}] = i
+        // for every particle with o_i > 0, then a CTA-wide max-scan gives
+        // a_k = max{i : E_{i-1} <= k}; aligned vector stores except at the CTA's two ends.
+        {
+            const uint32_t K1 = s_lastE[kFR - 1][kFW - 1];
             int32_t carry = -1;
-            for (uint32_t c0 = S0 & ~3u; c0 < S1; c0 += kChunk) {
-                b4[2 * lane] = make_int4(-1, -1, -1, -1);
-                b4[2 * lane + 1] = make_int4(-1, -1, -1, -1);
-                __syncwarp();
+            for (uint32_t c0 = k_lo & ~7u; c0 < K1; c0 += kXS) {
+                cta_clear8(s_head, tid);
+                __syncthreads();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                    const uint32_t rel = pe - c0;  // wraps when pe < c0
-                    if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kChunk))
-                        s_buf[warp][rel] = idbase + j * (kFT * 4) + q;
+                for (int j = 0; j < kFR; ++j) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                        const uint32_t rel = pe - c0;  // wraps when pe < c0
+                        if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kXS))
+                            s_head[rel] = idbase + j * (kFT * 4) + q;
+                    }
                 }
-                __syncwarp();
-                const int4 lo = b4[2 * lane], hi = b4[2 * lane + 1];
-                int32_t h[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
-                int32_t incl = h[7];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t u = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl = max(incl, u);
-                }
-                int32_t pre = __shfl_up_sync(kFull, incl, 1);
-                pre = max(carry, (lane == 0) ? -1 : pre);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
-                carry = max(carry, __shfl_sync(kFull, incl, 31));
-                const uint32_t k0 = c0 + 8 * lane;
-                if (a.anc_vec && k0 >= S0 && k0 + 8 <= S1) {
+                __syncthreads();
+                int32_t h[8];
+                cta_max_scan8(s_head, s_wmax, h, carry, tid, warp, lane);
+                const uint32_t k0 = c0 + 8 * tid;
+                if (a.anc_vec && k0 >= k_lo && k0 + 8 <= K1) {
                     int4* dst = reinterpret_cast<int4*>(arow + k0);
                     __stcs(dst, make_int4(h[0], h[1], h[2], h[3]));
                     __stcs(dst + 1, make_int4(h[4], h[5], h[6], h[7]));
-                } else {
+                } else if (k0 + 8 > k_lo && k0 < K1) {
 #pragma unroll
                     for (int t = 0; t < 8; ++t)
-                        if (k0 + t >= S0 && k0 + t < S1) arow[k0 + t] = h[t];
+                        if (k0 + t >= k_lo && k0 + t < K1) arow[k0 + t] = h[t];
                 }
-                __syncwarp();
             }
         }
         if (PERM) {
@@ -522,60 +555,53 @@ __global__ void __launch_bounds__(kFT, 1) k_fused_sorted(FusedArgs a) {
                 }
             }
             cluster.sync();  // #4 every CTA's free-slot list complete
-            // survivors' extra copies: per (row, warp) the extras ranks are contiguous
-#pragma unroll
-            for (int j = 0; j < kFR; ++j) {
-                const uint64_t base = poff + s_wt[j][warp] + pex[j];
-                uint32_t eloc = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                    const uint32_t o = E[j * 4 + q] - pe;
-                    eloc += o > 1 ? o - 1 : 0;
-                }
-                const uint32_t my_x0 = static_cast<uint32_t>(base >> 31);  // this lane's first extras rank
-                const uint32_t X0 = __shfl_sync(kFull, my_x0, 0);
-                uint32_t xincl = eloc;
-#pragma unroll
-                for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                    const uint32_t u = __shfl_up_sync(kFull, xincl, o2);
-                    if (lane >= o2) xincl += u;
-                }
-                const uint32_t XW = __shfl_sync(kFull, xincl, 31);
-                // 32 ranks per pass, one per lane: head-mark in 32 smem slots, shuffle max-scan
+            // Survivors' extra copies, CTA-wide: the CTA's extras ranks are [XC0, XC0 + XC).  Per
+            // 8192-rank chunk: heads[first extras rank of i] = i, CTA max-scan gives the owner of
+            // every rank r; the r-th global free slot (this CTA's list or a peer's, DSMEM) gets it.
+            {
+                const uint32_t XC0 = static_cast<uint32_t>(poff >> 31);
+                const uint32_t XC = static_cast<uint32_t>(s_x.ptot >> 31);
                 int32_t carry = -1;
-                int32_t* hb = s_buf[warp];
-                for (uint32_t c0 = 0; c0 < XW; c0 += 32) {
-                    hb[lane] = -1;
-                    __syncwarp();
-                    uint32_t rel0 = my_x0 - X0;
+                for (uint32_t c0 = 0; c0 < XC; c0 += kXS) {
+                    cta_clear8(s_head, tid);
+                    __syncthreads();
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                        const uint32_t o = E[j * 4 + q] - pe;
-                        const uint32_t e = o > 1 ? o - 1 : 0;
-                        const uint32_t rel = rel0 - c0;
-                        if (e > 0 && rel < 32u) hb[rel] = idbase + j * (kFT * 4) + q;
-                        rel0 += e;
-                    }
-                    __syncwarp();
-                    int32_t h = hb[lane];
+                    for (int j = 0; j < kFR; ++j) {
+                        uint64_t run = poff + s_wt[j][warp] + pex[j];
 #pragma unroll
-                    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                        const int32_t u = __shfl_up_sync(kFull, h, o2);
-                        if (lane >= o2) h = max(h, u);
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                            const uint32_t o = E[j * 4 + q] - pe;
+                            const uint32_t rel = static_cast<uint32_t>(run >> 31) - XC0 - c0;
+                            if (o > 1 && rel < static_cast<uint32_t>(kXS)) s_head[rel] = idbase + j * (kFT * 4) + q;
+                            run += static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31;  // the free bit never carries
+                        }
                     }
-                    h = max(h, carry);
-                    carry = __shfl_sync(kFull, h, 31);
-                    const uint32_t rl = c0 + lane;
-                    if (rl < XW) {
-                        const uint32_t r = X0 + rl;  // global free rank
+                    __syncthreads();
+                    int32_t h[8];
+                    cta_max_scan8(s_head, s_wmax, h, carry, tid, warp, lane);
+                    const uint32_t r0 = c0 + 8 * tid;
+                    if (r0 < XC) {
+                        uint32_t R = XC0 + r0;  // global free rank of this thread's first extra
                         int cc = 0;
-                        for (int q2 = 1; q2 < CL; ++q2) cc += (s_rf[q2] <= r) ? 1 : 0;
+#pragma unroll
+                        for (int q2 = 1; q2 < 8; ++q2) cc += (q2 < CL && s_rf[q2] <= R) ? 1 : 0;
+                        uint32_t rb = s_rf[cc], nxt = s_rf[cc + 1];
                         const int32_t* rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
-                        prow[rfs[r - s_rf[cc]]] = h;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            if (r0 + t < XC) {
+                                while (R >= nxt) {  // next CTA's free list (rare)
+                                    ++cc;
+                                    rb = nxt;
+                                    nxt = s_rf[cc + 1];
+                                    rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
+                                }
+                                prow[rfs[R - rb]] = h[t];
+                                ++R;
+                            }
+                        }
                     }
-                    __syncwarp();
                 }
             }
         }
@@ -621,7 +647,7 @@ struct CoopArgs {
 };
 
 template <int SCHEME, bool SUMS>
-__global__ void __launch_bounds__(kFT, 1) k_coop_sorted(CoopArgs a) {
+__global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];

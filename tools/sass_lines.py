@@ -20,18 +20,20 @@ import tempfile
 from collections import defaultdict
 
 
-def line_map(so: str, mangled_sub: str) -> list[tuple[str, int]]:
+def line_map(so: str, mangled_sub: str, outer: bool = False) -> list[tuple[str, int]]:
     """Per instruction (in order) of the first function whose name contains
-    ``mangled_sub``: the innermost (file, line) nvdisasm attributes it to."""
+    ``mangled_sub``: the innermost (file, line) nvdisasm attributes it to, or with
+    ``outer`` the kernel-level line it is inlined at."""
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, check=True,
                    stdout=subprocess.DEVNULL)
     out = []
     for cub in sorted(os.listdir(tmp)):
-        txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True,
+        txt = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True,
                              text=True).stdout
         inside = False
         cur = ("?", 0)
+        fresh = True  # first "//## File" line of a group = innermost; the last = outermost
         for ln in txt.splitlines():
             if ln.startswith(".text."):
                 if inside:
@@ -42,10 +44,13 @@ def line_map(so: str, mangled_sub: str) -> list[tuple[str, int]]:
                 continue
             m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
             if m:
-                cur = (os.path.basename(m.group(1)), int(m.group(2)))
+                if fresh or outer:
+                    cur = (os.path.basename(m.group(1)), int(m.group(2)))
+                fresh = False
                 continue
             if re.match(r"\s*/\*[0-9a-f]{4,}\*/", ln):
                 out.append(cur)
+                fresh = True
         if out:
             return out
     raise SystemExit(f"function containing {mangled_sub!r} not found in {so}")
@@ -58,6 +63,7 @@ def main():
     ap.add_argument("mangled")
     ap.add_argument("--so", default="paper_1202_6163_b200/libpfresample.so")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--outer", action="store_true", help="attribute inlined code to the kernel-level line")
     a = ap.parse_args()
     csv_txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--kernel-name",
                               f"regex:{a.kernel}", "--print-source", "sass"], capture_output=True,
@@ -67,7 +73,7 @@ def main():
     hdr = rows[hdr_i]
     body = [r for r in rows[hdr_i + 1:] if r and r[0].startswith("0x")]
     i_s, i_e = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
-    lm = line_map(a.so, a.mangled)
+    lm = line_map(a.so, a.mangled, a.outer)
     if len(lm) != len(body):
         print(f"warning: {len(lm)} instructions in the .so vs {len(body)} in the report")
     agg = defaultdict(lambda: [0, 0])
