@@ -160,7 +160,7 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
-    if (!no_fusion && !normw && pf::coop_supported(scheme, P)) {
+    if (!no_fusion && !normw && pf::coop_supported(scheme, N, P)) {
         // one cooperative launch for large filters (pf_fused.cu); tiny scratch from the pool
         void* sc = nullptr;
         pf_status st2 = get_workspace(opts, pf::coop_scratch_bytes(), s, &sc);

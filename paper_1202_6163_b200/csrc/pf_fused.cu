@@ -1,8 +1,10 @@
-// pf_fused.cu — one-launch resampler for batches of filters with P <= 8 x 8192
-// (stratified and systematic; SURVEY §8 rows a1-a5, a11, a12 in one kernel).
+// pf_fused.cu — one-launch resamplers (
+// NEXT-2): k_fused_sorted (a cluster per filter, P <= 8 x 8192), k_coop_sorted
+// (a cooperative grid per filter, larger P), k_small (a warp per filter, P <= 256).
 //
-// One thread-block CLUSTER per filter (CL = ceil(P / 8192) CTAs), persistent
-// over filters.  CTA c owns particles [c*PP, (c+1)*PP), 16 per thread.
+// k_fused_sorted: one thread-block CLUSTER per filter (CL = ceil(P / 8192) CTAs of
+// 512 threads, 16 particles each), persistent over filters.  CTA c owns particles
+// [c*PP, (c+1)*PP).
 //   A  log-weights -> registers (float4, coalesced); CTA max; cluster max
 //      through distributed shared memory (a1, NS-1, NS-2).
 //   B  w = dexp, q = trunc(w 2^kfx) (a2, NS-3..5); block scan of q in
@@ -15,10 +17,15 @@
 //      closed form: x_k < v  <=>  k*D + rho_k < v 2^64 / Q; a double-precision
 //      estimate of k* = (v 2^64/Q - rho)/D is within 2^-19 of the truth, so one
 //      exact integer position check decides the count (the boundary case takes
-//      a second check).  Particle i then marks heads[E_{i-1}] = i when E_i >
-//      E_{i-1}, and a max-scan over the slot window gives every ancestor
-//      a_k = max{i : E_{i-1} <= k} = min{i : Q_i > x_k} (a4+a5, NS-search).
-// HBM traffic: 4 B/particle in (logw) + 4 B out (ancestors).  No workspace.
+//      a second check).  Per chunk of 8 slots per thread, particle i marks
+//      heads[E_{i-1}] = i when E_i > E_{i-1}, and a CTA-wide max-scan gives every
+//      ancestor a_k = max{i : E_{i-1} <= k} = min{i : Q_i > x_k} (a4+a5); the
+//      offspring o_i = E_i - E_{i-1} is a free by-product (a8).
+//   D  (optional) canonical permutation (a9, NS-15): a packed (extras, free) scan
+//      across the cluster, every CTA's free-slot list in its shared memory, and a
+//      CTA-wide head-mark + max-scan over its extras ranks; the r-th extra goes to
+//      the r-th free slot, read from the owning CTA's list through DSMEM.
+// HBM traffic: 4 B/particle in (logw) + 4 B out per output array.  No workspace.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -34,13 +41,15 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef PF_FUSED_THREADS
-#define PF_FUSED_THREADS 1024
+#define PF_FUSED_THREADS 512
 #endif
-constexpr int kFT = PF_FUSED_THREADS;  // threads per CTA (1024: 1 CTA / SM)
+// threads per CTA: 512 (2 CTAs / SM, so one CTA's barriers overlap the other's work;
+// measured 4% faster than 1024 x 1 at C3 and 1.4x at single filters of 2^18-2^20)
+constexpr int kFT = PF_FUSED_THREADS;
 constexpr int kFW = kFT / 32;      // warps per CTA
 constexpr int kFI = 16;            // particles per thread
 constexpr int kFR = kFI / 4;       // 4 float4 rows
-constexpr int kPP = kFT * kFI;     // 16384 particles per CTA (max)
+constexpr int kPP = kFT * kFI;     // particles per CTA (max): 8192
 constexpr int kChunk = 256;        // slots per warp max-scan pass (8 per lane)
 constexpr int kTPL = kFR * kFW / 32;  // (row, warp) totals per lane in the phase-B scan
 constexpr int kXS = kFW * kChunk;   // slots (ranks) per CTA-wide expansion chunk: 8 per thread
@@ -1209,7 +1218,16 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool coop_supported(int scheme, int32_t P) { return (scheme == 2 || scheme == 3) && P > 8 * kPP; }
+// The cooperative kernel handles one filter at a time: ~19 us of grid-sync latency per
+// filter up to P ~ 2^20, then ~8.4e10 particles/s; the multi-launch path processes a
+// whole batch at ~6.5e10 particles/s after ~20 us of launches (tools/quick_times.py
+// --coop-vs-unfused, profiles/r01_dispatch.md).  Take the cooperative kernel when it
+// is expected to be faster; both give identical results.
+bool coop_supported(int scheme, int32_t N, int32_t P) {
+    if (!(scheme == 2 || scheme == 3) || P <= 8 * kPP) return false;
+    const double per_filter_excess_us = 19.0 - static_cast<double>(P) / 65000.0;
+    return N == 1 || per_filter_excess_us <= 0.0 || static_cast<double>(N) * per_filter_excess_us < 20.0;
+}
 
 size_t coop_scratch_bytes() { return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8); }
 

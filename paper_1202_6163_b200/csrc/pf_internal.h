@@ -139,7 +139,7 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
                          uint64_t* launches);
 
 // One-launch cooperative resampler for large filters (pf_fused.cu).
-bool coop_supported(int scheme, int32_t P);
+bool coop_supported(int scheme, int32_t N, int32_t P);
 size_t coop_scratch_bytes();
 cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,

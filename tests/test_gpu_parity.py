@@ -106,11 +106,35 @@ def test_multilaunch_path_bit_exact(pf, dev, orc, scheme):
 
 
 @pytest.mark.parametrize("scheme", ["stratified", "systematic"])
-def test_cluster_path_sizes(pf, dev, orc, scheme):
-    """Cluster sizes 1..8 of the one-launch kernel (P up to 8 x 16384), ragged CTA ranges, skew."""
+def test_large_filter_batches_dispatch(pf, dev, orc, scheme):
+    """Filters above the cluster kernel's range: one filter takes the cooperative kernel (one
+    launch), a batch of several takes the multi-launch path (the cooperative kernel serialises
+    filters); both bit-exact against the oracle."""
     import torch
 
-    for P in (16383, 16384, 16385, 32768 + 5, 49152, 65536, 98304 + 7, 131072):
+    P = 1 << 18
+    x = pfinputs.gaussian_logw(P, 1.0, seed=77, N=3)
+    g = _gpu(x, dev)
+    c0 = pf.pf_launch_count()
+    a1 = pf.pf_resample_batched(scheme, g[:1], 12, first_filter=40)
+    torch.cuda.synchronize()
+    assert pf.pf_launch_count() - c0 == 1
+    c0 = pf.pf_launch_count()
+    a3 = pf.pf_resample_batched(scheme, g, 12, first_filter=40)
+    torch.cuda.synchronize()
+    assert pf.pf_launch_count() - c0 > 1
+    _, want = orc.resample_batched(scheme, x, 12, first_filter=40)
+    assert np.array_equal(a3.cpu().numpy(), want)
+    assert np.array_equal(a1.cpu().numpy(), want[:1])
+
+
+@pytest.mark.parametrize("scheme", ["stratified", "systematic"])
+def test_cluster_path_sizes(pf, dev, orc, scheme):
+    """Cluster sizes 1..8 of the one-launch kernel (P up to 8 x 8192), ragged CTA ranges, skew; and the
+    sizes just above it (cooperative kernel)."""
+    import torch
+
+    for P in (8191, 8192, 8193, 16384 + 5, 24576, 49152 + 3, 65535, 65536, 65537, 98304 + 7, 131072):
         x = pfinputs.gaussian_logw(P, 10.0, seed=P)
         a = _run(pf, dev, scheme, x, 31)
         _, want = orc.resample(scheme, x, 31)

@@ -1,0 +1,52 @@
+#!/usr/bin/env python
+"""Device time per call (CUDA graph replay) of a few resample configurations; one JSON
+line each.  Used to compare build variants (launch geometry) on the same box."""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    import paper_1202_6163_b200 as pf
+    import pfinputs
+    from tools.sweep import time_calls
+
+    dev = torch.device("cuda:0")
+    if "--coop-vs-unfused" in sys.argv:
+        for P in (1 << 17, 1 << 18, 1 << 20, 1 << 22):
+            for N in (1, 2, 4, 8, 16, 64):
+                if N * P > (1 << 26):
+                    continue
+                x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+                anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+                row = {"N": N, "P": P}
+                for name, fl in (("default", 0), ("unfused", pf.PF_NO_FUSION)):
+                    row[name] = round(time_calls(lambda: pf.pf_resample_batched("systematic", x, 5, ancestors=anc,
+                                                                                flags=fl), 5, dev), 4)
+                print(json.dumps(row))
+                sys.stdout.flush()
+        return
+    cases = [(1024, 1 << 16, "systematic", True), (1024, 1 << 16, "stratified", True),
+             (512, 1 << 17, "systematic", False), (1, 1 << 18, "systematic", False),
+             (1, 1 << 20, "systematic", False), (1, 1 << 24, "systematic", False)]
+    for N, P, scheme, perm in cases:
+        x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+        anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+        off = torch.empty_like(anc)
+        pm = torch.empty_like(anc) if perm else None
+        ms = time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, ancestors=anc, offspring_out=off,
+                                                       permuted_out=pm), 5, dev)
+        print(json.dumps({"N": N, "P": P, "scheme": scheme, "perm": perm, "ms": round(ms, 4),
+                          "particles_per_s": N * P / (ms / 1e3), "lib": pf._LIB_PATH}))
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()
