@@ -3,12 +3,13 @@
 
 One step = one pass of the whole hot path over a batch of synthetic filters
 (BASELINE.json configs[2], "batched PMCMC: 1024 independent filters x 2^16"):
-  pf_resample_batched (a1-a5: max, dexp + u64 scan, ancestor search; a8:
-      offspring counts and a9: the canonical in-place permutation as side
-      outputs, all in the one-launch cluster kernel)
-  -> pf_gather_state_batched (a10: in-place gather of a D=16 float32 state).
-The generic chain through pf_permute(ancestors) (histogram path) is timed
-as an extra (`extras.step_via_pf_permute_of_ancestors`).
+  pf_resample_batched(..., offspring_out, permuted_out, state=X): a1-a5 (max,
+      dexp + u64 scan, ancestor search), a8 (offspring), a9 (the canonical
+      in-place permutation) and a10 (the in-place gather of a D=16 float32
+      state) in the one-launch cluster kernel.
+The same step as two calls (resample with permutation, then
+pf_gather_state_batched) and the generic chain through pf_permute(ancestors)
+(histogram path) are timed as extras.
 Metric: resampled particles/s (whole job, all ranks).  Multi-GPU: one process
 per GPU (torchrun); rank g owns filters [g*N, (g+1)*N) (global Philox filter
 indices), no data-path collective -> weak scaling; --strong splits a fixed N.
@@ -296,11 +297,10 @@ def run_ours(args):
     perm = torch.empty((N, P), dtype=torch.int32, device=dev)
 
     def step():
-        # a1-a5, a8 (offspring) and a9 (canonical permutation) as side outputs of the resampler
-        # (fused into the cluster kernel for P <= 65536), then a10 (in-place gather)
+        # a1-a5, a8 (offspring), a9 (canonical permutation) and a10 (in-place state gather) in one
+        # call (fused into the cluster kernel for P <= 65536)
         pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
-                               permuted_out=perm, stream=stream)
-        pf.pf_gather_state(X, perm, stream=stream)
+                               permuted_out=perm, state=X, stream=stream)
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -341,7 +341,7 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
 
     # algorithmic bytes per launch of each kernel of the step
-    o = pf.pf_ancestors_to_offspring(anc)
+    o = off
     survivors = int((o > 0).sum().item())
     free = N * P - survivors
     row = args.D * 4
@@ -357,7 +357,8 @@ def run_ours(args):
         "k_hist": 8 * NP,
         "k_pscan": 12 * NP,
         "k_push": 8 * NP + 8 * free,
-        "k_fused_sorted": 16 * NP,  # logw in; ancestors, offspring, permutation out
+        # logw in; ancestors, offspring, permutation out; moved state rows read + written
+        "k_fused_sorted": 16 * NP + 2 * row * free,
         "k_coop_sorted": 12 * NP,
         "k_gather_inplace": 4 * NP + 2 * row * free,
     }
@@ -459,6 +460,23 @@ def run_ours(args):
                 1e3 * time_calls(lambda: pf.pf_resample_ex(sch, x16, seed, b, ancestors=a16), 50, dev), 2)
         extras["c1_latency_us_per_call_P16"] = c1
 
+        # ---------------- the same step as two calls: resample + permutation, then the gather
+        def step_two_calls():
+            pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
+                                   permuted_out=perm, stream=stream)
+            pf.pf_gather_state(X, perm, stream=stream)
+
+        step_two_calls()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(max(3, min(args.steps, 10))):
+            step_two_calls()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gms = g0.elapsed_time(g1) / max(3, min(args.steps, 10))
+        extras["step_two_calls_resample_then_gather"] = {"ms": round(gms, 4), "particles_per_s": N * P / (gms / 1e3)}
+
         # ---------------- generic chain: permutation from arbitrary ancestors (histogram path)
         def step_generic():
             pf.pf_resample_batched(scheme, logw, seed, B=B, first_filter=first, ancestors=anc, stream=stream)
@@ -484,8 +502,7 @@ def run_ours(args):
         def e2e_step():
             d_logw.copy_(h_logw, non_blocking=True)
             pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
-                                   permuted_out=perm, stream=stream)
-            pf.pf_gather_state(X, perm, stream=stream)
+                                   permuted_out=perm, state=X, stream=stream)
             h_out.copy_(perm, non_blocking=True)
 
         for _ in range(2):

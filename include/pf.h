@@ -97,6 +97,18 @@ typedef struct {
                               from the offspring after the search                           */
     void* workspace;       /* device, 256-byte aligned, nullable -> library pool            */
     size_t workspace_bytes;
+    /* Optional fused state gather (a10, NS-16; "redraw"): if state is non-NULL, after
+     * resampling every filter's rows are gathered IN PLACE with the canonical permutation a'
+     * (NS-15): row i <- row a'_i for the non-survivors, survivors untouched.  Filter n's rows
+     * start at state + n * state_filter_ld_bytes, row i at + i * state_ld_bytes, each
+     * state_row_bytes long (device).  Same result as pf_permute + pf_gather_state_batched;
+     * fused into the cluster kernel for power-of-two rows of 16..512 bytes (16-byte aligned
+     * strides), otherwise run as a separate gather after the permutation.  Requires
+     * state_ld_bytes >= state_row_bytes and non-overlapping filters. */
+    void* state;
+    int64_t state_row_bytes;
+    int64_t state_ld_bytes;
+    int64_t state_filter_ld_bytes;
 } pf_opts;
 
 /*

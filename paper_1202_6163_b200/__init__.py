@@ -40,6 +40,10 @@ class _Opts(ctypes.Structure):
         ("permuted_out", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
+        ("state", ctypes.c_void_p),
+        ("state_row_bytes", ctypes.c_int64),
+        ("state_ld_bytes", ctypes.c_int64),
+        ("state_filter_ld_bytes", ctypes.c_int64),
     ]
 
 
@@ -158,11 +162,45 @@ def _scheme(s):
     return SCHEMES[s] if isinstance(s, str) else int(s)
 
 
+def _state_layout(X, batched: bool):
+    """(row_bytes, ld_bytes, filter_ld_bytes) of a state tensor [P, ...] or [N, P, ...] whose
+    rows (the trailing dims) are contiguous."""
+    if not X.is_cuda:
+        raise PfError("X must be a CUDA tensor")
+    lead = 2 if batched else 1
+    if X.dim() < lead:
+        raise PfError("state tensor has too few dimensions")
+    es = X.element_size()
+    inner = X.shape[lead:]
+    expect = 1
+    for d in range(X.dim() - 1, lead - 1, -1):
+        if X.shape[d] != 1 and X.stride(d) != expect:
+            raise PfError("state rows (trailing dimensions) must be contiguous")
+        expect *= X.shape[d]
+    row = es
+    for d in inner:
+        row *= d
+    ld = X.stride(lead - 1) * es
+    ldf = X.stride(0) * es if batched else 0
+    return row, ld, ldf
+
+
+def _set_state(opts, state, batched: bool):
+    if state is None:
+        return
+    row, ld, ldf = _state_layout(state, batched)
+    opts.state = state.data_ptr()
+    opts.state_row_bytes = row
+    opts.state_ld_bytes = ld
+    opts.state_filter_ld_bytes = ldf
+
+
 # ----------------------------------------------------------------------------- resamplers
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
                    lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                   permuted_out=None, flags: int = 0, stream=None):
-    """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor."""
+                   permuted_out=None, flags: int = 0, state=None, stream=None):
+    """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor.
+    state: optional [P, ...] tensor gathered in place with the canonical permutation (NS-15/16)."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
     if logw.dim() != 1 or logw.stride(0) != 1:
@@ -184,6 +222,7 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
         _need_cuda(offspring_out, torch.int32, "offspring_out"); opts.offspring_out = offspring_out.data_ptr()
     if permuted_out is not None:
         _need_cuda(permuted_out, torch.int32, "permuted_out"); opts.permuted_out = permuted_out.data_ptr()
+    _set_state(opts, state, False)
     rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
                               ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_ex")
@@ -218,8 +257,9 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
                         lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                        permuted_out=None, flags: int = 0, stream=None):
-    """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P]."""
+                        permuted_out=None, flags: int = 0, state=None, stream=None):
+    """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P].
+    state: optional [N, P, ...] tensor gathered in place with the canonical permutation."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
     if logw.dim() != 2:
@@ -237,6 +277,7 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
         if t is not None:
             _need_cuda(t, dt, name)
             setattr(opts, name, t.data_ptr())
+    _set_state(opts, state, True)
     rc = lib().pf_resample_batched(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
                                    aptr, ald, ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_batched")
@@ -308,19 +349,13 @@ def pf_gather_state(X, permuted, stream=None):
     contiguous rows; permuted from pf_permute."""
     torch = _torch()
     _need_cuda(permuted, torch.int32, "permuted")
-    if not X.is_cuda:
-        raise PfError("X must be a CUDA tensor")
-    es = X.element_size()
     if permuted.dim() == 1:
         P = permuted.shape[0]
-        row = X[0].numel() * es if X.dim() > 1 else es
-        ld = X.stride(0) * es
+        row, ld, _ = _state_layout(X, False)
         rc = lib().pf_gather_state(X.data_ptr(), row, ld, P, permuted.data_ptr(), _stream(X, stream))
     else:
         N, P = permuted.shape
-        row = X[0, 0].numel() * es if X.dim() > 2 else es
-        ld = X.stride(1) * es
-        ldf = X.stride(0) * es
+        row, ld, ldf = _state_layout(X, True)
         pp, pld = _rows(permuted, "permuted")
         rc = lib().pf_gather_state_batched(X.data_ptr(), row, ld, ldf, N, P, pp, pld, _stream(X, stream))
     _check(rc, "pf_gather_state")
@@ -333,11 +368,13 @@ def pf_gather_state_out(X, anc, Y=None, stream=None):
     _need_cuda(anc, torch.int32, "anc")
     if Y is None:
         Y = torch.empty_like(X)
-    es = X.element_size()
     P = anc.shape[0]
-    row = X[0].numel() * es if X.dim() > 1 else es
-    rc = lib().pf_gather_state_out(X.data_ptr(), Y.data_ptr(), row, X.stride(0) * es, Y.stride(0) * es, P,
-                                   anc.data_ptr(), _stream(X, stream))
+    row, ldx, _ = _state_layout(X, False)
+    rowy, ldy, _ = _state_layout(Y, False)
+    if rowy != row:
+        raise PfError("X and Y rows differ in size")
+    rc = lib().pf_gather_state_out(X.data_ptr(), Y.data_ptr(), row, ldx, ldy, P, anc.data_ptr(),
+                                   _stream(X, stream))
     _check(rc, "pf_gather_state_out")
     return Y
 

@@ -115,8 +115,14 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     int32_t* offspring_out = opts ? opts->offspring_out : nullptr;
     int32_t* permuted_out = opts ? opts->permuted_out : nullptr;
 
+    void* state = opts ? opts->state : nullptr;
+    const int64_t x_row = opts ? opts->state_row_bytes : 0, x_ld = opts ? opts->state_ld_bytes : 0;
+    const int64_t x_fld = opts ? opts->state_filter_ld_bytes : 0;
+    if (state && (x_row < 1 || x_ld < x_row || (N > 1 && x_fld < x_ld * static_cast<int64_t>(P))))
+        return PF_ERR_INVALID_ARG;
+
     const bool no_fusion = (opts && (opts->flags & PF_NO_FUSION)) || g_no_fusion.load();
-    if (!no_fusion && pf::small_supported(P) && !permuted_out) {
+    if (!no_fusion && pf::small_supported(P) && !permuted_out && !state) {
         // one warp per filter, every scheme, one launch (pf_fused.cu k_small)
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_small(scheme, sorted_multi, logw, ld, N, P, seed, first_filter, B, anc, ld_anc,
@@ -124,31 +130,48 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
-    if (!no_fusion && pf::fused_supported(scheme, P)) {
-        // one launch per batch: cluster-per-filter kernel, no workspace (pf_fused.cu)
+    if (!no_fusion && pf::fused_supported(scheme, P) &&
+        (!state || pf::fused_gather_supported(state, x_row, x_ld, x_fld))) {
+        // one launch per batch: cluster-per-filter kernel (ancestors, offspring, permutation and
+        // the state gather), no workspace except the permutation when the state is gathered
+        // without permuted_out (pf_fused.cu)
+        int32_t* perm = permuted_out;
+        if (state && !perm) {
+            void* p = nullptr;
+            const pf_status st = get_workspace(opts, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4, s, &p);
+            if (st != PF_OK) return st;
+            perm = static_cast<int32_t*>(p);
+        }
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
-                                                      ess, normw, status_out, offspring_out, permuted_out, s, &nl);
+                                                      ess, normw, status_out, offspring_out, perm, state,
+                                                      x_row, x_ld, x_fld, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }
-    if (permuted_out) {
-        // not fused for this size/scheme: resample (offspring as a side output), then the
-        // canonical permutation from the offspring (k_pscan + k_push).  One pool block holds
-        // [permutation scratch | offspring (if the caller gave none) | resample workspace].
+    if (permuted_out || state) {
+        // not fused for this size/scheme/row layout: resample (offspring as a side output), then
+        // the canonical permutation from the offspring (k_pscan + k_push), then the gather.  One
+        // pool block holds [permutation scratch | offspring (if the caller gave none) | permutation
+        // (if the caller gave none) | resample workspace].
         if (opts && opts->workspace) return PF_ERR_UNSUPPORTED;
         const pf::Layout LP = pf::make_layout(N, P, pf::kNeedPermute);
         const pf::Layout LR = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u));
-        const size_t off_bytes = offspring_out ? 0 : static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4;
+        const size_t plane = static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4;
+        const size_t off_bytes = offspring_out ? 0 : plane;
+        const size_t perm_bytes = permuted_out ? 0 : plane;
         const size_t o1 = (LP.total + 255) / 256 * 256;
-        const size_t o2b = (o1 + off_bytes + 255) / 256 * 256;
+        const size_t o1p = (o1 + off_bytes + 255) / 256 * 256;
+        const size_t o2b = (o1p + perm_bytes + 255) / 256 * 256;
         void* big = nullptr;
         pf_status st0 = pool_get(o2b + LR.total, s, &big);
         if (st0 != PF_OK) return st0;
         const pf::Ws wp = pf::carve(big, LP);
         int32_t* off = offspring_out ? offspring_out : reinterpret_cast<int32_t*>(static_cast<char*>(big) + o1);
+        int32_t* perm = permuted_out ? permuted_out : reinterpret_cast<int32_t*>(static_cast<char*>(big) + o1p);
         pf_opts o2 = opts ? *opts : pf_opts{};
         o2.permuted_out = nullptr;
+        o2.state = nullptr;
         o2.offspring_out = off;
         o2.workspace = static_cast<char*>(big) + o2b;
         o2.workspace_bytes = LR.total;
@@ -156,7 +179,9 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         if (st2 != PF_OK) return st2;
         uint64_t nl = 0;
         cudaError_t e = cudaMemsetAsync(static_cast<char*>(big) + LP.zero_begin, 0, LP.zero_end - LP.zero_begin, s);
-        if (e == cudaSuccess) e = pf::launch_permute_from_offspring(off, ld_anc, N, P, LP, wp, permuted_out, ld_anc, s, &nl);
+        if (e == cudaSuccess) e = pf::launch_permute_from_offspring(off, ld_anc, N, P, LP, wp, perm, ld_anc, s, &nl);
+        if (e == cudaSuccess && state)
+            e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }

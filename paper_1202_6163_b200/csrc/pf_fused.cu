@@ -83,7 +83,11 @@ struct FusedArgs {
     float* normw;
     int32_t* status_out;
     int32_t* off;   // offspring out (row stride ld_anc), nullable
-    int32_t* perm;  // canonical permutation out (row stride ld_anc), nullable (PERM)
+    int32_t* perm;  // canonical permutation out (row stride ld_anc), nullable
+    char* X;        // state rows gathered in place (PERM), nullable: filter n at X + n * xfld
+    int64_t xld;    // bytes between rows
+    int64_t xfld;   // bytes between filters
+    int xlg;        // log2 of the 16-byte chunks per row (row bytes = 16 << xlg)
 };
 
 struct Pos {
@@ -173,9 +177,41 @@ __device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_
     carry = max(carry, tot);
 }
 
-template <int SCHEME, bool SUMS, bool PERM>
+// a10 fused: one warp copies npairs rows X[slot[p]] <- X[owner[p]] of filter n
+// ((16 << xlg) bytes each), 16 bytes per lane, kCopyU chunks in flight per lane.
+#ifndef PF_COPY_U
+#define PF_COPY_U 4
+#endif
+constexpr int kCopyU = PF_COPY_U;
+__device__ __forceinline__ void copy_rows_warp(const FusedArgs& a, int n, const int32_t* owner, const int32_t* slot,
+                                               int npairs, int lane) {
+    char* Xf = a.X + static_cast<int64_t>(n) * a.xfld;
+    const int items = npairs << a.xlg;
+    const int cmask = (1 << a.xlg) - 1;
+    for (int b = 0; b < items; b += 32 * kCopyU) {
+        int4 v[kCopyU];
+#pragma unroll
+        for (int u = 0; u < kCopyU; ++u) {
+            const int idx = b + 32 * u + lane;
+            if (idx < items)
+                v[u] = __ldcg(reinterpret_cast<const int4*>(Xf + static_cast<int64_t>(owner[idx >> a.xlg]) * a.xld +
+                                                            (idx & cmask) * 16));
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyU; ++u) {
+            const int idx = b + 32 * u + lane;
+            if (idx < items)
+                __stcg(reinterpret_cast<int4*>(Xf + static_cast<int64_t>(slot[idx >> a.xlg]) * a.xld + (idx & cmask) * 16),
+                       v[u]);
+        }
+    }
+}
+
+// PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
+template <int SCHEME, bool SUMS, int PERM>
 __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
     extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
+    int32_t* s_pslot = s_fs + kPP;                    // PERM == 2: free slot of each extras rank of a chunk
     __shared__ Exchange s_x;
     __shared__ uint32_t s_rf[9];
     __shared__ uint64_t s_poff;
@@ -270,7 +306,8 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
             if (a.off)
                 for (int64_t k = p0 + tid; k < p1; k += kFT) a.off[static_cast<int64_t>(n) * a.ld_anc + k] = 1;
             if (PERM)
-                for (int64_t k = p0 + tid; k < p1; k += kFT) a.perm[static_cast<int64_t>(n) * a.ld_anc + k] = static_cast<int32_t>(k);
+                if (a.perm)
+                    for (int64_t k = p0 + tid; k < p1; k += kFT) a.perm[static_cast<int64_t>(n) * a.ld_anc + k] = static_cast<int32_t>(k);
             if (a.normw)
                 for (int64_t k = p0 + tid; k < p1; k += kFT) a.normw[static_cast<int64_t>(n) * a.P + k] = NAN;
             if (c == 0 && tid == 0) {
@@ -401,7 +438,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
         if (a.P == 1) {
             if (tid == 0) a.anc[static_cast<int64_t>(n) * a.ld_anc] = 0;
             if (tid == 0 && a.off) a.off[static_cast<int64_t>(n) * a.ld_anc] = 1;
-            if (PERM && tid == 0) a.perm[static_cast<int64_t>(n) * a.ld_anc] = 0;
+            if (PERM && a.perm && tid == 0) a.perm[static_cast<int64_t>(n) * a.ld_anc] = 0;
             __syncthreads();
             continue;
         }
@@ -557,8 +594,9 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
                     const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
                     const uint32_t o = E[j * 4 + q] - pe;
                     if (i < np) {
-                        if (o > 0) prow[p0 + i] = static_cast<int32_t>(p0 + i);
-                        else s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull) - rf_c] = static_cast<int32_t>(p0 + i);
+                        if (o > 0) {
+                            if (a.perm) prow[p0 + i] = static_cast<int32_t>(p0 + i);
+                        } else s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull) - rf_c] = static_cast<int32_t>(p0 + i);
                     }
                     run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
                 }
@@ -606,10 +644,25 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
                                     nxt = s_rf[cc + 1];
                                     rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
                                 }
-                                prow[rfs[R - rb]] = h[t];
+                                const int32_t slot = rfs[R - rb];
+                                prow[slot] = h[t];
+                                if (PERM == 2) s_pslot[8 * tid + t] = slot;
                                 ++R;
                             }
                         }
+                    }
+                    if (PERM == 2) {
+                        // a10 fused (NS-16): X[free slot] <- X[owner] for this warp's (slot, owner)
+                        // pairs; reads touch survivor rows only, writes free rows only
+                        int4* hh = reinterpret_cast<int4*>(s_head);
+                        hh[2 * tid] = make_int4(h[0], h[1], h[2], h[3]);
+                        hh[2 * tid + 1] = make_int4(h[4], h[5], h[6], h[7]);
+                        __syncwarp();
+                        const int64_t wfirst = static_cast<int64_t>(c0) + 256 * warp;
+                        const int npairs = static_cast<int>(
+                            min(int64_t{256}, max(int64_t{0}, static_cast<int64_t>(XC) - wfirst)));
+                        copy_rows_warp(a, n, s_head + 256 * warp, s_pslot + 256 * warp, npairs, lane);
+                        __syncwarp();
                     }
                 }
             }
@@ -1181,9 +1234,9 @@ int device_sms() {
     return sms;
 }
 
-template <int SCHEME, bool SUMS, bool PERM>
+template <int SCHEME, bool SUMS, int PERM>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    const size_t smem = PERM ? static_cast<size_t>(kPP) * sizeof(int32_t) : 0;
+    const size_t smem = PERM ? static_cast<size_t>(kPP + (PERM == 2 ? kXS : 0)) * sizeof(int32_t) : 0;
     auto kern = k_fused_sorted<SCHEME, SUMS, PERM>;
     static bool smem_attr_set = false;
     if (PERM && !smem_attr_set) {
@@ -1203,8 +1256,8 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(a.CL, 1, 1);
     // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us)
-    static int cached[2][2][2][17] = {};
-    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][PERM ? 1 : 0][a.CL];
+    static int cached[2][2][3][17] = {};
+    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][PERM][a.CL];
     if (max_clusters == 0) {
         if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
             cudaGetLastError();
@@ -1320,6 +1373,13 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
     return cudaPeekAtLastError();
 }
 
+// the in-place state gather fuses into k_fused_sorted for rows of 16 << k bytes (k <= 5),
+// 16-byte aligned rows
+bool fused_gather_supported(const void* X, int64_t row_bytes, int64_t ld, int64_t fld) {
+    if (!X || row_bytes < 16 || row_bytes > 512 || (row_bytes & (row_bytes - 1)) != 0) return false;
+    return (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 16 == 0 && fld % 16 == 0;
+}
+
 bool fused_supported(int scheme, int32_t P) {
     return (scheme == 2 || scheme == 3) && P >= 1 && P <= 8 * kPP;
 }
@@ -1327,7 +1387,8 @@ bool fused_supported(int scheme, int32_t P) {
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
-                                int32_t* permuted, cudaStream_t s, uint64_t* launches) {
+                                int32_t* permuted, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
+                                cudaStream_t s, uint64_t* launches) {
     FusedArgs a{};
     a.logw = logw;
     a.ld = ld;
@@ -1353,15 +1414,22 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.status_out = status_out;
     a.off = offspring;
     a.perm = permuted;
+    a.X = static_cast<char*>(X);
+    a.xld = x_ld;
+    a.xfld = x_fld;
+    a.xlg = 0;
+    while ((int64_t{16} << a.xlg) < x_row_bytes) ++a.xlg;
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
-    const bool pm = a.perm != nullptr;
+    const int pm = a.X ? 2 : (a.perm ? 1 : 0);
     if (scheme == 2) {
-        if (pm) e = a.sums ? launch_fused_t<2, true, true>(a, s) : launch_fused_t<2, false, true>(a, s);
-        else e = a.sums ? launch_fused_t<2, true, false>(a, s) : launch_fused_t<2, false, false>(a, s);
+        if (pm == 2) e = a.sums ? launch_fused_t<2, true, 2>(a, s) : launch_fused_t<2, false, 2>(a, s);
+        else if (pm == 1) e = a.sums ? launch_fused_t<2, true, 1>(a, s) : launch_fused_t<2, false, 1>(a, s);
+        else e = a.sums ? launch_fused_t<2, true, 0>(a, s) : launch_fused_t<2, false, 0>(a, s);
     } else {
-        if (pm) e = a.sums ? launch_fused_t<3, true, true>(a, s) : launch_fused_t<3, false, true>(a, s);
-        else e = a.sums ? launch_fused_t<3, true, false>(a, s) : launch_fused_t<3, false, false>(a, s);
+        if (pm == 2) e = a.sums ? launch_fused_t<3, true, 2>(a, s) : launch_fused_t<3, false, 2>(a, s);
+        else if (pm == 1) e = a.sums ? launch_fused_t<3, true, 1>(a, s) : launch_fused_t<3, false, 1>(a, s);
+        else e = a.sums ? launch_fused_t<3, true, 0>(a, s) : launch_fused_t<3, false, 0>(a, s);
     }
     ++*launches;
     if (e != cudaSuccess) return e;

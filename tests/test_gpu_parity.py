@@ -375,6 +375,57 @@ def test_batched_offspring_permute_gather(pf, dev, orc):
         assert np.array_equal(gX[n].cpu().numpy(), orc.gather_inplace(X[n], wp))
 
 
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_fused_state_gather(pf, dev, orc, scheme):
+    """pf_opts.state: the in-place state gather with the canonical permutation (NS-15/16), fused
+    into the cluster kernel (power-of-two rows of 16..512 bytes) or run after the permutation
+    (other schemes / sizes / row layouts).  Rows, ancestors, offspring and permutation bit-exact
+    against the oracle; padding between rows and filters untouched; an invalid filter."""
+    import torch
+
+    B = 5 if scheme == "metropolis" else 0
+    cases = [(3, 1000, 16, 16), (5, 8192, 4, 4), (2, 8193, 16, 20), (4, 65536, 128, 128), (2, 30000, 3, 3),
+             (1, 100003, 16, 16), (3, 200, 8, 8), (1, 1, 16, 16)]
+    for N, P, D, ldD in cases:
+        x = pfinputs.gaussian_logw(P, 1.0, seed=P + D, N=N)
+        if N > 2:
+            x[1, 7] = np.nan
+        X = np.stack([np.pad(pfinputs.state_matrix(P, D, seed=n), ((0, 0), (0, ldD - D)), constant_values=-3.0)
+                      for n in range(N)])
+        Xp = np.concatenate([X, np.full((N, 5, ldD), -9.0, np.float32)], axis=1)  # filter padding rows
+        gXp = _gpu(Xp, dev)
+        gX = gXp[:, :P, :D]
+        off = torch.empty((N, P), dtype=torch.int32, device=dev)
+        perm = torch.empty((N, P), dtype=torch.int32, device=dev)
+        c0 = pf.pf_launch_count()
+        a = pf.pf_resample_batched(scheme, _gpu(x, dev), 29, B=B, offspring_out=off, permuted_out=perm, state=gX)
+        torch.cuda.synchronize()
+        nl = pf.pf_launch_count() - c0
+        if scheme in ("stratified", "systematic") and P <= 65536 and D * 4 in (16, 32, 64, 128, 256, 512) \
+                and D == ldD:
+            assert nl == 1, (N, P, D, nl)
+        _, want = orc.resample_batched(scheme, x, 29, B=B)
+        assert np.array_equal(a.cpu().numpy(), want)
+        got = gXp.cpu().numpy()
+        for n in range(N):
+            wp = orc.permute(want[n])
+            assert np.array_equal(perm[n].cpu().numpy(), wp)
+            assert np.array_equal(off[n].cpu().numpy(), orc.ancestors_to_offspring(want[n]))
+            assert np.array_equal(got[n, :P, :D], orc.gather_inplace(X[n, :, :D], wp)), (scheme, N, P, D, n)
+        assert np.all(got[:, :P, D:] == -3.0) and np.all(got[:, P:] == -9.0)
+    # state without permuted_out / offspring_out (fused path writes neither)
+    N, P, D = 4, 20000, 16
+    x = pfinputs.gaussian_logw(P, 10.0, seed=3, N=N)
+    X = np.stack([pfinputs.state_matrix(P, D, seed=n + 50) for n in range(N)])
+    gX = _gpu(X, dev)
+    a = pf.pf_resample_batched(scheme, _gpu(x, dev), 30, B=B, state=gX)
+    torch.cuda.synchronize()
+    _, want = orc.resample_batched(scheme, x, 30, B=B)
+    assert np.array_equal(a.cpu().numpy(), want)
+    for n in range(N):
+        assert np.array_equal(gX[n].cpu().numpy(), orc.gather_inplace(X[n], orc.permute(want[n])))
+
+
 def test_repeatability_and_launch_count(pf, dev):
     import torch
 
@@ -384,7 +435,7 @@ def test_repeatability_and_launch_count(pf, dev):
     a2 = pf.pf_resample_stratified(x, 11)
     torch.cuda.synchronize()
     assert torch.equal(a1, a2)
-    assert pf.pf_launch_count() - c0 == 2  # one cluster kernel per call (P <= 8 x 16384)
+    assert pf.pf_launch_count() - c0 == 2  # one cluster kernel per call (P <= 8 x 8192)
     c0 = pf.pf_launch_count()
     pf.pf_resample_ex("stratified", x, 11, flags=pf.PF_NO_FUSION)
     torch.cuda.synchronize()
