@@ -186,23 +186,23 @@ constexpr int kCopyU = PF_COPY_U;
 __device__ __forceinline__ void copy_rows_warp(const FusedArgs& a, int n, const int32_t* owner, const int32_t* slot,
                                                int npairs, int lane) {
     char* Xf = a.X + static_cast<int64_t>(n) * a.xfld;
-    const int items = npairs << a.xlg;
-    const int cmask = (1 << a.xlg) - 1;
-    for (int b = 0; b < items; b += 32 * kCopyU) {
+    // a lane always handles the same 16-byte chunk of a row (32 is a multiple of the chunks per
+    // row); rows of one filter are < 2^32 bytes apart (P <= 65536 rows of <= 512 bytes)
+    const uint32_t ch = static_cast<uint32_t>(lane & ((1 << a.xlg) - 1)) * 16u;
+    const int rstep = 32 >> a.xlg;  // rows per warp instruction
+    const uint32_t xld = static_cast<uint32_t>(a.xld);
+    for (int p = lane >> a.xlg; p < npairs; p += kCopyU * rstep) {
         int4 v[kCopyU];
 #pragma unroll
         for (int u = 0; u < kCopyU; ++u) {
-            const int idx = b + 32 * u + lane;
-            if (idx < items)
-                v[u] = __ldcg(reinterpret_cast<const int4*>(Xf + static_cast<int64_t>(owner[idx >> a.xlg]) * a.xld +
-                                                            (idx & cmask) * 16));
+            const int q = p + u * rstep;
+            if (q < npairs)
+                v[u] = __ldcg(reinterpret_cast<const int4*>(Xf + (static_cast<uint32_t>(owner[q]) * xld + ch)));
         }
 #pragma unroll
         for (int u = 0; u < kCopyU; ++u) {
-            const int idx = b + 32 * u + lane;
-            if (idx < items)
-                __stcg(reinterpret_cast<int4*>(Xf + static_cast<int64_t>(slot[idx >> a.xlg]) * a.xld + (idx & cmask) * 16),
-                       v[u]);
+            const int q = p + u * rstep;
+            if (q < npairs) __stcg(reinterpret_cast<int4*>(Xf + (static_cast<uint32_t>(slot[q]) * xld + ch)), v[u]);
         }
     }
 }
@@ -1377,7 +1377,9 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
 // 16-byte aligned rows
 bool fused_gather_supported(const void* X, int64_t row_bytes, int64_t ld, int64_t fld) {
     if (!X || row_bytes < 16 || row_bytes > 512 || (row_bytes & (row_bytes - 1)) != 0) return false;
-    return (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 16 == 0 && fld % 16 == 0;
+    // row offsets inside a filter are computed in 32 bits: (8 x kPP) rows x ld < 2^32
+    return (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 16 == 0 && fld % 16 == 0 &&
+           ld * static_cast<int64_t>(8 * kPP) <= (int64_t{1} << 32);
 }
 
 bool fused_supported(int scheme, int32_t P) {
