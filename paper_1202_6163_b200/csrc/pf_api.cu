@@ -99,6 +99,24 @@ unsigned needs_for(int scheme) {
     return pf::kNeedQ;
 }
 
+// k_medium (one CTA per filter) against the cluster kernel and the multi-launch path, from
+// the measured table in profiles/r01_dispatch.md: it wins everywhere up to P = 2048 (the
+// cluster kernel idles most of its 8192-slot CTAs there), stays ahead for stratified and
+// small multinomial batches up to 4096, and loses above (a single CTA per filter limits the
+// parallelism of one filter to one SM).  Metropolis: only up to P = 1024.
+// P <= 256: the warp-per-filter kernel packs 8 filters per CTA and wins for batches of
+// >= 256 filters; below that the CTA-per-filter kernel has the lower latency
+// (3.3-3.8 us vs 5-8 us at N <= 64, profiles/r01_dispatch.md)
+#ifndef PF_SMALL_MIN_N
+#define PF_SMALL_MIN_N 256
+#endif
+bool medium_preferred(int scheme, int32_t N, int32_t P) {
+    if (P <= 1024) return true;
+    if (P <= 2048) return scheme != PF_METROPOLIS;
+    if (P <= 4096) return scheme == PF_STRATIFIED || (scheme == PF_MULTINOMIAL && N <= 128);
+    return false;
+}
+
 pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
                         cudaStream_t s) {
@@ -122,11 +140,19 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         return PF_ERR_INVALID_ARG;
 
     const bool no_fusion = (opts && (opts->flags & PF_NO_FUSION)) || g_no_fusion.load();
-    if (!no_fusion && pf::small_supported(P) && !permuted_out && !state) {
+    if (!no_fusion && pf::small_supported(P) && !permuted_out && !state && N >= PF_SMALL_MIN_N) {
         // one warp per filter, every scheme, one launch (pf_fused.cu k_small)
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_small(scheme, sorted_multi, logw, ld, N, P, seed, first_filter, B, anc, ld_anc,
                                                lse, ess, normw, status_out, offspring_out, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
+    if (!no_fusion && pf::medium_supported(P) && !permuted_out && !state && medium_preferred(scheme, N, P)) {
+        // one CTA per filter, every scheme, one launch (pf_fused.cu k_medium)
+        uint64_t nl = 0;
+        const cudaError_t e = pf::launch_medium(scheme, sorted_multi, logw, ld, N, P, seed, first_filter, B, anc,
+                                                ld_anc, lse, ess, normw, status_out, offspring_out, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }

@@ -1223,6 +1223,244 @@ __global__ void __launch_bounds__(kSmallWarps * 32) k_small(SmallArgs a) {
     }
 }
 
+// ============================================================================ medium filters
+// k_medium: ONE CTA per filter for 256 < P <= 8192, every scheme, everything in shared
+// memory (one launch; the latency path for single and few filters, Fig. 2's P range):
+//   a1   max + validation over float4 loads (log-weights kept in smem)
+//   a2+3 4-item-per-thread tiles: dexp, quantise, block scan with a running carry -> Q (smem)
+//   a6   the same tile scan of the spacings e_0..e_P -> G (smem)
+//   a4+5 slot k: its position (NS-8..NS-10, NS-12), a_k = upper_bound(Q, x_k) by binary
+//        search in smem (13 probes at 8192); Metropolis (a7): chains over the smem weights
+//   a8   offspring by shared-memory atomics
+// (256 threads up to P = 2048, 1024 threads above: the per-filter latency is serial work per
+// thread, profiles/r01_dispatch.md)
+constexpr int kMedP = 8192;
+
+template <int kMedT>
+__device__ __forceinline__ uint64_t med_block_excl_scan(uint64_t v, uint64_t* s_wt, int tid, uint64_t* total) {
+    constexpr int kMedW = kMedT / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint64_t incl = warp_incl_scan_u64(v, lane);
+    if (lane == 31) s_wt[warp] = incl;
+    __syncthreads();
+    uint64_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kMedW; ++w) {
+        const uint64_t t = s_wt[w];
+        wpre += (w < warp) ? t : 0ull;
+        tot += t;
+    }
+    __syncthreads();  // s_wt is reused by the next tile
+    *total = tot;
+    return wpre + incl - v;
+}
+
+template <int kMedT>
+__global__ void __launch_bounds__(kMedT) k_medium(SmallArgs a) {
+    constexpr int kMedW = kMedT / 32;
+    extern __shared__ __align__(16) unsigned char s_med[];
+    __shared__ uint64_t s_wt[kMedW];
+    __shared__ float s_fm[kMedW];
+    __shared__ int s_ib[kMedW];
+    __shared__ double s_dd[2][kMedW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int P = a.P;
+    const int P4 = (P + 3) & ~3;
+    uint64_t* Q = reinterpret_cast<uint64_t*>(s_med);               // [P4]
+    float* W = reinterpret_cast<float*>(Q + P4);                    // [P4]  logw, then w
+    int32_t* O = reinterpret_cast<int32_t*>(W + P4);                // [P4]  offspring counts
+    uint64_t* G = reinterpret_cast<uint64_t*>(O + P4);              // [P4 + 4] spacings scan (a6)
+    for (int n = blockIdx.x; n < a.N; n += gridDim.x) {
+        const float* row = a.logw + static_cast<int64_t>(n) * a.ld;
+        int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
+        int32_t* orow = a.off ? a.off + static_cast<int64_t>(n) * a.ld_anc : nullptr;
+        const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+        // ---- a1
+        float m = -INFINITY;
+        int bad = 0;
+        const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
+        for (int i0 = 4 * tid; i0 < P4; i0 += 4 * kMedT) {
+            float4 t;
+            if (vec && i0 + 3 < P) {
+                t = __ldcs(reinterpret_cast<const float4*>(row + i0));
+            } else {
+                t.x = (i0 + 0 < P) ? row[i0 + 0] : -INFINITY;
+                t.y = (i0 + 1 < P) ? row[i0 + 1] : -INFINITY;
+                t.z = (i0 + 2 < P) ? row[i0 + 2] : -INFINITY;
+                t.w = (i0 + 3 < P) ? row[i0 + 3] : -INFINITY;
+            }
+            reinterpret_cast<float4*>(W)[i0 >> 2] = t;
+            const float q4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                bad |= (isnan(q4[c]) || q4[c] == INFINITY) ? 1 : 0;
+                m = fmaxf(m, q4[c]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+            bad |= __shfl_xor_sync(kFull, bad, o);
+        }
+        if (lane == 0) { s_fm[warp] = m; s_ib[warp] = bad; }
+        __syncthreads();
+        m = -INFINITY;
+        bad = 0;
+#pragma unroll
+        for (int w = 0; w < kMedW; ++w) { m = fmaxf(m, s_fm[w]); bad |= s_ib[w]; }
+        if (bad || m == -INFINITY) {
+            for (int i = tid; i < P; i += kMedT) {
+                arow[i] = i;
+                if (orow) orow[i] = 1;
+                if (a.normw) a.normw[static_cast<int64_t>(n) * P + i] = NAN;
+            }
+            if (tid == 0) {
+                if (a.lse_out) a.lse_out[n] = NAN;
+                if (a.ess_out) a.ess_out[n] = NAN;
+                if (a.status_out) a.status_out[n] = 1;
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---- a2+a3: tiles of 4 x kMedT, running carry
+        double sw = 0.0, sw2 = 0.0;
+        uint64_t carry = 0;
+        for (int base = 0; base < P4; base += 4 * kMedT) {
+            const int i0 = base + 4 * tid;
+            uint64_t q[4] = {0, 0, 0, 0};
+            if (i0 < P4) {
+                float4 t = reinterpret_cast<float4*>(W)[i0 >> 2];
+                float* tv = reinterpret_cast<float*>(&t);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float w = weight(tv[c], m);
+                    tv[c] = w;
+                    sw += static_cast<double>(w);
+                    sw2 += static_cast<double>(w) * static_cast<double>(w);
+                    q[c] = quantise(w, a.kfx);
+                }
+                reinterpret_cast<float4*>(W)[i0 >> 2] = t;
+            }
+            uint64_t tot;
+            uint64_t run = carry + med_block_excl_scan<kMedT>(q[0] + q[1] + q[2] + q[3], s_wt, tid, &tot);
+            if (i0 < P4) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    run += q[c];
+                    Q[i0 + c] = run;
+                }
+            }
+            carry += tot;
+        }
+        const uint64_t Qtot = carry;
+        // sums in a fixed order: warp trees, then warps in order (deterministic)
+        sw = warp_sum_f64(sw);
+        sw2 = warp_sum_f64(sw2);
+        if (lane == 0) { s_dd[0][warp] = sw; s_dd[1][warp] = sw2; }
+        if (a.off)
+            for (int i = tid; i < P; i += kMedT) O[i] = 0;
+        __syncthreads();
+        double S = 0.0, S2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < kMedW; ++w) { S += s_dd[0][w]; S2 += s_dd[1][w]; }
+        if (tid == 0) {
+            if (a.lse_out) a.lse_out[n] = static_cast<double>(m) + log(S);
+            if (a.ess_out) a.ess_out[n] = S * S / S2;
+            if (a.status_out) a.status_out[n] = 0;
+        }
+        if (a.normw)
+            for (int i = tid; i < P; i += kMedT)
+                a.normw[static_cast<int64_t>(n) * P + i] = static_cast<float>(static_cast<double>(W[i]) / S);
+        // ---- a4+a5 / a6 / a7
+        if (a.scheme == 4) {
+            const float kU = __uint_as_float(0x33800000u);
+            for (int i = tid; i < P; i += kMedT) {
+                int32_t k = i;
+                float wk = W[i];
+                for (int32_t b = 0; b < a.B; b += 2) {
+                    const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>(b >> 1), 4u, filt,
+                                             a.key.k0, a.key.k1);
+                    const uint32_t j0 = __umulhi(r.x, static_cast<uint32_t>(P));
+                    const float u0 = __fmul_rn(static_cast<float>(r.y >> 8), kU);
+                    const float w0 = W[j0];
+                    if (__fmul_rn(u0, wk) < w0) { k = j0; wk = w0; }
+                    if (b + 1 < a.B) {
+                        const uint32_t j1 = __umulhi(r.z, static_cast<uint32_t>(P));
+                        const float u1 = __fmul_rn(static_cast<float>(r.w >> 8), kU);
+                        const float w1 = W[j1];
+                        if (__fmul_rn(u1, wk) < w1) { k = j1; wk = w1; }
+                    }
+                }
+                arow[i] = k;
+                if (a.off) atomicAdd(&O[k], 1);
+            }
+        } else if (a.sorted) {
+            // spacings e_0..e_P (NS-12), tile scan into G
+            uint64_t gc = 0;
+            const int PG = P + 1;
+            for (int base = 0; base < PG; base += 4 * kMedT) {
+                const int k0 = base + 4 * tid;
+                uint64_t e[4] = {0, 0, 0, 0};
+                if (k0 < PG) {
+                    const u32x4 r = philox10(static_cast<uint32_t>(k0 >> 2), 0u, 5u, filt, a.key.k0, a.key.k1);
+                    const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) e[c] = (k0 + c < PG) ? spacing_from_word(wd[c]) : 0ull;
+                }
+                uint64_t tot;
+                uint64_t run = gc + med_block_excl_scan<kMedT>(e[0] + e[1] + e[2] + e[3], s_wt, tid, &tot);
+                if (k0 < PG) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        run += e[c];
+                        if (k0 + c < PG) G[k0 + c] = run;
+                    }
+                }
+                gc += tot;
+            }
+            __syncthreads();
+            const uint64_t GP = gc;
+            for (int k = tid; k < P; k += kMedT) {
+                const int32_t anc = small_upper_bound(Q, P, muldiv_floor(G[k], Qtot, GP));
+                arow[k] = anc;
+                if (a.off) atomicAdd(&O[anc], 1);
+            }
+        } else {
+            __syncthreads();  // Q complete
+            uint64_t rho = 0;
+            if (a.scheme == 3) rho = mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D);
+            for (int k = 2 * tid; k < P; k += 2 * kMedT) {
+                const u32x4 r = (a.scheme == 3) ? u32x4{0u, 0u, 0u, 0u}
+                                                : philox10(static_cast<uint32_t>(k >> 1), 0u,
+                                                           static_cast<uint32_t>(a.scheme), filt, a.key.k0, a.key.k1);
+                uint64_t x0, x1;
+                if (a.scheme == 1) {
+                    x0 = mulhi64(lo_word(r), Qtot);
+                    x1 = mulhi64(hi_word(r), Qtot);
+                } else {
+                    const uint64_t r0 = (a.scheme == 2) ? mulhi64(lo_word(r), a.D) : rho;
+                    const uint64_t r1 = (a.scheme == 2) ? mulhi64(hi_word(r), a.D) : rho;
+                    x0 = mulhi64(static_cast<uint64_t>(k) * a.D + r0, Qtot);
+                    x1 = mulhi64(static_cast<uint64_t>(k + 1) * a.D + r1, Qtot);
+                }
+                const int32_t a0 = small_upper_bound(Q, P, x0);
+                arow[k] = a0;
+                if (a.off) atomicAdd(&O[a0], 1);
+                if (k + 1 < P) {
+                    const int32_t a1 = small_upper_bound(Q, P, x1);
+                    arow[k + 1] = a1;
+                    if (a.off) atomicAdd(&O[a1], 1);
+                }
+            }
+        }
+        if (a.off) {
+            __syncthreads();
+            for (int i = tid; i < P; i += kMedT) orow[i] = O[i];
+        }
+        __syncthreads();  // smem reused by the next filter
+    }
+}
+
 int device_sms() {
     static int sms = 0;
     if (!sms) {
@@ -1371,6 +1609,59 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
     }
     ++*launches;
     return cudaPeekAtLastError();
+}
+
+bool medium_supported(int32_t P) { return P >= 1 && P <= kMedP; }
+
+template <int T>
+cudaError_t launch_medium_t(const SmallArgs& a, size_t smem, cudaStream_t s, uint64_t* launches) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_medium<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kMedP * (8 + 4 + 4) + (kMedP + 4) * 8));
+        attr = true;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_medium<T>, T, smem) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.N, static_cast<int64_t>(device_sms()) * occ));
+    {
+        ProfScope ps_("k_medium", s);
+        k_medium<T><<<grid, T, smem, s>>>(a);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_medium(int scheme, bool sorted, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                          uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, double* lse_out,
+                          double* ess_out, float* normw, int32_t* status_out, int32_t* offspring, cudaStream_t s,
+                          uint64_t* launches) {
+    SmallArgs a{};
+    a.logw = logw;
+    a.ld = ld;
+    a.N = N;
+    a.P = P;
+    a.scheme = scheme;
+    a.B = B;
+    a.sorted = sorted ? 1 : 0;
+    const int m = ceil_log2(P);
+    a.kfx = 61 - m;
+    a.D = (P <= 1) ? 0 : (((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P)));
+    a.key = make_key(seed);
+    a.filt0 = first_filter;
+    a.anc = anc;
+    a.ld_anc = ld_anc;
+    a.lse_out = lse_out;
+    a.ess_out = ess_out;
+    a.normw = normw;
+    a.status_out = status_out;
+    a.off = offspring;
+    const size_t P4 = (static_cast<size_t>(P) + 3) & ~size_t{3};
+    const size_t smem = P4 * (8 + 4 + 4) + (sorted ? (P4 + 4) * 8 : 0);
+    return (P <= 2048) ? launch_medium_t<256>(a, smem, s, launches) : launch_medium_t<1024>(a, smem, s, launches);
 }
 
 // the in-place state gather fuses into k_fused_sorted for rows of 16 << k bytes (k <= 5),

@@ -140,6 +140,13 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
                          double* ess_out, float* normw, int32_t* status_out, int32_t* offspring, cudaStream_t s,
                          uint64_t* launches);
 
+// One-CTA-per-filter kernel for 256 < P <= 8192, every scheme (pf_fused.cu).
+bool medium_supported(int32_t P);
+cudaError_t launch_medium(int scheme, bool sorted, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                          uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, double* lse_out,
+                          double* ess_out, float* normw, int32_t* status_out, int32_t* offspring, cudaStream_t s,
+                          uint64_t* launches);
+
 // One-launch cooperative resampler for large filters (pf_fused.cu).
 bool coop_supported(int scheme, int32_t N, int32_t P);
 size_t coop_scratch_bytes();

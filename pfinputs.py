@@ -6,8 +6,9 @@ Recipe:
   * Gaussian log-weights logw_i = sigma * z_i, z ~ N(0,1) from numpy PCG64,
     cast to float32; sigma^2 in {0.1, 1, 10}.
   * Paper-matched Dirichlet(alpha) weights as log Gamma(alpha)
-    draws: logw_i = log G_i, G_i ~ Gamma(alpha) (normalisation is irrelevant
-    to every scheme: only ratios enter).
+    draws: logw_i = log G_i, G_i ~ Gamma(alpha), drawn in log space (no underflow
+    at alpha = .01); normalisation is irrelevant to every scheme: only ratios
+    enter, P:125-131.
   * Edge-case sets: all-equal, single support (-inf elsewhere), runs of -inf,
     NaN / +inf / all -inf (invalid).
   * Replicate r uses resampling seed splitmix64(BASE_SEED + r).
@@ -53,10 +54,14 @@ def gaussian_logw_torch(P: int, var: float, seed: int, N: int, device):
 
 
 def dirichlet_logw(P: int, alpha: float, seed: int = BASE_SEED) -> np.ndarray:
+    """log G_i, G_i ~ Gamma(alpha), drawn in log space so that small alpha does not
+    underflow to zero weights: G_alpha = G_{alpha+1} U^{1/alpha} (Marsaglia & Tsang),
+    so log G = log G_{alpha+1} + log(U) / alpha (same law)."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    g = rng.standard_gamma(alpha, size=P)
+    g1 = rng.standard_gamma(alpha + 1.0, size=P)
+    u = rng.random(size=P)
     with np.errstate(divide="ignore"):
-        return np.log(g).astype(np.float32)
+        return (np.log(g1) + np.log(u) / alpha).astype(np.float32)
 
 
 def equal_logw(P: int, value: float = 0.0) -> np.ndarray:

@@ -245,6 +245,35 @@ def test_bench_config_sampled(pf, dev, orc, scheme):
         assert np.array_equal(a[n].cpu().numpy(), want), (scheme, n)
 
 
+@pytest.mark.parametrize("scheme", ["systematic", "stratified"])
+def test_bench_step_sampled(pf, dev, orc, scheme):
+    """The exact step bench.py times (C3 at full size: 1024 filters x 2^16, sigma^2 = 1, one
+    pf_resample_batched call with offspring, permutation and the D = 16 state gather, one launch);
+    sampled filters checked in full against the oracle: ancestors, offspring, permutation, rows."""
+    import torch
+
+    N, P, D = 1024, 1 << 16, 16
+    x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+    X = torch.randn((N, P, D), generator=torch.Generator(device=dev).manual_seed(1), device=dev)
+    X0 = {n: X[n].cpu().numpy() for n in (0, 3, 500, 1023)}
+    anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+    off = torch.empty_like(anc)
+    perm = torch.empty_like(anc)
+    c0 = pf.pf_launch_count()
+    pf.pf_resample_batched(scheme, x, pfinputs.seed_for(0), ancestors=anc, offspring_out=off, permuted_out=perm,
+                           state=X)
+    torch.cuda.synchronize()
+    assert pf.pf_launch_count() - c0 == 1
+    for n, Xn in X0.items():
+        _, want = orc.resample(scheme, x[n].cpu().numpy(), pfinputs.seed_for(0), filter_index=n)
+        assert np.array_equal(anc[n].cpu().numpy(), want), n
+        assert np.array_equal(off[n].cpu().numpy(), orc.ancestors_to_offspring(want)), n
+        wp = orc.permute(want)
+        assert np.array_equal(perm[n].cpu().numpy(), wp), n
+        assert np.array_equal(X[n].cpu().numpy(), orc.gather_inplace(Xn, wp)), n
+    del X
+
+
 @pytest.mark.parametrize("P", [1 << 20, (1 << 22) + 12345, 1 << 24])
 def test_large_single_filter(pf, dev, orc, P):
     """C2 (2^20) and larger single filters in full, all prefix-sum schemes; Metropolis on sampled chains."""
@@ -563,6 +592,54 @@ def test_small_filters_warp_kernel(pf, dev, orc, scheme):
                     assert (np.isnan(wl) and np.isnan(L[n])) or abs(L[n] - wl) <= 1e-6 * max(1.0, abs(wl))
         finally:
             pf.pf_set_fusion(True)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES + ["sorted"])
+def test_medium_filters_cta_kernel(pf, dev, orc, scheme):
+    """256 < P <= 8192: the one-CTA-per-filter kernel (every scheme, a6 included; one launch; taken
+    up to P = 1024 always, above per the measured dispatch rule) and whatever the dispatch picks
+    above it, against the oracle: ragged sizes, batched with invalid filters, ld > P, -inf runs,
+    heavy weights, side outputs (lse, ESS, normalised weights, status) and offspring."""
+    import torch
+
+    sch = "multinomial" if scheme == "sorted" else scheme
+    flags = pf.PF_SORTED if scheme == "sorted" else 0
+    B = 13 if scheme == "metropolis" else 0
+    for N, P in ((1, 257), (1, 1000), (3, 4096), (2, 4097), (5, 8191), (1, 8192), (40, 777)):
+        ld = P + 5
+        x = pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(ld, 1.0 if N % 2 else 10.0, seed=N + P, N=N))
+        if N > 4:
+            x[2, 9] = np.nan
+            x[3, :] = -np.inf
+        g = _gpu(x, dev)[:, :P]
+        st = torch.empty(N, dtype=torch.int32, device=dev)
+        lse = torch.empty(N, dtype=torch.float64, device=dev)
+        ess = torch.empty(N, dtype=torch.float64, device=dev)
+        nw = torch.empty((N, P), dtype=torch.float32, device=dev)
+        off = torch.empty((N, P), dtype=torch.int32, device=dev)
+        c0 = pf.pf_launch_count()
+        a = pf.pf_resample_batched(sch, g, 1234, B=B, first_filter=9, status_out=st, lse_out=lse, ess_out=ess,
+                                   normw_out=nw, offspring_out=off, flags=flags)
+        torch.cuda.synchronize()
+        if P <= 1024:
+            assert pf.pf_launch_count() - c0 == 1, (scheme, N, P)
+        A, O, S, L, E, V = (a.cpu().numpy(), off.cpu().numpy(), st.cpu().numpy(), lse.cpu().numpy(),
+                            ess.cpu().numpy(), nw.cpu().numpy())
+        for n in range(N):
+            xn = np.ascontiguousarray(x[n, :P])
+            s_, w_, wl, wv, we = orc.resample("systematic", xn, 1, side=True)
+            if scheme == "sorted":
+                s_, want = orc.resample_sorted_multinomial(xn, 1234, filter_index=9 + n)
+            else:
+                s_, want = orc.resample(sch, xn, 1234, B=B, filter_index=9 + n)
+            assert S[n] == s_ and np.array_equal(A[n], want), (scheme, N, P, n)
+            assert np.array_equal(O[n], orc.ancestors_to_offspring(want))
+            if s_:
+                assert np.isnan(L[n]) and np.isnan(E[n])
+                continue
+            assert abs(L[n] - wl) <= 1e-6 * max(1.0, abs(wl))
+            assert abs(E[n] - we) <= 1e-6 * we
+            assert np.all(np.abs(V[n] - wv) <= 1e-6 * np.maximum(np.abs(wv), 1e-30) + 1e-12)
 
 
 def test_pf_linear_gaussian_c4(pf, dev, orc):

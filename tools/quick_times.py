@@ -19,6 +19,34 @@ def main():
     from tools.sweep import time_calls
 
     dev = torch.device("cuda:0")
+    if "--small" in sys.argv:
+        for P in (16, 64, 256):
+            for scheme in ("systematic", "multinomial", "metropolis"):
+                for N in (1, 4, 16, 64, 1024):
+                    x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+                    anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+                    b = 32 if scheme == "metropolis" else 0
+                    us = round(1e3 * time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, B=b, ancestors=anc), 10,
+                                                dev), 2)
+                    print(json.dumps({"P": P, "scheme": scheme, "N": N, "us": us}))
+                    sys.stdout.flush()
+        return
+    if "--medium" in sys.argv:
+        # k_medium (one CTA per filter) against the cluster kernel (N = 64 vs 65 straddles the
+        # k_medium batch limit of stratified/systematic) and against the multi-launch path
+        for P in (512, 1024, 2048, 4096, 8192):
+            for scheme in ("systematic", "stratified", "multinomial", "metropolis"):
+                for N in (1, 16, 64, 1024):
+                    x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+                    anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+                    b = 32 if scheme == "metropolis" else 0
+                    row = {"P": P, "scheme": scheme, "N": N}
+                    for name, fl in (("default", 0), ("unfused", pf.PF_NO_FUSION)):
+                        row[name + "_us"] = round(1e3 * time_calls(
+                            lambda: pf.pf_resample_batched(scheme, x, 5, B=b, ancestors=anc, flags=fl), 5, dev), 2)
+                    print(json.dumps(row))
+                    sys.stdout.flush()
+        return
     if "--coop-vs-unfused" in sys.argv:
         for P in (1 << 17, 1 << 18, 1 << 20, 1 << 22):
             for N in (1, 2, 4, 8, 16, 64):
