@@ -1461,25 +1461,19 @@ __global__ void __launch_bounds__(kMedT) k_medium(SmallArgs a) {
     }
 }
 
-int device_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+int device_sms() { return sm_count(); }
 
 template <int SCHEME, bool SUMS, int PERM>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     const size_t smem = PERM ? static_cast<size_t>(kPP + (PERM == 2 ? kXS : 0)) * sizeof(int32_t) : 0;
     auto kern = k_fused_sorted<SCHEME, SUMS, PERM>;
-    static bool smem_attr_set = false;
-    if (PERM && !smem_attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        smem_attr_set = true;
+    if (PERM) {
+        // a per-device function attribute: set once per device
+        static std::atomic<int> attr_set[kMaxDevices];
+        cached_per_device(attr_set, [&] {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            return 1;
+        });
     }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1494,14 +1488,15 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(a.CL, 1, 1);
     // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us)
-    static int cached[2][2][3][17] = {};
-    int& max_clusters = cached[SCHEME - 2][SUMS ? 1 : 0][PERM][a.CL];
-    if (max_clusters == 0) {
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+    static std::atomic<int> cached[17][kMaxDevices];
+    const int max_clusters = cached_per_device(cached[a.CL], [&] {
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
             cudaGetLastError();
-            max_clusters = std::max(1, device_sms() / a.CL);
+            mc = std::max(1, device_sms() / a.CL);
         }
-    }
+        return mc;
+    });
     const int clusters = std::max(1, std::min(a.N, max_clusters));
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * a.CL), 1, 1);
     return cudaLaunchKernelEx(&cfg, kern, a);
@@ -1530,14 +1525,15 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     const bool sums = lse_out || ess_out;
     void* kern = (scheme == 2) ? (sums ? (void*)k_coop_sorted<2, true> : (void*)k_coop_sorted<2, false>)
                                : (sums ? (void*)k_coop_sorted<3, true> : (void*)k_coop_sorted<3, false>);
-    static int per_sm[2][2] = {};
-    int& occ = per_sm[scheme - 2][sums ? 1 : 0];
-    if (occ == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, 0) != cudaSuccess || occ < 1) {
+    static std::atomic<int> per_sm[2][2][kMaxDevices];
+    const int occ = cached_per_device(per_sm[scheme - 2][sums ? 1 : 0], [&] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kFT, 0) != cudaSuccess || o < 1) {
             cudaGetLastError();
-            occ = 1;
+            o = 1;
         }
-    }
+        return o;
+    });
     int G = std::min(device_sms() * occ, 4096);
     // chunks are whole 8192-particle sub-tiles; never more CTAs than sub-tiles
     const int64_t tiles = (static_cast<int64_t>(P) + kPP - 1) / kPP;
@@ -1615,17 +1611,24 @@ bool medium_supported(int32_t P) { return P >= 1 && P <= kMedP; }
 
 template <int T>
 cudaError_t launch_medium_t(const SmallArgs& a, size_t smem, cudaStream_t s, uint64_t* launches) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<int> attr_set[kMaxDevices];
+    cached_per_device(attr_set, [] {
         cudaFuncSetAttribute(k_medium<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kMedP * (8 + 4 + 4) + (kMedP + 4) * 8));
-        attr = true;
-    }
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_medium<T>, T, smem) != cudaSuccess || occ < 1) {
-        cudaGetLastError();
-        occ = 1;
-    }
+        return 1;
+    });
+    // occupancy per (device, shared-memory size in KiB)
+    constexpr int kKiB = (kMedP * (8 + 4 + 4) + (kMedP + 4) * 8) / 1024 + 2;
+    static std::atomic<int> occ_cache[kKiB][kMaxDevices];
+    const size_t kib = (smem + 1023) / 1024;
+    const int occ = cached_per_device(occ_cache[kib], [&] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_medium<T>, T, kib * 1024) != cudaSuccess || o < 1) {
+            cudaGetLastError();
+            o = 1;
+        }
+        return o;
+    });
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.N, static_cast<int64_t>(device_sms()) * occ));
     {
         ProfScope ps_("k_medium", s);

@@ -1,11 +1,36 @@
 // pf_internal.h — internal launcher interface between the C ABI (pf_api.cu)
 // and the kernels (pf_kernels.cu).  Not installed; no torch types.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace pf {
+
+// Per-device cache of launch-geometry constants (SM count, occupancy): thread-safe (relaxed
+// atomics; a racing first use computes the same value twice) and correct for processes that
+// drive several devices.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        d = 0;
+    }
+    return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+template <class F>
+inline int cached_per_device(std::atomic<int>* slots, F&& compute) {
+    std::atomic<int>& slot = slots[current_device()];
+    int v = slot.load(std::memory_order_relaxed);
+    if (v == 0) {
+        v = compute();
+        slot.store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+int sm_count();  // SMs of the current device
 
 constexpr int kThreads = 256;           // every kernel: 8 warps
 constexpr int kItems = 16;              // items per thread in scan / merge tiles

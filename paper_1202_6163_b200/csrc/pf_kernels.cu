@@ -1605,17 +1605,6 @@ __global__ void k_lg_accumulate(const double* lse, double c, double* loglik) {
     if (threadIdx.x == 0) loglik[0] += lse[0] - c;
 }
 
-int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
 int64_t grid_for(int64_t work, int per_sm = 8) {
     const int64_t cap = static_cast<int64_t>(sm_count()) * per_sm;
     const int64_t need = cdiv(work, kThreads);
@@ -1623,6 +1612,20 @@ int64_t grid_for(int64_t work, int per_sm = 8) {
 }
 
 }  // namespace
+
+int sm_count() {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess ||
+            sms <= 0) {
+            cudaGetLastError();
+            sms = 148;
+        }
+        return sms;
+    });
+}
+
 
 // ============================================================================ host side
 Layout make_layout(int32_t N, int32_t P, unsigned need) {

@@ -43,6 +43,32 @@ def time_calls(fn, reps, dev):
     return e0.elapsed_time(e1) / (3 * reps)
 
 
+def write_md(rows, path):
+    """Markdown tables (particles/s) from the JSON rows of main()."""
+    schemes = []
+    for r in rows:
+        if r["scheme"] not in schemes:
+            schemes.append(r["scheme"])
+    out = ["# Round 1 sweep: resample-only throughput vs P and weight variance (tools/sweep.py)", "",
+           "One B200, device time per call of `pf_resample_batched` (calls captured in a CUDA graph; inputs "
+           "resident in HBM). Single filters (N = 1) and batches with N x P = 2^26. Values are particles/s. "
+           "Raw: `profiles/r01_sweep.jsonl`.", ""]
+    for batched in (False, True):
+        out += ["## " + ("batches (N x P = 2^26)" if batched else "single filter (N = 1)"), "",
+                "| P | sigma^2 | " + " | ".join(schemes) + " |", "|---|---|" + "---|" * len(schemes)]
+        cells = {}
+        for r in rows:
+            if r["batched"] == batched:
+                cells[(r["P"], r["var"], r["scheme"])] = r["particles_per_s"]
+        for P, var in sorted({(k[0], k[1]) for k in cells}):
+            lp = P.bit_length() - 1
+            vals = [f"{cells.get((P, var, sc), float('nan')):.2e}" for sc in schemes]
+            out.append(f"| 2^{lp} | {var} | " + " | ".join(vals) + " |")
+        out.append("")
+    with open(path, "w") as f:
+        f.write("\n".join(out) + "\n")
+
+
 def main():
     import torch
 
@@ -50,7 +76,8 @@ def main():
     import pfinputs
 
     dev = torch.device("cuda:0")
-    stream = torch.cuda.current_stream(dev)
+    md = sys.argv[sys.argv.index("--md") + 1] if "--md" in sys.argv else None
+    rows = []
     cases = [("systematic", 0, 0), ("stratified", 0, 0), ("multinomial", 0, 0),
              ("multinomial", 0, pf.PF_SORTED), ("metropolis", 32, 0)]
     for batched in (False, True):
@@ -67,10 +94,13 @@ def main():
                     ms = time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, B=B, ancestors=anc, flags=flags),
                                     reps, dev)
                     name = scheme + ("_sorted_a6" if flags else "") + (f"_B{B}" if B else "")
-                    print(json.dumps({"batched": batched, "N": N, "P": P, "var": var, "scheme": name,
-                                      "us_per_call": round(ms * 1e3, 2),
-                                      "particles_per_s": N * P / (ms / 1e3)}))
+                    row = {"batched": batched, "N": N, "P": P, "var": var, "scheme": name,
+                           "us_per_call": round(ms * 1e3, 2), "particles_per_s": N * P / (ms / 1e3)}
+                    rows.append(row)
+                    print(json.dumps(row))
                     sys.stdout.flush()
+    if md:
+        write_md(rows, md)
 
 
 if __name__ == "__main__":
