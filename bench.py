@@ -494,16 +494,17 @@ def run_ours(args):
         gms = g0.elapsed_time(g1) / max(3, min(args.steps, 10))
         extras["step_via_pf_permute_of_ancestors"] = {"ms": round(gms, 4), "particles_per_s": N * P / (gms / 1e3)}
 
-        # ---------------- end to end through the public API with host buffers
+        # ---------------- end to end through the public API with host buffers: the chunked
+        # host pipeline (paper_1202_6163_b200.pipeline) overlaps each chunk's H2D copy, kernel
+        # and D2H copy of the permutation on three streams
+        from paper_1202_6163_b200.pipeline import HostPipeline
+
         h_logw = logw.cpu().pin_memory()
         h_out = torch.empty((N, P), dtype=torch.int32).pin_memory()
-        d_logw = torch.empty_like(logw)
+        pipe = HostPipeline(N, P, dev, chunks=16)
 
         def e2e_step():
-            d_logw.copy_(h_logw, non_blocking=True)
-            pf.pf_resample_batched(scheme, d_logw, seed, B=B, first_filter=first, ancestors=anc, offspring_out=off,
-                                   permuted_out=perm, state=X, stream=stream)
-            h_out.copy_(perm, non_blocking=True)
+            pipe.run(scheme, h_logw, seed, h_out, B=B, first_filter=first, state=X, stream=stream)
 
         for _ in range(2):
             e2e_step()
@@ -522,7 +523,8 @@ def run_ours(args):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": N * P * world * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": N * P * 4, "d2h_bytes_per_step": N * P * 4,
-               "note": "host logw (pinned) -> H2D -> resample/permute/gather -> D2H permuted ancestors; "
+               "note": "host logw (pinned) -> H2D -> resample/permute/gather -> D2H permuted ancestors, "
+                       "16 chunks of filters overlapped on three streams (paper_1202_6163_b200.pipeline); "
                        "state X stays resident"}
     clocks = sampler.stop()
 
