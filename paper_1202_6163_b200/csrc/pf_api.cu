@@ -156,12 +156,17 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
-    if (!no_fusion && pf::fused_supported(scheme, P) &&
-        (!state || pf::fused_gather_supported(state, x_row, x_ld, x_fld))) {
+    // The cluster kernel gathers the state itself when the batch spans the GPU; a batch of few
+    // filters (one cluster each) would copy its rows through a handful of SMs, so there the
+    // permutation is fused and the gather runs as its own full-GPU kernel.
+    const bool fuse_gather = state && pf::fused_gather_supported(state, x_row, x_ld, x_fld) &&
+                             static_cast<int64_t>(N) * pf::fused_cluster_ctas(P) >= pf::sm_count();
+    if (!no_fusion && pf::fused_supported(scheme, N, P)) {
         // one launch per batch: cluster-per-filter kernel (ancestors, offspring, permutation and
         // the state gather), no workspace except the permutation when the state is gathered
         // without permuted_out (pf_fused.cu)
         int32_t* perm = permuted_out;
+        void* fstate = fuse_gather ? state : nullptr;
         if (state && !perm) {
             void* p = nullptr;
             const pf_status st = get_workspace(opts, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4, s, &p);
@@ -169,9 +174,11 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
             perm = static_cast<int32_t*>(p);
         }
         uint64_t nl = 0;
-        const cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
-                                                      ess, normw, status_out, offspring_out, perm, state,
-                                                      x_row, x_ld, x_fld, s, &nl);
+        cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse, ess,
+                                                normw, status_out, offspring_out, perm, fstate, x_row, x_ld, x_fld,
+                                                s, &nl);
+        if (e == cudaSuccess && state && !fstate)
+            e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }

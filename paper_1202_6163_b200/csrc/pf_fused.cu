@@ -40,12 +40,12 @@ namespace pf {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-#ifndef PF_FUSED_THREADS
-#define PF_FUSED_THREADS 512
-#endif
-// threads per CTA: 512 (2 CTAs / SM, so one CTA's barriers overlap the other's work;
-// measured 4% faster than 1024 x 1 at C3 and 1.4x at single filters of 2^18-2^20)
-constexpr int kFT = PF_FUSED_THREADS;
+// threads per CTA of the cooperative kernel and of the cluster kernel up to P = 65536: 512
+// (2 CTAs / SM, so one CTA's barriers overlap the other's work; measured 4% faster than
+// 1024 x 1 at C3 and 1.4x at single filters of 2^18-2^20).  The cluster kernel takes 1024
+// threads (16384 particles per CTA, clusters of up to 16) for 65536 < P <= 262144.
+constexpr int kFT = 512;
+constexpr int kMaxCL = 16;  // largest cluster (non-portable above 8)
 constexpr int kFW = kFT / 32;      // warps per CTA
 constexpr int kFI = 16;            // particles per thread
 constexpr int kFR = kFI / 4;       // 4 float4 rows
@@ -146,6 +146,7 @@ __device__ __forceinline__ void cta_clear8(int32_t* s_head, int tid) {
 // CTA-wide inclusive max-scan of the kXS marks in s_head, 8 consecutive per thread (the
 // caller has synchronised after marking): h[t] = max(carry, marks [0, 8 tid + t]); carry
 // (block-uniform) becomes the chunk maximum.  One barrier.
+template <int FW>
 __device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_wmax, int32_t h[8], int32_t& carry,
                                               int tid, int warp, int lane) {
     const int4* h4 = reinterpret_cast<const int4*>(s_head);
@@ -161,7 +162,7 @@ __device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_
     }
     if (lane == 31) s_wmax[warp] = incl;
     __syncthreads();
-    int32_t w = (lane < kFW) ? s_wmax[lane] : -1;
+    int32_t w = (lane < FW) ? s_wmax[lane] : -1;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int32_t u = __shfl_up_sync(kFull, w, o);
@@ -208,12 +209,20 @@ __device__ __forceinline__ void copy_rows_warp(const FusedArgs& a, int n, const 
 }
 
 // PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
-template <int SCHEME, bool SUMS, int PERM>
-__global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
+template <int SCHEME, bool SUMS, int PERM, int FT>
+__global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
+    // geometry of this instantiation (FT = 512: 8192 particles per CTA, clusters of <= 8;
+    // FT = 1024: 16384 per CTA, clusters of <= 16 for 65536 < P <= 262144)
+    constexpr int kFT = FT;
+    constexpr int kFW = FT / 32;
+    constexpr int kPP = FT * kFI;
+    constexpr int kTPL = kFR * kFW / 32;
+    constexpr int kXS = kFW * kChunk;
+    static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
     extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
     int32_t* s_pslot = s_fs + kPP;                    // PERM == 2: free slot of each extras rank of a chunk
     __shared__ Exchange s_x;
-    __shared__ uint32_t s_rf[9];
+    __shared__ uint32_t s_rf[kMaxCL + 1];
     __shared__ uint64_t s_poff;
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
@@ -513,7 +522,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
                 }
                 __syncthreads();
                 int32_t h[8];
-                cta_max_scan8(s_head, s_wmax, h, carry, tid, warp, lane);
+                cta_max_scan8<kFW>(s_head, s_wmax, h, carry, tid, warp, lane);
                 const uint32_t k0 = c0 + 8 * tid;
                 if (a.anc_vec && k0 >= k_lo && k0 + 8 <= K1) {
                     int4* dst = reinterpret_cast<int4*>(arow + k0);
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
                     if (lane >= o2) incl += u;
                 }
                 const uint64_t excl = incl - pt;
-                if (lane <= CL && lane < 9) s_rf[lane] = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
+                if (lane <= CL) s_rf[lane] = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
                 if (lane == c) s_poff = excl;
             }
             __syncthreads();
@@ -626,13 +635,13 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_fused_sorted(FusedArgs a) {
                     }
                     __syncthreads();
                     int32_t h[8];
-                    cta_max_scan8(s_head, s_wmax, h, carry, tid, warp, lane);
+                    cta_max_scan8<kFW>(s_head, s_wmax, h, carry, tid, warp, lane);
                     const uint32_t r0 = c0 + 8 * tid;
                     if (r0 < XC) {
                         uint32_t R = XC0 + r0;  // global free rank of this thread's first extra
                         int cc = 0;
 #pragma unroll
-                        for (int q2 = 1; q2 < 8; ++q2) cc += (q2 < CL && s_rf[q2] <= R) ? 1 : 0;
+                        for (int q2 = 1; q2 < kMaxCL; ++q2) cc += (q2 < CL && s_rf[q2] <= R) ? 1 : 0;
                         uint32_t rb = s_rf[cc], nxt = s_rf[cc + 1];
                         const int32_t* rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
 #pragma unroll
@@ -1463,43 +1472,91 @@ __global__ void __launch_bounds__(kMedT) k_medium(SmallArgs a) {
 
 int device_sms() { return sm_count(); }
 
-template <int SCHEME, bool SUMS, int PERM>
+template <int FT>
+constexpr size_t fused_smem(int perm) {
+    return perm ? static_cast<size_t>(FT * kFI + (perm == 2 ? (FT / 32) * kChunk : 0)) * sizeof(int32_t) : 0;
+}
+
+template <int SCHEME, bool SUMS, int PERM, int FT>
+void fused_set_attributes() {
+    // per-device function attributes: set once per device
+    static std::atomic<int> attr_set[kMaxDevices];
+    cached_per_device(attr_set, [] {
+        auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT>;
+        if (PERM)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(fused_smem<FT>(PERM)));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaGetLastError();
+        return 1;
+    });
+}
+
+template <int SCHEME, bool SUMS, int PERM, int FT>
+int fused_max_clusters(int CL) {
+    // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us);
+    // -1 = a cluster of this size cannot be scheduled on this device (0 = not queried yet)
+    static std::atomic<int> cached[kMaxCL + 1][kMaxDevices];
+    return cached_per_device(cached[CL], [&] {
+        fused_set_attributes<SCHEME, SUMS, PERM, FT>();
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(FT, 1, 1);
+        cfg.dynamicSmemBytes = fused_smem<FT>(PERM);
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(CL, 1, 1);
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, k_fused_sorted<SCHEME, SUMS, PERM, FT>, &cfg) != cudaSuccess ||
+            mc < 1) {
+            cudaGetLastError();
+            mc = -1;
+        }
+        return mc;
+    });
+}
+
+template <int SCHEME, bool SUMS, int PERM, int FT>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    const size_t smem = PERM ? static_cast<size_t>(kPP + (PERM == 2 ? kXS : 0)) * sizeof(int32_t) : 0;
-    auto kern = k_fused_sorted<SCHEME, SUMS, PERM>;
-    if (PERM) {
-        // a per-device function attribute: set once per device
-        static std::atomic<int> attr_set[kMaxDevices];
-        cached_per_device(attr_set, [&] {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            return 1;
-        });
-    }
+    fused_set_attributes<SCHEME, SUMS, PERM, FT>();
+    const int max_clusters = fused_max_clusters<SCHEME, SUMS, PERM, FT>(a.CL);
+    if (max_clusters < 1) return cudaErrorNotSupported;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = a.CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(kFT, 1, 1);
-    cfg.dynamicSmemBytes = smem;
+    cfg.blockDim = dim3(FT, 1, 1);
+    cfg.dynamicSmemBytes = fused_smem<FT>(PERM);
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(a.CL, 1, 1);
-    // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us)
-    static std::atomic<int> cached[17][kMaxDevices];
-    const int max_clusters = cached_per_device(cached[a.CL], [&] {
-        int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
-            cudaGetLastError();
-            mc = std::max(1, device_sms() / a.CL);
-        }
-        return mc;
-    });
     const int clusters = std::max(1, std::min(a.N, max_clusters));
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * a.CL), 1, 1);
-    return cudaLaunchKernelEx(&cfg, kern, a);
+    return cudaLaunchKernelEx(&cfg, k_fused_sorted<SCHEME, SUMS, PERM, FT>, a);
+}
+
+template <int FT>
+cudaError_t launch_fused_ft(int scheme, int pm, const FusedArgs& a, cudaStream_t s) {
+    if (scheme == 2) {
+        if (pm == 2) return a.sums ? launch_fused_t<2, true, 2, FT>(a, s) : launch_fused_t<2, false, 2, FT>(a, s);
+        if (pm == 1) return a.sums ? launch_fused_t<2, true, 1, FT>(a, s) : launch_fused_t<2, false, 1, FT>(a, s);
+        return a.sums ? launch_fused_t<2, true, 0, FT>(a, s) : launch_fused_t<2, false, 0, FT>(a, s);
+    }
+    if (pm == 2) return a.sums ? launch_fused_t<3, true, 2, FT>(a, s) : launch_fused_t<3, false, 2, FT>(a, s);
+    if (pm == 1) return a.sums ? launch_fused_t<3, true, 1, FT>(a, s) : launch_fused_t<3, false, 1, FT>(a, s);
+    return a.sums ? launch_fused_t<3, true, 0, FT>(a, s) : launch_fused_t<3, false, 0, FT>(a, s);
+}
+
+// can a 16-CTA cluster of 1024-thread CTAs be scheduled (one per GPC)?  cached per device
+bool big_clusters_ok() {
+    static std::atomic<int> ok[kMaxDevices];
+    return cached_per_device(ok, [] { return fused_max_clusters<3, false, 2, 1024>(kMaxCL) >= 1 ? 1 : -1; }) > 0;
 }
 
 }  // namespace
@@ -1671,13 +1728,24 @@ cudaError_t launch_medium(int scheme, bool sorted, const float* logw, int64_t ld
 // 16-byte aligned rows
 bool fused_gather_supported(const void* X, int64_t row_bytes, int64_t ld, int64_t fld) {
     if (!X || row_bytes < 16 || row_bytes > 512 || (row_bytes & (row_bytes - 1)) != 0) return false;
-    // row offsets inside a filter are computed in 32 bits: (8 x kPP) rows x ld < 2^32
+    // row offsets inside a filter are computed in 32 bits: (16 x 16384) rows x ld <= 2^32
     return (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ld % 16 == 0 && fld % 16 == 0 &&
-           ld * static_cast<int64_t>(8 * kPP) <= (int64_t{1} << 32);
+           ld * static_cast<int64_t>(kMaxCL * 1024 * kFI) <= (int64_t{1} << 32);
 }
 
-bool fused_supported(int scheme, int32_t P) {
-    return (scheme == 2 || scheme == 3) && P >= 1 && P <= 8 * kPP;
+int fused_cluster_ctas(int32_t P) {
+    const int FT = (P <= 8 * 512 * kFI) ? 512 : 1024;
+    return static_cast<int>((P + FT * kFI - 1) / (FT * kFI));
+}
+
+// P <= 65536: any batch.  65536 < P <= 262144 (clusters of 5..16 CTAs of 1024 threads): only
+// batches that span the GPU; a single big cluster per filter runs on <= 16 SMs, where the
+// cooperative kernel uses all of them (C4: 55.7 vs 62.6 us per PF step).
+bool fused_supported(int scheme, int32_t N, int32_t P) {
+    if (!(scheme == 2 || scheme == 3) || P < 1) return false;
+    if (P <= 8 * 512 * kFI) return true;
+    return P <= kMaxCL * 1024 * kFI && static_cast<int64_t>(N) * fused_cluster_ctas(P) >= sm_count() &&
+           big_clusters_ok();
 }
 
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
@@ -1690,7 +1758,9 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.ld = ld;
     a.N = N;
     a.P = P;
-    a.CL = static_cast<int32_t>((P + kPP - 1) / kPP);
+    // geometry: 512 threads (8192 particles per CTA) up to 8 CTAs, else 1024 threads (16384)
+    const int FT = (P <= 8 * 512 * kFI) ? 512 : 1024;
+    a.CL = static_cast<int32_t>((P + FT * kFI - 1) / (FT * kFI));
     int64_t pp = (P + a.CL - 1) / a.CL;
     pp = (pp + 3) / 4 * 4;
     a.PP = static_cast<int32_t>(pp);
@@ -1718,15 +1788,7 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
     const int pm = a.X ? 2 : (a.perm ? 1 : 0);
-    if (scheme == 2) {
-        if (pm == 2) e = a.sums ? launch_fused_t<2, true, 2>(a, s) : launch_fused_t<2, false, 2>(a, s);
-        else if (pm == 1) e = a.sums ? launch_fused_t<2, true, 1>(a, s) : launch_fused_t<2, false, 1>(a, s);
-        else e = a.sums ? launch_fused_t<2, true, 0>(a, s) : launch_fused_t<2, false, 0>(a, s);
-    } else {
-        if (pm == 2) e = a.sums ? launch_fused_t<3, true, 2>(a, s) : launch_fused_t<3, false, 2>(a, s);
-        else if (pm == 1) e = a.sums ? launch_fused_t<3, true, 1>(a, s) : launch_fused_t<3, false, 1>(a, s);
-        else e = a.sums ? launch_fused_t<3, true, 0>(a, s) : launch_fused_t<3, false, 0>(a, s);
-    }
+    e = (FT == 512) ? launch_fused_ft<512>(scheme, pm, a, s) : launch_fused_ft<1024>(scheme, pm, a, s);
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

@@ -150,8 +150,9 @@ cudaError_t launch_lg_accumulate(const double* lse, int32_t P, float sigma_y, do
                                  uint64_t* launches);
 
 // One-launch cluster-per-filter resampler for stratified/systematic (pf_fused.cu).
-bool fused_supported(int scheme, int32_t P);
+bool fused_supported(int scheme, int32_t N, int32_t P);
 bool fused_gather_supported(const void* X, int64_t row_bytes, int64_t ld, int64_t fld);
+int fused_cluster_ctas(int32_t P);  // CTAs per filter (cluster size) of the cluster kernel
 cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,

@@ -46,12 +46,13 @@ class LinearGaussianPF:
         pf = self.pf
         self.t += 1
         pf.pf_lg_propagate_weight(self.X, self.phi, self.sx, self.sy, y, self.seed, self.t, self.logw)
+        logw_snap = self.logw.cpu().numpy() if check else None
+        # resample (lse, offspring, canonical permutation) and gather the state in place: one launch
+        # of the cluster kernel for stratified / systematic up to P = 2^18
         pf.pf_resample_ex(self.scheme, self.logw, step_seed(self.seed, self.t), self.B, ancestors=self.anc,
-                          lse_out=self.lse, offspring_out=self.off)
-        snap = (self.logw.cpu().numpy(), self.anc.cpu().numpy(), step_seed(self.seed, self.t)) if check else None
+                          lse_out=self.lse, offspring_out=self.off, permuted_out=self.perm, state=self.X)
+        snap = (logw_snap, self.anc.cpu().numpy(), step_seed(self.seed, self.t)) if check else None
         pf.pf_lg_accumulate(self.lse, self.P, self.sy, self.loglik)
-        pf.pf_permute_offspring(self.off, permuted=self.perm)
-        pf.pf_gather_state(self.X, self.perm)
         return snap
 
     def run(self, ys):

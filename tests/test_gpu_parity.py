@@ -112,7 +112,7 @@ def test_large_filter_batches_dispatch(pf, dev, orc, scheme):
     filters); both bit-exact against the oracle."""
     import torch
 
-    P = 1 << 18
+    P = 1 << 19
     x = pfinputs.gaussian_logw(P, 1.0, seed=77, N=3)
     g = _gpu(x, dev)
     c0 = pf.pf_launch_count()
@@ -130,15 +130,27 @@ def test_large_filter_batches_dispatch(pf, dev, orc, scheme):
 
 @pytest.mark.parametrize("scheme", ["stratified", "systematic"])
 def test_cluster_path_sizes(pf, dev, orc, scheme):
-    """Cluster sizes 1..8 of the one-launch kernel (P up to 8 x 8192), ragged CTA ranges, skew; and the
-    sizes just above it (cooperative kernel)."""
+    """Cluster sizes 1..8 of the one-launch kernel (512 threads, P up to 8 x 8192) and 5..16 of its
+    1024-thread form (P up to 16 x 16384, non-portable cluster sizes), ragged CTA ranges, skew."""
     import torch
 
-    for P in (8191, 8192, 8193, 16384 + 5, 24576, 49152 + 3, 65535, 65536, 65537, 98304 + 7, 131072):
+    for P in (8191, 8192, 8193, 16384 + 5, 24576, 49152 + 3, 65535, 65536, 65537, 98304 + 7, 131072,
+              131073, 200003, 262143, 262144):
         x = pfinputs.gaussian_logw(P, 10.0, seed=P)
         a = _run(pf, dev, scheme, x, 31)
         _, want = orc.resample(scheme, x, 31)
         assert np.array_equal(a, want), (scheme, P)
+    # the 1024-thread form (clusters of 5..16) runs for batches that span the GPU
+    for N, P in ((40, 65537), (20, 131072 + 5), (10, 262144)):
+        x = pfinputs.gaussian_logw(P, 10.0, seed=P + N, N=N)
+        c0 = pf.pf_launch_count()
+        a = pf.pf_resample_batched(scheme, _gpu(x, dev), 32, first_filter=7)
+        torch.cuda.synchronize()
+        assert pf.pf_launch_count() - c0 == 1
+        A = a.cpu().numpy()
+        for n in (0, N // 2, N - 1):
+            _, want = orc.resample(scheme, x[n], 32, filter_index=7 + n)
+            assert np.array_equal(A[n], want), (scheme, N, P, n)
     # batched with more filters than resident clusters, ld > P, an invalid filter
     N, P, ld = 300, 20000, 20004
     x = pfinputs.gaussian_logw(ld, 1.0, seed=5, N=N)
@@ -444,7 +456,8 @@ def test_fused_state_gather(pf, dev, orc, scheme):
 
     B = 5 if scheme == "metropolis" else 0
     cases = [(3, 1000, 16, 16), (5, 8192, 4, 4), (2, 8193, 16, 20), (4, 65536, 128, 128), (2, 30000, 3, 3),
-             (1, 100003, 16, 16), (3, 200, 8, 8), (1, 1, 16, 16)]
+             (1, 100003, 16, 16), (3, 200, 8, 8), (1, 1, 16, 16), (2, 1 << 18, 16, 16), (1, 300000, 16, 16),
+             (150, 3000, 16, 16), (20, 65536, 16, 16), (10, 1 << 18, 16, 16)]
     for N, P, D, ldD in cases:
         x = pfinputs.gaussian_logw(P, 1.0, seed=P + D, N=N)
         if N > 2:
@@ -460,9 +473,13 @@ def test_fused_state_gather(pf, dev, orc, scheme):
         a = pf.pf_resample_batched(scheme, _gpu(x, dev), 29, B=B, offspring_out=off, permuted_out=perm, state=gX)
         torch.cuda.synchronize()
         nl = pf.pf_launch_count() - c0
-        if scheme in ("stratified", "systematic") and P <= 65536 and D * 4 in (16, 32, 64, 128, 256, 512) \
-                and D == ldD:
-            assert nl == 1, (N, P, D, nl)
+        cl = -(-P // 8192) if P <= 65536 else -(-P // 16384)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        if scheme in ("stratified", "systematic") and (P <= 65536 or (P <= (1 << 18) and N * cl >= sms)):
+            # one cluster-kernel launch; the gather is fused when the batch spans the GPU (N x cluster
+            # CTAs >= SMs) and the rows allow it, else it follows as one more launch
+            fused = D * 4 in (16, 32, 64, 128, 256, 512) and D == ldD and N * cl >= sms
+            assert nl == (1 if fused else 2), (N, P, D, nl)
         _, want = orc.resample_batched(scheme, x, 29, B=B)
         assert np.array_equal(a.cpu().numpy(), want)
         got = gXp.cpu().numpy()
