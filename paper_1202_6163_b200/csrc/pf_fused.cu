@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     __shared__ int s_bad;
     __shared__ uint64_t s_u64[4];
     __shared__ uint32_t s_prevE;
+    __shared__ int32_t s_wmax[kFW];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
@@ -961,50 +962,38 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     }
                 }
             }
-            int4* b4 = reinterpret_cast<int4*>(s_buf[warp]);
-#pragma unroll
-            for (int j = 0; j < kFR; ++j) {
-                const uint32_t S0 = __shfl_sync(kFull, first[j], 0);
-                const uint32_t S1 = __shfl_sync(kFull, E[j * 4 + 3], 31);
+            // the sub-tile's slots [K0, K1): CTA-wide chunks of kXS slots, head marks + max-scan,
+            // aligned vector stores except at the two ends (as in k_fused_sorted phase C)
+            {
+                int32_t* s_head = &s_buf[0][0];
+                const uint32_t K0 = s_prevE, K1 = s_lastE[kFR - 1][kFW - 1];
                 int32_t cy = -1;
-                for (uint32_t q0 = S0 & ~3u; q0 < S1; q0 += kChunk) {
-                    b4[2 * lane] = make_int4(-1, -1, -1, -1);
-                    b4[2 * lane + 1] = make_int4(-1, -1, -1, -1);
-                    __syncwarp();
+                for (uint32_t q0 = K0 & ~7u; q0 < K1; q0 += kXS) {
+                    cta_clear8(s_head, tid);
+                    __syncthreads();
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                        const uint32_t rel = pe - q0;
-                        if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kChunk))
-                            s_buf[warp][rel] = idbase + j * (kFT * 4) + q;
+                    for (int j = 0; j < kFR; ++j) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
+                            const uint32_t rel = pe - q0;
+                            if (E[j * 4 + q] > pe && rel < static_cast<uint32_t>(kXS))
+                                s_head[rel] = idbase + j * (kFT * 4) + q;
+                        }
                     }
-                    __syncwarp();
-                    const int4 lo = b4[2 * lane], hi = b4[2 * lane + 1];
-                    int32_t h[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                    for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
-                    int32_t incl = h[7];
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int32_t u = __shfl_up_sync(kFull, incl, o);
-                        if (lane >= o) incl = max(incl, u);
-                    }
-                    int32_t pre = __shfl_up_sync(kFull, incl, 1);
-                    pre = max(cy, (lane == 0) ? -1 : pre);
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
-                    cy = max(cy, __shfl_sync(kFull, incl, 31));
-                    const uint32_t k0 = q0 + 8 * lane;
-                    if (a.anc_vec && k0 >= S0 && k0 + 8 <= S1) {
+                    __syncthreads();
+                    int32_t h[8];
+                    cta_max_scan8<kFW>(s_head, s_wmax, h, cy, tid, warp, lane);
+                    const uint32_t k0 = q0 + 8 * tid;
+                    if (a.anc_vec && k0 >= K0 && k0 + 8 <= K1) {
                         int4* dst = reinterpret_cast<int4*>(arow + k0);
                         __stcs(dst, make_int4(h[0], h[1], h[2], h[3]));
                         __stcs(dst + 1, make_int4(h[4], h[5], h[6], h[7]));
-                    } else {
+                    } else if (k0 + 8 > K0 && k0 < K1) {
 #pragma unroll
                         for (int t = 0; t < 8; ++t)
-                            if (k0 + t >= S0 && k0 + t < S1) arow[k0 + t] = h[t];
+                            if (k0 + t >= K0 && k0 + t < K1) arow[k0 + t] = h[t];
                     }
-                    __syncwarp();
                 }
             }
             carry += s_u64[2];
