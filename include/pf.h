@@ -148,8 +148,14 @@ pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_lo
                               uint64_t seed, uint32_t first_filter, int32_t B,
                               int32_t* ancestors, int64_t ld_anc, const pf_opts* opts, pf_stream_t stream);
 
-/* Workspace bytes a call with these sizes needs (for explicit workspaces). */
+/* Workspace bytes a call with these sizes needs (for explicit workspaces, pf_opts.workspace):
+ * the maximum over every path the call may take.  _ex takes the pf_opts.flags (PF_SORTED needs
+ * the spacings scan) and the ancestors' row stride; pf_workspace_bytes(s, N, P) =
+ * pf_workspace_bytes_ex(s, N, P, 0, P).  Returns 0 for invalid arguments.  An explicit workspace
+ * is not supported together with permuted_out or state on the multi-launch path (multinomial,
+ * Metropolis, P above the cluster kernel): those calls return PF_ERR_UNSUPPORTED. */
 size_t pf_workspace_bytes(pf_scheme scheme, int32_t N, int32_t P);
+size_t pf_workspace_bytes_ex(pf_scheme scheme, int32_t N, int32_t P, uint32_t flags, int64_t ld_anc);
 
 /*
  * Ancestors -> offspring (NS-14): offspring[i] = #{k : anc[k] == i}.

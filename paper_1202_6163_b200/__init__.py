@@ -60,6 +60,7 @@ _SIGS = {
     "pf_resample_ex": ([ctypes.c_int, _V, _I32, _U64, _I32, _V, _V, _V], ctypes.c_int),
     "pf_resample_batched": ([ctypes.c_int, _V, _I64, _I32, _I32, _U64, _U32, _I32, _V, _I64, _V, _V], ctypes.c_int),
     "pf_workspace_bytes": ([ctypes.c_int, _I32, _I32], _SZ),
+    "pf_workspace_bytes_ex": ([ctypes.c_int, _I32, _I32, _U32, _I64], _SZ),
     "pf_ancestors_to_offspring": ([_V, _I32, _V, _V], ctypes.c_int),
     "pf_ancestors_to_offspring_batched": ([_V, _I64, _I32, _I32, _V, _I64, _V], ctypes.c_int),
     "pf_permute": ([_V, _I32, _V, _V], ctypes.c_int),
@@ -198,8 +199,9 @@ def _set_state(opts, state, batched: bool):
 # ----------------------------------------------------------------------------- resamplers
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
                    lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                   permuted_out=None, flags: int = 0, state=None, stream=None):
+                   permuted_out=None, flags: int = 0, state=None, workspace=None, stream=None):
     """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor.
+    workspace: optional device tensor (256-byte aligned, >= pf_workspace_bytes) instead of the pool.
     state: optional [P, ...] tensor gathered in place with the canonical permutation (NS-15/16)."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -223,6 +225,7 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
     if permuted_out is not None:
         _need_cuda(permuted_out, torch.int32, "permuted_out"); opts.permuted_out = permuted_out.data_ptr()
     _set_state(opts, state, False)
+    _set_workspace(opts, workspace)
     rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
                               ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_ex")
@@ -257,8 +260,9 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
                         lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
-                        permuted_out=None, flags: int = 0, state=None, stream=None):
+                        permuted_out=None, flags: int = 0, state=None, workspace=None, stream=None):
     """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P].
+    workspace: optional device tensor (256-byte aligned, >= pf_workspace_bytes) instead of the pool.
     state: optional [N, P, ...] tensor gathered in place with the canonical permutation."""
     torch = _torch()
     _need_cuda(logw, torch.float32, "logw")
@@ -278,14 +282,27 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
             _need_cuda(t, dt, name)
             setattr(opts, name, t.data_ptr())
     _set_state(opts, state, True)
+    _set_workspace(opts, workspace)
     rc = lib().pf_resample_batched(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
                                    aptr, ald, ctypes.byref(opts), _stream(logw, stream))
     _check(rc, "pf_resample_batched")
     return ancestors
 
 
-def pf_workspace_bytes(scheme, N: int, P: int) -> int:
-    return int(lib().pf_workspace_bytes(_scheme(scheme), N, P))
+def pf_workspace_bytes(scheme, N: int, P: int, flags: int = 0, ld_anc: int | None = None) -> int:
+    if flags == 0 and ld_anc is None:
+        return int(lib().pf_workspace_bytes(_scheme(scheme), N, P))
+    return int(lib().pf_workspace_bytes_ex(_scheme(scheme), N, P, flags, P if ld_anc is None else ld_anc))
+
+
+def _set_workspace(opts, workspace):
+    if workspace is None:
+        return
+    torch = _torch()
+    if not isinstance(workspace, torch.Tensor) or not workspace.is_cuda:
+        raise PfError("workspace must be a CUDA tensor")
+    opts.workspace = workspace.data_ptr()
+    opts.workspace_bytes = workspace.numel() * workspace.element_size()
 
 
 # ----------------------------------------------------------------------------- conversions

@@ -350,10 +350,20 @@ pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_lo
                          static_cast<cudaStream_t>(stream));
 }
 
+size_t pf_workspace_bytes_ex(pf_scheme scheme, int32_t N, int32_t P, uint32_t flags, int64_t ld_anc) {
+    if (N < 1 || P < 1 || ld_anc < P || scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return 0;
+    const bool sorted_multi = (flags & PF_SORTED) && scheme == PF_MULTINOMIAL;
+    // the largest need over the paths a call with these arguments may take: the multi-launch
+    // layout, the cooperative kernel's scratch, and the permutation the cluster kernel writes
+    // when the state is gathered without permuted_out
+    size_t need = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u)).total;
+    need = std::max(need, pf::coop_scratch_bytes());
+    need = std::max(need, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4);
+    return need;
+}
+
 size_t pf_workspace_bytes(pf_scheme scheme, int32_t N, int32_t P) {
-    if (N < 1 || P < 1) return 0;
-    const pf::Layout a = pf::make_layout(N, P, needs_for(scheme));
-    return a.total;
+    return pf_workspace_bytes_ex(scheme, N, P, 0u, P);
 }
 
 pf_status pf_ancestors_to_offspring_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P,

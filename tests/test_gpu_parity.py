@@ -502,6 +502,56 @@ def test_fused_state_gather(pf, dev, orc, scheme):
         assert np.array_equal(gX[n].cpu().numpy(), orc.gather_inplace(X[n], orc.permute(want[n])))
 
 
+@pytest.mark.parametrize("scheme", SCHEMES + ["sorted"])
+def test_explicit_workspace(pf, dev, orc, scheme):
+    """pf_opts.workspace: a caller buffer of pf_workspace_bytes(_ex) bytes serves every path the
+    dispatch takes (warp / CTA / cluster / cooperative / multi-launch kernels; the permutation
+    scratch of the fused state gather); results equal the pool's; too small or misaligned buffers
+    and the unsupported combination (permutation on the multi-launch path) are refused."""
+    import torch
+
+    sch = "multinomial" if scheme == "sorted" else scheme
+    flags = pf.PF_SORTED if scheme == "sorted" else 0
+    B = 7 if scheme == "metropolis" else 0
+    for N, P in ((300, 16), (3, 700), (5, 6000), (2, 65536), (1, 300000), (4, 300000)):
+        x = pfinputs.gaussian_logw(P, 1.0, seed=N + P, N=N)
+        g = _gpu(x, dev)
+        nbytes = pf.pf_workspace_bytes(sch, N, P, flags=flags)
+        assert nbytes > 0
+        ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        off = (-ws.data_ptr()) % 256
+        wsv = ws[off:off + nbytes]
+        a = pf.pf_resample_batched(sch, g, 41, B=B, flags=flags, workspace=wsv)
+        torch.cuda.synchronize()
+        _, want = orc.resample_batched(sch, x, 41, B=B) if scheme != "sorted" else (None, np.stack(
+            [orc.resample_sorted_multinomial(x[n], 41, filter_index=n)[1] for n in range(N)]))
+        assert np.array_equal(a.cpu().numpy(), want), (scheme, N, P)
+        if scheme in ("stratified", "systematic") and P <= 65536:
+            X = torch.randn((N, P, 16), device=dev)
+            X0 = X.cpu().numpy()
+            pf.pf_resample_batched(sch, g, 41, state=X, workspace=wsv)
+            torch.cuda.synchronize()
+            for n in range(N):
+                assert np.array_equal(X[n].cpu().numpy(), orc.gather_inplace(X0[n], orc.permute(want[n])))
+    # refusals
+    x = _gpu(pfinputs.gaussian_logw(5000, 1.0, seed=1, N=2), dev)
+    tiny = torch.empty(256, dtype=torch.uint8, device=dev)
+    need_ws = scheme in ("multinomial", "sorted", "metropolis")
+    if need_ws:
+        with pytest.raises(pf.PfError):
+            pf.pf_resample_batched(sch, _gpu(pfinputs.gaussian_logw(300000, 1.0, seed=2, N=2), dev), 1, B=B,
+                                   flags=flags, workspace=tiny)
+    big = torch.empty(pf.pf_workspace_bytes(sch, 2, 300000, flags=flags) + 512, dtype=torch.uint8, device=dev)
+    mis = big[((-big.data_ptr()) % 256) + 8:]
+    with pytest.raises(pf.PfError):
+        pf.pf_resample_batched(sch, _gpu(pfinputs.gaussian_logw(300000, 1.0, seed=2, N=2), dev), 1, B=B, flags=flags,
+                               workspace=mis)
+    if need_ws:
+        perm = torch.empty((2, 5000), dtype=torch.int32, device=dev)
+        with pytest.raises(pf.PfError):
+            pf.pf_resample_batched(sch, x, 1, B=B, flags=flags, permuted_out=perm, workspace=big)
+
+
 def test_repeatability_and_launch_count(pf, dev):
     import torch
 
