@@ -185,6 +185,30 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
+    if ((permuted_out || state) && !no_fusion && !normw && pf::coop_supported(scheme, N, P)) {
+        // large filters, few of them: the cooperative kernel writes the permutation too (and gathers
+        // the state when the rows allow it); scratch = [coop scratch + free list | offspring | perm]
+        const size_t plane = static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4;
+        const size_t o1 = (pf::coop_scratch_bytes(P) + 255) / 256 * 256;
+        const size_t o2 = o1 + (offspring_out ? 0 : (plane + 255) / 256 * 256);
+        const size_t need = o2 + (permuted_out ? 0 : plane);
+        void* big = nullptr;
+        const pf_status st0 = get_workspace(opts, need, s, &big);
+        if (st0 != PF_OK) return st0;
+        char* b = static_cast<char*>(big);
+        int32_t* off = offspring_out ? offspring_out : reinterpret_cast<int32_t*>(b + o1);
+        int32_t* perm = permuted_out ? permuted_out : reinterpret_cast<int32_t*>(b + o2);
+        // the state gather runs as its own full-GPU kernel: inside the cooperative kernel the copies
+        // of each CTA's chunk serialise behind its permutation work (P = 2^18: 51.7 vs 41.2 us;
+        // 2^20: 66.2 vs 61.2 us, profiles/r01_dispatch.md)
+        uint64_t nl = 0;
+        cudaError_t e = pf::launch_coop_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse, ess,
+                                               status_out, off, perm, nullptr, 0, 0, 0, big, s, &nl);
+        if (e == cudaSuccess && state)
+            e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     if (permuted_out || state) {
         // not fused for this size/scheme/row layout: resample (offspring as a side output), then
         // the canonical permutation from the offspring (k_pscan + k_push), then the gather.  One
@@ -224,11 +248,12 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     if (!no_fusion && !normw && pf::coop_supported(scheme, N, P)) {
         // one cooperative launch for large filters (pf_fused.cu); tiny scratch from the pool
         void* sc = nullptr;
-        pf_status st2 = get_workspace(opts, pf::coop_scratch_bytes(), s, &sc);
+        pf_status st2 = get_workspace(opts, pf::coop_scratch_bytes(P), s, &sc);
         if (st2 != PF_OK) return st2;
         uint64_t nl = 0;
         const cudaError_t e = pf::launch_coop_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse,
-                                                     ess, status_out, offspring_out, sc, s, &nl);
+                                                     ess, status_out, offspring_out, nullptr, nullptr, 0, 0, 0, sc,
+                                                     s, &nl);
         g_launches += nl;
         return cuda_status(e);
     }
@@ -357,8 +382,8 @@ size_t pf_workspace_bytes_ex(pf_scheme scheme, int32_t N, int32_t P, uint32_t fl
     // layout, the cooperative kernel's scratch, and the permutation the cluster kernel writes
     // when the state is gathered without permuted_out
     size_t need = pf::make_layout(N, P, needs_for(scheme) | (sorted_multi ? pf::kNeedG : 0u)).total;
-    need = std::max(need, pf::coop_scratch_bytes());
-    need = std::max(need, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4);
+    const size_t plane = (static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4 + 255) / 256 * 256;
+    need = std::max(need, (pf::coop_scratch_bytes(P) + 255) / 256 * 256 + 2 * plane);
     return need;
 }
 

@@ -184,7 +184,8 @@ __device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_
 #define PF_COPY_U 4
 #endif
 constexpr int kCopyU = PF_COPY_U;
-__device__ __forceinline__ void copy_rows_warp(const FusedArgs& a, int n, const int32_t* owner, const int32_t* slot,
+template <class Args>
+__device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32_t* owner, const int32_t* slot,
                                                int npairs, int lane) {
     char* Xf = a.X + static_cast<int64_t>(n) * a.xfld;
     // a lane always handles the same 16-byte chunk of a row (32 is a multiple of the chunks per
@@ -708,7 +709,10 @@ struct CoopArgs {
     double* lse_out;
     double* ess_out;
     int32_t* status_out;
-    int32_t* off;  // offspring out (row stride ld_anc), nullable
+    int32_t* off;  // offspring out (row stride ld_anc), nullable (required with PERM)
+    int32_t* perm;  // canonical permutation out (row stride ld_anc), PERM
+    int32_t* freelist;  // scratch [P]: the filter's free slots in rank order (PERM)
+    uint64_t* g_ptot;   // scratch [G]: packed (extras, free) totals of the chunks (PERM)
     // scratch (device): [G] per-CTA values
     float* g_max;
     int32_t* g_bad;
@@ -717,7 +721,68 @@ struct CoopArgs {
     double* g_sw2;
 };
 
-template <int SCHEME, bool SUMS>
+// packed (extras << 31 | free) value of a particle with offspring o (NS-15)
+__device__ __forceinline__ uint64_t packed_of(int32_t o, bool real) {
+    return (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && real) ? 1ull : 0ull);
+}
+
+// this thread's 16 offspring of the sub-tile at t0 (rows of 4, natural order), 0 past c1
+__device__ __forceinline__ void coop_load_o(const int32_t* orow, int64_t t0, int64_t c1, int tid, int vec,
+                                            int32_t ov[kFI]) {
+#pragma unroll
+    for (int j = 0; j < kFR; ++j) {
+        const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+        if (vec && i0 + 3 < c1) {
+            const int4 t = __ldcg(reinterpret_cast<const int4*>(orow + i0));
+            ov[j * 4 + 0] = t.x; ov[j * 4 + 1] = t.y; ov[j * 4 + 2] = t.z; ov[j * 4 + 3] = t.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ov[j * 4 + q] = (i0 + q < c1) ? __ldcg(orow + i0 + q) : 0;
+        }
+    }
+}
+
+// block exclusive scan of the packed values of a sub-tile: pex[j] = this lane's offset in row j's
+// warp segment, s_wt[j][warp] = the (row, warp) segment offset, *total = the sub-tile's total
+__device__ __forceinline__ void coop_packed_scan(const int32_t ov[kFI], int64_t t0, int64_t c1, int tid, int warp,
+                                                 int lane, uint64_t (*s_wt)[kFW], uint64_t* s_u64, uint64_t pex[kFR],
+                                                 uint64_t* total) {
+#pragma unroll
+    for (int j = 0; j < kFR; ++j) {
+        uint64_t loc = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) loc += packed_of(ov[j * 4 + q], t0 + j * (kFT * 4) + tid * 4 + q < c1);
+        const uint64_t incl = warp_incl_scan_u64(loc, lane);
+        pex[j] = incl - loc;
+        const uint64_t wt = __shfl_sync(kFull, incl, 31);
+        if (lane == 0) s_wt[j][warp] = wt;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t t4[kTPL];
+        uint64_t tsum = 0;
+#pragma unroll
+        for (int q = 0; q < kTPL; ++q) {
+            const int idx = lane * kTPL + q;
+            t4[q] = s_wt[idx / kFW][idx % kFW];
+            tsum += t4[q];
+        }
+        const uint64_t incl = warp_incl_scan_u64(tsum, lane);
+        uint64_t run = incl - tsum;
+#pragma unroll
+        for (int q = 0; q < kTPL; ++q) {
+            const int idx = lane * kTPL + q;
+            s_wt[idx / kFW][idx % kFW] = run;
+            run += t4[q];
+        }
+        if (lane == 31) s_u64[2] = incl;
+    }
+    __syncthreads();
+    *total = s_u64[2];
+}
+
+// PERM: 0 ancestors (+ offspring), 1 + the canonical permutation (offspring required)
+template <int SCHEME, bool SUMS, int PERM>
 __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
@@ -1000,6 +1065,104 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             __syncthreads();
             if (tid == 0) s_prevE = s_lastE[kFR - 1][kFW - 1];
             __syncthreads();
+        }
+        if (PERM) {
+            // ---------------- D: canonical permutation (NS-15) of this filter from the offspring
+            // written in phase C
+            // (this CTA's own chunk: visible to it after the barrier)
+            __syncthreads();
+            const int32_t* orow = a.off + static_cast<int64_t>(n) * a.ld_anc;
+            int32_t* prow = a.perm + static_cast<int64_t>(n) * a.ld_anc;
+            // D1: packed (extras << 31 | free) total of the chunk
+            uint64_t ploc = 0;
+            for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+                int32_t ov[kFI];
+                coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+#pragma unroll
+                for (int t = 0; t < kFI; ++t) ploc += packed_of(ov[t], t0 + (t >> 2) * (kFT * 4) + tid * 4 + (t & 3) < c1);
+            }
+            ploc = warp_sum_u64(ploc);
+            if (lane == 0) s_wt[0][warp] = ploc;
+            __syncthreads();
+            if (tid == 0) {
+                uint64_t t = 0;
+                for (int w = 0; w < kFW; ++w) t += s_wt[0][w];
+                a.g_ptot[c] = t;
+            }
+            grid.sync();
+            if (warp == 0) {
+                uint64_t off = 0;
+                for (int r = lane; r < c; r += 32) off += __ldcg(a.g_ptot + r);
+                off = warp_sum_u64(off);
+                if (lane == 0) s_u64[3] = off;
+            }
+            __syncthreads();
+            // D2: survivors keep their slot; free slots into the global free list (rank order)
+            {
+                uint64_t run0 = s_u64[3];
+                for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+                    int32_t ov[kFI];
+                    coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+                    uint64_t pex[kFR], stot;
+                    coop_packed_scan(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+#pragma unroll
+                    for (int j = 0; j < kFR; ++j) {
+                        uint64_t run = run0 + s_wt[j][warp] + pex[j];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int64_t i = t0 + j * (kFT * 4) + tid * 4 + q;
+                            const int32_t o = ov[j * 4 + q];
+                            if (i < c1) {
+                                if (o > 0) prow[i] = static_cast<int32_t>(i);
+                                else a.freelist[run & 0x7FFFFFFFull] = static_cast<int32_t>(i);
+                            }
+                            run += packed_of(o, i < c1);
+                        }
+                    }
+                    run0 += stot;
+                    __syncthreads();  // s_wt is reused by the next sub-tile
+                }
+            }
+            grid.sync();  // the filter's free list is complete
+            // D3: the r-th extra copy goes to the r-th free slot
+            {
+                uint64_t run0 = s_u64[3];
+                int32_t* s_head = &s_buf[0][0];
+                for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
+                    int32_t ov[kFI];
+                    coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+                    uint64_t pex[kFR], stot;
+                    coop_packed_scan(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+                    const uint32_t XS = static_cast<uint32_t>(run0 >> 31);          // first extras rank
+                    const uint32_t XT = static_cast<uint32_t>((run0 + stot) >> 31) - XS;
+                    const int32_t idbase = static_cast<int32_t>(t0) + tid * 4;
+                    int32_t cy = -1;
+                    for (uint32_t q0 = 0; q0 < XT; q0 += kXS) {
+                        cta_clear8(s_head, tid);
+                        __syncthreads();
+#pragma unroll
+                        for (int j = 0; j < kFR; ++j) {
+                            uint64_t run = run0 + s_wt[j][warp] + pex[j];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int32_t o = ov[j * 4 + q];
+                                const uint32_t rel = static_cast<uint32_t>(run >> 31) - XS - q0;
+                                if (o > 1 && rel < static_cast<uint32_t>(kXS)) s_head[rel] = idbase + j * (kFT * 4) + q;
+                                run += static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31;
+                            }
+                        }
+                        __syncthreads();
+                        int32_t h[8];
+                        cta_max_scan8<kFW>(s_head, s_wmax, h, cy, tid, warp, lane);
+                        const uint32_t r0 = q0 + 8 * tid;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (r0 + t < XT) prow[__ldcg(a.freelist + XS + r0 + t)] = h[t];
+                        __syncthreads();  // s_head is cleared by the next chunk
+                    }
+                    run0 += stot;
+                }
+            }
         }
         grid.sync();  // scratch arrays are rewritten by the next filter
     }
@@ -1561,32 +1724,52 @@ bool coop_supported(int scheme, int32_t N, int32_t P) {
     return N == 1 || per_filter_excess_us <= 0.0 || static_cast<double>(N) * per_filter_excess_us < 20.0;
 }
 
-size_t coop_scratch_bytes() { return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8); }
+size_t coop_scratch_bytes(int32_t P) {
+    return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(P) * 4 + 256;
+}
 
-cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
-                               uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
-                               double* ess_out, int32_t* status_out, int32_t* offspring, void* scratch,
-                               cudaStream_t s, uint64_t* launches) {
-    CoopArgs a{};
-    const bool sums = lse_out || ess_out;
-    void* kern = (scheme == 2) ? (sums ? (void*)k_coop_sorted<2, true> : (void*)k_coop_sorted<2, false>)
-                               : (sums ? (void*)k_coop_sorted<3, true> : (void*)k_coop_sorted<3, false>);
-    static std::atomic<int> per_sm[2][2][kMaxDevices];
-    const int occ = cached_per_device(per_sm[scheme - 2][sums ? 1 : 0], [&] {
+template <int SCHEME, bool SUMS, int PERM>
+int coop_occupancy() {
+    static std::atomic<int> per_sm[kMaxDevices];
+    return cached_per_device(per_sm, [] {
         int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kFT, 0) != cudaSuccess || o < 1) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_coop_sorted<SCHEME, SUMS, PERM>, kFT, 0) !=
+                cudaSuccess ||
+            o < 1) {
             cudaGetLastError();
             o = 1;
         }
         return o;
     });
-    int G = std::min(device_sms() * occ, 4096);
+}
+
+template <int SCHEME, bool SUMS, int PERM>
+cudaError_t launch_coop_t(CoopArgs& a, cudaStream_t s) {
+    int G = std::min(device_sms() * coop_occupancy<SCHEME, SUMS, PERM>(), 4096);
     // chunks are whole 8192-particle sub-tiles; never more CTAs than sub-tiles
-    const int64_t tiles = (static_cast<int64_t>(P) + kPP - 1) / kPP;
+    const int64_t tiles = (static_cast<int64_t>(a.P) + kPP - 1) / kPP;
     G = static_cast<int>(std::min<int64_t>(G, tiles));
     const int64_t per = (tiles + G - 1) / G;
     a.CH = per * kPP;
-    G = static_cast<int>((static_cast<int64_t>(P) + a.CH - 1) / a.CH);
+    G = static_cast<int>((static_cast<int64_t>(a.P) + a.CH - 1) / a.CH);
+    void* args[] = {&a};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_coop_sorted<SCHEME, SUMS, PERM>), dim3(G), dim3(kFT),
+                                       args, 0, s);
+}
+
+template <int PERM>
+cudaError_t launch_coop_p(int scheme, bool sums, CoopArgs& a, cudaStream_t s) {
+    if (scheme == 2) return sums ? launch_coop_t<2, true, PERM>(a, s) : launch_coop_t<2, false, PERM>(a, s);
+    return sums ? launch_coop_t<3, true, PERM>(a, s) : launch_coop_t<3, false, PERM>(a, s);
+}
+
+cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                               uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
+                               double* ess_out, int32_t* status_out, int32_t* offspring, int32_t* permuted,
+                               void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld, void* scratch,
+                               cudaStream_t s, uint64_t* launches) {
+    CoopArgs a{};
+    const bool sums = lse_out || ess_out;
     a.logw = logw;
     a.ld = ld;
     a.N = N;
@@ -1599,20 +1782,27 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     a.vec = ((reinterpret_cast<uintptr_t>(logw) & 15) == 0 && ld % 4 == 0) ? 1 : 0;
     a.anc = anc;
     a.ld_anc = ld_anc;
-    a.anc_vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0) ? 1 : 0;
+    a.anc_vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0 &&
+                 (!offspring || (reinterpret_cast<uintptr_t>(offspring) & 15) == 0)) ? 1 : 0;
     a.lse_out = lse_out;
     a.ess_out = ess_out;
     a.status_out = status_out;
     a.off = offspring;
+    a.perm = permuted;
+    (void)x_row_bytes;
+    (void)x_ld;
+    (void)x_fld;
     char* sc = static_cast<char*>(scratch);
     a.g_max = reinterpret_cast<float*>(sc);
     a.g_bad = reinterpret_cast<int32_t*>(sc + 4096 * 4);
     a.g_tot = reinterpret_cast<uint64_t*>(sc + 4096 * 8);
     a.g_sw = reinterpret_cast<double*>(sc + 4096 * 16);
     a.g_sw2 = reinterpret_cast<double*>(sc + 4096 * 24);
-    void* args[] = {&a};
+    a.g_ptot = reinterpret_cast<uint64_t*>(sc + 4096 * 32);
+    a.freelist = reinterpret_cast<int32_t*>(sc + 4096 * 40);
     ProfScope ps_("k_coop_sorted", s);
-    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kFT), args, 0, s);
+    if (X) return cudaErrorNotSupported;  // the state gather runs as its own kernel (pf_api.cu)
+    cudaError_t e = permuted ? launch_coop_p<1>(scheme, sums, a, s) : launch_coop_p<0>(scheme, sums, a, s);
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

@@ -175,10 +175,13 @@ cudaError_t launch_medium(int scheme, bool sorted, const float* logw, int64_t ld
 
 // One-launch cooperative resampler for large filters (pf_fused.cu).
 bool coop_supported(int scheme, int32_t N, int32_t P);
-size_t coop_scratch_bytes();
+size_t coop_scratch_bytes(int32_t P);  // includes the free list of the permutation (4 P bytes)
+// with permuted (and optionally X, rows gathered in place as FusedArgs) the kernel also writes
+// the canonical permutation; then offspring must be non-null (scratch is fine)
 cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                                uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
-                               double* ess_out, int32_t* status_out, int32_t* offspring, void* scratch,
+                               double* ess_out, int32_t* status_out, int32_t* offspring, int32_t* permuted,
+                               void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld, void* scratch,
                                cudaStream_t s, uint64_t* launches);
 
 }  // namespace pf
