@@ -739,6 +739,23 @@ def test_medium_filters_cta_kernel(pf, dev, orc, scheme):
             assert np.all(np.abs(V[n] - wv) <= 1e-6 * np.maximum(np.abs(wv), 1e-30) + 1e-12)
 
 
+def test_lg_step_layouts_agree(pf, dev):
+    """The C4 propagate + weight kernel gives identical states and log-weights on 16-byte-aligned
+    rows (float4 path) and on unaligned rows (scalar path)."""
+    import torch
+
+    P, D = 5000, 16
+    Xa = torch.empty((P, D), device=dev)
+    pf.pf_lg_init(Xa, 0.9, 1.0, 77)
+    Xb = torch.zeros((P, D + 1), device=dev)[:, :D]  # ld = 17 floats: not 16-byte aligned rows
+    Xb.copy_(Xa)
+    for t in (1, 2, 3):
+        la = pf.pf_lg_propagate_weight(Xa, 0.9, 1.0, 1.0, 0.3 * t, 77, t)
+        lb = pf.pf_lg_propagate_weight(Xb, 0.9, 1.0, 1.0, 0.3 * t, 77, t)
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb) and torch.equal(Xa, Xb), t
+
+
 def test_pf_linear_gaussian_c4(pf, dev, orc):
     """C4: bootstrap PF (propagate + weight kernels, resample, permute, gather) on the 16-dim
     linear-Gaussian model: log-likelihood within Monte Carlo error of the Kalman filter, and every
