@@ -316,6 +316,53 @@ def test_host_pipeline_matches_direct_call(pf, dev, orc):
             assert np.array_equal(ref_perm[n].cpu().numpy(), orc.permute(want))
 
 
+@pytest.mark.parametrize("scheme", ["systematic", "stratified", "multinomial", "sorted", "metropolis"])
+def test_maximum_sizes(pf, dev, orc, scheme):
+    """Maximum sizes: a batch of 2^15 filters x 2^16 = 2^31 particles (8 GiB of log-weights; 64-bit
+    indexing of rows, tiles and workspace) with sampled filters checked in full, and a single filter
+    of 2^28 + 3 particles with sampled slots (chains) checked against the oracle."""
+    import torch
+
+    sch = "multinomial" if scheme == "sorted" else scheme
+    flags = pf.PF_SORTED if scheme == "sorted" else 0
+    B = 4 if scheme == "metropolis" else 0
+    N, P = 1 << 15, 1 << 16
+    x = pfinputs.gaussian_logw_torch(P, 1.0, 99, N, dev)
+    a = pf.pf_resample_batched(sch, x, 0x5EED, B=B, first_filter=3, flags=flags)
+    torch.cuda.synchronize()
+    for n in (0, 1, N // 2 + 1, N - 1):
+        xn = x[n].cpu().numpy()
+        if scheme == "sorted":
+            _, want = orc.resample_sorted_multinomial(xn, 0x5EED, filter_index=3 + n)
+        else:
+            _, want = orc.resample(sch, xn, 0x5EED, B=B, filter_index=3 + n)
+        assert np.array_equal(a[n].cpu().numpy(), want), (scheme, n)
+    del x, a
+    torch.cuda.empty_cache()
+    if scheme == "sorted":
+        return  # the oracle's 2^28-spacings scan would dominate the test; the batch above covers a6
+    P1 = (1 << 28) + 3
+    g = pfinputs.gaussian_logw_torch(P1, 1.0, 7, 1, dev)[0].contiguous()
+    a = pf.pf_resample_ex(sch, g, 0xB16, B, filter_index=1)
+    torch.cuda.synchronize()
+    xh = g.cpu().numpy()
+    rng = np.random.default_rng(1)
+    ks = np.unique(np.concatenate([[0, 1, P1 - 2, P1 - 1], rng.integers(0, P1, 2000)]))
+    ah = a[torch.from_numpy(ks).to(dev)].cpu().numpy()
+    if scheme == "metropolis":
+        _, w = orc.weights(xh)
+        for k, got in zip(ks[:300], ah[:300]):
+            assert got == orc.metropolis_chains(w, int(k), 1, 0xB16, B, 1)[0], int(k)
+        return
+    _, Q = orc.cumulative(xh)
+    Qtot = int(Q[-1])
+    for k, got in zip(ks, ah):
+        want = orc.upper_bound(Q, orc.position(sch, P1, Qtot, 0xB16, 1, int(k)))
+        assert got == want, (scheme, int(k))
+    if scheme != "multinomial":
+        assert bool((a[1:] >= a[:-1]).all())
+
+
 @pytest.mark.parametrize("P", [1 << 20, (1 << 22) + 12345, 1 << 24])
 def test_large_single_filter(pf, dev, orc, P):
     """C2 (2^20) and larger single filters in full, all prefix-sum schemes; Metropolis on sampled chains."""
