@@ -525,6 +525,10 @@ def pf_launch_count() -> int:
     return int(lib().pf_launch_count())
 
 
+def pf_status_string(status: int) -> str:
+    return lib().pf_status_string(int(status)).decode()
+
+
 class _KernelTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
 

@@ -200,6 +200,40 @@ def test_invalid_inputs(pf, dev, orc, scheme):
         assert math.isnan(lse) and math.isnan(ess) and np.all(np.isnan(v))
 
 
+def test_argument_errors_enqueue_nothing(pf, dev):
+    """include/pf.h error conventions: empty inputs (P = 0, N = 0), NULL pointers, B < 0, ld < P,
+    a bad scheme and unknown flags are refused synchronously with the documented status and no
+    kernel is enqueued."""
+    import ctypes
+
+    import torch
+
+    L = pf.lib()
+    x = torch.zeros(64, device=dev)
+    a = torch.empty(64, dtype=torch.int32, device=dev)
+    s0 = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    c0 = pf.pf_launch_count()
+    INVALID, UNSUPPORTED = 1, 4
+    assert L.pf_resample_systematic(x.data_ptr(), 0, 1, 0, a.data_ptr(), s0) == INVALID  # P = 0
+    assert L.pf_resample_systematic(None, 64, 1, 0, a.data_ptr(), s0) == INVALID
+    assert L.pf_resample_systematic(x.data_ptr(), 64, 1, 0, None, s0) == INVALID
+    assert L.pf_resample_metropolis(x.data_ptr(), 64, 1, -1, a.data_ptr(), s0) == INVALID  # B < 0
+    assert L.pf_resample_batched(3, x.data_ptr(), 8, 0, 8, 1, 0, 0, a.data_ptr(), 8, None, s0) == INVALID  # N = 0
+    assert L.pf_resample_batched(3, x.data_ptr(), 7, 2, 8, 1, 0, 0, a.data_ptr(), 8, None, s0) == INVALID  # ld < P
+    assert L.pf_resample_batched(3, x.data_ptr(), 8, 2, 8, 1, 0, 0, a.data_ptr(), 7, None, s0) == INVALID
+    assert L.pf_resample_ex(9, x.data_ptr(), 64, 1, 0, a.data_ptr(), None, s0) == INVALID  # bad scheme
+    opts = pf._Opts(flags=1 << 7)
+    assert L.pf_resample_ex(3, x.data_ptr(), 64, 1, 0, a.data_ptr(), ctypes.byref(opts), s0) == UNSUPPORTED
+    opts = pf._Opts(flags=pf.PF_SORTED)
+    assert L.pf_resample_ex(3, x.data_ptr(), 64, 1, 0, a.data_ptr(), ctypes.byref(opts), s0) == UNSUPPORTED
+    assert L.pf_ancestors_to_offspring(None, 64, a.data_ptr(), s0) == INVALID
+    assert L.pf_permute(a.data_ptr(), 0, a.data_ptr(), s0) == INVALID
+    assert pf.pf_launch_count() == c0
+    assert pf.pf_status_string(INVALID) == "PF_ERR_INVALID_ARG"
+    with pytest.raises(pf.PfError):
+        pf.pf_resample_systematic(torch.zeros(0, device=dev), 1)
+
+
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_side_outputs(pf, dev, orc, scheme):
     """lse, ess and normalised weights within 1e-6 relative of the oracle (NS-13)."""
