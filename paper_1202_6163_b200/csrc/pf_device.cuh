@@ -81,17 +81,13 @@ __device__ __forceinline__ float dexp(float t) {
 }
 
 // ---------------------------------------------------------------- NS-5
-// q = trunc(w * 2^kfx) computed on the float's bit fields (exact), without
-// branches: w is 0 or a normal float in [2^-126, 1] (NS-4 flushes), so the
-// value is mant * 2^(e - 150 + kfx) with a left or right shift.
+// q = trunc(w * 2^kfx): w is 0 or a normal float in [2^-126, 1] (NS-4 flushes).
 __device__ __forceinline__ uint64_t quantise(float w, int kfx) {
-    const uint32_t b = __float_as_uint(w);
-    const uint32_t e = b >> 23;
-    const uint64_t mant = (b & 0x7FFFFFu) | (e ? 0x800000u : 0u);
-    const int s = static_cast<int>(e) - 150 + kfx;
-    const uint64_t left = mant << (s > 0 ? s : 0);
-    const uint64_t right = mant >> min(-s, 63);
-    return (s >= 0) ? left : right;
+    // w * 2^kfx is exact in float (a power-of-two scale of a normal float in [2^-126, 1] with
+    // 30 <= kfx <= 61 stays normal and below 2^62), and the conversion truncates toward zero:
+    // q = trunc(w 2^kfx) exactly, as NS-5 defines it
+    const float scaled = __fmul_rn(w, __uint_as_float(static_cast<uint32_t>(127 + kfx) << 23));
+    return static_cast<uint64_t>(__float2ull_rz(scaled));
 }
 
 // w_i = dexp(fl(logw_i - lmax)) (NS-3)
