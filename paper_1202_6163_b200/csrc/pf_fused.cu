@@ -210,13 +210,16 @@ __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32
 }
 
 // PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
-template <int SCHEME, bool SUMS, int PERM, int FT>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
 __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
-    // geometry of this instantiation (FT = 512: 8192 particles per CTA, clusters of <= 8;
-    // FT = 1024: 16384 per CTA, clusters of <= 16 for 65536 < P <= 262144)
+    // geometry of this instantiation: FT threads x FI particles per thread (FT = 512, FI = 16:
+    // 8192 particles per CTA, clusters of <= 8; FT = 1024, FI = 16: 16384 per CTA, clusters of
+    // <= 16 for 65536 < P <= 262144)
     constexpr int kFT = FT;
     constexpr int kFW = FT / 32;
-    constexpr int kPP = FT * kFI;
+    constexpr int kFI = FI;
+    constexpr int kFR = FI / 4;
+    constexpr int kPP = FT * FI;
     constexpr int kTPL = kFR * kFW / 32;
     constexpr int kXS = kFW * kChunk;
     static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
@@ -1624,33 +1627,33 @@ __global__ void __launch_bounds__(kMedT) k_medium(SmallArgs a) {
 
 int device_sms() { return sm_count(); }
 
-template <int FT>
+template <int FT, int FI>
 constexpr size_t fused_smem(int perm) {
-    return perm ? static_cast<size_t>(FT * kFI + (perm == 2 ? (FT / 32) * kChunk : 0)) * sizeof(int32_t) : 0;
+    return perm ? static_cast<size_t>(FT * FI + (perm == 2 ? (FT / 32) * kChunk : 0)) * sizeof(int32_t) : 0;
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
 void fused_set_attributes() {
     // per-device function attributes: set once per device
     static std::atomic<int> attr_set[kMaxDevices];
     cached_per_device(attr_set, [] {
-        auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT>;
+        auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>;
         if (PERM)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(fused_smem<FT>(PERM)));
+                                 static_cast<int>(fused_smem<FT, FI>(PERM)));
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaGetLastError();
         return 1;
     });
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
 int fused_max_clusters(int CL) {
     // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us);
     // -1 = a cluster of this size cannot be scheduled on this device (0 = not queried yet)
     static std::atomic<int> cached[kMaxCL + 1][kMaxDevices];
     return cached_per_device(cached[CL], [&] {
-        fused_set_attributes<SCHEME, SUMS, PERM, FT>();
+        fused_set_attributes<SCHEME, SUMS, PERM, FT, FI>();
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1658,12 +1661,12 @@ int fused_max_clusters(int CL) {
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.blockDim = dim3(FT, 1, 1);
-        cfg.dynamicSmemBytes = fused_smem<FT>(PERM);
+        cfg.dynamicSmemBytes = fused_smem<FT, FI>(PERM);
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cfg.gridDim = dim3(CL, 1, 1);
         int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, k_fused_sorted<SCHEME, SUMS, PERM, FT>, &cfg) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveClusters(&mc, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>, &cfg) != cudaSuccess ||
             mc < 1) {
             cudaGetLastError();
             mc = -1;
@@ -1672,10 +1675,10 @@ int fused_max_clusters(int CL) {
     });
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    fused_set_attributes<SCHEME, SUMS, PERM, FT>();
-    const int max_clusters = fused_max_clusters<SCHEME, SUMS, PERM, FT>(a.CL);
+    fused_set_attributes<SCHEME, SUMS, PERM, FT, FI>();
+    const int max_clusters = fused_max_clusters<SCHEME, SUMS, PERM, FT, FI>(a.CL);
     if (max_clusters < 1) return cudaErrorNotSupported;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1684,31 +1687,31 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(FT, 1, 1);
-    cfg.dynamicSmemBytes = fused_smem<FT>(PERM);
+    cfg.dynamicSmemBytes = fused_smem<FT, FI>(PERM);
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const int clusters = std::max(1, std::min(a.N, max_clusters));
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * a.CL), 1, 1);
-    return cudaLaunchKernelEx(&cfg, k_fused_sorted<SCHEME, SUMS, PERM, FT>, a);
+    return cudaLaunchKernelEx(&cfg, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>, a);
 }
 
-template <int FT>
+template <int FT, int FI>
 cudaError_t launch_fused_ft(int scheme, int pm, const FusedArgs& a, cudaStream_t s) {
     if (scheme == 2) {
-        if (pm == 2) return a.sums ? launch_fused_t<2, true, 2, FT>(a, s) : launch_fused_t<2, false, 2, FT>(a, s);
-        if (pm == 1) return a.sums ? launch_fused_t<2, true, 1, FT>(a, s) : launch_fused_t<2, false, 1, FT>(a, s);
-        return a.sums ? launch_fused_t<2, true, 0, FT>(a, s) : launch_fused_t<2, false, 0, FT>(a, s);
+        if (pm == 2) return a.sums ? launch_fused_t<2, true, 2, FT, FI>(a, s) : launch_fused_t<2, false, 2, FT, FI>(a, s);
+        if (pm == 1) return a.sums ? launch_fused_t<2, true, 1, FT, FI>(a, s) : launch_fused_t<2, false, 1, FT, FI>(a, s);
+        return a.sums ? launch_fused_t<2, true, 0, FT, FI>(a, s) : launch_fused_t<2, false, 0, FT, FI>(a, s);
     }
-    if (pm == 2) return a.sums ? launch_fused_t<3, true, 2, FT>(a, s) : launch_fused_t<3, false, 2, FT>(a, s);
-    if (pm == 1) return a.sums ? launch_fused_t<3, true, 1, FT>(a, s) : launch_fused_t<3, false, 1, FT>(a, s);
-    return a.sums ? launch_fused_t<3, true, 0, FT>(a, s) : launch_fused_t<3, false, 0, FT>(a, s);
+    if (pm == 2) return a.sums ? launch_fused_t<3, true, 2, FT, FI>(a, s) : launch_fused_t<3, false, 2, FT, FI>(a, s);
+    if (pm == 1) return a.sums ? launch_fused_t<3, true, 1, FT, FI>(a, s) : launch_fused_t<3, false, 1, FT, FI>(a, s);
+    return a.sums ? launch_fused_t<3, true, 0, FT, FI>(a, s) : launch_fused_t<3, false, 0, FT, FI>(a, s);
 }
 
 // can a 16-CTA cluster of 1024-thread CTAs be scheduled (one per GPC)?  cached per device
 bool big_clusters_ok() {
     static std::atomic<int> ok[kMaxDevices];
-    return cached_per_device(ok, [] { return fused_max_clusters<3, false, 2, 1024>(kMaxCL) >= 1 ? 1 : -1; }) > 0;
+    return cached_per_device(ok, [] { return fused_max_clusters<3, false, 2, 1024, 16>(kMaxCL) >= 1 ? 1 : -1; }) > 0;
 }
 
 }  // namespace
@@ -1967,7 +1970,7 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
     const int pm = a.X ? 2 : (a.perm ? 1 : 0);
-    e = (FT == 512) ? launch_fused_ft<512>(scheme, pm, a, s) : launch_fused_ft<1024>(scheme, pm, a, s);
+    e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();
