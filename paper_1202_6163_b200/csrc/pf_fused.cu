@@ -137,6 +137,49 @@ __device__ __forceinline__ uint32_t count_below(const Pos& z, uint64_t v) {
     return static_cast<uint32_t>(min(max(c, int64_t{0}), z.P));
 }
 
+// Systematic: the common case of count_below without branches (32-bit clamp); *slow is set
+// when k* is within 2^-12 of an integer, where the caller recomputes with count_below.
+__device__ __forceinline__ uint32_t count_below_sys_fast(const Pos& z, uint64_t v, bool* slow) {
+    const double kf = fma(static_cast<double>(v), z.A, -z.Bc);
+    const double fl = floor(kf);
+    const double fr = kf - fl;
+    *slow = !(fr > 0x1p-12 && fr < 1.0 - 0x1p-12);
+    const int n1 = static_cast<int>(fl) + 1;  // kf in [-1, P]: fits in 32 bits
+    return static_cast<uint32_t>(min(max(n1, 0), static_cast<int>(z.P)));
+}
+
+// E for the 4 particles of a row: running sum from run0, systematic fast path with an exact
+// redo of the (rare) rows holding a near-integer k*
+template <int SCHEME>
+__device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const float* w4, int kfx, uint32_t* E4) {
+    if (SCHEME == 3) {
+        bool any_slow = false;
+        uint64_t run = run0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            run += quantise(w4[q], kfx);
+            bool sl;
+            E4[q] = count_below_sys_fast(z, run, &sl);
+            any_slow |= sl;
+        }
+        if (any_slow) {
+            run = run0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                run += quantise(w4[q], kfx);
+                E4[q] = count_below<SCHEME>(z, run);
+            }
+        }
+    } else {
+        uint64_t run = run0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            run += quantise(w4[q], kfx);
+            E4[q] = count_below<SCHEME>(z, run);
+        }
+    }
+}
+
 __device__ __forceinline__ void cta_clear8(int32_t* s_head, int tid) {
     int4* h4 = reinterpret_cast<int4*>(s_head);
     h4[2 * tid] = make_int4(-1, -1, -1, -1);
@@ -460,12 +503,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         uint32_t E[kFI];
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
-            uint64_t run = O + s_wt[j][warp] + ex[j];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                run += quantise(v[j * 4 + q], a.kfx);
-                E[j * 4 + q] = count_below<SCHEME>(z, run);
-            }
+            count_row<SCHEME>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
             if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
         }
         if (tid == 0) s_klo = count_below<SCHEME>(z, O);
@@ -992,12 +1030,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             uint32_t E[kFI];
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
-                uint64_t run = carry + s_wt[j][warp] + ex[j];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    run += quantise(v[j * 4 + q], a.kfx);
-                    E[j * 4 + q] = count_below<SCHEME>(z, run);
-                }
+                count_row<SCHEME>(z, carry + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
                 if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
             }
             __syncthreads();
