@@ -148,8 +148,24 @@ __device__ __forceinline__ uint32_t count_below_sys_fast(const Pos& z, uint64_t 
     return static_cast<uint32_t>(min(max(n1, 0), static_cast<int>(z.P)));
 }
 
-// E for the 4 particles of a row: running sum from run0, systematic fast path with an exact
-// redo of the (rare) rows holding a near-integer k*
+// Stratified: the common case (k* not within 2^-12 of an integer), branch-free: stratum n
+// decides itself by one exact position check (strata below n lie below v, above n above).
+__device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_t v, bool* slow) {
+    const double kf = fma(static_cast<double>(v), z.A, -z.Bc);
+    const double fl = floor(kf);
+    const double fr = kf - fl;
+    *slow = !(fr > 0x1p-12 && fr < 1.0 - 0x1p-12);
+    const int P = static_cast<int>(z.P);
+    const int n = static_cast<int>(fl);
+    const int nc = min(max(n, 0), P - 1);
+    const u32x4 r = philox10(static_cast<uint32_t>(nc >> 1), 0u, 2u, z.filt, z.key.k0, z.key.k1);
+    const uint64_t rho = mulhi64((nc & 1) ? hi_word(r) : lo_word(r), z.D);
+    const uint32_t below = (mulhi64(static_cast<uint64_t>(nc) * z.D + rho, z.Qtot) < v) ? 1u : 0u;
+    return (n < 0) ? 0u : (n >= P ? static_cast<uint32_t>(P) : static_cast<uint32_t>(n) + below);
+}
+
+// E for the 4 particles of a row: running sum from run0, fast paths with an exact redo of the
+// (rare) rows holding a near-integer k*
 template <int SCHEME>
 __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const float* w4, int kfx, uint32_t* E4) {
     if (SCHEME == 3) {
@@ -171,11 +187,22 @@ __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const flo
             }
         }
     } else {
+        bool any_slow = false;
         uint64_t run = run0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             run += quantise(w4[q], kfx);
-            E4[q] = count_below<SCHEME>(z, run);
+            bool sl;
+            E4[q] = count_below_strat_fast(z, run, &sl);
+            any_slow |= sl;
+        }
+        if (any_slow) {
+            run = run0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                run += quantise(w4[q], kfx);
+                E4[q] = count_below<SCHEME>(z, run);
+            }
         }
     }
 }
