@@ -159,10 +159,7 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     // The cluster kernel gathers the state itself when the batch spans the GPU; a batch of few
     // filters (one cluster each) would copy its rows through a handful of SMs, so there the
     // permutation is fused and the gather runs as its own full-GPU kernel.
-    // Stratified: the extra Philox state of its slot counts leaves too few registers for the
-    // fused copy (2.83 ms vs 2.38 ms with the separate gather at C3), so only systematic fuses it.
-    const bool fuse_gather = state && scheme == PF_SYSTEMATIC &&
-                             pf::fused_gather_supported(state, x_row, x_ld, x_fld) &&
+    const bool fuse_gather = state && pf::fused_gather_supported(state, x_row, x_ld, x_fld) &&
                              static_cast<int64_t>(N) * pf::fused_cluster_ctas(P) >= pf::sm_count();
     if (!no_fusion && pf::fused_supported(scheme, N, P)) {
         // one launch per batch: cluster-per-filter kernel (ancestors, offspring, permutation and

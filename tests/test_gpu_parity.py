@@ -309,7 +309,7 @@ def test_bench_step_sampled(pf, dev, orc, scheme):
     pf.pf_resample_batched(scheme, x, pfinputs.seed_for(0), ancestors=anc, offspring_out=off, permuted_out=perm,
                            state=X)
     torch.cuda.synchronize()
-    assert pf.pf_launch_count() - c0 == (1 if scheme == "systematic" else 2)
+    assert pf.pf_launch_count() - c0 == 1
     for n, Xn in X0.items():
         _, want = orc.resample(scheme, x[n].cpu().numpy(), pfinputs.seed_for(0), filter_index=n)
         assert np.array_equal(anc[n].cpu().numpy(), want), n
@@ -559,7 +559,7 @@ def test_fused_state_gather(pf, dev, orc, scheme):
         if scheme in ("stratified", "systematic") and (P <= 65536 or (P <= (1 << 18) and N * cl >= sms)):
             # one cluster-kernel launch; the gather is fused when the batch spans the GPU (N x cluster
             # CTAs >= SMs) and the rows allow it, else it follows as one more launch
-            fused = scheme == "systematic" and D * 4 in (16, 32, 64, 128, 256, 512) and D == ldD and N * cl >= sms
+            fused = D * 4 in (16, 32, 64, 128, 256, 512) and D == ldD and N * cl >= sms
             assert nl == (1 if fused else 2), (N, P, D, nl)
         _, want = orc.resample_batched(scheme, x, 29, B=B)
         assert np.array_equal(a.cpu().numpy(), want)
