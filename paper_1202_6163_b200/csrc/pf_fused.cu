@@ -606,7 +606,15 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         }
         if (PERM) {
             // ---------------- D: canonical permutation (NS-15) from o_i = E_i - E_{i-1}
-            // packed value per particle: (extras << 31) | free; padding particles are neither
+            // packed value per particle: (extras << 31) | free; padding particles are neither.
+            // E becomes the offspring in place (first[] dies here: fewer live registers in D)
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+#pragma unroll
+                for (int q = 3; q > 0; --q) E[j * 4 + q] -= E[j * 4 + q - 1];
+                E[j * 4] -= first[j];
+            }
+            uint32_t* const O4 = E;  // O4[j * 4 + q] = o of particle (j, q)
             uint64_t pex[kFR];
             __syncthreads();  // s_wt is reused
 #pragma unroll
@@ -614,8 +622,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 uint64_t loc = 0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                    const uint32_t o = E[j * 4 + q] - pe;
+                    const uint32_t o = O4[j * 4 + q];
                     const bool real = (j * (kFT * 4) + tid * 4 + q) < np;
                     loc += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && real) ? 1ull : 0ull);
                 }
@@ -669,8 +676,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int i = j * (kFT * 4) + tid * 4 + q;
-                    const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                    const uint32_t o = E[j * 4 + q] - pe;
+                    const uint32_t o = O4[j * 4 + q];
                     if (i < np) {
                         if (o > 0) {
                             if (a.perm) prow[p0 + i] = static_cast<int32_t>(p0 + i);
@@ -695,8 +701,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                         uint64_t run = poff + s_wt[j][warp] + pex[j];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
-                            const uint32_t o = E[j * 4 + q] - pe;
+                            const uint32_t o = O4[j * 4 + q];
                             const uint32_t rel = static_cast<uint32_t>(run >> 31) - XC0 - c0;
                             if (o > 1 && rel < static_cast<uint32_t>(kXS)) s_head[rel] = idbase + j * (kFT * 4) + q;
                             run += static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31;  // the free bit never carries
