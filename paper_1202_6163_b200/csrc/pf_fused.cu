@@ -207,6 +207,17 @@ __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const flo
     }
 }
 
+// Cluster-wide barrier without a cluster-scope release on every thread: only the threads that
+// wrote data other CTAs (or other threads) read after the barrier fence their writes
+// (fence.acq_rel.cluster, the documented release pattern for barrier.cluster.arrive.relaxed);
+// the wait keeps its acquire semantics.  Every other thread skips the memory barrier, which
+// otherwise waits for all of its outstanding global stores (the state copies, the outputs).
+__device__ __forceinline__ void cluster_sync_publish(bool publisher) {
+    if (publisher) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void cta_clear8(int32_t* s_head, int tid) {
     int4* h4 = reinterpret_cast<int4*>(s_head);
     h4[2 * tid] = make_int4(-1, -1, -1, -1);
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             }
             if (lane == 0) { s_x.m = mm; s_x.bad = bb; }
         }
-        cluster.sync();  // #1
+        cluster_sync_publish(warp == 0 && lane == 0);  // #1 (s_x.m, s_x.bad)
         if (warp == 0) {
             float gm = -INFINITY;
             int gb = 0;
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 if (a.ess_out) a.ess_out[n] = NAN;
                 if (a.status_out) a.status_out[n] = 1;
             }
-            cluster.sync();  // remote readers of s_x are done before the next filter writes it
+            cluster_sync_publish(false);  // remote readers of s_x are done before the next filter writes it
             continue;
         }
         const float lm = s_lmax;
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 s_x.sw2 = Bv;
             }
         }
-        cluster.sync();  // #2
+        cluster_sync_publish(warp == 0);  // #2 (s_wt, s_x.tot / sw / sw2, s_tot)
         if (warp == 0) {
             uint64_t tot = 0, off = 0;
             double S = 0.0, S2 = 0.0;
@@ -651,7 +662,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 }
                 if (lane == 31) s_x.ptot = incl;
             }
-            cluster.sync();  // #3 packed CTA totals published
+            cluster_sync_publish(warp == 0);  // #3 packed CTA totals (s_wt, s_x.ptot) published
             if (warp == 0) {
                 uint64_t pt = 0;
                 if (lane < CL) pt = cluster.map_shared_rank(&s_x, lane)->ptot;
@@ -685,7 +696,8 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                     run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
                 }
             }
-            cluster.sync();  // #4 every CTA's free-slot list complete
+            __syncthreads();
+            cluster_sync_publish(tid == 0);  // #4 every CTA's free-slot list complete
             // Survivors' extra copies, CTA-wide: the CTA's extras ranks are [XC0, XC0 + XC).  Per
             // 8192-rank chunk: heads[first extras rank of i] = i, CTA max-scan gives the owner of
             // every rank r; the r-th global free slot (this CTA's list or a peer's, DSMEM) gets it.
