@@ -762,7 +762,9 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 }
             }
         }
-        __syncthreads();
+        // no barrier here: the next filter first writes shared memory (s_f, s_i, s_x.m) that no
+        // thread reads any more in this filter, and its first barrier follows its loads, so warps
+        // that finish their copies early start the next filter's loads under the stragglers' copies
     }
     cluster.sync();  // keep this CTA's shared memory alive for remote readers
 }
