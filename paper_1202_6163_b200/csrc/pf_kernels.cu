@@ -697,6 +697,50 @@ __global__ void __launch_bounds__(kThreads) k_metro(int32_t N, int32_t P, Ws ws,
     *out = k;
 }
 
+// Filter-per-CTA form: one 1024-thread CTA per SM walks whole filters, so an SM's L1 holds (most
+// of) one filter's weight vector and the B random proposals per chain hit L1 instead of L2
+// (the kernel is launched with the maximum L1 carve-out).  Same chains, same results as k_metro.
+__global__ void __launch_bounds__(1024, 1) k_metro_fpc(int32_t N, int32_t P, Ws ws, int64_t ldq, Key key,
+                                                        uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc) {
+    const float kU = __uint_as_float(0x33800000u);  // 2^-24
+    for (int n = blockIdx.x; n < N; n += gridDim.x) {
+        int32_t* out = anc + static_cast<int64_t>(n) * ld_anc;
+        if (B == 0 || ws.fstatus[n] != 0) {
+            for (int32_t i = threadIdx.x; i < P; i += blockDim.x) out[i] = i;
+            continue;
+        }
+        const float* w = ws.w + static_cast<int64_t>(n) * ldq;
+        const uint32_t filt = filt0 + static_cast<uint32_t>(n);
+        for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+            int32_t k = i;
+            float wk = __ldg(w + i);
+            for (int32_t b = 0; b < B; b += 8) {
+                uint32_t j[8];
+                float u[8], wj[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>((b >> 1) + t), 4u, filt,
+                                             key.k0, key.k1);
+                    j[2 * t] = __umulhi(r.x, static_cast<uint32_t>(P));
+                    u[2 * t] = __fmul_rn(static_cast<float>(r.y >> 8), kU);
+                    j[2 * t + 1] = __umulhi(r.z, static_cast<uint32_t>(P));
+                    u[2 * t + 1] = __fmul_rn(static_cast<float>(r.w >> 8), kU);
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t) wj[t] = (b + t < B) ? __ldg(w + j[t]) : 0.0f;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if (b + t < B && __fmul_rn(u[t], wk) < wj[t]) {
+                        k = static_cast<int32_t>(j[t]);
+                        wk = wj[t];
+                    }
+                }
+            }
+            out[i] = k;
+        }
+    }
+}
+
 // ============================================================================ a12: normalised weights
 __global__ void __launch_bounds__(kThreads) k_normw(const float* __restrict__ logw, int64_t ld, int32_t N,
                                                     int32_t P, Ws ws, float* normw) {
@@ -1797,8 +1841,23 @@ cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t 
         }
         ++*launches;
     }
-    { ProfScope ps_("k_metro", s); k_metro<<<static_cast<unsigned>(cdiv(total, kThreads)), kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed),
-                                                                              first_filter, B, anc, ld_anc); }
+    // batches that fill the GPU: the filter-per-CTA kernel (L1-resident weights; C3: 6.84 ->
+    // 4.28 ms at B = 32, tools/metro_times.py); fewer filters: one thread per chain over all SMs
+    if (N >= sm_count()) {
+        static std::atomic<int> attr_set[kMaxDevices];
+        cached_per_device(attr_set, [] {
+            cudaFuncSetAttribute(k_metro_fpc, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            cudaGetLastError();
+            return 1;
+        });
+        ProfScope ps_("k_metro", s);
+        k_metro_fpc<<<static_cast<unsigned>(std::min<int64_t>(N, sm_count())), 1024, 0, s>>>(
+            N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc);
+    } else {
+        ProfScope ps_("k_metro", s);
+        k_metro<<<static_cast<unsigned>(cdiv(total, kThreads)), kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed),
+                                                                               first_filter, B, anc, ld_anc);
+    }
     ++*launches;
     return cudaPeekAtLastError();
 }
