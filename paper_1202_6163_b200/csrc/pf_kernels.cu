@@ -240,6 +240,99 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const float* __restrict__ 
     }
 }
 
+// CTA-per-filter form of the scan for batches that fill the GPU (N >= SMs, P <= 2^17): a
+// 512-thread CTA walks its filter in 4096-particle tiles with a running carry, so there is no
+// decoupled lookback (whose latency bounds k_scan) and no tile-status traffic.  Same outputs as
+// k_scan (Q, Qtot, S, lse, ESS; invalid filters: NaN side outputs).
+constexpr int kScanCtaT = 512;
+template <bool VEC>
+__global__ void __launch_bounds__(kScanCtaT, 2) k_scan_cta(const float* __restrict__ logw, int64_t ld, int32_t N,
+                                                           int32_t P, int kfx, Ws ws, int64_t ldq, int write_q,
+                                                           double* lse_out, double* ess_out) {
+    constexpr int W = kScanCtaT / 32;
+    __shared__ uint64_t s_wt[W];
+    __shared__ double s_a[W], s_b[W];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int n = blockIdx.x; n < N; n += gridDim.x) {
+        if (ws.fstatus[n] != 0) {
+            if (tid == 0) {
+                if (lse_out) lse_out[n] = NAN;
+                if (ess_out) ess_out[n] = NAN;
+                ws.S[n] = NAN;
+            }
+            continue;
+        }
+        const float lm = ws.lmax[n];
+        const float* row = logw + static_cast<int64_t>(n) * ld;
+        uint64_t* qrow = ws.Q + static_cast<int64_t>(n) * ldq;
+        uint64_t carry = 0;
+        double sw = 0.0, sw2 = 0.0;
+        for (int base = 0; base < P; base += 8 * kScanCtaT) {
+            const int i0 = base + 8 * tid;
+            float w[8];
+            if (VEC && i0 + 7 < P) {
+                const float4 t0 = __ldg(reinterpret_cast<const float4*>(row + i0));
+                const float4 t1 = __ldg(reinterpret_cast<const float4*>(row + i0 + 4));
+                w[0] = t0.x; w[1] = t0.y; w[2] = t0.z; w[3] = t0.w; w[4] = t1.x; w[5] = t1.y; w[6] = t1.z; w[7] = t1.w;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) w[c] = (i0 + c < P) ? row[i0 + c] : -INFINITY;
+            }
+            uint64_t loc = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                w[c] = weight(w[c], lm);
+                sw += static_cast<double>(w[c]);
+                sw2 += static_cast<double>(w[c]) * static_cast<double>(w[c]);
+                loc += quantise(w[c], kfx);
+            }
+            const uint64_t incl = warp_incl_scan_u64(loc, lane);
+            if (lane == 31) s_wt[warp] = incl;
+            __syncthreads();
+            uint64_t wpre = 0, tot = 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const uint64_t t = s_wt[k];
+                wpre += (k < warp) ? t : 0ull;
+                tot += t;
+            }
+            __syncthreads();  // s_wt is rewritten by the next tile
+            if (write_q) {
+                uint64_t run = carry + wpre + incl - loc;
+                uint64_t q8[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    run += quantise(w[c], kfx);
+                    q8[c] = run;
+                }
+                if (i0 + 7 < P) {
+                    ulonglong2* dst = reinterpret_cast<ulonglong2*>(qrow + i0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) __stcg(dst + c, make_ulonglong2(q8[2 * c], q8[2 * c + 1]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (i0 + c < P) qrow[i0 + c] = q8[c];
+                }
+            }
+            carry += tot;
+        }
+        sw = warp_sum_f64(sw);
+        sw2 = warp_sum_f64(sw2);
+        if (lane == 0) { s_a[warp] = sw; s_b[warp] = sw2; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int k = 0; k < W; ++k) { a += s_a[k]; b += s_b[k]; }
+            ws.Qtot[n] = carry;
+            ws.S[n] = a;
+            if (lse_out) lse_out[n] = static_cast<double>(lm) + log(a);
+            if (ess_out) ess_out[n] = a * a / b;
+        }
+        __syncthreads();  // s_a / s_b reuse
+    }
+}
+
 // ============================================================================ a4+a5: merge path
 // Merged sequence of A (positions x_k, sorted) and B (cumulative Q_i, sorted);
 // B_i precedes A_k iff Q_i <= x_k, so when x_k is emitted the number of B
@@ -1768,6 +1861,15 @@ cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, con
                         int kfx_override) {
     const int kfx = (kfx_override >= 0) ? kfx_override : 61 - ceil_log2(P);
     const bool vec = aligned16(logw) && (ld % 4 == 0);
+    if (N >= sm_count() && P <= (1 << 17)) {
+        // a CTA per filter (no lookback): 2 CTAs per SM, persistent over the filters
+        const unsigned g = static_cast<unsigned>(std::min<int64_t>(N, 2LL * sm_count()));
+        ProfScope ps_("k_scan", s);
+        if (vec) k_scan_cta<true><<<g, kScanCtaT, 0, s>>>(logw, ld, N, P, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out);
+        else k_scan_cta<false><<<g, kScanCtaT, 0, s>>>(logw, ld, N, P, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out);
+        ++*launches;
+        return cudaPeekAtLastError();
+    }
     const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * L.T));
     if (vec)
         { ProfScope ps_("k_scan", s); k_scan<true><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
