@@ -218,47 +218,6 @@ __device__ __forceinline__ void cluster_sync_publish(bool publisher) {
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void cta_clear8(int32_t* s_head, int tid) {
-    int4* h4 = reinterpret_cast<int4*>(s_head);
-    h4[2 * tid] = make_int4(-1, -1, -1, -1);
-    h4[2 * tid + 1] = make_int4(-1, -1, -1, -1);
-}
-
-// CTA-wide inclusive max-scan of the kXS marks in s_head, 8 consecutive per thread (the
-// caller has synchronised after marking): h[t] = max(carry, marks [0, 8 tid + t]); carry
-// (block-uniform) becomes the chunk maximum.  One barrier.
-template <int FW>
-__device__ __forceinline__ void cta_max_scan8(const int32_t* s_head, int32_t* s_wmax, int32_t h[8], int32_t& carry,
-                                              int tid, int warp, int lane) {
-    const int4* h4 = reinterpret_cast<const int4*>(s_head);
-    const int4 lo = h4[2 * tid], hi = h4[2 * tid + 1];
-    h[0] = lo.x; h[1] = lo.y; h[2] = lo.z; h[3] = lo.w; h[4] = hi.x; h[5] = hi.y; h[6] = hi.z; h[7] = hi.w;
-#pragma unroll
-    for (int t = 1; t < 8; ++t) h[t] = max(h[t], h[t - 1]);
-    int32_t incl = h[7];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t u = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl = max(incl, u);
-    }
-    if (lane == 31) s_wmax[warp] = incl;
-    __syncthreads();
-    int32_t w = (lane < FW) ? s_wmax[lane] : -1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t u = __shfl_up_sync(kFull, w, o);
-        if (lane >= o) w = max(w, u);
-    }
-    const int32_t wpre = __shfl_sync(kFull, w, (warp + 31) & 31);  // inclusive of warp - 1
-    const int32_t tot = __shfl_sync(kFull, w, 31);
-    int32_t pre = __shfl_up_sync(kFull, incl, 1);
-    pre = (lane == 0) ? -1 : pre;
-    pre = max(max(pre, carry), (warp == 0) ? -1 : wpre);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) h[t] = max(h[t], pre);
-    carry = max(carry, tot);
-}
-
 // a10 fused: one warp copies npairs rows X[slot[p]] <- X[owner[p]] of filter n
 // ((16 << xlg) bytes each), 16 bytes per lane, kCopyU chunks in flight per lane.
 #ifndef PF_COPY_U
