@@ -105,6 +105,27 @@ def test_multilaunch_path_bit_exact(pf, dev, orc, scheme):
             assert abs(lse - wlse) <= 1e-6 * max(1.0, abs(wlse))
 
 
+def test_multinomial_per_filter_scan(pf, dev, orc):
+    """Batches that fill the GPU scan each filter in one CTA (no decoupled lookback): ragged sizes,
+    -inf runs, heavy weights, an invalid filter; multinomial ancestors bit-exact against the oracle
+    on sampled filters, lse within 1e-6."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    for P, var in ((5000, 10.0), (4097, 1.0), (65536, 1.0), (100003, 0.1), (131072, 10.0), (300, 1.0)):
+        N = sms + 3
+        x = pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(P, var, seed=P, N=N))
+        x[4, 11] = np.nan
+        lse = torch.empty(N, dtype=torch.float64, device=dev)
+        a = pf.pf_resample_batched("multinomial", _gpu(x, dev), 88, first_filter=2, lse_out=lse)
+        torch.cuda.synchronize()
+        A, L = a.cpu().numpy(), lse.cpu().numpy()
+        for n in (0, 4, N // 2, N - 1):
+            st, want, wl, _, _ = orc.resample("multinomial", x[n], 88, filter_index=2 + n, side=True)
+            assert np.array_equal(A[n], want), (P, n)
+            assert (st and np.isnan(L[n])) or abs(L[n] - wl) <= 1e-6 * max(1.0, abs(wl))
+
+
 @pytest.mark.parametrize("scheme", ["stratified", "systematic"])
 def test_large_filter_batches_dispatch(pf, dev, orc, scheme):
     """Filters above the cluster kernel's range: one filter takes the cooperative kernel (one
