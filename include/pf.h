@@ -89,12 +89,15 @@ typedef struct {
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */
     int32_t* status_out;   /* [N] PF_FILTER_* per filter                                    */
     int32_t* offspring_out; /* [N][P] (row stride = ancestors' ld) o_i = #{k : a_k = i} (NS-14);
-                              the one-launch stratified/systematic kernel derives it from its
-                              slot counts at no extra pass; other paths run the histogram   */
+                              the one-launch stratified/systematic kernels (warp, CTA, cluster,
+                              cooperative) derive it from their slot counts at no extra pass;
+                              the other paths run the histogram                             */
     int32_t* permuted_out;  /* [N][P] (row stride = ancestors' ld) the canonical in-place
                               permutation of the ancestors (NS-15, = pf_permute(ancestors));
-                              fused into the cluster kernel (P <= 65536), otherwise computed
-                              from the offspring after the search                           */
+                              stratified/systematic: written by the cluster kernel (P <= 65536,
+                              or P <= 262144 for batches spanning the GPU) or the cooperative
+                              kernel (large filters, few of them); otherwise computed from the
+                              offspring after the search                                    */
     void* workspace;       /* device, 256-byte aligned, nullable -> library pool            */
     size_t workspace_bytes;
     /* Optional fused state gather (a10, NS-16; "redraw"): if state is non-NULL, after
