@@ -89,9 +89,9 @@ typedef struct {
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */
     int32_t* status_out;   /* [N] PF_FILTER_* per filter                                    */
     int32_t* offspring_out; /* [N][P] (row stride = ancestors' ld) o_i = #{k : a_k = i} (NS-14);
-                              the one-launch stratified/systematic kernels (warp, CTA, cluster,
-                              cooperative) derive it from their slot counts at no extra pass;
-                              the other paths run the histogram                             */
+                              the cluster and cooperative kernels derive it from their slot
+                              counts at no extra pass, the warp / CTA-per-filter kernels count
+                              in shared memory, the multi-launch path runs a histogram      */
     int32_t* permuted_out;  /* [N][P] (row stride = ancestors' ld) the canonical in-place
                               permutation of the ancestors (NS-15, = pf_permute(ancestors));
                               stratified/systematic: written by the cluster kernel (P <= 65536,
