@@ -882,6 +882,48 @@ __global__ void __launch_bounds__(kThreads) k_hist(const int32_t* __restrict__ a
 // issues one reduction per run of equal values (a run head adds the distance
 // to the next head), so sorted ancestors (stratified / systematic) cost one
 // atomic per surviving particle and unsorted ones one per slot.
+// Shared-memory histogram for batches of filters with P <= 65536: two CTAs per filter, each
+// counting the ancestors that fall in its half of the particle range (<= 32768 u32 counters,
+// 128 KB), reading the filter's ancestors once each (the second read is L2-resident); no global
+// atomics, no memset, and the counts are written with coalesced stores.
+constexpr int kHistT = 1024;
+__global__ void __launch_bounds__(kHistT) k_hist_smem(const int32_t* __restrict__ anc, int64_t ld_anc, int32_t N,
+                                                       int32_t P, int32_t* o, int64_t ld_o, int vec) {
+    extern __shared__ uint32_t s_cnt[];
+    const int half = (P + 1) / 2;
+    for (int64_t job = blockIdx.x; job < 2LL * N; job += gridDim.x) {
+        const int64_t n = job >> 1;
+        const int lo = (job & 1) ? half : 0;
+        const int hi = (job & 1) ? P : half;
+        for (int i = threadIdx.x; i < hi - lo; i += kHistT) s_cnt[i] = 0u;
+        __syncthreads();
+        const int32_t* arow = anc + n * ld_anc;
+        if (vec) {
+            const int4* a4 = reinterpret_cast<const int4*>(arow);
+            for (int k = threadIdx.x; k < P / 4; k += kHistT) {
+                const int4 v = __ldg(a4 + k);
+                const int32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (vv[c] >= lo && vv[c] < hi) atomicAdd(&s_cnt[vv[c] - lo], 1u);
+            }
+            for (int k = (P / 4) * 4 + threadIdx.x; k < P; k += kHistT) {
+                const int32_t v = __ldg(arow + k);
+                if (v >= lo && v < hi) atomicAdd(&s_cnt[v - lo], 1u);
+            }
+        } else {
+            for (int k = threadIdx.x; k < P; k += kHistT) {
+                const int32_t v = __ldg(arow + k);
+                if (v >= lo && v < hi) atomicAdd(&s_cnt[v - lo], 1u);
+            }
+        }
+        __syncthreads();
+        int32_t* orow = o + n * ld_o;
+        for (int i = threadIdx.x; i < hi - lo; i += kHistT) orow[lo + i] = static_cast<int32_t>(s_cnt[i]);
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_hist_runs(const int32_t* __restrict__ anc, int64_t ld_anc,
                                                         int32_t N, int32_t P, int32_t* o, int64_t ld_o) {
     const int lane = threadIdx.x & 31;
@@ -1982,6 +2024,21 @@ cudaError_t launch_identity(int32_t N, int32_t P, int32_t* anc, int64_t ld_anc, 
 
 cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int32_t P, int32_t* o, int64_t ld_o,
                              cudaStream_t s, uint64_t* launches) {
+    if (N >= sm_count() / 2 && P >= 2 && P <= 65536) {
+        const int half = (P + 1) / 2;
+        const size_t smem = static_cast<size_t>(half) * 4;
+        static std::atomic<int> attr_set[kMaxDevices];
+        cached_per_device(attr_set, [] {
+            cudaFuncSetAttribute(k_hist_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+            return 1;
+        });
+        const int vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0) ? 1 : 0;
+        const unsigned g = static_cast<unsigned>(std::min<int64_t>(2LL * N, sm_count()));
+        ProfScope ps_("k_hist", s);
+        k_hist_smem<<<g, kHistT, smem, s>>>(anc, ld_anc, N, P, o, ld_o, vec);
+        ++*launches;
+        return cudaPeekAtLastError();
+    }
     cudaError_t e = cudaMemset2DAsync(o, static_cast<size_t>(ld_o) * 4, 0, static_cast<size_t>(P) * 4,
                                       static_cast<size_t>(N), s);
     if (e != cudaSuccess) return e;

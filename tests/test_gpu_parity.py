@@ -528,6 +528,29 @@ def test_offspring_out_and_permute_offspring(pf, dev, orc, scheme, fusion):
         pf.pf_set_fusion(True)
 
 
+def test_offspring_histogram_batches(pf, dev, orc):
+    """The shared-memory histogram (two CTAs per filter, batches of >= half the SMs, P <= 65536):
+    offspring of random, skewed (one particle takes every slot) and identity ancestors, odd P,
+    ld > P, against the oracle; and the permutation built on it."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    for N, P in ((200, 65536), (150, 5001), (100, 2), (90, 777)):
+        ld = P + 4
+        A = rng.integers(0, P, size=(N, ld)).astype(np.int32)
+        A[1, :P] = P - 1            # every slot on the last particle (count = P)
+        A[2, :P] = np.arange(P)     # identity
+        A[3, :P] = 0                # every slot on particle 0
+        g = _gpu(A, dev)[:, :P]
+        o = pf.pf_ancestors_to_offspring(g)
+        pm = pf.pf_permute(g)
+        torch.cuda.synchronize()
+        O, Pm = o.cpu().numpy(), pm.cpu().numpy()
+        for n in (0, 1, 2, 3, N - 1):
+            assert np.array_equal(O[n], orc.ancestors_to_offspring(A[n, :P])), (N, P, n)
+            assert np.array_equal(Pm[n], orc.permute(A[n, :P])), (N, P, n)
+
+
 def test_batched_offspring_permute_gather(pf, dev, orc):
     import torch
 
