@@ -233,20 +233,21 @@ __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32
     const uint32_t ch = static_cast<uint32_t>(lane & ((1 << a.xlg) - 1)) * 16u;
     const int rstep = 32 >> a.xlg;  // rows per warp instruction
     const uint32_t xld = static_cast<uint32_t>(a.xld);
-    for (int p = lane >> a.xlg; p < npairs; p += kCopyU * rstep) {
+    int p = lane >> a.xlg;
+    // full rounds without per-item predicates (no divergent branches around the loads), then
+    // the tail item by item
+    for (; p + (kCopyU - 1) * rstep < npairs; p += kCopyU * rstep) {
         int4 v[kCopyU];
 #pragma unroll
-        for (int u = 0; u < kCopyU; ++u) {
-            const int q = p + u * rstep;
-            if (q < npairs)
-                v[u] = __ldcg(reinterpret_cast<const int4*>(Xf + (static_cast<uint32_t>(owner[q]) * xld + ch)));
-        }
+        for (int u = 0; u < kCopyU; ++u)
+            v[u] = __ldcg(reinterpret_cast<const int4*>(Xf + (static_cast<uint32_t>(owner[p + u * rstep]) * xld + ch)));
 #pragma unroll
-        for (int u = 0; u < kCopyU; ++u) {
-            const int q = p + u * rstep;
-            if (q < npairs) __stcg(reinterpret_cast<int4*>(Xf + (static_cast<uint32_t>(slot[q]) * xld + ch)), v[u]);
-        }
+        for (int u = 0; u < kCopyU; ++u)
+            __stcg(reinterpret_cast<int4*>(Xf + (static_cast<uint32_t>(slot[p + u * rstep]) * xld + ch)), v[u]);
     }
+    for (; p < npairs; p += rstep)
+        __stcg(reinterpret_cast<int4*>(Xf + (static_cast<uint32_t>(slot[p]) * xld + ch)),
+               __ldcg(reinterpret_cast<const int4*>(Xf + (static_cast<uint32_t>(owner[p]) * xld + ch))));
 }
 
 // PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
