@@ -285,6 +285,57 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
                                      const int32_t* d_gbad, int32_t* anc, pf_stream_t stream);
 
 /*
+ * Cross-GPU particle migration of a sharded filter:
+ * the in-place permutation (a9, NS-15) and state gather (a10, NS-16) of the WHOLE filter,
+ * applied shard by shard.  After resampling, shard g's particles [p0, p0 + Pl) have
+ * offspring o_i; the global extras list (particle i repeated o_i - 1 times, ascending i)
+ * is the concatenation of the shards' own extras lists, and the global free-slot list
+ * (o_i = 0, ascending) the concatenation of their own free lists, so the r-th global
+ * extra goes to the r-th global free slot exactly as NS-15 on the whole filter:
+ *   4a pf_shard_offspring         o_i of the shard's particles (prefix-sum schemes: every
+ *                                 ancestor of a particle of shard g was written by rank g)
+ *                                 (Metropolis: histogram the rank's slots over the whole
+ *                                 filter, then reduce_scatter(SUM) of the counts)
+ *   4b pf_shard_migration_counts  d_counts = {E_g extras, F_g free slots}
+ *      -> all_gather of the counts; exclusive prefixes give each rank's ranges of the
+ *         global extras / free lists, hence the split sizes of one variable all-to-all
+ *   4c pf_shard_migrate_pack      the shard's extra rows (+ their global indices), in order
+ *      -> all_to_all of the rows (rank g receives exactly its F_g rows, in global order)
+ *   4d pf_shard_migrate_unpack    received rows into the free slots; survivors stay
+ * Afterwards shard g holds rows [p0, p0 + Pl) of pf_gather_state(X, pf_permute(anc)) on the
+ * whole filter, and perm_out[i] = pf_permute(anc)[p0 + i].  Rows that stay on their shard
+ * go through the all-to-all's self-copy.  Sum over shards of E_g = sum of F_g.
+ */
+/* offspring[Pw] (device) = #{k in the slot window : anc[k] - win0 = i} for i in [0, Pw).
+ * anc[n_anc] (device) holds global ancestor indices; the slot window is
+ * [d_slot_range[0], d_slot_range[1]) clamped to [0, n_anc) (d_slot_range: device, as
+ * written by pf_shard_search / pf_shard_search_sorted), or all n_anc entries when
+ * d_slot_range is NULL (the unsorted multinomial, whose shard writes scattered slots;
+ * entries it did not write must lie outside [win0, win0 + Pw), e.g. -1).  Entries outside
+ * [win0, win0 + Pw) are ignored.  d_gmax / d_gbad (device, both or neither): when they
+ * mark the global filter invalid (bad, or max = -inf), offspring = 1 everywhere (the
+ * identity ancestors NS-1 gives; the searches then report an empty slot range). */
+pf_status pf_shard_offspring(const int32_t* anc, int64_t n_anc, const int64_t* d_slot_range, int64_t win0,
+                             int32_t Pw, const float* d_gmax, const int32_t* d_gbad, int32_t* offspring,
+                             pf_stream_t stream);
+/* d_counts[0] = E = sum_i max(o_i - 1, 0), d_counts[1] = F = #{i : o_i = 0} (device int64). */
+pf_status pf_shard_migration_counts(const int32_t* offspring, int32_t Pl, int64_t* d_counts, pf_stream_t stream);
+/* send_rows[E][row_bytes] (device, packed) = the shard's extra rows in NS-15 order: for
+ * ascending i with o_i > 1, o_i - 1 copies of X[i]; send_src[E] (device int32, nullable) =
+ * their global indices p0 + i.  X: [Pl] rows of row_bytes at stride ld_bytes; X and
+ * send_rows may be NULL when row_bytes = 0 (indices only).  Must not overlap. */
+pf_status pf_shard_migrate_pack(const void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
+                                const int32_t* offspring, void* send_rows, int32_t* send_src, pf_stream_t stream);
+/* In place: the r-th free slot (o_i = 0, ascending i) of the shard <- recv_rows[r]
+ * (packed rows, F of them, device); survivors are untouched.  perm_out[Pl] (device int32,
+ * nullable unless row_bytes = 0) = p0 + i for survivors, recv_src[r] for the r-th free
+ * slot.  recv_rows (when row_bytes > 0) and recv_src (when perm_out is given) must hold F
+ * entries; they are not read, and may be NULL, when F = 0.  X may be NULL when row_bytes = 0. */
+pf_status pf_shard_migrate_unpack(void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
+                                  const int32_t* offspring, const void* recv_rows, const int32_t* recv_src,
+                                  int32_t* perm_out, pf_stream_t stream);
+
+/*
  * Bootstrap particle filter demo model (BASELINE config C4; P:43-68 steps 1-3;
  * DESIGN.md R-20): a diagonal AR(1) state in D dimensions, x_t = phi x_{t-1} +
  * sigma_x eps_t, observed through y_t = x_t[0] + sigma_y eta_t.  X is float32

@@ -80,6 +80,10 @@ _SIGS = {
                                ctypes.c_int),
     "pf_shard_weights": ([_V, _I32, _V, _V, _V], ctypes.c_int),
     "pf_metropolis_from_weights": ([_V, _I64, _I64, _I32, _U64, _I32, _U32, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_offspring": ([_V, _I64, _V, _I64, _I32, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_migration_counts": ([_V, _I32, _V, _V], ctypes.c_int),
+    "pf_shard_migrate_pack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_migrate_unpack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
     "pf_lg_init": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, _U64, _V], ctypes.c_int),
     "pf_lg_propagate_weight": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                 ctypes.c_float, _U64, _I32, _V, _V], ctypes.c_int),
@@ -486,6 +490,68 @@ def pf_metropolis_from_weights(w_full, slot0: int, nslots: int, seed: int, B: in
                                             seed & (2 ** 64 - 1), B, filter_index, _ptr(gmax), _ptr(gbad),
                                             anc.data_ptr(), _stream(w_full, stream)), "pf_metropolis_from_weights")
     return anc
+
+
+# ----------------------------------------------------------------------------- particle migration
+def pf_shard_offspring(anc, win0: int, Pw: int, slot_range=None, gmax=None, gbad=None, out=None, stream=None):
+    """Stage 4a: offspring[Pw] (int32) of particles [win0, win0 + Pw) from the global ancestors in
+    ``anc`` (entries slot_range[0]..slot_range[1], or all of them when slot_range is None)."""
+    torch = _torch()
+    _need_cuda(anc, torch.int32, "anc")
+    if out is None:
+        out = torch.empty(Pw, dtype=torch.int32, device=anc.device)
+    _check(lib().pf_shard_offspring(anc.data_ptr(), anc.shape[0], _ptr(slot_range), win0, Pw, _ptr(gmax),
+                                    _ptr(gbad), out.data_ptr(), _stream(anc, stream)), "pf_shard_offspring")
+    return out
+
+
+def pf_shard_migration_counts(offspring, stream=None):
+    """Stage 4b: int64[2] device tensor {E extras, F free slots} of the shard."""
+    torch = _torch()
+    _need_cuda(offspring, torch.int32, "offspring")
+    c = torch.empty(2, dtype=torch.int64, device=offspring.device)
+    _check(lib().pf_shard_migration_counts(offspring.data_ptr(), offspring.shape[0], c.data_ptr(),
+                                           _stream(offspring, stream)), "pf_shard_migration_counts")
+    return c
+
+
+def _rows_view(X):
+    if X is None:
+        return 0, 0
+    row, ld, _ = _state_layout(X, False)
+    return row, ld
+
+
+def pf_shard_migrate_pack(X, offspring, p0: int, E: int, stream=None):
+    """Stage 4c: (send_rows uint8 [E, row_bytes] or None, send_src int32 [E]) — the shard's
+    extras in NS-15 order.  E = this shard's extras count (pf_shard_migration_counts)."""
+    torch = _torch()
+    _need_cuda(offspring, torch.int32, "offspring")
+    dev = offspring.device
+    row, ld = _rows_view(X)
+    src = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    rows = torch.empty((max(E, 1), row), dtype=torch.uint8, device=dev) if row else None
+    _check(lib().pf_shard_migrate_pack(_ptr(X), row, ld, offspring.shape[0], p0, offspring.data_ptr(), _ptr(rows),
+                                       src.data_ptr(), _stream(offspring, stream)), "pf_shard_migrate_pack")
+    return (rows[:E] if rows is not None else None), src[:E]
+
+
+def pf_shard_migrate_unpack(X, offspring, p0: int, recv_rows, recv_src, perm_out=None, stream=None):
+    """Stage 4d: free slots of X (in place) <- recv_rows; returns perm_out (int32 [Pl]) when
+    recv_src is given: the global index of the particle each slot now holds."""
+    torch = _torch()
+    _need_cuda(offspring, torch.int32, "offspring")
+    row, ld = _rows_view(X)
+    if perm_out is None and recv_src is not None:
+        perm_out = torch.empty(offspring.shape[0], dtype=torch.int32, device=offspring.device)
+    if recv_rows is not None and recv_rows.numel() == 0:
+        recv_rows = None
+    if row and recv_rows is not None and (recv_rows.dim() != 2 or recv_rows.shape[1] != row):
+        raise PfError("recv_rows must be [F, row_bytes] uint8")
+    _check(lib().pf_shard_migrate_unpack(_ptr(X), row, ld, offspring.shape[0], p0, offspring.data_ptr(),
+                                         _ptr(recv_rows), _ptr(recv_src), _ptr(perm_out),
+                                         _stream(offspring, stream)), "pf_shard_migrate_unpack")
+    return perm_out
 
 
 # ----------------------------------------------------------------------------- C4 demo model

@@ -1,0 +1,332 @@
+// pf_migrate.cu — cross-GPU particle migration of a sharded filter (include/pf.h 4a-4d;
+// SURVEY §8(f) NEXT-4).
+//
+// The canonical permutation NS-15 of the whole filter, shard by shard: each shard packs its
+// own extras (particle i repeated o_i - 1 times, ascending i) and fills its own free slots
+// (o_i = 0, ascending) from the rows the all-to-all delivers.  Both lists are built per
+// 2048-particle tile from a tile-level exclusive scan, then expanded item by item (one
+// 4/16-byte chunk of one row per thread), so the copies are coalesced on the packed side and
+// load-balanced whatever the offspring distribution.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "pf_internal.h"
+
+namespace pf {
+namespace {
+
+constexpr int kMigItems = 8;
+constexpr int kMigTile = kThreads * kMigItems;  // particles per tile
+constexpr unsigned kFullMask = 0xffffffffu;
+
+template <int CH>
+struct MigChunk;
+template <> struct MigChunk<16> { using T = int4; };
+template <> struct MigChunk<4> { using T = int32_t; };
+template <> struct MigChunk<1> { using T = char; };
+
+__host__ __device__ inline int64_t mig_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Exclusive block scan of one value per thread (kThreads threads); returns the block total.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* excl, int64_t* s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t t = __shfl_up_sync(kFullMask, inc, d);
+        if (lane >= d) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    int64_t before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const int64_t s = s_warp[w];
+        if (w < warp) before += s;
+        total += s;
+    }
+    *excl = before + inc - v;
+    __syncthreads();  // s_warp reusable
+    return total;
+}
+
+// 4a: histogram of the window's ancestors; warp-aggregated (sorted ancestors come in runs).
+__global__ void __launch_bounds__(kThreads) k_mig_offspring(const int32_t* __restrict__ anc, int64_t n_anc,
+                                                            const int64_t* __restrict__ range, int64_t win0,
+                                                            int32_t Pw, const float* gmax, const int32_t* gbad,
+                                                            int32_t* __restrict__ o) {
+    const bool invalid = gbad != nullptr && (*gbad != 0 || *gmax == -INFINITY);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    if (invalid) {
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < Pw; i += stride) o[i] = 1;
+        return;
+    }
+    int64_t lo = 0, hi = n_anc;
+    if (range != nullptr) {
+        lo = max(range[0], static_cast<int64_t>(0));
+        hi = min(range[1], n_anc);
+    }
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count so __match_any_sync sees the whole warp
+    for (int64_t base = lo + blockIdx.x * static_cast<int64_t>(kThreads) + (threadIdx.x & ~31); base < hi;
+         base += stride) {
+        const int64_t k = base + lane;
+        int32_t v = -1;
+        if (k < hi) {
+            const int64_t a = static_cast<int64_t>(__ldg(anc + k)) - win0;
+            if (a >= 0 && a < Pw) v = static_cast<int32_t>(a);
+        }
+        const unsigned peers = __match_any_sync(kFullMask, v);
+        if (v >= 0 && lane == __ffs(peers) - 1) atomicAdd(o + v, static_cast<int32_t>(__popc(peers)));
+    }
+}
+
+// Per-tile counts: tE[t] = sum max(o - 1, 0), tF[t] = #{o = 0} over tile t.
+__global__ void __launch_bounds__(kThreads) k_mig_tile_counts(const int32_t* __restrict__ o, int32_t Pl,
+                                                              int64_t* __restrict__ tE, int64_t* __restrict__ tF) {
+    __shared__ int64_t s_warp[kThreads / 32];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kMigTile + threadIdx.x * kMigItems;
+    int64_t e = 0, f = 0;
+#pragma unroll
+    for (int j = 0; j < kMigItems; ++j) {
+        const int64_t i = i0 + j;
+        if (i < Pl) {
+            const int32_t v = __ldg(o + i);
+            e += v > 1 ? v - 1 : 0;
+            f += v == 0;
+        }
+    }
+    int64_t ex;
+    const int64_t E = block_excl_scan(e, &ex, s_warp);
+    const int64_t F = block_excl_scan(f, &ex, s_warp);
+    if (threadIdx.x == 0) {
+        tE[blockIdx.x] = E;
+        tF[blockIdx.x] = F;
+    }
+}
+
+// One CTA: exclusive scans of tE and tF in place; totals into counts[0..1].
+__global__ void __launch_bounds__(1024) k_mig_tile_scan(int64_t* __restrict__ tE, int64_t* __restrict__ tF,
+                                                        int64_t ntiles, int64_t* __restrict__ counts) {
+    __shared__ int64_t s_warp[2][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t per = mig_cdiv(ntiles, 1024);
+    const int64_t b = threadIdx.x * per, e = min(ntiles, b + per);
+    int64_t sE = 0, sF = 0;
+    for (int64_t t = b; t < e; ++t) {
+        sE += tE[t];
+        sF += tF[t];
+    }
+    int64_t iE = sE, iF = sF;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t a = __shfl_up_sync(kFullMask, iE, d), c = __shfl_up_sync(kFullMask, iF, d);
+        if (lane >= d) {
+            iE += a;
+            iF += c;
+        }
+    }
+    if (lane == 31) {
+        s_warp[0][warp] = iE;
+        s_warp[1][warp] = iF;
+    }
+    __syncthreads();
+    int64_t bE = 0, bF = 0, TE = 0, TF = 0;
+    for (int w = 0; w < 32; ++w) {
+        if (w < warp) {
+            bE += s_warp[0][w];
+            bF += s_warp[1][w];
+        }
+        TE += s_warp[0][w];
+        TF += s_warp[1][w];
+    }
+    int64_t rE = bE + iE - sE, rF = bF + iF - sF;
+    for (int64_t t = b; t < e; ++t) {
+        const int64_t ve = tE[t], vf = tF[t];
+        tE[t] = rE;
+        tF[t] = rF;
+        rE += ve;
+        rF += vf;
+    }
+    if (threadIdx.x == 0 && counts != nullptr) {
+        counts[0] = TE;
+        counts[1] = TF;
+    }
+}
+
+// 4c: the tile's extras in NS-15 order.  s_inc[q] = inclusive count of extras of the tile's
+// particles 0..q; extra j of the tile belongs to the first q with s_inc[q] > j.
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_mig_pack(const char* __restrict__ X, int64_t ld, int64_t row_bytes,
+                                                       int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
+                                                       const int64_t* __restrict__ tE, char* __restrict__ send,
+                                                       int32_t* __restrict__ send_src) {
+    using T = typename MigChunk<CH>::T;
+    __shared__ int32_t s_inc[kMigTile];
+    __shared__ int64_t s_warp[kThreads / 32];
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMigTile;
+    int32_t e[kMigItems];
+    int32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kMigItems; ++j) {
+        const int64_t i = t0 + threadIdx.x * kMigItems + j;
+        const int32_t v = i < Pl ? __ldg(o + i) : 1;
+        e[j] = v > 1 ? v - 1 : 0;
+        sum += e[j];
+    }
+    int64_t ex;
+    const int64_t Et = block_excl_scan(sum, &ex, s_warp);
+    int32_t run = static_cast<int32_t>(ex);
+#pragma unroll
+    for (int j = 0; j < kMigItems; ++j) {
+        run += e[j];
+        s_inc[threadIdx.x * kMigItems + j] = run;
+    }
+    __syncthreads();
+    if (Et == 0) return;
+    const int64_t base = tE[blockIdx.x];
+    const int64_t cpr = row_bytes / CH;
+    const int64_t items = cpr > 0 ? Et * cpr : Et;
+    for (int64_t g = threadIdx.x; g < items; g += kThreads) {
+        const int64_t j = cpr > 0 ? g / cpr : g;
+        const int64_t c = cpr > 0 ? g - j * cpr : 0;
+        int lo = 0, hi = kMigTile - 1;  // first q with s_inc[q] > j
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_inc[mid] > j) hi = mid;
+            else lo = mid + 1;
+        }
+        const int64_t i = t0 + lo;
+        if (cpr > 0)
+            reinterpret_cast<T*>(send + (base + j) * row_bytes)[c] = __ldg(reinterpret_cast<const T*>(X + i * ld) + c);
+        if (c == 0 && send_src != nullptr) send_src[base + j] = static_cast<int32_t>(p0 + i);
+    }
+}
+
+// 4d: the tile's free slots take rows tF[t] + r, r = their rank in the tile.
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_mig_unpack(char* __restrict__ X, int64_t ld, int64_t row_bytes,
+                                                         int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
+                                                         const int64_t* __restrict__ tF,
+                                                         const char* __restrict__ recv,
+                                                         const int32_t* __restrict__ recv_src,
+                                                         int32_t* __restrict__ perm) {
+    using T = typename MigChunk<CH>::T;
+    __shared__ int32_t s_free[kMigTile];
+    __shared__ int64_t s_warp[kThreads / 32];
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMigTile;
+    const int64_t base = tF[blockIdx.x];
+    bool fr[kMigItems];
+    int32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kMigItems; ++j) {
+        const int64_t i = t0 + threadIdx.x * kMigItems + j;
+        fr[j] = i < Pl && __ldg(o + i) == 0;
+        cnt += fr[j];
+    }
+    int64_t ex;
+    const int64_t Ft = block_excl_scan(cnt, &ex, s_warp);
+    int32_t r = static_cast<int32_t>(ex);
+#pragma unroll
+    for (int j = 0; j < kMigItems; ++j) {
+        const int q = threadIdx.x * kMigItems + j;
+        const int64_t i = t0 + q;
+        if (fr[j]) {
+            s_free[r] = q;
+            if (perm != nullptr) perm[i] = __ldg(recv_src + base + r);
+            ++r;
+        } else if (perm != nullptr && i < Pl) {
+            perm[i] = static_cast<int32_t>(p0 + i);
+        }
+    }
+    __syncthreads();
+    const int64_t cpr = row_bytes / CH;
+    if (cpr == 0) return;
+    const int64_t items = Ft * cpr;
+    for (int64_t g = threadIdx.x; g < items; g += kThreads) {
+        const int64_t j = g / cpr, c = g - j * cpr;
+        const int64_t i = t0 + s_free[j];
+        reinterpret_cast<T*>(X + i * ld)[c] = __ldg(reinterpret_cast<const T*>(recv + (base + j) * row_bytes) + c);
+    }
+}
+
+int mig_chunk(const void* a, const void* b, int64_t row_bytes, int64_t ld) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b);
+    if ((p & 15) == 0 && row_bytes % 16 == 0 && ld % 16 == 0) return 16;
+    if ((p & 3) == 0 && row_bytes % 4 == 0 && ld % 4 == 0) return 4;
+    return 1;
+}
+
+}  // namespace
+
+size_t mig_scratch_bytes(int32_t Pl) { return 2 * sizeof(int64_t) * static_cast<size_t>(mig_cdiv(Pl, kMigTile)) + 256; }
+
+cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_t* range, int64_t win0, int32_t Pw,
+                                 const float* gmax, const int32_t* gbad, int32_t* o, cudaStream_t s,
+                                 uint64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(o, 0, sizeof(int32_t) * static_cast<size_t>(Pw), s);
+    if (e != cudaSuccess) return e;
+    const int64_t work = std::max<int64_t>(n_anc, Pw);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(mig_cdiv(work, kThreads), static_cast<int64_t>(sm_count()) * 8)));
+    ProfScope ps_("k_mig_offspring", s);
+    k_mig_offspring<<<grid, kThreads, 0, s>>>(anc, n_anc, range, win0, Pw, gmax, gbad, o);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+// tile prefixes in scratch (tE = scratch, tF = scratch + ntiles); counts nullable
+cudaError_t launch_mig_prefix(const int32_t* o, int32_t Pl, void* scratch, int64_t* counts, cudaStream_t s,
+                              uint64_t* launches) {
+    const int64_t nt = mig_cdiv(Pl, kMigTile);
+    int64_t* tE = static_cast<int64_t*>(scratch);
+    int64_t* tF = tE + nt;
+    {
+        ProfScope ps_("k_mig_tile_counts", s);
+        k_mig_tile_counts<<<static_cast<unsigned>(nt), kThreads, 0, s>>>(o, Pl, tE, tF);
+    }
+    {
+        ProfScope ps_("k_mig_tile_scan", s);
+        k_mig_tile_scan<<<1, 1024, 0, s>>>(tE, tF, nt, counts);
+    }
+    *launches += 2;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_mig_pack(const void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
+                            void* send, int32_t* send_src, void* scratch, cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = launch_mig_prefix(o, Pl, scratch, nullptr, s, launches);
+    if (e != cudaSuccess) return e;
+    const int64_t* tE = static_cast<const int64_t*>(scratch);
+    const char* x = static_cast<const char*>(X);
+    char* y = static_cast<char*>(send);
+    const int ch = row_bytes > 0 ? mig_chunk(x, y, row_bytes, std::max<int64_t>(ld, row_bytes)) : 16;
+    const unsigned grid = static_cast<unsigned>(mig_cdiv(Pl, kMigTile));
+    ProfScope ps_("k_mig_pack", s);
+    if (ch == 16) k_mig_pack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
+    else if (ch == 4) k_mig_pack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
+    else k_mig_pack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_mig_unpack(void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
+                              const void* recv, const int32_t* recv_src, int32_t* perm, void* scratch,
+                              cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = launch_mig_prefix(o, Pl, scratch, nullptr, s, launches);
+    if (e != cudaSuccess) return e;
+    const int64_t* tF = static_cast<const int64_t*>(scratch) + mig_cdiv(Pl, kMigTile);
+    char* x = static_cast<char*>(X);
+    const char* y = static_cast<const char*>(recv);
+    const int ch = row_bytes > 0 ? mig_chunk(x, y, row_bytes, std::max<int64_t>(ld, row_bytes)) : 16;
+    const unsigned grid = static_cast<unsigned>(mig_cdiv(Pl, kMigTile));
+    ProfScope ps_("k_mig_unpack", s);
+    if (ch == 16) k_mig_unpack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
+    else if (ch == 4) k_mig_unpack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
+    else k_mig_unpack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+}  // namespace pf

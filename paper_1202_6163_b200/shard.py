@@ -17,6 +17,11 @@ into a per-GPU scan plus an 8-byte-per-rank exchange):
   Metropolis:          max  -> all_reduce(MAX); weights -> all_gather of the
                        weight vector; chains for the rank's own slots
                        (no collective inside the resampler).
+  migration            (``migrate_sharded``; NEXT-4) the in-place permutation and state
+                       gather of the whole filter: offspring of the rank's particles
+                       (Metropolis: reduce_scatter of slot histograms), all_gather of the
+                       16-byte (extras, free) counts, one variable all_to_all of the
+                       extra rows (and their indices); survivors never move.
 
 The arithmetic of every stage is the single-GPU numeric spec evaluated with the
 global max and k_fx(P_global), so the result is bit-identical to
@@ -62,6 +67,28 @@ class TorchComm:
         self.dist.all_gather(out, t, group=self.group)
         return torch.cat(out)
 
+    def reduce_scatter_sum(self, t):
+        """t: [world * n]; returns this rank's n-slice of the sum over ranks."""
+        import torch
+
+        n = t.shape[0] // self.world
+        out = torch.empty(n, dtype=t.dtype, device=t.device)
+        if self.dist.get_backend(self.group) == "gloo":  # gloo has no reduce_scatter
+            self.dist.all_reduce(t, group=self.group)
+            out.copy_(t[self.rank * n:(self.rank + 1) * n])
+        else:
+            self.dist.reduce_scatter_tensor(out, t, group=self.group)
+        return out
+
+    def all_to_all_v(self, t, send_splits, recv_splits):
+        """Rows t[sum(send_splits[:g]) : ...] go to rank g; returns the rows received, in rank order."""
+        import torch
+
+        out = torch.empty((sum(recv_splits),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=list(recv_splits),
+                                    input_split_sizes=list(send_splits), group=self.group)
+        return out
+
 
 class SingleComm:
     """World of one (no communication): the sharded path on a single GPU."""
@@ -72,6 +99,12 @@ class SingleComm:
         return t
 
     def all_gather_cat(self, t):
+        return t
+
+    def reduce_scatter_sum(self, t):
+        return t
+
+    def all_to_all_v(self, t, send_splits, recv_splits):
         return t
 
 
@@ -106,6 +139,18 @@ class GpuStages:
     def metropolis(self, w_full, slot0, nslots, seed, B, filter_index, gmax, gbad):
         return self.pf.pf_metropolis_from_weights(w_full, slot0, nslots, seed, B, filter_index, gmax, gbad)
 
+    def offspring(self, anc, win0, Pw, slot_range, gmax, gbad):
+        return self.pf.pf_shard_offspring(anc, win0, Pw, slot_range=slot_range, gmax=gmax, gbad=gbad)
+
+    def migration_counts(self, o):
+        return self.pf.pf_shard_migration_counts(o)
+
+    def pack(self, X, o, p0, E):
+        return self.pf.pf_shard_migrate_pack(X, o, p0, E)
+
+    def unpack(self, X, o, p0, rows, src):
+        return self.pf.pf_shard_migrate_unpack(X, o, p0, rows, src)
+
 
 def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, filter_index: int = 0,
                      comm=None, stages=None, assemble: bool = True, flags: int = 0):
@@ -132,7 +177,8 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     lmax, bad = stages.max(logw_local)
     gmax = comm.all_reduce_max(lmax.clone())
     gbad = comm.all_reduce_max(bad.clone())
-    info = {"p0": p0, "Pl": Pl}
+    info = {"p0": p0, "Pl": Pl, "P_global": P_global, "scheme": scheme_id, "sorted": is_sorted, "gmax": gmax,
+            "gbad": gbad}
     if scheme_id == 4:
         w = stages.weights(logw_local, gmax)
         per = -(-P_global // world)
@@ -162,6 +208,90 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     if not assemble:
         return anc, info
     return comm.all_reduce_max(anc), info
+
+
+def _overlap(a0, a1, b0, b1):
+    return max(0, min(a1, b1) - max(a0, b0))
+
+
+def migration_splits(counts, rank: int):
+    """Split sizes of the migration all-to-all from the all-gathered (E_g, F_g) of every rank:
+    rank r's extras occupy [Epre_r, Epre_r + E_r) of the global extras list (NS-15 order),
+    rank g's free slots [Fpre_g, Fpre_g + F_g) of the global free list; extra n goes to free
+    slot n.  Returns (send_splits, recv_splits) of ``rank``."""
+    E = [int(e) for e, _ in counts]
+    F = [int(f) for _, f in counts]
+    if sum(E) != sum(F):
+        raise RuntimeError(f"migration counts disagree: sum E = {sum(E)}, sum F = {sum(F)}")
+    Epre = [sum(E[:g]) for g in range(len(E))]
+    Fpre = [sum(F[:g]) for g in range(len(F))]
+    send = [_overlap(Epre[rank], Epre[rank] + E[rank], Fpre[g], Fpre[g] + F[g]) for g in range(len(F))]
+    recv = [_overlap(Epre[g], Epre[g] + E[g], Fpre[rank], Fpre[rank] + F[rank]) for g in range(len(E))]
+    return send, recv
+
+
+def migrate_sharded(X_local, anc, info, comm=None, stages=None):
+    """Cross-GPU particle migration (include/pf.h 4a-4d).
+
+    After ``resample_sharded(..., assemble=False)`` (``anc``, ``info`` as it returned; an
+    assembled [P_global] vector works too), applies the whole filter's canonical permutation
+    (NS-15) and in-place gather (NS-16) to this rank's state rows ``X_local`` [Pl, ...] (or
+    None: indices only).  Returns this rank's slice of the permutation (int32 [Pl]: global
+    index of the particle each slot now holds).  Survivors stay; only extra rows travel, in
+    one variable all_to_all; the host reads back 16 bytes per rank for the split sizes.
+    """
+    import torch
+
+    comm = comm or TorchComm()
+    stages = stages or GpuStages()
+    p0, Pl, P_global = info["p0"], info["Pl"], info["P_global"]
+    if X_local is not None and X_local.shape[0] != Pl:
+        raise ValueError(f"X_local has {X_local.shape[0]} rows, expected {Pl}")
+    if anc.shape[0] == P_global:
+        # prefix-sum schemes (or any assembled vector): the rank's particles' ancestors are all here
+        # (stratified, systematic, sorted multinomial: within the slot range the search reported)
+        rng = info.get("slot_range_dev") if (info["scheme"] in (2, 3) or info["sorted"]) else None
+        o = stages.offspring(anc, p0, Pl, rng, info["gmax"], info["gbad"])
+    else:
+        # Metropolis slots [p0, p0 + Pl): ancestors anywhere -> slot histogram, summed over ranks
+        per = -(-P_global // comm.world)
+        h = stages.offspring(anc, 0, per * comm.world, None, None, None)
+        o = comm.reduce_scatter_sum(h)[:Pl].contiguous()
+    counts = comm.all_gather_cat(stages.migration_counts(o)).cpu().view(-1, 2).tolist()
+    send, recv = migration_splits(counts, comm.rank)
+    rows, src = stages.pack(X_local, o, p0, int(counts[comm.rank][0]))
+    rsrc = comm.all_to_all_v(src, send, recv)
+    rrows = comm.all_to_all_v(rows, send, recv) if rows is not None else None
+    return stages.unpack(X_local, o, p0, rrows, rsrc)
+
+
+def migrate_sharded_local(X_full, anc_full, nshards: int, stages=None):
+    """Fake-shard mode of ``migrate_sharded``: every shard's stages on one device, the
+    all-to-all done by slicing.  X_full [P, ...] is updated in place (shard by shard);
+    returns the assembled permutation.  Exercises exactly the kernels and split logic."""
+    import torch
+
+    stages = stages or GpuStages()
+    P = anc_full.shape[0]
+    parts = [shard_range(P, nshards, g) for g in range(nshards)]
+    Xs = [X_full[p0:p0 + Pl] if X_full is not None else None for p0, Pl in parts]
+    os_ = [stages.offspring(anc_full, p0, Pl, None, None, None) for p0, Pl in parts]
+    counts = [[int(v) for v in stages.migration_counts(o).cpu().tolist()] for o in os_]
+    packed = [stages.pack(x, o, p0, counts[g][0]) for g, (x, o, (p0, _)) in enumerate(zip(Xs, os_, parts))]
+    splits = [migration_splits(counts, g) for g in range(nshards)]
+    perms = []
+    for g, (p0, Pl) in enumerate(parts):
+        rows, srcs = [], []
+        for h in range(nshards):
+            a = sum(splits[h][0][:g])
+            n = splits[h][0][g]
+            srcs.append(packed[h][1][a:a + n])
+            if packed[h][0] is not None:
+                rows.append(packed[h][0][a:a + n])
+        rsrc = torch.cat(srcs)
+        rrows = torch.cat(rows) if rows else None
+        perms.append(stages.unpack(Xs[g], os_[g], p0, rrows, rsrc))
+    return torch.cat(perms)
 
 
 def _sorted(scheme_id: int, flags: int) -> bool:

@@ -85,3 +85,35 @@ class CpuOracleStages:
             return torch.arange(slot0, slot0 + nslots, dtype=torch.int32)
         a = oracle.metropolis_chains(w_full.numpy(), slot0, nslots, seed, B, filter_index)
         return torch.from_numpy(a)
+
+    # migration stages (include/pf.h 4a-4d) in plain numpy, for the gloo decomposition tests
+    def offspring(self, anc, win0, Pw, slot_range, gmax, gbad):
+        if gbad is not None and (int(gbad.item()) or float(gmax.item()) == -np.inf):
+            return torch.ones(Pw, dtype=torch.int32)
+        a = anc.numpy().astype(np.int64)
+        if slot_range is not None:
+            lo, hi = (int(v) for v in slot_range.tolist())
+            a = a[max(lo, 0):min(hi, len(a))]
+        a = a[(a >= win0) & (a < win0 + Pw)] - win0
+        return torch.from_numpy(np.bincount(a, minlength=Pw).astype(np.int32))
+
+    def migration_counts(self, o):
+        v = o.numpy()
+        return torch.tensor([int(np.maximum(v - 1, 0).sum()), int((v == 0).sum())], dtype=torch.int64)
+
+    def pack(self, X, o, p0, E):
+        v = o.numpy()
+        idx = np.repeat(np.arange(len(v)), np.maximum(v - 1, 0))
+        assert len(idx) == E
+        rb = X[0].numel() * X.element_size() if X is not None else 0
+        rows = None if X is None else X[torch.from_numpy(idx)].contiguous().view(torch.uint8).reshape(E, rb)
+        return rows, torch.from_numpy((p0 + idx).astype(np.int32))
+
+    def unpack(self, X, o, p0, rows, src):
+        v = o.numpy()
+        free = np.flatnonzero(v == 0)
+        perm = (p0 + np.arange(len(v))).astype(np.int32)
+        perm[free] = src.numpy()
+        if X is not None and len(free):
+            X[torch.from_numpy(free)] = rows.view(X.dtype).reshape((len(free),) + tuple(X.shape[1:]))
+        return torch.from_numpy(perm)

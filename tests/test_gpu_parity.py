@@ -749,6 +749,106 @@ def test_giant_filter_fake_shards_sorted_multinomial(pf, dev, orc):
         assert np.array_equal(a.cpu().numpy(), want), (P, G, kind)
 
 
+MIGRATION_SCHEMES = [("systematic", 0), ("stratified", 0), ("multinomial", 0), ("multinomial", 1), ("metropolis", 0)]
+
+
+@pytest.mark.parametrize("scheme,flags", MIGRATION_SCHEMES)
+def test_particle_migration_ranks_on_one_gpu(pf, dev, orc, scheme, flags):
+    """Cross-GPU particle migration (include/pf.h 4a-4d; NEXT-4): G ranks run as threads on one
+    GPU through the real resample_sharded(assemble=False) + migrate_sharded code (slot ranges,
+    Metropolis reduce-scatter of slot histograms, split sizes, all-to-all by slicing).  Every
+    rank's rows and permutation slice equal the oracle's whole-filter permute + in-place gather,
+    element by element; a shard without weight (all its slots refilled from other shards), a
+    weight-skewed shard and an invalid filter (nothing moves) included."""
+    import torch
+
+    from paper_1202_6163_b200.shard import GpuStages, migrate_sharded, resample_sharded, shard_range
+    from tests._loopback_comm import run_ranks
+
+    B = 16 if scheme == "metropolis" else 0
+    cases = [(1000, 2, 1.0, ""), (4097, 3, 10.0, ""), (100003, 5, 1.0, ""), (1 << 18, 8, 1.0, ""),
+             (9000, 4, 1.0, "neg_inf_shard"), (20000, 4, 1.0, "skew"), (5000, 2, 1.0, "invalid"), (7, 3, 1.0, "")]
+    for P, G, var, kind in cases:
+        x = pfinputs.gaussian_logw(P, var, seed=P + G + 7)
+        if kind == "neg_inf_shard":
+            p0, Pl = shard_range(P, G, 1)
+            x[p0:p0 + Pl] = -np.inf
+        if kind == "skew":
+            p0, Pl = shard_range(P, G, 2)
+            x[p0:p0 + Pl] += 8.0
+        if kind == "invalid":
+            x[3] = np.nan
+        X = pfinputs.state_matrix(P, 16, seed=P)
+
+        def rank_fn(r, comm):
+            p0, Pl = shard_range(P, G, r)
+            anc, info = resample_sharded(scheme, _gpu(x[p0:p0 + Pl], dev), P, 777, B=B, filter_index=9, comm=comm,
+                                         stages=GpuStages(), assemble=False, flags=flags)
+            Xl = _gpu(X[p0:p0 + Pl], dev)
+            perm = migrate_sharded(Xl, anc, info, comm=comm)
+            return Xl.cpu().numpy(), perm.cpu().numpy()
+
+        out = run_ranks(G, rank_fn)
+        if flags:
+            _, want = orc.resample_sorted_multinomial(x, 777, filter_index=9)
+        else:
+            _, want = orc.resample(scheme, x, 777, B=B, filter_index=9)
+        wp = orc.permute(want)
+        assert np.array_equal(np.concatenate([p for _, p in out]), wp), (scheme, P, G, kind)
+        assert np.array_equal(np.concatenate([a for a, _ in out]), orc.gather_inplace(X, wp)), (scheme, P, G, kind)
+
+
+def test_particle_migration_layouts(pf, dev, orc):
+    """Migration stages on fake shards (migrate_sharded_local) for every copy width: 64-byte
+    float rows (16-byte chunks), 12-byte rows (4-byte chunks), 7-byte rows (bytes), rows with a
+    stride wider than the row, indices only; ancestors from the oracle with extreme offspring
+    (one particle takes every slot; the identity); P = 2^20 over 8 shards; argument errors."""
+    import torch
+
+    from paper_1202_6163_b200.shard import migrate_sharded_local
+
+    def check(Xh, anc, G, X_dev=None):
+        wp = orc.permute(anc)
+        Xd = X_dev if X_dev is not None else (_gpu(Xh, dev) if Xh is not None else None)
+        perm = migrate_sharded_local(Xd, _gpu(anc, dev), G)
+        torch.cuda.synchronize()
+        assert np.array_equal(perm.cpu().numpy(), wp), (G, len(anc))
+        if Xh is not None:
+            got = Xd.cpu().numpy()
+            assert np.array_equal(got, orc.gather_inplace(Xh, wp)), (G, len(anc), Xh.dtype, Xh.shape)
+
+    P = 5003
+    x = pfinputs.gaussian_logw(P, 1.0, seed=5)
+    _, anc = orc.resample("stratified", x, 31)
+    check(pfinputs.state_matrix(P, 16), anc, 3)
+    check(pfinputs.state_matrix(P, 3), anc, 4)
+    rng = np.random.default_rng(1)
+    check(rng.integers(0, 255, size=(P, 7), dtype=np.uint8), anc, 2)
+    check(None, anc, 5)
+    wide = pfinputs.state_matrix(P, 20)
+    Xw = _gpu(wide, dev)
+    wp = orc.permute(anc)
+    perm = migrate_sharded_local(Xw[:, :16], _gpu(anc, dev), 3)
+    torch.cuda.synchronize()
+    want = wide.copy()
+    want[:, :16] = orc.gather_inplace(np.ascontiguousarray(wide[:, :16]), wp)
+    assert np.array_equal(Xw.cpu().numpy(), want)
+    check(pfinputs.state_matrix(P, 16), np.full(P, P - 2, dtype=np.int32), 4)  # one particle takes all
+    check(pfinputs.state_matrix(P, 16), np.arange(P, dtype=np.int32), 4)  # nothing moves
+    Pb = 1 << 20
+    _, ancb = orc.resample("systematic", pfinputs.gaussian_logw(Pb, 1.0, seed=8), 3)
+    check(pfinputs.state_matrix(Pb, 16), ancb, 8)
+    a = _gpu(anc, dev)
+    o = torch.empty(P, dtype=torch.int32, device=dev)
+    L = pf.lib()
+    assert L.pf_shard_offspring(a.data_ptr(), P, None, 0, 0, None, None, o.data_ptr(), None) == 1
+    assert L.pf_shard_offspring(a.data_ptr(), P, None, 0, P, None, a.data_ptr(), o.data_ptr(), None) == 1
+    assert L.pf_shard_migration_counts(o.data_ptr(), 0, o.data_ptr(), None) == 1
+    assert L.pf_shard_migrate_pack(None, 64, 64, P, 0, o.data_ptr(), None, None, None) == 1
+    assert L.pf_shard_migrate_unpack(None, 0, 0, P, 0, o.data_ptr(), None, a.data_ptr(), None, None) == 1
+    assert L.pf_shard_migrate_unpack(None, 64, 64, P, 0, o.data_ptr(), None, None, None, None) == 1
+
+
 def test_sorted_multinomial_a6(pf, dev, orc):
     """a6 (PF_SORTED with the multinomial): spacings scan + exact 128/64 positions + merge,
     bit-exact against the oracle; batched with ld > P and an invalid filter; ragged sizes."""

@@ -6,6 +6,9 @@
   stages (oracle-based), assembled ancestors == the oracle's single-filter run.
   Includes the sorted multinomial (a6), whose ranks also all-gather the totals of
   their spacing shards.
+* Particle migration (migrate_sharded, include/pf.h 4a-4d): after the sharded resampling,
+  the ranks' state rows equal the oracle's in-place gather of the whole filter with its
+  canonical permutation (one variable all_to_all of the extra rows over gloo).
 * Batched filters sharded over ranks (config C3, bench.py): rank g owns filters
   [g N, (g+1) N) with first_filter = g N; the union equals a single-rank batch.
 """
@@ -36,7 +39,7 @@ def _worker(rank, world, port, outdir, cases):
     sys.path.insert(0, ROOT)
     import oracle
     import pfinputs
-    from paper_1202_6163_b200.shard import TorchComm, resample_sharded, shard_range
+    from paper_1202_6163_b200.shard import TorchComm, migrate_sharded, resample_sharded, shard_range
     from tests._cpu_shard_stages import CpuOracleStages
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -55,6 +58,13 @@ def _worker(rank, world, port, outdir, cases):
                                      filter_index=5, comm=comm, stages=stages, flags=flags)
         if rank == 0:
             np.save(os.path.join(outdir, f"shard_{ci}.npy"), anc.numpy())
+        # migration of the state rows (unassembled ancestors; the permuted form of the whole filter)
+        anc_u, info_u = resample_sharded(scheme, torch.from_numpy(x[p0:p0 + Pl].copy()), P, seed, B=B,
+                                         filter_index=5, comm=comm, stages=stages, flags=flags, assemble=False)
+        X = torch.from_numpy(pfinputs.state_matrix(P, 3, seed=ci)[p0:p0 + Pl].copy())
+        perm = migrate_sharded(X, anc_u, info_u, comm=comm, stages=stages)
+        np.save(os.path.join(outdir, f"mig_{ci}_{rank}.npy"), X.numpy())
+        np.save(os.path.join(outdir, f"migp_{ci}_{rank}.npy"), perm.numpy())
     # batched filters: rank g owns filters [g N, (g+1) N)
     N, P = 3, 500
     xs = pfinputs.gaussian_logw(P, 1.0, seed=11, N=N * world)
@@ -103,6 +113,13 @@ def test_two_rank_giant_filter_and_batches(tmp_path):
             _, want = oracle.resample(scheme, x, seed, B=B, filter_index=5)
         got = np.load(os.path.join(tmp_path, f"shard_{ci}.npy"))
         assert np.array_equal(got, want), (scheme, P, kind)
+        # migration: the ranks' rows = the whole filter's in-place gather with its permutation
+        wp = oracle.permute(want)
+        wX = oracle.gather_inplace(pfinputs.state_matrix(P, 3, seed=ci), wp)
+        gotX = np.concatenate([np.load(os.path.join(tmp_path, f"mig_{ci}_{r}.npy")) for r in range(world)])
+        gotp = np.concatenate([np.load(os.path.join(tmp_path, f"migp_{ci}_{r}.npy")) for r in range(world)])
+        assert np.array_equal(gotp, wp), (scheme, P, kind)
+        assert np.array_equal(gotX, wX), (scheme, P, kind)
     xs = pfinputs.gaussian_logw(500, 1.0, seed=11, N=3 * world)
     _, want = oracle.resample_batched("stratified", xs, 99, first_filter=0)
     assert np.array_equal(np.load(os.path.join(tmp_path, "batched.npy")), want)
