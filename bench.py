@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--strong", action="store_true", help="split a fixed N over ranks (strong scaling)")
     ap.add_argument("--sorted", action="store_true",
                     help="c5 with --scheme multinomial: the sorted-uniform multinomial (a6, PF_SORTED)")
+    ap.add_argument("--migrate", type=int, default=0, metavar="D",
+                    help="c5: also migrate D float32 state rows per particle across the shards (NEXT-4)")
     ap.add_argument("--no-extras", action="store_true", help="skip per-scheme / e2e / cpu_baseline extras")
     return ap.parse_args()
 
@@ -149,7 +151,7 @@ def run_c5(args):
 
     import paper_1202_6163_b200 as pf
     import pfinputs
-    from paper_1202_6163_b200.shard import SingleComm, TorchComm, resample_sharded, shard_range
+    from paper_1202_6163_b200.shard import SingleComm, TorchComm, migrate_sharded, resample_sharded, shard_range
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -167,8 +169,16 @@ def run_c5(args):
 
     flags = 1 if (args.sorted and scheme == "multinomial") else 0
 
+    X = None
+    if args.migrate:
+        gen = torch.Generator(device=dev).manual_seed(pfinputs.BASE_SEED + rank)
+        X = torch.randn((Pl, args.migrate), device=dev, generator=gen)
+
     def step():
-        return resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False, flags=flags)
+        anc, info = resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False, flags=flags)
+        if X is not None:  # cross-GPU particle migration of the state rows (include/pf.h 4a-4d)
+            migrate_sharded(X, anc, info, comm=comm)
+        return anc
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -200,10 +210,12 @@ def run_c5(args):
             "data": "synthetic",
             "config": {"workload": desc + f", P_global={P_global}, sigma^2={args.var}, scheme={scheme}"
                                   + (" (sorted-uniform, a6)" if flags else "")
-                                  + (f", B={B}" if scheme == "metropolis" else ""),
+                                  + (f", B={B}" if scheme == "metropolis" else "")
+                                  + (f", + migration of D={args.migrate} float32 state rows" if args.migrate else ""),
                        "parallelism": f"particle-sharded x{world}: all_reduce(MAX) + all_gather(totals)"
                                       + (" + all_gather(weights)" if scheme == "metropolis" else "")
-                                      + (" + all_gather(spacing totals)" if flags else ""),
+                                      + (" + all_gather(spacing totals)" if flags else "")
+                                      + (" + all_gather(counts) + all_to_all(extra rows)" if args.migrate else ""),
                        "l2": "inputs larger than L2 (logw 128 MiB/GPU, Q 256 MiB/GPU)"},
             "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks,
         }))

@@ -296,7 +296,7 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
  *                                 ancestor of a particle of shard g was written by rank g)
  *                                 (Metropolis: histogram the rank's slots over the whole
  *                                 filter, then reduce_scatter(SUM) of the counts)
- *   4b pf_shard_migration_counts  d_counts = {E_g extras, F_g free slots}
+ *   4b pf_shard_migration_counts  d_counts = {E_g extras, F_g free slots} + the tile plan
  *      -> all_gather of the counts; exclusive prefixes give each rank's ranges of the
  *         global extras / free lists, hence the split sizes of one variable all-to-all
  *   4c pf_shard_migrate_pack      the shard's extra rows (+ their global indices), in order
@@ -309,31 +309,40 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
 /* offspring[Pw] (device) = #{k in the slot window : anc[k] - win0 = i} for i in [0, Pw).
  * anc[n_anc] (device) holds global ancestor indices; the slot window is
  * [d_slot_range[0], d_slot_range[1]) clamped to [0, n_anc) (d_slot_range: device, as
- * written by pf_shard_search / pf_shard_search_sorted), or all n_anc entries when
- * d_slot_range is NULL (the unsorted multinomial, whose shard writes scattered slots;
- * entries it did not write must lie outside [win0, win0 + Pw), e.g. -1).  Entries outside
+ * written by pf_shard_search for stratified / systematic or pf_shard_search_sorted; the
+ * entries in it must be NONDECREASING, as those searches write them: each run's length is
+ * stored without atomics), or all n_anc entries, in any order, when d_slot_range is NULL
+ * (the unsorted multinomial, whose shard writes scattered slots, entries it did not write
+ * lying outside [win0, win0 + Pw), e.g. -1; Metropolis slot histograms).  Entries outside
  * [win0, win0 + Pw) are ignored.  d_gmax / d_gbad (device, both or neither): when they
  * mark the global filter invalid (bad, or max = -inf), offspring = 1 everywhere (the
  * identity ancestors NS-1 gives; the searches then report an empty slot range). */
 pf_status pf_shard_offspring(const int32_t* anc, int64_t n_anc, const int64_t* d_slot_range, int64_t win0,
                              int32_t Pw, const float* d_gmax, const int32_t* d_gbad, int32_t* offspring,
                              pf_stream_t stream);
-/* d_counts[0] = E = sum_i max(o_i - 1, 0), d_counts[1] = F = #{i : o_i = 0} (device int64). */
-pf_status pf_shard_migration_counts(const int32_t* offspring, int32_t Pl, int64_t* d_counts, pf_stream_t stream);
+/* Bytes of the migration plan of a shard of Pl particles (16 per 2048-particle tile). */
+size_t pf_shard_migration_plan_bytes(int32_t Pl);
+/* d_counts[0] = E = sum_i max(o_i - 1, 0), d_counts[1] = F = #{i : o_i = 0} (device int64);
+ * plan (device, caller-owned, 8-byte aligned, >= pf_shard_migration_plan_bytes(Pl)) receives
+ * every tile's offsets into the shard's extras and free lists, read by 4c and 4d (the
+ * offspring must not change in between). */
+pf_status pf_shard_migration_counts(const int32_t* offspring, int32_t Pl, void* plan, int64_t* d_counts,
+                                    pf_stream_t stream);
 /* send_rows[E][row_bytes] (device, packed) = the shard's extra rows in NS-15 order: for
  * ascending i with o_i > 1, o_i - 1 copies of X[i]; send_src[E] (device int32, nullable) =
  * their global indices p0 + i.  X: [Pl] rows of row_bytes at stride ld_bytes; X and
  * send_rows may be NULL when row_bytes = 0 (indices only).  Must not overlap. */
 pf_status pf_shard_migrate_pack(const void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
-                                const int32_t* offspring, void* send_rows, int32_t* send_src, pf_stream_t stream);
+                                const int32_t* offspring, const void* plan, void* send_rows, int32_t* send_src,
+                                pf_stream_t stream);
 /* In place: the r-th free slot (o_i = 0, ascending i) of the shard <- recv_rows[r]
  * (packed rows, F of them, device); survivors are untouched.  perm_out[Pl] (device int32,
  * nullable unless row_bytes = 0) = p0 + i for survivors, recv_src[r] for the r-th free
  * slot.  recv_rows (when row_bytes > 0) and recv_src (when perm_out is given) must hold F
  * entries; they are not read, and may be NULL, when F = 0.  X may be NULL when row_bytes = 0. */
 pf_status pf_shard_migrate_unpack(void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
-                                  const int32_t* offspring, const void* recv_rows, const int32_t* recv_src,
-                                  int32_t* perm_out, pf_stream_t stream);
+                                  const int32_t* offspring, const void* plan, const void* recv_rows,
+                                  const int32_t* recv_src, int32_t* perm_out, pf_stream_t stream);
 
 /*
  * Bootstrap particle filter demo model (BASELINE config C4; P:43-68 steps 1-3;

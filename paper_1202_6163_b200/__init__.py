@@ -81,9 +81,10 @@ _SIGS = {
     "pf_shard_weights": ([_V, _I32, _V, _V, _V], ctypes.c_int),
     "pf_metropolis_from_weights": ([_V, _I64, _I64, _I32, _U64, _I32, _U32, _V, _V, _V, _V], ctypes.c_int),
     "pf_shard_offspring": ([_V, _I64, _V, _I64, _I32, _V, _V, _V, _V], ctypes.c_int),
-    "pf_shard_migration_counts": ([_V, _I32, _V, _V], ctypes.c_int),
-    "pf_shard_migrate_pack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V], ctypes.c_int),
-    "pf_shard_migrate_unpack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_migration_plan_bytes": ([_I32], _SZ),
+    "pf_shard_migration_counts": ([_V, _I32, _V, _V, _V], ctypes.c_int),
+    "pf_shard_migrate_pack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_migrate_unpack": ([_V, _I64, _I64, _I32, _I64, _V, _V, _V, _V, _V, _V], ctypes.c_int),
     "pf_lg_init": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, _U64, _V], ctypes.c_int),
     "pf_lg_propagate_weight": ([_V, _I64, _I32, _I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                 ctypes.c_float, _U64, _I32, _V, _V], ctypes.c_int),
@@ -506,13 +507,17 @@ def pf_shard_offspring(anc, win0: int, Pw: int, slot_range=None, gmax=None, gbad
 
 
 def pf_shard_migration_counts(offspring, stream=None):
-    """Stage 4b: int64[2] device tensor {E extras, F free slots} of the shard."""
+    """Stage 4b: (counts int64[2] device {E extras, F free slots}, plan) of the shard; the plan
+    (device bytes) feeds pf_shard_migrate_pack / _unpack of the same offspring."""
     torch = _torch()
     _need_cuda(offspring, torch.int32, "offspring")
+    Pl = offspring.shape[0]
     c = torch.empty(2, dtype=torch.int64, device=offspring.device)
-    _check(lib().pf_shard_migration_counts(offspring.data_ptr(), offspring.shape[0], c.data_ptr(),
+    plan = torch.empty(max(1, lib().pf_shard_migration_plan_bytes(Pl) // 8), dtype=torch.int64,
+                       device=offspring.device)
+    _check(lib().pf_shard_migration_counts(offspring.data_ptr(), Pl, plan.data_ptr(), c.data_ptr(),
                                            _stream(offspring, stream)), "pf_shard_migration_counts")
-    return c
+    return c, plan
 
 
 def _rows_view(X):
@@ -522,7 +527,7 @@ def _rows_view(X):
     return row, ld
 
 
-def pf_shard_migrate_pack(X, offspring, p0: int, E: int, stream=None):
+def pf_shard_migrate_pack(X, offspring, plan, p0: int, E: int, stream=None):
     """Stage 4c: (send_rows uint8 [E, row_bytes] or None, send_src int32 [E]) — the shard's
     extras in NS-15 order.  E = this shard's extras count (pf_shard_migration_counts)."""
     torch = _torch()
@@ -531,12 +536,13 @@ def pf_shard_migrate_pack(X, offspring, p0: int, E: int, stream=None):
     row, ld = _rows_view(X)
     src = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     rows = torch.empty((max(E, 1), row), dtype=torch.uint8, device=dev) if row else None
-    _check(lib().pf_shard_migrate_pack(_ptr(X), row, ld, offspring.shape[0], p0, offspring.data_ptr(), _ptr(rows),
-                                       src.data_ptr(), _stream(offspring, stream)), "pf_shard_migrate_pack")
+    _check(lib().pf_shard_migrate_pack(_ptr(X), row, ld, offspring.shape[0], p0, offspring.data_ptr(),
+                                       plan.data_ptr(), _ptr(rows), src.data_ptr(), _stream(offspring, stream)),
+           "pf_shard_migrate_pack")
     return (rows[:E] if rows is not None else None), src[:E]
 
 
-def pf_shard_migrate_unpack(X, offspring, p0: int, recv_rows, recv_src, perm_out=None, stream=None):
+def pf_shard_migrate_unpack(X, offspring, plan, p0: int, recv_rows, recv_src, perm_out=None, stream=None):
     """Stage 4d: free slots of X (in place) <- recv_rows; returns perm_out (int32 [Pl]) when
     recv_src is given: the global index of the particle each slot now holds."""
     torch = _torch()
@@ -549,7 +555,7 @@ def pf_shard_migrate_unpack(X, offspring, p0: int, recv_rows, recv_src, perm_out
     if row and recv_rows is not None and (recv_rows.dim() != 2 or recv_rows.shape[1] != row):
         raise PfError("recv_rows must be [F, row_bytes] uint8")
     _check(lib().pf_shard_migrate_unpack(_ptr(X), row, ld, offspring.shape[0], p0, offspring.data_ptr(),
-                                         _ptr(recv_rows), _ptr(recv_src), _ptr(perm_out),
+                                         plan.data_ptr(), _ptr(recv_rows), _ptr(recv_src), _ptr(perm_out),
                                          _stream(offspring, stream)), "pf_shard_migrate_unpack")
     return perm_out
 

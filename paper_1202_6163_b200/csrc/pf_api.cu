@@ -609,47 +609,41 @@ pf_status pf_shard_offspring(const int32_t* anc, int64_t n_anc, const int64_t* d
     return cuda_status(e);
 }
 
-pf_status pf_shard_migration_counts(const int32_t* offspring, int32_t Pl, int64_t* d_counts, pf_stream_t stream) {
-    if (!offspring || !d_counts || Pl < 1) return PF_ERR_INVALID_ARG;
-    const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    pf_status st = pool_get(pf::mig_scratch_bytes(Pl), s, &scratch);
-    if (st != PF_OK) return st;
+size_t pf_shard_migration_plan_bytes(int32_t Pl) { return Pl < 1 ? 0 : pf::mig_plan_bytes(Pl); }
+
+pf_status pf_shard_migration_counts(const int32_t* offspring, int32_t Pl, void* plan, int64_t* d_counts,
+                                    pf_stream_t stream) {
+    if (!offspring || !plan || !d_counts || Pl < 1 || (reinterpret_cast<uintptr_t>(plan) & 7) != 0)
+        return PF_ERR_INVALID_ARG;
     uint64_t nl = 0;
-    const cudaError_t e = pf::launch_mig_prefix(offspring, Pl, scratch, d_counts, s, &nl);
+    const cudaError_t e =
+        pf::launch_mig_plan(offspring, Pl, plan, d_counts, static_cast<cudaStream_t>(stream), &nl);
     g_launches += nl;
     return cuda_status(e);
 }
 
 pf_status pf_shard_migrate_pack(const void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
-                                const int32_t* offspring, void* send_rows, int32_t* send_src, pf_stream_t stream) {
-    if (!offspring || Pl < 1 || p0 < 0 || p0 + Pl > INT32_MAX || row_bytes < 0 ||
+                                const int32_t* offspring, const void* plan, void* send_rows, int32_t* send_src,
+                                pf_stream_t stream) {
+    if (!offspring || !plan || Pl < 1 || p0 < 0 || p0 + Pl > INT32_MAX || row_bytes < 0 ||
         (row_bytes > 0 && (!X || !send_rows || ld_bytes < row_bytes)) || (row_bytes == 0 && !send_src))
         return PF_ERR_INVALID_ARG;
-    const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    pf_status st = pool_get(pf::mig_scratch_bytes(Pl), s, &scratch);
-    if (st != PF_OK) return st;
     uint64_t nl = 0;
-    const cudaError_t e =
-        pf::launch_mig_pack(X, row_bytes, ld_bytes, Pl, p0, offspring, send_rows, send_src, scratch, s, &nl);
+    const cudaError_t e = pf::launch_mig_pack(X, row_bytes, ld_bytes, Pl, p0, offspring, plan, send_rows, send_src,
+                                              static_cast<cudaStream_t>(stream), &nl);
     g_launches += nl;
     return cuda_status(e);
 }
 
 pf_status pf_shard_migrate_unpack(void* X, int64_t row_bytes, int64_t ld_bytes, int32_t Pl, int64_t p0,
-                                  const int32_t* offspring, const void* recv_rows, const int32_t* recv_src,
-                                  int32_t* perm_out, pf_stream_t stream) {
-    if (!offspring || Pl < 1 || p0 < 0 || p0 + Pl > INT32_MAX || row_bytes < 0 ||
+                                  const int32_t* offspring, const void* plan, const void* recv_rows,
+                                  const int32_t* recv_src, int32_t* perm_out, pf_stream_t stream) {
+    if (!offspring || !plan || Pl < 1 || p0 < 0 || p0 + Pl > INT32_MAX || row_bytes < 0 ||
         (row_bytes > 0 && (!X || ld_bytes < row_bytes)) || (row_bytes == 0 && !perm_out))
         return PF_ERR_INVALID_ARG;
-    const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    pf_status st = pool_get(pf::mig_scratch_bytes(Pl), s, &scratch);
-    if (st != PF_OK) return st;
     uint64_t nl = 0;
-    const cudaError_t e = pf::launch_mig_unpack(X, row_bytes, ld_bytes, Pl, p0, offspring, recv_rows, recv_src,
-                                                perm_out, scratch, s, &nl);
+    const cudaError_t e = pf::launch_mig_unpack(X, row_bytes, ld_bytes, Pl, p0, offspring, plan, recv_rows, recv_src,
+                                                perm_out, static_cast<cudaStream_t>(stream), &nl);
     g_launches += nl;
     return cuda_status(e);
 }

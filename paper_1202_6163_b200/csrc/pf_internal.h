@@ -185,16 +185,16 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
                                cudaStream_t s, uint64_t* launches);
 
 // Cross-GPU particle migration of a sharded filter (pf_migrate.cu; include/pf.h 4a-4d).
-size_t mig_scratch_bytes(int32_t Pl);  // tile prefixes of pack / unpack / counts
+size_t mig_plan_bytes(int32_t Pl);  // the tiles' prefixes of extras / free slots
 cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_t* range, int64_t win0, int32_t Pw,
                                  const float* gmax, const int32_t* gbad, int32_t* o, cudaStream_t s,
                                  uint64_t* launches);
-cudaError_t launch_mig_prefix(const int32_t* o, int32_t Pl, void* scratch, int64_t* counts, cudaStream_t s,
-                              uint64_t* launches);
+cudaError_t launch_mig_plan(const int32_t* o, int32_t Pl, void* plan, int64_t* counts, cudaStream_t s,
+                            uint64_t* launches);
 cudaError_t launch_mig_pack(const void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
-                            void* send, int32_t* send_src, void* scratch, cudaStream_t s, uint64_t* launches);
+                            const void* plan, void* send, int32_t* send_src, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_mig_unpack(void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
-                              const void* recv, const int32_t* recv_src, int32_t* perm, void* scratch,
+                              const void* plan, const void* recv, const int32_t* recv_src, int32_t* perm,
                               cudaStream_t s, uint64_t* launches);
 
 }  // namespace pf

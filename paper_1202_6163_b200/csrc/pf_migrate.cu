@@ -51,34 +51,67 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* excl, int
     return total;
 }
 
-// 4a: histogram of the window's ancestors; warp-aggregated (sorted ancestors come in runs).
+// 4a: histogram of the window's ancestors; warp-aggregated atomics (unsorted ancestors).
 __global__ void __launch_bounds__(kThreads) k_mig_offspring(const int32_t* __restrict__ anc, int64_t n_anc,
-                                                            const int64_t* __restrict__ range, int64_t win0,
-                                                            int32_t Pw, const float* gmax, const int32_t* gbad,
-                                                            int32_t* __restrict__ o) {
+                                                            int64_t win0, int32_t Pw, const float* gmax,
+                                                            const int32_t* gbad, int32_t* __restrict__ o) {
     const bool invalid = gbad != nullptr && (*gbad != 0 || *gmax == -INFINITY);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
     if (invalid) {
         for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < Pw; i += stride) o[i] = 1;
         return;
     }
-    int64_t lo = 0, hi = n_anc;
-    if (range != nullptr) {
-        lo = max(range[0], static_cast<int64_t>(0));
-        hi = min(range[1], n_anc);
-    }
     const int lane = threadIdx.x & 31;
     // warp-uniform trip count so __match_any_sync sees the whole warp
-    for (int64_t base = lo + blockIdx.x * static_cast<int64_t>(kThreads) + (threadIdx.x & ~31); base < hi;
+    for (int64_t base = blockIdx.x * static_cast<int64_t>(kThreads) + (threadIdx.x & ~31); base < n_anc;
          base += stride) {
         const int64_t k = base + lane;
         int32_t v = -1;
-        if (k < hi) {
+        if (k < n_anc) {
             const int64_t a = static_cast<int64_t>(__ldg(anc + k)) - win0;
             if (a >= 0 && a < Pw) v = static_cast<int32_t>(a);
         }
         const unsigned peers = __match_any_sync(kFullMask, v);
         if (v >= 0 && lane == __ffs(peers) - 1) atomicAdd(o + v, static_cast<int32_t>(__popc(peers)));
+    }
+}
+
+// 4a with a slot range (stratified, systematic, sorted multinomial): the range's ancestors are
+// nondecreasing, so o_a is the length of a's run.  Per warp of 32 slots: run boundaries from
+// neighbour shuffles; a run that starts and ends inside the warp is stored by its first lane
+// (no atomics); a run crossing a warp boundary is summed from per-warp pieces with atomics.
+__global__ void __launch_bounds__(kThreads) k_mig_offspring_runs(const int32_t* __restrict__ anc, int64_t n_anc,
+                                                                 const int64_t* __restrict__ range, int64_t win0,
+                                                                 int32_t Pw, const float* gmax, const int32_t* gbad,
+                                                                 int32_t* __restrict__ o) {
+    const bool invalid = gbad != nullptr && (*gbad != 0 || *gmax == -INFINITY);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    if (invalid) {
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < Pw; i += stride) o[i] = 1;
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t lo = max(range[0], static_cast<int64_t>(0)), hi = min(range[1], n_anc);
+    for (int64_t base = lo + blockIdx.x * static_cast<int64_t>(kThreads) + (threadIdx.x & ~31); base < hi;
+         base += stride) {
+        const int64_t k = base + lane;
+        const bool in = k < hi;
+        const int32_t a = in ? __ldg(anc + k) : 0;
+        int32_t prev = __shfl_up_sync(kFullMask, a, 1), next = __shfl_down_sync(kFullMask, a, 1);
+        if (lane == 0 && in && k > lo) prev = __ldg(anc + k - 1);
+        if (lane == 31 && k + 1 < hi) next = __ldg(anc + k + 1);
+        const bool start = in && (k == lo || prev != a);
+        const bool end = in && (k == hi - 1 || next != a);
+        const unsigned ends = __ballot_sync(kFullMask, end);
+        const int64_t v = static_cast<int64_t>(a) - win0;
+        if (!in || v < 0 || v >= Pw) continue;
+        if (start) {
+            const unsigned m = ends >> lane;  // ends at this lane or later
+            if (m != 0) o[v] = __ffs(m);      // the whole run is inside the warp
+            else atomicAdd(o + v, 32 - lane);
+        } else if (lane == 0) {  // the warp's first run began in an earlier warp
+            atomicAdd(o + v, ends != 0 ? __ffs(ends) : 32);
+        }
     }
 }
 
@@ -106,64 +139,109 @@ __global__ void __launch_bounds__(kThreads) k_mig_tile_counts(const int32_t* __r
     }
 }
 
-// One CTA: exclusive scans of tE and tF in place; totals into counts[0..1].
+// One CTA: exclusive scans of tE and tF in place; totals into counts[0..1].  Thread t owns
+// kScanPer consecutive tiles of each round of 1024 * kScanPer (all loads issued at once).
+constexpr int kScanPer = 16;
 __global__ void __launch_bounds__(1024) k_mig_tile_scan(int64_t* __restrict__ tE, int64_t* __restrict__ tF,
                                                         int64_t ntiles, int64_t* __restrict__ counts) {
     __shared__ int64_t s_warp[2][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t per = mig_cdiv(ntiles, 1024);
-    const int64_t b = threadIdx.x * per, e = min(ntiles, b + per);
-    int64_t sE = 0, sF = 0;
-    for (int64_t t = b; t < e; ++t) {
-        sE += tE[t];
-        sF += tF[t];
-    }
-    int64_t iE = sE, iF = sF;
+    int64_t cE = 0, cF = 0;
+    for (int64_t r0 = 0; r0 < ntiles; r0 += 1024 * kScanPer) {
+        const int64_t b = r0 + static_cast<int64_t>(threadIdx.x) * kScanPer;
+        int64_t vE[kScanPer], vF[kScanPer];
+        int64_t sE = 0, sF = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int64_t a = __shfl_up_sync(kFullMask, iE, d), c = __shfl_up_sync(kFullMask, iF, d);
-        if (lane >= d) {
-            iE += a;
-            iF += c;
+        for (int u = 0; u < kScanPer; ++u) {
+            const bool in = b + u < ntiles;
+            vE[u] = in ? tE[b + u] : 0;
+            vF[u] = in ? tF[b + u] : 0;
+            sE += vE[u];
+            sF += vF[u];
         }
-    }
-    if (lane == 31) {
-        s_warp[0][warp] = iE;
-        s_warp[1][warp] = iF;
-    }
-    __syncthreads();
-    int64_t bE = 0, bF = 0, TE = 0, TF = 0;
-    for (int w = 0; w < 32; ++w) {
-        if (w < warp) {
-            bE += s_warp[0][w];
-            bF += s_warp[1][w];
+        int64_t iE = sE, iF = sF;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t a = __shfl_up_sync(kFullMask, iE, d), c = __shfl_up_sync(kFullMask, iF, d);
+            if (lane >= d) {
+                iE += a;
+                iF += c;
+            }
         }
-        TE += s_warp[0][w];
-        TF += s_warp[1][w];
-    }
-    int64_t rE = bE + iE - sE, rF = bF + iF - sF;
-    for (int64_t t = b; t < e; ++t) {
-        const int64_t ve = tE[t], vf = tF[t];
-        tE[t] = rE;
-        tF[t] = rF;
-        rE += ve;
-        rF += vf;
+        if (lane == 31) {
+            s_warp[0][warp] = iE;
+            s_warp[1][warp] = iF;
+        }
+        __syncthreads();
+        int64_t bE = 0, bF = 0, TE = 0, TF = 0;
+#pragma unroll 8
+        for (int w = 0; w < 32; ++w) {
+            const int64_t a = s_warp[0][w], c = s_warp[1][w];
+            if (w < warp) {
+                bE += a;
+                bF += c;
+            }
+            TE += a;
+            TF += c;
+        }
+        int64_t rE = cE + bE + iE - sE, rF = cF + bF + iF - sF;
+#pragma unroll
+        for (int u = 0; u < kScanPer; ++u) {
+            if (b + u < ntiles) {
+                tE[b + u] = rE;
+                tF[b + u] = rF;
+            }
+            rE += vE[u];
+            rF += vF[u];
+        }
+        cE += TE;
+        cF += TF;
+        __syncthreads();  // s_warp reused by the next round
     }
     if (threadIdx.x == 0 && counts != nullptr) {
-        counts[0] = TE;
-        counts[1] = TF;
+        counts[0] = cE;
+        counts[1] = cF;
     }
 }
 
-// 4c: the tile's extras in NS-15 order.  s_inc[q] = inclusive count of extras of the tile's
-// particles 0..q; extra j of the tile belongs to the first q with s_inc[q] > j.
+// Row copies of one tile: row j of the tile's list (j < n) goes from src_row(j) to dst_row(j).
+// When a row is cpr = 2^lg <= 32 chunks, each row is handled by a group of cpr lanes and each
+// thread keeps 4 rows' loads in flight; otherwise one chunk per thread and iteration.
+template <int CH, class Src, class Dst>
+__device__ __forceinline__ void copy_tile_rows(int64_t n, int64_t cpr, int lg, Src src_row, Dst dst_row) {
+    using T = typename MigChunk<CH>::T;
+    if (lg >= 0) {
+        const int c = threadIdx.x & ((1 << lg) - 1);
+        const int64_t step = kThreads >> lg;
+        int64_t j = threadIdx.x >> lg;
+        for (; j + 3 * step < n; j += 4 * step) {
+            T v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const T*>(src_row(j + u * step)) + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) reinterpret_cast<T*>(dst_row(j + u * step))[c] = v[u];
+        }
+        for (; j < n; j += step) reinterpret_cast<T*>(dst_row(j))[c] = __ldcs(reinterpret_cast<const T*>(src_row(j)) + c);
+        return;
+    }
+    for (int64_t g = threadIdx.x; g < n * cpr; g += kThreads) {
+        const int64_t j = g / cpr, c = g - j * cpr;
+        reinterpret_cast<T*>(dst_row(j))[c] = __ldcs(reinterpret_cast<const T*>(src_row(j)) + c);
+    }
+}
+
+// 4c: the tile's extras in NS-15 order.  s_inc[q] = inclusive count of the extras of the
+// tile's particles 0..q; extra j belongs to the first q with s_inc[q] > j, tabulated in s_map
+// when the tile has at most kMapCap extras (binary search otherwise).
+constexpr int kMapCap = 2 * kMigTile;
+
 template <int CH>
 __global__ void __launch_bounds__(kThreads) k_mig_pack(const char* __restrict__ X, int64_t ld, int64_t row_bytes,
-                                                       int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
+                                                       int lg, int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
                                                        const int64_t* __restrict__ tE, char* __restrict__ send,
                                                        int32_t* __restrict__ send_src) {
-    using T = typename MigChunk<CH>::T;
     __shared__ int32_t s_inc[kMigTile];
+    __shared__ int16_t s_map[kMapCap];
     __shared__ int64_t s_warp[kThreads / 32];
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMigTile;
     int32_t e[kMigItems];
@@ -177,43 +255,46 @@ __global__ void __launch_bounds__(kThreads) k_mig_pack(const char* __restrict__ 
     }
     int64_t ex;
     const int64_t Et = block_excl_scan(sum, &ex, s_warp);
+    if (Et == 0) return;
+    const bool mapped = Et <= kMapCap;
     int32_t run = static_cast<int32_t>(ex);
 #pragma unroll
     for (int j = 0; j < kMigItems; ++j) {
+        const int q = threadIdx.x * kMigItems + j;
+        if (mapped)
+            for (int c = 0; c < e[j]; ++c) s_map[run + c] = static_cast<int16_t>(q);
         run += e[j];
-        s_inc[threadIdx.x * kMigItems + j] = run;
+        s_inc[q] = run;
     }
     __syncthreads();
-    if (Et == 0) return;
     const int64_t base = tE[blockIdx.x];
-    const int64_t cpr = row_bytes / CH;
-    const int64_t items = cpr > 0 ? Et * cpr : Et;
-    for (int64_t g = threadIdx.x; g < items; g += kThreads) {
-        const int64_t j = cpr > 0 ? g / cpr : g;
-        const int64_t c = cpr > 0 ? g - j * cpr : 0;
-        int lo = 0, hi = kMigTile - 1;  // first q with s_inc[q] > j
+    auto owner = [&](int64_t j) -> int64_t {
+        if (mapped) return s_map[j];
+        int lo = 0, hi = kMigTile - 1;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (s_inc[mid] > j) hi = mid;
             else lo = mid + 1;
         }
-        const int64_t i = t0 + lo;
-        if (cpr > 0)
-            reinterpret_cast<T*>(send + (base + j) * row_bytes)[c] = __ldg(reinterpret_cast<const T*>(X + i * ld) + c);
-        if (c == 0 && send_src != nullptr) send_src[base + j] = static_cast<int32_t>(p0 + i);
-    }
+        return lo;
+    };
+    if (send_src != nullptr)
+        for (int64_t j = threadIdx.x; j < Et; j += kThreads) send_src[base + j] = static_cast<int32_t>(p0 + t0 + owner(j));
+    if (row_bytes == 0) return;
+    copy_tile_rows<CH>(Et, row_bytes / CH, lg, [&](int64_t j) { return X + (t0 + owner(j)) * ld; },
+                       [&](int64_t j) { return send + (base + j) * row_bytes; });
 }
 
 // 4d: the tile's free slots take rows tF[t] + r, r = their rank in the tile.
 template <int CH>
-__global__ void __launch_bounds__(kThreads) k_mig_unpack(char* __restrict__ X, int64_t ld, int64_t row_bytes,
+__global__ void __launch_bounds__(kThreads) k_mig_unpack(char* __restrict__ X, int64_t ld, int64_t row_bytes, int lg,
                                                          int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
                                                          const int64_t* __restrict__ tF,
                                                          const char* __restrict__ recv,
                                                          const int32_t* __restrict__ recv_src,
                                                          int32_t* __restrict__ perm) {
-    using T = typename MigChunk<CH>::T;
-    __shared__ int32_t s_free[kMigTile];
+    __shared__ int16_t s_free[kMigTile];
+    __shared__ int32_t s_perm[kMigTile];
     __shared__ int64_t s_warp[kThreads / 32];
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMigTile;
     const int64_t base = tF[blockIdx.x];
@@ -231,24 +312,15 @@ __global__ void __launch_bounds__(kThreads) k_mig_unpack(char* __restrict__ X, i
 #pragma unroll
     for (int j = 0; j < kMigItems; ++j) {
         const int q = threadIdx.x * kMigItems + j;
-        const int64_t i = t0 + q;
-        if (fr[j]) {
-            s_free[r] = q;
-            if (perm != nullptr) perm[i] = __ldg(recv_src + base + r);
-            ++r;
-        } else if (perm != nullptr && i < Pl) {
-            perm[i] = static_cast<int32_t>(p0 + i);
-        }
+        if (perm != nullptr) s_perm[q] = fr[j] ? __ldg(recv_src + base + r) : static_cast<int32_t>(p0 + t0 + q);
+        if (fr[j]) s_free[r++] = static_cast<int16_t>(q);
     }
     __syncthreads();
-    const int64_t cpr = row_bytes / CH;
-    if (cpr == 0) return;
-    const int64_t items = Ft * cpr;
-    for (int64_t g = threadIdx.x; g < items; g += kThreads) {
-        const int64_t j = g / cpr, c = g - j * cpr;
-        const int64_t i = t0 + s_free[j];
-        reinterpret_cast<T*>(X + i * ld)[c] = __ldg(reinterpret_cast<const T*>(recv + (base + j) * row_bytes) + c);
-    }
+    if (perm != nullptr)
+        for (int q = threadIdx.x; q < kMigTile && t0 + q < Pl; q += kThreads) perm[t0 + q] = s_perm[q];
+    if (row_bytes == 0 || Ft == 0) return;
+    copy_tile_rows<CH>(Ft, row_bytes / CH, lg, [&](int64_t j) { return recv + (base + j) * row_bytes; },
+                       [&](int64_t j) { return X + (t0 + s_free[j]) * ld; });
 }
 
 int mig_chunk(const void* a, const void* b, int64_t row_bytes, int64_t ld) {
@@ -258,9 +330,16 @@ int mig_chunk(const void* a, const void* b, int64_t row_bytes, int64_t ld) {
     return 1;
 }
 
+// log2 of the chunks per row when that is a power of two <= 32, else -1
+int mig_lg(int64_t cpr) {
+    for (int lg = 0; lg <= 5; ++lg)
+        if (cpr == (int64_t{1} << lg)) return lg;
+    return -1;
+}
+
 }  // namespace
 
-size_t mig_scratch_bytes(int32_t Pl) { return 2 * sizeof(int64_t) * static_cast<size_t>(mig_cdiv(Pl, kMigTile)) + 256; }
+size_t mig_plan_bytes(int32_t Pl) { return 2 * sizeof(int64_t) * static_cast<size_t>(mig_cdiv(Pl, kMigTile)); }
 
 cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_t* range, int64_t win0, int32_t Pw,
                                  const float* gmax, const int32_t* gbad, int32_t* o, cudaStream_t s,
@@ -271,16 +350,17 @@ cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(mig_cdiv(work, kThreads), static_cast<int64_t>(sm_count()) * 8)));
     ProfScope ps_("k_mig_offspring", s);
-    k_mig_offspring<<<grid, kThreads, 0, s>>>(anc, n_anc, range, win0, Pw, gmax, gbad, o);
+    if (range != nullptr) k_mig_offspring_runs<<<grid, kThreads, 0, s>>>(anc, n_anc, range, win0, Pw, gmax, gbad, o);
+    else k_mig_offspring<<<grid, kThreads, 0, s>>>(anc, n_anc, win0, Pw, gmax, gbad, o);
     ++*launches;
     return cudaPeekAtLastError();
 }
 
-// tile prefixes in scratch (tE = scratch, tF = scratch + ntiles); counts nullable
-cudaError_t launch_mig_prefix(const int32_t* o, int32_t Pl, void* scratch, int64_t* counts, cudaStream_t s,
-                              uint64_t* launches) {
+// the plan = the tiles' exclusive prefixes (tE = plan, tF = plan + ntiles); counts nullable
+cudaError_t launch_mig_plan(const int32_t* o, int32_t Pl, void* plan, int64_t* counts, cudaStream_t s,
+                            uint64_t* launches) {
     const int64_t nt = mig_cdiv(Pl, kMigTile);
-    int64_t* tE = static_cast<int64_t*>(scratch);
+    int64_t* tE = static_cast<int64_t*>(plan);
     int64_t* tF = tE + nt;
     {
         ProfScope ps_("k_mig_tile_counts", s);
@@ -295,36 +375,34 @@ cudaError_t launch_mig_prefix(const int32_t* o, int32_t Pl, void* scratch, int64
 }
 
 cudaError_t launch_mig_pack(const void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
-                            void* send, int32_t* send_src, void* scratch, cudaStream_t s, uint64_t* launches) {
-    cudaError_t e = launch_mig_prefix(o, Pl, scratch, nullptr, s, launches);
-    if (e != cudaSuccess) return e;
-    const int64_t* tE = static_cast<const int64_t*>(scratch);
+                            const void* plan, void* send, int32_t* send_src, cudaStream_t s, uint64_t* launches) {
+    const int64_t* tE = static_cast<const int64_t*>(plan);
     const char* x = static_cast<const char*>(X);
     char* y = static_cast<char*>(send);
     const int ch = row_bytes > 0 ? mig_chunk(x, y, row_bytes, std::max<int64_t>(ld, row_bytes)) : 16;
+    const int lg = row_bytes > 0 ? mig_lg(row_bytes / ch) : 0;
     const unsigned grid = static_cast<unsigned>(mig_cdiv(Pl, kMigTile));
     ProfScope ps_("k_mig_pack", s);
-    if (ch == 16) k_mig_pack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
-    else if (ch == 4) k_mig_pack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
-    else k_mig_pack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tE, y, send_src);
+    if (ch == 16) k_mig_pack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
+    else if (ch == 4) k_mig_pack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
+    else k_mig_pack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
     ++*launches;
     return cudaPeekAtLastError();
 }
 
 cudaError_t launch_mig_unpack(void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
-                              const void* recv, const int32_t* recv_src, int32_t* perm, void* scratch,
+                              const void* plan, const void* recv, const int32_t* recv_src, int32_t* perm,
                               cudaStream_t s, uint64_t* launches) {
-    cudaError_t e = launch_mig_prefix(o, Pl, scratch, nullptr, s, launches);
-    if (e != cudaSuccess) return e;
-    const int64_t* tF = static_cast<const int64_t*>(scratch) + mig_cdiv(Pl, kMigTile);
+    const int64_t* tF = static_cast<const int64_t*>(plan) + mig_cdiv(Pl, kMigTile);
     char* x = static_cast<char*>(X);
     const char* y = static_cast<const char*>(recv);
     const int ch = row_bytes > 0 ? mig_chunk(x, y, row_bytes, std::max<int64_t>(ld, row_bytes)) : 16;
+    const int lg = row_bytes > 0 ? mig_lg(row_bytes / ch) : 0;
     const unsigned grid = static_cast<unsigned>(mig_cdiv(Pl, kMigTile));
     ProfScope ps_("k_mig_unpack", s);
-    if (ch == 16) k_mig_unpack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
-    else if (ch == 4) k_mig_unpack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
-    else k_mig_unpack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, Pl, p0, o, tF, y, recv_src, perm);
+    if (ch == 16) k_mig_unpack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tF, y, recv_src, perm);
+    else if (ch == 4) k_mig_unpack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tF, y, recv_src, perm);
+    else k_mig_unpack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tF, y, recv_src, perm);
     ++*launches;
     return cudaPeekAtLastError();
 }

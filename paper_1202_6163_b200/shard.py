@@ -145,11 +145,11 @@ class GpuStages:
     def migration_counts(self, o):
         return self.pf.pf_shard_migration_counts(o)
 
-    def pack(self, X, o, p0, E):
-        return self.pf.pf_shard_migrate_pack(X, o, p0, E)
+    def pack(self, X, o, plan, p0, E):
+        return self.pf.pf_shard_migrate_pack(X, o, plan, p0, E)
 
-    def unpack(self, X, o, p0, rows, src):
-        return self.pf.pf_shard_migrate_unpack(X, o, p0, rows, src)
+    def unpack(self, X, o, plan, p0, rows, src):
+        return self.pf.pf_shard_migrate_unpack(X, o, plan, p0, rows, src)
 
 
 def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, filter_index: int = 0,
@@ -257,12 +257,13 @@ def migrate_sharded(X_local, anc, info, comm=None, stages=None):
         per = -(-P_global // comm.world)
         h = stages.offspring(anc, 0, per * comm.world, None, None, None)
         o = comm.reduce_scatter_sum(h)[:Pl].contiguous()
-    counts = comm.all_gather_cat(stages.migration_counts(o)).cpu().view(-1, 2).tolist()
+    cnt, plan = stages.migration_counts(o)
+    counts = comm.all_gather_cat(cnt).cpu().view(-1, 2).tolist()
     send, recv = migration_splits(counts, comm.rank)
-    rows, src = stages.pack(X_local, o, p0, int(counts[comm.rank][0]))
+    rows, src = stages.pack(X_local, o, plan, p0, int(counts[comm.rank][0]))
     rsrc = comm.all_to_all_v(src, send, recv)
     rrows = comm.all_to_all_v(rows, send, recv) if rows is not None else None
-    return stages.unpack(X_local, o, p0, rrows, rsrc)
+    return stages.unpack(X_local, o, plan, p0, rrows, rsrc)
 
 
 def migrate_sharded_local(X_full, anc_full, nshards: int, stages=None):
@@ -276,8 +277,9 @@ def migrate_sharded_local(X_full, anc_full, nshards: int, stages=None):
     parts = [shard_range(P, nshards, g) for g in range(nshards)]
     Xs = [X_full[p0:p0 + Pl] if X_full is not None else None for p0, Pl in parts]
     os_ = [stages.offspring(anc_full, p0, Pl, None, None, None) for p0, Pl in parts]
-    counts = [[int(v) for v in stages.migration_counts(o).cpu().tolist()] for o in os_]
-    packed = [stages.pack(x, o, p0, counts[g][0]) for g, (x, o, (p0, _)) in enumerate(zip(Xs, os_, parts))]
+    cp = [stages.migration_counts(o) for o in os_]
+    counts = [[int(v) for v in c.cpu().tolist()] for c, _ in cp]
+    packed = [stages.pack(x, o, cp[g][1], p0, counts[g][0]) for g, (x, o, (p0, _)) in enumerate(zip(Xs, os_, parts))]
     splits = [migration_splits(counts, g) for g in range(nshards)]
     perms = []
     for g, (p0, Pl) in enumerate(parts):
@@ -290,7 +292,7 @@ def migrate_sharded_local(X_full, anc_full, nshards: int, stages=None):
                 rows.append(packed[h][0][a:a + n])
         rsrc = torch.cat(srcs)
         rrows = torch.cat(rows) if rows else None
-        perms.append(stages.unpack(Xs[g], os_[g], p0, rrows, rsrc))
+        perms.append(stages.unpack(Xs[g], os_[g], cp[g][1], p0, rrows, rsrc))
     return torch.cat(perms)
 
 

@@ -99,9 +99,9 @@ class CpuOracleStages:
 
     def migration_counts(self, o):
         v = o.numpy()
-        return torch.tensor([int(np.maximum(v - 1, 0).sum()), int((v == 0).sum())], dtype=torch.int64)
+        return torch.tensor([int(np.maximum(v - 1, 0).sum()), int((v == 0).sum())], dtype=torch.int64), None
 
-    def pack(self, X, o, p0, E):
+    def pack(self, X, o, plan, p0, E):
         v = o.numpy()
         idx = np.repeat(np.arange(len(v)), np.maximum(v - 1, 0))
         assert len(idx) == E
@@ -109,7 +109,7 @@ class CpuOracleStages:
         rows = None if X is None else X[torch.from_numpy(idx)].contiguous().view(torch.uint8).reshape(E, rb)
         return rows, torch.from_numpy((p0 + idx).astype(np.int32))
 
-    def unpack(self, X, o, p0, rows, src):
+    def unpack(self, X, o, plan, p0, rows, src):
         v = o.numpy()
         free = np.flatnonzero(v == 0)
         perm = (p0 + np.arange(len(v))).astype(np.int32)

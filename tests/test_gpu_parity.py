@@ -843,10 +843,14 @@ def test_particle_migration_layouts(pf, dev, orc):
     L = pf.lib()
     assert L.pf_shard_offspring(a.data_ptr(), P, None, 0, 0, None, None, o.data_ptr(), None) == 1
     assert L.pf_shard_offspring(a.data_ptr(), P, None, 0, P, None, a.data_ptr(), o.data_ptr(), None) == 1
-    assert L.pf_shard_migration_counts(o.data_ptr(), 0, o.data_ptr(), None) == 1
-    assert L.pf_shard_migrate_pack(None, 64, 64, P, 0, o.data_ptr(), None, None, None) == 1
-    assert L.pf_shard_migrate_unpack(None, 0, 0, P, 0, o.data_ptr(), None, a.data_ptr(), None, None) == 1
-    assert L.pf_shard_migrate_unpack(None, 64, 64, P, 0, o.data_ptr(), None, None, None, None) == 1
+    plan = torch.empty(L.pf_shard_migration_plan_bytes(P) // 8, dtype=torch.int64, device=dev)
+    assert L.pf_shard_migration_counts(o.data_ptr(), 0, plan.data_ptr(), o.data_ptr(), None) == 1
+    assert L.pf_shard_migration_counts(o.data_ptr(), P, None, o.data_ptr(), None) == 1
+    assert L.pf_shard_migrate_pack(None, 64, 64, P, 0, o.data_ptr(), plan.data_ptr(), None, None, None) == 1
+    assert L.pf_shard_migrate_pack(None, 0, 0, P, 0, o.data_ptr(), None, None, a.data_ptr(), None) == 1
+    assert L.pf_shard_migrate_unpack(None, 0, 0, P, 0, o.data_ptr(), plan.data_ptr(), None, a.data_ptr(), None,
+                                     None) == 1
+    assert L.pf_shard_migrate_unpack(None, 64, 64, P, 0, o.data_ptr(), plan.data_ptr(), None, None, None, None) == 1
 
 
 def test_sorted_multinomial_a6(pf, dev, orc):
