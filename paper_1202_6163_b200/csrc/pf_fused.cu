@@ -224,6 +224,9 @@ __device__ __forceinline__ void cluster_sync_publish(bool publisher) {
 #define PF_COPY_U 4
 #endif
 constexpr int kCopyU = PF_COPY_U;
+#ifndef PF_PREFETCH_NEXT
+#define PF_PREFETCH_NEXT 1
+#endif
 template <class Args>
 __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32_t* owner, const int32_t* slot,
                                                int npairs, int lane) {
@@ -373,6 +376,15 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             continue;
         }
         const float lm = s_lmax;
+#if PF_PREFETCH_NEXT
+        // the next filter's log-weights of this CTA into L2 (one bulk prefetch), so its phase A
+        // loads come from L2 instead of HBM
+        if (tid == 0 && n + num_clusters < a.N && a.vec && (np & 3) == 0 && np > 0) {
+            const float* nrow = a.logw + static_cast<int64_t>(n + num_clusters) * a.ld + p0;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nrow), "r"(static_cast<uint32_t>(np) * 4u)
+                         : "memory");
+        }
+#endif
 
         // ---------------- B: weights, quantise, block scan, cluster offsets
         double sw = 0.0, sw2 = 0.0;
