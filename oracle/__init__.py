@@ -78,6 +78,8 @@ def lib():
         L.pfo_spacing.restype = u64
         L.pfo_spacings.argtypes = [i32, u64, u32, P]
         L.pfo_resample_sorted_multinomial.argtypes = [P, i32, u64, u32, P]
+        L.pfo_shift_f64.argtypes = [P, i32, P, P]
+        L.pfo_resample_f64.argtypes = [ctypes.c_int, ctypes.c_int, P, i32, u64, i32, u32, P, P, P, P]
         L.pfo_metropolis_required_B.argtypes = [i64, f64, f64]
         L.pfo_metropolis_required_B.restype = i32
         _lib = L
@@ -194,6 +196,31 @@ def resample_batched(scheme, logw: np.ndarray, seed: int, B: int = 0, first_filt
     a = np.zeros((N, P), dtype=np.int32)
     st = np.zeros(N, dtype=np.int32)
     lib().pfo_resample_batched(_scheme(scheme), _p(logw), P, N, P, seed, first_filter, B, _p(a), P, _p(st))
+    return st, a
+
+
+def shift_f64(logw: np.ndarray):
+    """NS-3d (R-21): (status, t float32[P], lmax float64) of binary64 log-weights."""
+    logw = np.ascontiguousarray(logw, dtype=np.float64)
+    t = np.zeros(len(logw), dtype=np.float32)
+    lm = ctypes.c_double()
+    st = lib().pfo_shift_f64(_p(logw), len(logw), _p(t), ctypes.byref(lm))
+    return st, t, lm.value
+
+
+def resample_f64(scheme, logw: np.ndarray, seed: int, B: int = 0, filter_index: int = 0, side: bool = False,
+                 sorted: bool = False):
+    """binary64 log-weights (NS-3d): returns (status, ancestors[, lse, normw, ess])."""
+    logw = np.ascontiguousarray(logw, dtype=np.float64)
+    P = len(logw)
+    a = np.zeros(P, dtype=np.int32)
+    lse, ess = ctypes.c_double(), ctypes.c_double()
+    v = np.zeros(P, dtype=np.float32)
+    st = lib().pfo_resample_f64(_scheme(scheme), int(sorted), _p(logw), P, seed, B, filter_index, _p(a),
+                                ctypes.byref(lse) if side else None, _p(v) if side else None,
+                                ctypes.byref(ess) if side else None)
+    if side:
+        return st, a, lse.value, v, ess.value
     return st, a
 
 

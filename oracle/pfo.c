@@ -15,6 +15,7 @@
  */
 #include "pfo.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -431,6 +432,56 @@ int pfo_resample_sorted_multinomial(const float* logw, int32_t P, uint64_t seed,
     free(G);
     free(Q);
     return PFO_FILTER_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NS-3d  binary64 log-weights (the paper computes in double;        */
+/* reading R-21).  NS-1 validation and the NS-2 max on the doubles; then    */
+/* t_i = the binary64 difference logw_i - lmax rounded ONCE to binary32      */
+/* (nearest; below -FLT_MAX it is -inf, and any t < -88 weighs 0 by NS-4),  */
+/* and the float32 path NS-3..NS-12 runs on t, whose maximum is exactly 0.  */
+/* lse = lmax + ln S (NS-13 with the double maximum).                       */
+/* ------------------------------------------------------------------------ */
+int pfo_shift_f64(const double* logw, int32_t P, float* t, double* lmax)
+{
+    double m = -INFINITY;
+    int bad = 0;
+    for (int32_t i = 0; i < P; ++i) {
+        double v = logw[i];
+        if (isnan(v) || (isinf(v) && v > 0)) bad = 1;
+        else if (v > m) m = v;
+    }
+    *lmax = m;
+    if (bad || m == -INFINITY) {
+        for (int32_t i = 0; i < P; ++i) t[i] = NAN; /* invalid for the float path too (NS-1) */
+        return PFO_FILTER_INVALID_WEIGHTS;
+    }
+    for (int32_t i = 0; i < P; ++i) {
+        double d = logw[i] - m; /* one binary64 subtraction, RN */
+        t[i] = (d < -FLT_MAX) ? -INFINITY : (float)d;
+    }
+    return PFO_FILTER_OK;
+}
+
+int pfo_resample_f64(int scheme, int sorted, const double* logw, int32_t P, uint64_t seed, int32_t B,
+                     uint32_t filter_index, int32_t* anc, double* lse, float* normw, double* ess)
+{
+    float* t = (float*)malloc(sizeof(float) * (size_t)P);
+    double lm;
+    int st = pfo_shift_f64(logw, P, t, &lm);
+    if (sorted) {
+        pfo_resample_sorted_multinomial(t, P, seed, filter_index, anc);
+        if (lse || normw || ess) { /* side outputs do not depend on the positions */
+            int32_t* scratch = (int32_t*)malloc(sizeof(int32_t) * (size_t)P);
+            pfo_resample(PFO_SYSTEMATIC, t, P, seed, 0, filter_index, scratch, lse, normw, ess);
+            free(scratch);
+        }
+    } else {
+        pfo_resample(scheme, t, P, seed, B, filter_index, anc, lse, normw, ess);
+    }
+    if (lse && st == PFO_FILTER_OK) *lse = lm + *lse; /* the float path's lse is 0 + ln S */
+    free(t);
+    return st;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -78,6 +78,13 @@ void pfo_spacings(int32_t P, uint64_t seed, uint32_t filter_index, uint64_t* G);
 int pfo_resample_sorted_multinomial(const float* logw, int32_t P, uint64_t seed, uint32_t filter_index,
                                     int32_t* anc);
 
+/* NS-3d (reading R-21): binary64 log-weights.  t[P] = fl32(logw_i - lmax) with
+ * the binary64 max (NaN everywhere when invalid); returns PFO_FILTER_*. */
+int pfo_shift_f64(const double* logw, int32_t P, float* t, double* lmax);
+/* The float32 path on t; lse = lmax + ln S.  sorted != 0: the a6 multinomial. */
+int pfo_resample_f64(int scheme, int sorted, const double* logw, int32_t P, uint64_t seed, int32_t B,
+                     uint32_t filter_index, int32_t* anc, double* lse, float* normw, double* ess);
+
 /* NS-14 / SPEC S:60-77 conversions. */
 void pfo_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* o);
 void pfo_offspring_to_ancestors(const int32_t* o, int32_t P, int32_t* anc);

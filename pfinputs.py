@@ -105,3 +105,21 @@ def lg_observations(T: int, phi: float = 0.9, sigma_x: float = 1.0, sigma_y: flo
         x = phi * x + sigma_x * rng.standard_normal(D)
         ys[t] = x[0] + sigma_y * rng.standard_normal()
     return ys
+
+
+def gaussian_logw_f64(P: int, var: float = 1.0, offset: float = 0.0, seed: int = BASE_SEED,
+                      N: int | None = None) -> np.ndarray:
+    """binary64 logw = offset + sqrt(var) * z, z ~ N(0,1) in float64: log-weights that carry a
+    large common offset (e.g. an accumulated log-likelihood, offset ~ -1e7), the case the
+    double-precision entry points (NS-3d, R-21) exist for."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shape = (P,) if N is None else (N, P)
+    return offset + np.sqrt(var) * rng.standard_normal(size=shape)
+
+
+def grid_logw(P: int, var: float = 1.0, seed: int = BASE_SEED, N: int | None = None) -> np.ndarray:
+    """float32 Gaussian log-weights rounded to multiples of 2^-12 (|x| < 2^11): adding a
+    power-of-two offset up to 2^40 to them is exact in binary64 and their differences are
+    exact in binary32 (the exact-shift pins of NS-3d)."""
+    x = gaussian_logw(P, var, seed, N).astype(np.float64)
+    return (np.clip(np.round(x * 4096.0), -(2 ** 22) + 1, 2 ** 22 - 1) / 4096.0).astype(np.float32)

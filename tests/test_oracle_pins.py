@@ -671,3 +671,65 @@ def test_kalman_oracle_against_joint_gaussian():
         C = s0 * phi ** np.abs(idx[:, None] - idx[None, :]) + sy * sy * np.eye(T)
         want = multivariate_normal(mean=np.zeros(T), cov=C).logpdf(ys)
         assert abs(ll - want) < 1e-9 * max(1.0, abs(want)), (ll, want)
+
+
+# --------------------------------------------------------------------------- NS-3d (R-21)
+@pytest.mark.parametrize("c", [0.0, 2.0 ** 30, -(2.0 ** 40)])
+def test_f64_exact_shift_reduces_to_f32(orc, c):
+    """NS-3d: resampling depends on the log-weights only through logw_i - max, so
+    binary64 inputs x + c with an EXACT shift c give the float32 path's ancestors on x, and
+    lse(x + c) = lse(x) + c.  Catches rounding logw or lmax to float before subtracting
+    (x + 2^30 in float32 keeps only multiples of 64), a float max, and a dropped lmax in lse."""
+    for P, seed in [(1, 1), (16, 2), (1000, 3), (4097, 4)]:
+        x = pfinputs.grid_logw(P, 4.0, seed=seed)
+        x64 = x.astype(np.float64) + c
+        assert np.all(x64 - c == x.astype(np.float64))  # the shift is exact
+        for s in ("multinomial", "stratified", "systematic", "metropolis"):
+            st, a, lse, v, ess = orc.resample_f64(s, x64, seed=seed, B=9, side=True)
+            st2, a2, lse2, v2, ess2 = orc.resample(s, x, seed=seed, B=9, side=True)
+            assert st == st2 == 0
+            assert np.array_equal(a, a2), s
+            assert np.array_equal(v, v2) and ess == ess2
+            assert abs(lse - (lse2 + c)) <= 1e-12 * max(1.0, abs(c))
+        st, a = orc.resample_f64("multinomial", x64, seed=seed, sorted=True)
+        assert np.array_equal(a, orc.resample_sorted_multinomial(x, seed)[1])
+
+
+def test_f64_large_offset_against_logsumexp(orc):
+    """NS-3d / NS-13 at an inexact offset (-1e7, where float32 log-weights would keep only
+    multiples of 1): lse - offset against the fp64 log-sum-exp, normalised weights against
+    exp(logw - lse) (numpy fp64), and a float32 path that ignores the offset would fail it."""
+    for P, var in [(16, 1.0), (1000, 10.0), (3000, 0.1)]:
+        x = pfinputs.gaussian_logw_f64(P, var, offset=-1e7, seed=P)
+        st, a, lse, v, ess = orc.resample_f64("stratified", x, seed=5, side=True)
+        assert st == 0
+        m = float(np.max(x))
+        want = m + math.log(float(np.sum(np.exp(x - m))))
+        assert abs((lse + 1e7) - (want + 1e7)) <= 1e-5
+        vv = np.exp(x - want)
+        assert np.all(np.abs(v - vv) <= 2e-6 * vv + 1e-12)
+        ess_exact = 1.0 / float(np.sum(vv * vv))
+        assert abs(ess - ess_exact) <= 1e-5 * ess_exact
+        # the offspring track P * v within one (stratified, P:98-100)
+        o = orc.ancestors_to_offspring(a)
+        assert np.all(np.abs(o - P * vv) < 2.0 + 1e-9)
+
+
+def test_f64_invalid_and_zero_weights(orc):
+    """NS-1 on the doubles: NaN, +inf, all -inf -> status 1, identity, NaN lse.  Entries more
+    than 88 below the maximum (down to -1e300, beyond float range) weigh zero (NS-4 step 1)
+    and are never selected; a lone finite entry takes every slot."""
+    bad = [np.array([0.0, np.nan, 1.0]), np.array([0.0, np.inf]), np.full(4, -np.inf)]
+    for x in bad:
+        for s in ("multinomial", "stratified", "systematic", "metropolis"):
+            st, a, lse, v, ess = orc.resample_f64(s, x, seed=3, B=4, side=True)
+            assert st == 1 and list(a) == list(range(len(x))) and math.isnan(lse)
+    x = np.array([-1e300, 5.0e8, 5.0e8 - 100.0, -np.inf, 5.0e8 - 1.0, 5.0e8 - 3e38])
+    for s in ("multinomial", "stratified", "systematic", "metropolis"):
+        st, a = orc.resample_f64(s, x, seed=7, B=200)
+        assert st == 0 and set(a.tolist()) <= {1, 4}
+    x = np.array([-np.inf, -1e300, 12345.678, -np.inf])
+    for s in ("multinomial", "stratified", "systematic", "metropolis"):
+        st, a, lse, v, ess = orc.resample_f64(s, x, seed=8, B=200, side=True)  # (3/4)^200 to stay at a zero weight
+        assert st == 0 and list(a) == [2, 2, 2, 2]
+        assert lse == 12345.678 and list(v) == [0.0, 0.0, 1.0, 0.0] and ess == 1.0
