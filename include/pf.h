@@ -151,6 +151,24 @@ pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_lo
                               uint64_t seed, uint32_t first_filter, int32_t B,
                               int32_t* ancestors, int64_t ld_anc, const pf_opts* opts, pf_stream_t stream);
 
+/*
+ * Binary64 log-weights (the paper's precision; NS-3d / R-21).  Same
+ * arguments, outputs and error behaviour as pf_resample_ex / pf_resample_batched, with logw
+ * double [N][ld_logw] (device).  The filter's maximum is taken in binary64 (NaN, +inf or
+ * all -inf -> invalid, NS-1), t_i = logw_i - lmax is computed in binary64 and rounded once
+ * to binary32, and the float32 path runs on t (every option, flag and kernel applies); lse
+ * = lmax + ln sum_i w_i keeps the binary64 maximum.  Use it when the log-weights carry a
+ * large common offset (an accumulated log-likelihood) that float32 would round away.  The
+ * shifted weights (4 B per particle + 12 B per filter) always come from the library pool
+ * (pf_opts.workspace, when given, serves the float path only).  Two extra launches (max,
+ * shift) before the float path, one after it when lse_out is set.
+ */
+pf_status pf_resample_ex_f64(pf_scheme scheme, const double* logw, int32_t P, uint64_t seed, int32_t B,
+                             int32_t* ancestors, const pf_opts* opts, pf_stream_t stream);
+pf_status pf_resample_batched_f64(pf_scheme scheme, const double* logw, int64_t ld_logw, int32_t N, int32_t P,
+                                  uint64_t seed, uint32_t first_filter, int32_t B,
+                                  int32_t* ancestors, int64_t ld_anc, const pf_opts* opts, pf_stream_t stream);
+
 /* Workspace bytes a call with these sizes needs (for explicit workspaces, pf_opts.workspace):
  * the maximum over every path the call may take.  _ex takes the pf_opts.flags (PF_SORTED needs
  * the spacings scan) and the ancestors' row stride; pf_workspace_bytes(s, N, P) =

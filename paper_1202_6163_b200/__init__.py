@@ -59,6 +59,9 @@ _SIGS = {
     "pf_resample_metropolis": ([_V, _I32, _U64, _I32, _V, _V], ctypes.c_int),
     "pf_resample_ex": ([ctypes.c_int, _V, _I32, _U64, _I32, _V, _V, _V], ctypes.c_int),
     "pf_resample_batched": ([ctypes.c_int, _V, _I64, _I32, _I32, _U64, _U32, _I32, _V, _I64, _V, _V], ctypes.c_int),
+    "pf_resample_ex_f64": ([ctypes.c_int, _V, _I32, _U64, _I32, _V, _V, _V], ctypes.c_int),
+    "pf_resample_batched_f64": ([ctypes.c_int, _V, _I64, _I32, _I32, _U64, _U32, _I32, _V, _I64, _V, _V],
+                                ctypes.c_int),
     "pf_workspace_bytes": ([ctypes.c_int, _I32, _I32], _SZ),
     "pf_workspace_bytes_ex": ([ctypes.c_int, _I32, _I32, _U32, _I64], _SZ),
     "pf_ancestors_to_offspring": ([_V, _I32, _V, _V], ctypes.c_int),
@@ -205,11 +208,13 @@ def _set_state(opts, state, batched: bool):
 def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_index: int = 0,
                    lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
                    permuted_out=None, flags: int = 0, state=None, workspace=None, stream=None):
-    """One filter.  logw: float32 [P] CUDA.  Returns the int32 ancestors tensor.
+    """One filter.  logw: float32 [P] CUDA, or float64 (pf_resample_ex_f64, NS-3d).
+    Returns the int32 ancestors tensor.
     workspace: optional device tensor (256-byte aligned, >= pf_workspace_bytes) instead of the pool.
     state: optional [P, ...] tensor gathered in place with the canonical permutation (NS-15/16)."""
     torch = _torch()
-    _need_cuda(logw, torch.float32, "logw")
+    f64 = isinstance(logw, torch.Tensor) and logw.dtype == torch.float64
+    _need_cuda(logw, torch.float64 if f64 else torch.float32, "logw")
     if logw.dim() != 1 or logw.stride(0) != 1:
         raise PfError("logw must be a contiguous 1-D tensor")
     P = logw.shape[0]
@@ -231,9 +236,10 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
         _need_cuda(permuted_out, torch.int32, "permuted_out"); opts.permuted_out = permuted_out.data_ptr()
     _set_state(opts, state, False)
     _set_workspace(opts, workspace)
-    rc = lib().pf_resample_ex(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
-                              ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
-    _check(rc, "pf_resample_ex")
+    fn = "pf_resample_ex_f64" if f64 else "pf_resample_ex"
+    rc = getattr(lib(), fn)(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
+                            ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
+    _check(rc, fn)
     return ancestors
 
 
@@ -266,11 +272,13 @@ pf_resample_metropolis = _single("pf_resample_metropolis", "Metropolis, Fig. 1(d
 def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int = 0, ancestors=None,
                         lse_out=None, normw_out=None, ess_out=None, status_out=None, offspring_out=None,
                         permuted_out=None, flags: int = 0, state=None, workspace=None, stream=None):
-    """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P].
+    """N independent filters: logw float32 [N, P] (row-strided) -> int32 ancestors [N, P];
+    float64 logw goes through pf_resample_batched_f64 (NS-3d).
     workspace: optional device tensor (256-byte aligned, >= pf_workspace_bytes) instead of the pool.
     state: optional [N, P, ...] tensor gathered in place with the canonical permutation."""
     torch = _torch()
-    _need_cuda(logw, torch.float32, "logw")
+    f64 = isinstance(logw, torch.Tensor) and logw.dtype == torch.float64
+    _need_cuda(logw, torch.float64 if f64 else torch.float32, "logw")
     if logw.dim() != 2:
         raise PfError("logw must be [N, P]")
     N, P = logw.shape
@@ -288,9 +296,10 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
             setattr(opts, name, t.data_ptr())
     _set_state(opts, state, True)
     _set_workspace(opts, workspace)
-    rc = lib().pf_resample_batched(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
-                                   aptr, ald, ctypes.byref(opts), _stream(logw, stream))
-    _check(rc, "pf_resample_batched")
+    fn = "pf_resample_batched_f64" if f64 else "pf_resample_batched"
+    rc = getattr(lib(), fn)(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
+                            aptr, ald, ctypes.byref(opts), _stream(logw, stream))
+    _check(rc, fn)
     return ancestors
 
 

@@ -7,7 +7,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpfresample.so")
-SOURCES = ["pf_kernels.cu", "pf_fused.cu", "pf_migrate.cu", "pf_api.cu"]
+SOURCES = ["pf_kernels.cu", "pf_fused.cu", "pf_migrate.cu", "pf_f64.cu", "pf_api.cu"]
 HEADERS = ["pf_device.cuh", "pf_internal.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,14 +36,31 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles in its own nvcc process (in parallel), then one link."""
     if not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    from concurrent.futures import ThreadPoolExecutor
+
+    tag = f".tmp{os.getpid()}"
+    objs = [os.path.join(PKG, f"_{os.path.splitext(s)[0]}{tag}.o") for s in SOURCES]
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    cmds = [[_nvcc(), *cflags, "-c", os.path.join(CSRC, s), "-o", o] for s, o in zip(SOURCES, objs)]
+    try:
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+            for cmd in cmds:
+                if verbose:
+                    print(" ".join(cmd))
+            list(ex.map(subprocess.check_call, cmds))
+        tmp = LIB + tag
+        link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp]
+        if verbose:
+            print(" ".join(link))
+        subprocess.check_call(link)
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return LIB
 
 

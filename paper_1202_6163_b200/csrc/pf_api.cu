@@ -7,6 +7,7 @@
 #include <mutex>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -25,19 +26,20 @@ struct PoolBlock {
 };
 
 std::mutex g_pool_mu;
-std::map<std::pair<int, void*>, PoolBlock>& pool() {
-    static auto* m = new std::map<std::pair<int, void*>, PoolBlock>();
+std::map<std::tuple<int, void*, int>, PoolBlock>& pool() {
+    static auto* m = new std::map<std::tuple<int, void*, int>, PoolBlock>();
     return *m;
 }
 
-// Returns a device workspace of >= bytes for (current device, stream).  Growth
+// Returns a device workspace of >= bytes for (current device, stream, slot).  Growth
 // is stream-ordered (cudaFreeAsync / cudaMallocAsync) and happens only when a
-// call needs more than any earlier call on that stream.
-pf_status pool_get(size_t bytes, cudaStream_t s, void** out) {
+// call needs more than any earlier call on that stream.  Slot 1 holds the binary64
+// entry points' shifted log-weights, which stay live while the float path uses slot 0.
+pf_status pool_get(size_t bytes, cudaStream_t s, void** out, int slot = 0) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return PF_ERR_CUDA;
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    PoolBlock& b = pool()[{dev, static_cast<void*>(s)}];
+    PoolBlock& b = pool()[{dev, static_cast<void*>(s), slot}];
     if (b.bytes < bytes) {
         if (b.ptr) cudaFreeAsync(b.ptr, s);
         b.ptr = nullptr;
@@ -284,6 +286,34 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     return cuda_status(e);
 }
 
+// NS-3d: binary64 log-weights -> t = fl32(logw - lmax) in a slot-1 pool block -> the float32
+// path on t (every dispatch of resample_impl applies) -> lse += lmax
+pf_status resample_f64_impl(int scheme, const double* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                            uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
+                            cudaStream_t s) {
+    if (!logw || !anc) return PF_ERR_INVALID_ARG;
+    if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
+    if (N < 1 || P < 1 || B < 0 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
+    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORTED)) != 0) return PF_ERR_UNSUPPORTED;
+    if (opts && (opts->flags & PF_SORTED) && scheme != PF_MULTINOMIAL) return PF_ERR_UNSUPPORTED;
+    void* ws = nullptr;
+    pf_status st = pool_get(pf::f64_ws_bytes(N, P), s, &ws, 1);
+    if (st != PF_OK) return st;
+    float* t = nullptr;
+    int64_t ldt = 0;
+    unsigned long long* key = nullptr;
+    uint64_t nl = 0;
+    cudaError_t e = pf::launch_shift64(logw, ld, N, P, ws, &t, &ldt, &key, s, &nl);
+    g_launches += nl;
+    if (e != cudaSuccess) return cuda_status(e);
+    st = resample_impl(scheme, t, ldt, N, P, seed, first_filter, B, anc, ld_anc, opts, s);
+    if (st != PF_OK || !opts || !opts->lse_out) return st;
+    nl = 0;
+    e = pf::launch_lse64(key, N, opts->lse_out, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
 }  // namespace
 
 namespace pf {
@@ -370,6 +400,19 @@ pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_lo
                               const pf_opts* opts, pf_stream_t stream) {
     return resample_impl(scheme, logw, ld_logw, N, P, seed, first_filter, B, ancestors, ld_anc, opts,
                          static_cast<cudaStream_t>(stream));
+}
+
+pf_status pf_resample_ex_f64(pf_scheme scheme, const double* logw, int32_t P, uint64_t seed, int32_t B,
+                             int32_t* ancestors, const pf_opts* opts, pf_stream_t stream) {
+    const uint32_t f = opts ? opts->filter_index : 0u;
+    return resample_f64_impl(scheme, logw, P, 1, P, seed, f, B, ancestors, P, opts, static_cast<cudaStream_t>(stream));
+}
+
+pf_status pf_resample_batched_f64(pf_scheme scheme, const double* logw, int64_t ld_logw, int32_t N, int32_t P,
+                                  uint64_t seed, uint32_t first_filter, int32_t B, int32_t* ancestors, int64_t ld_anc,
+                                  const pf_opts* opts, pf_stream_t stream) {
+    return resample_f64_impl(scheme, logw, ld_logw, N, P, seed, first_filter, B, ancestors, ld_anc, opts,
+                             static_cast<cudaStream_t>(stream));
 }
 
 size_t pf_workspace_bytes_ex(pf_scheme scheme, int32_t N, int32_t P, uint32_t flags, int64_t ld_anc) {

@@ -197,4 +197,12 @@ cudaError_t launch_mig_unpack(void* X, int64_t row_bytes, int64_t ld, int32_t Pl
                               const void* plan, const void* recv, const int32_t* recv_src, int32_t* perm,
                               cudaStream_t s, uint64_t* launches);
 
+// pf_f64.cu: binary64 log-weights (NS-3d).  ws holds f64_ws_bytes(N, P): t [N][ldt] float
+// (ldt = P rounded up to 4), then the per-filter max keys (u64) and bad flags (i32).
+size_t f64_ws_bytes(int32_t N, int32_t P);
+cudaError_t launch_shift64(const double* logw, int64_t ld, int32_t N, int32_t P, void* ws, float** t_out,
+                           int64_t* ldt_out, unsigned long long** key_out, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_lse64(const unsigned long long* key, int32_t N, double* lse, cudaStream_t s,
+                         uint64_t* launches);
+
 }  // namespace pf
