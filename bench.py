@@ -480,6 +480,29 @@ def run_ours(args):
         per_scheme["multinomial_sorted_a6"] = {"ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
         extras["resample_only"] = per_scheme
 
+        # binary64 log-weights (NS-3d): the same weights with an accumulated-log-likelihood offset,
+        # resample only and the full step (offspring, permutation, D-dim state gather)
+        logw64 = logw.double() - 1e7
+        f64 = {}
+        for label, kw in (("systematic_resample_only", {}),
+                          ("systematic_step", {"offspring_out": off, "permuted_out": perm, "state": X})):
+            def call64():
+                pf.pf_resample_batched("systematic", logw64, seed, first_filter=first, ancestors=anc, stream=stream,
+                                       **kw)
+            for _ in range(2):
+                call64()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                call64()
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            sms = a0.elapsed_time(a1) / reps
+            f64[label] = {"ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
+        del logw64
+        extras["f64_logw"] = f64
+
         # C1 (BASELINE configs[0]): single resampling of P = 16, latency per call with the calls
         # captured in a CUDA graph (device time, no host overhead on the timeline)
         from tools.sweep import time_calls
