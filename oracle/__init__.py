@@ -80,6 +80,7 @@ def lib():
         L.pfo_resample_sorted_multinomial.argtypes = [P, i32, u64, u32, P]
         L.pfo_shift_f64.argtypes = [P, i32, P, P]
         L.pfo_resample_f64.argtypes = [ctypes.c_int, ctypes.c_int, P, i32, u64, i32, u32, P, P, P, P]
+        L.pfo_resample_sorted_weights.argtypes = [ctypes.c_int, P, i32, u64, u32, P, P, P, P]
         L.pfo_metropolis_required_B.argtypes = [i64, f64, f64]
         L.pfo_metropolis_required_B.restype = i32
         _lib = L
@@ -219,6 +220,21 @@ def resample_f64(scheme, logw: np.ndarray, seed: int, B: int = 0, filter_index: 
     st = lib().pfo_resample_f64(_scheme(scheme), int(sorted), _p(logw), P, seed, B, filter_index, _p(a),
                                 ctypes.byref(lse) if side else None, _p(v) if side else None,
                                 ctypes.byref(ess) if side else None)
+    if side:
+        return st, a, lse.value, v, ess.value
+    return st, a
+
+
+def resample_sorted_weights(scheme, logw: np.ndarray, seed: int, filter_index: int = 0, side: bool = False):
+    """NS-17 pre-sorted weights: returns (status, ancestors[, lse, normw, ess])."""
+    logw = np.ascontiguousarray(logw, dtype=np.float32)
+    P = len(logw)
+    a = np.zeros(P, dtype=np.int32)
+    lse, ess = ctypes.c_double(), ctypes.c_double()
+    v = np.zeros(P, dtype=np.float32)
+    st = lib().pfo_resample_sorted_weights(_scheme(scheme), _p(logw), P, seed, filter_index, _p(a),
+                                           ctypes.byref(lse) if side else None, _p(v) if side else None,
+                                           ctypes.byref(ess) if side else None)
     if side:
         return st, a, lse.value, v, ess.value
     return st, a

@@ -485,6 +485,52 @@ int pfo_resample_f64(int scheme, int sorted, const double* logw, int32_t P, uint
 }
 
 /* ------------------------------------------------------------------------ */
+/* NS-17  pre-sorted weights (the paper's "sorting enabled" series,         */
+/* P:226-231; reading R-14).  sigma = the indices in DESCENDING order of    */
+/* logw, equal values (+0 == -0) in ascending index order; the float32 path */
+/* resamples y_j = logw[sigma_j] (same seed and filter index) into b, and   */
+/* a_k = sigma[b_k]; v_{sigma_j} = the normalised weight of y_j.  Invalid   */
+/* filters (NS-1) give the identity.                                        */
+/* ------------------------------------------------------------------------ */
+static const float* g_sort_keys; /* qsort context (single-threaded oracle) */
+
+static int desc_then_index(const void* pa, const void* pb)
+{
+    int32_t a = *(const int32_t*)pa, b = *(const int32_t*)pb;
+    float x = g_sort_keys[a], y = g_sort_keys[b];
+    if (x > y) return -1;
+    if (x < y) return 1;
+    return (a < b) ? -1 : (a > b); /* equal values (incl. +0 / -0): index order */
+}
+
+int pfo_resample_sorted_weights(int scheme, const float* logw, int32_t P, uint64_t seed, uint32_t filter_index,
+                                int32_t* anc, double* lse, float* normw, double* ess)
+{
+    float lm;
+    int st = pfo_lmax(logw, P, &lm);
+    if (st != PFO_FILTER_OK) /* NS-1 outputs, no sort */
+        return pfo_resample(scheme, logw, P, seed, 0, filter_index, anc, lse, normw, ess);
+    int32_t* sigma = (int32_t*)malloc(sizeof(int32_t) * (size_t)P);
+    for (int32_t i = 0; i < P; ++i) sigma[i] = i;
+    g_sort_keys = logw;
+    qsort(sigma, (size_t)P, sizeof(int32_t), desc_then_index);
+    float* y = (float*)malloc(sizeof(float) * (size_t)P);
+    for (int32_t j = 0; j < P; ++j) y[j] = logw[sigma[j]];
+    int32_t* b = (int32_t*)malloc(sizeof(int32_t) * (size_t)P);
+    float* vy = normw ? (float*)malloc(sizeof(float) * (size_t)P) : NULL;
+    pfo_resample(scheme, y, P, seed, 0, filter_index, b, lse, vy, ess);
+    for (int32_t k = 0; k < P; ++k) anc[k] = sigma[b[k]];
+    if (normw) {
+        for (int32_t j = 0; j < P; ++j) normw[sigma[j]] = vy[j];
+        free(vy);
+    }
+    free(b);
+    free(y);
+    free(sigma);
+    return PFO_FILTER_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* NS-14 conversions ("Converting between the two is straightforward"). */
 /* ------------------------------------------------------------------------ */
 void pfo_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* o)

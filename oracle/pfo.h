@@ -85,6 +85,11 @@ int pfo_shift_f64(const double* logw, int32_t P, float* t, double* lmax);
 int pfo_resample_f64(int scheme, int sorted, const double* logw, int32_t P, uint64_t seed, int32_t B,
                      uint32_t filter_index, int32_t* anc, double* lse, float* normw, double* ess);
 
+/* NS-17 (R-14): pre-sorted weights (descending, ties by index), resampled by the
+ * float32 path, ancestors mapped back to the original indices.  Prefix-sum schemes. */
+int pfo_resample_sorted_weights(int scheme, const float* logw, int32_t P, uint64_t seed, uint32_t filter_index,
+                                int32_t* anc, double* lse, float* normw, double* ess);
+
 /* NS-14 / SPEC S:60-77 conversions. */
 void pfo_ancestors_to_offspring(const int32_t* anc, int32_t P, int32_t* o);
 void pfo_offspring_to_ancestors(const int32_t* o, int32_t P, int32_t* anc);

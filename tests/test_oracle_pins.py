@@ -733,3 +733,81 @@ def test_f64_invalid_and_zero_weights(orc):
         st, a, lse, v, ess = orc.resample_f64(s, x, seed=8, B=200, side=True)  # (3/4)^200 to stay at a zero weight
         assert st == 0 and list(a) == [2, 2, 2, 2]
         assert lse == 12345.678 and list(v) == [0.0, 0.0, 1.0, 0.0] and ess == 1.0
+
+
+# --------------------------------------------------------------------------- NS-17 (R-14)
+SORTED_SCHEMES = ("multinomial", "stratified", "systematic")
+
+
+def test_sorted_weights_bruteforce(orc):
+    """NS-17: the paper's 'sorting enabled' series: an independent re-derivation:
+    Python's stable sort by (-logw, index) (so +0 == -0 and ties keep index order), the
+    linear-scan big-int ancestors of the sorted weights, mapped back through sigma.  Catches
+    an ascending sort, unstable ties, and mapping with sigma^-1 instead of sigma."""
+    rng = np.random.default_rng(17)
+    for trial in range(60):
+        P = int(rng.integers(1, 40))
+        x = pfinputs.gaussian_logw(P, float(rng.choice([0.1, 1, 10])), seed=trial)
+        if trial % 3 == 0:  # ties, signed zeros and zero weights
+            x = np.round(x).astype(np.float32)
+            x[x == 0] = np.float32(-0.0) if trial % 2 else np.float32(0.0)
+            x[:: max(1, P // 3)] = -np.inf
+            if not np.any(np.isfinite(x)):
+                x[0] = 0.0
+        sigma = sorted(range(P), key=lambda i: (-float(x[i]), i))
+        y = np.ascontiguousarray(x[sigma])
+        for s in SORTED_SCHEMES:
+            seed = 1000 + trial
+            st, a = orc.resample_sorted_weights(s, x, seed)
+            assert st == 0
+            assert [int(v) for v in a] == [sigma[b] for b in _brute(s, y, seed)], (trial, s)
+
+
+def test_sorted_weights_rotation_and_side_outputs(orc):
+    """Distinct descending y rotated by r: sigma(j) = (j + r) mod P, so a_k = (b_k + r) mod P
+    with b the plain ancestors of y; v_x[i] = v_y[(i - r) mod P]; lse and ESS unchanged.
+    Already-sorted input (r = 0) is the plain resampler."""
+    for P, r in [(5, 0), (100, 1), (4097, 1234)]:
+        y = np.sort(pfinputs.gaussian_logw(P, 1.0, seed=P))[::-1].copy()
+        assert np.all(np.diff(y) < 0)  # distinct, descending
+        x = np.roll(y, r)
+        for s in SORTED_SCHEMES:
+            st, a, lse, v, ess = orc.resample_sorted_weights(s, x, 77, side=True)
+            _, b, lse_y, v_y, ess_y = orc.resample(s, y, 77, side=True)
+            assert np.array_equal(a, (b + r) % P)
+            assert np.array_equal(v, np.roll(v_y, r))
+            assert lse == lse_y and ess == ess_y
+
+
+def test_sorted_weights_laws(orc):
+    """Sorting changes which uniforms land on which particle, not the per-particle law:
+    systematic o_i in {floor(P q_i/Q), ceil(P q_i/Q)} exactly; multinomial and stratified
+    unbiased (E[o_i] = P v_i, z-test over seeds); invalid filters give the identity."""
+    for trial in range(100):
+        P = 2 + trial % 150
+        x = pfinputs.gaussian_logw(P, 4.0, seed=trial)
+        st, Q = orc.cumulative(x)
+        Qi = [int(v) for v in Q]
+        q = [Qi[0]] + [Qi[i] - Qi[i - 1] for i in range(1, P)]
+        o = orc.ancestors_to_offspring(orc.resample_sorted_weights("systematic", x, trial)[1])
+        for i in range(P):
+            e = Fraction(P * q[i], Qi[-1])
+            assert math.floor(e) <= o[i] <= math.ceil(e), (trial, i)
+    P, R = 50, 3000
+    x = pfinputs.gaussian_logw(P, 2.0, seed=5)
+    _, _, _, v, _ = orc.resample("systematic", x, 1, side=True)
+    for s in ("multinomial", "stratified"):
+        tot = np.zeros(P)
+        tot2 = np.zeros(P)
+        for r in range(R):
+            o = orc.ancestors_to_offspring(orc.resample_sorted_weights(s, x, pfinputs.seed_for(r))[1]).astype(float)
+            tot += o
+            tot2 += o * o
+        mean = tot / R
+        var = np.maximum(tot2 / R - mean * mean, 1e-12)
+        z = (mean - P * v.astype(float)) / np.sqrt(var / R)
+        assert np.max(np.abs(z)) < 4.5, s
+    for bad in (np.float32([0, np.nan, 1]), np.full(3, -np.inf, np.float32)):
+        for s in SORTED_SCHEMES:
+            st, a = orc.resample_sorted_weights(s, bad, 3)
+            assert st == 1 and list(a) == [0, 1, 2]
