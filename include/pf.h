@@ -74,7 +74,17 @@ enum {
     PF_SORTED = 1u << 0,
     /* diagnostics: force the multi-launch path (max -> lookback scan -> search)
      * even where the one-launch cluster kernel applies.  Results are identical. */
-    PF_NO_FUSION = 1u << 1
+    PF_NO_FUSION = 1u << 1,
+    /* with PF_MULTINOMIAL / PF_STRATIFIED / PF_SYSTEMATIC: the paper's pre-sorted weight
+     * series (NS-17): each filter's log-weights are stably sorted in
+     * descending order (equal values, +0 = -0, in index order) by a segmented radix sort,
+     * resampled by the same scheme, seed and filter index, and the ancestors are mapped back
+     * to the original indices (a_k = sigma[b_k]); normw_out / offspring_out / permuted_out /
+     * state are in the original order.  Same law as the unsorted scheme; the paper found the
+     * sort to cost more than the faster search saves.  Not with PF_SORTED or
+     * PF_METROPOLIS (-> PF_ERR_UNSUPPORTED).  Its scratch (~20 B per particle) always comes from
+     * the library pool. */
+    PF_SORT_WEIGHTS = 1u << 2
 };
 
 /*
@@ -83,7 +93,7 @@ enum {
  */
 typedef struct {
     uint32_t filter_index; /* Philox c3 of a single-filter call (batched: first_filter+n) */
-    uint32_t flags;        /* PF_SORTED (multinomial only) | PF_NO_FUSION; other bits -> PF_ERR_UNSUPPORTED */
+    uint32_t flags;        /* PF_SORTED (multinomial only) | PF_NO_FUSION | PF_SORT_WEIGHTS; other bits -> PF_ERR_UNSUPPORTED */
     double* lse_out;       /* [N] ln sum_i exp(logw_i)  (NS-13; 1e-6 rel. of oracle)       */
     float* normw_out;      /* [N][P] (row stride P) v_i = w_i / sum_j w_j  (NS-13)          */
     double* ess_out;       /* [N] (sum w)^2 / sum w^2                          */

@@ -22,6 +22,7 @@ SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
 PF_FILTER_OK, PF_FILTER_INVALID_WEIGHTS = 0, 1
 PF_SORTED = 1 << 0  # pf_opts.flags with multinomial: sorted-uniform variant (a6, NS-12)
 PF_NO_FUSION = 1 << 1  # pf_opts.flags: force the multi-launch path (diagnostics)
+PF_SORT_WEIGHTS = 1 << 2  # pf_opts.flags: the paper's pre-sorted weight series (NS-17)
 
 
 class PfError(RuntimeError):

@@ -7,7 +7,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpfresample.so")
-SOURCES = ["pf_kernels.cu", "pf_fused.cu", "pf_migrate.cu", "pf_f64.cu", "pf_api.cu"]
+SOURCES = ["pf_kernels.cu", "pf_fused.cu", "pf_migrate.cu", "pf_f64.cu", "pf_wsort.cu", "pf_api.cu"]
 HEADERS = ["pf_device.cuh", "pf_internal.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

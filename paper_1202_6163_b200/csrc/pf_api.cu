@@ -119,7 +119,7 @@ bool medium_preferred(int scheme, int32_t N, int32_t P) {
     return false;
 }
 
-pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
                         cudaStream_t s) {
     if (!logw || !anc) return PF_ERR_INVALID_ARG;
@@ -234,7 +234,7 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
         o2.offspring_out = off;
         o2.workspace = static_cast<char*>(big) + o2b;
         o2.workspace_bytes = LR.total;
-        pf_status st2 = resample_impl(scheme, logw, ld, N, P, seed, first_filter, B, anc, ld_anc, &o2, s);
+        pf_status st2 = resample_core(scheme, logw, ld, N, P, seed, first_filter, B, anc, ld_anc, &o2, s);
         if (st2 != PF_OK) return st2;
         uint64_t nl = 0;
         cudaError_t e = cudaMemsetAsync(static_cast<char*>(big) + LP.zero_begin, 0, LP.zero_end - LP.zero_begin, s);
@@ -286,6 +286,70 @@ pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, in
     return cuda_status(e);
 }
 
+// NS-17 (PF_SORT_WEIGHTS): segmented radix sort of the log-weights (descending) into a
+// slot-2 pool block, the float path on the sorted weights (ancestors b in sorted space), then
+// a_k = sigma[b_k] and normw back in the original order; offspring / permutation / state run
+// on the mapped ancestors (histogram, k_pscan + k_push, gather).
+pf_status resample_sorted_weights(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                                  uint32_t first_filter, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
+                                  cudaStream_t s) {
+    if (!logw || !anc) return PF_ERR_INVALID_ARG;
+    if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
+    if (N < 1 || P < 1 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
+    const uint32_t flags = opts->flags;
+    if ((flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORT_WEIGHTS)) != 0 || scheme == PF_METROPOLIS)
+        return PF_ERR_UNSUPPORTED;
+    void* state = opts->state;
+    const int64_t x_row = opts->state_row_bytes, x_ld = opts->state_ld_bytes, x_fld = opts->state_filter_ld_bytes;
+    if (state && (x_row < 1 || x_ld < x_row || (N > 1 && x_fld < x_ld * static_cast<int64_t>(P))))
+        return PF_ERR_INVALID_ARG;
+    const size_t sort_bytes = (pf::wsort_ws_bytes(N, P, opts->normw_out != nullptr) + 255) / 256 * 256;
+    const bool own_perm = state && !opts->permuted_out;
+    void* ws = nullptr;
+    pf_status st = pool_get(sort_bytes + (own_perm ? static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4 : 0),
+                            s, &ws, 2);
+    if (st != PF_OK) return st;
+    pf::WsortBufs w{};
+    uint64_t nl = 0;
+    cudaError_t e = pf::launch_wsort(logw, ld, N, P, ws, opts->normw_out != nullptr, &w, s, &nl);
+    g_launches += nl;
+    if (e != cudaSuccess) return cuda_status(e);
+    pf_opts o2{};
+    o2.flags = flags & PF_NO_FUSION;
+    o2.lse_out = opts->lse_out;
+    o2.ess_out = opts->ess_out;
+    o2.status_out = w.fstatus;
+    o2.normw_out = w.vs;
+    o2.workspace = opts->workspace;
+    o2.workspace_bytes = opts->workspace_bytes;
+    st = resample_core(scheme, w.y, w.ldk, N, P, seed, first_filter, 0, w.b, w.ldk, &o2, s);
+    if (st != PF_OK) return st;
+    nl = 0;
+    e = pf::launch_unsort(w, N, P, anc, ld_anc, opts->normw_out, s, &nl);
+    g_launches += nl;
+    if (e == cudaSuccess && opts->status_out)
+        e = cudaMemcpyAsync(opts->status_out, w.fstatus, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (opts->offspring_out) {
+        st = pf_ancestors_to_offspring_batched(anc, ld_anc, N, P, opts->offspring_out, ld_anc, s);
+        if (st != PF_OK) return st;
+    }
+    if (opts->permuted_out || state) {
+        int32_t* perm = own_perm ? reinterpret_cast<int32_t*>(static_cast<char*>(ws) + sort_bytes) : opts->permuted_out;
+        st = pf_permute_batched(anc, ld_anc, N, P, perm, ld_anc, s);
+        if (st == PF_OK && state) st = pf_gather_state_batched(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s);
+    }
+    return st;
+}
+
+pf_status resample_impl(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
+                        uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
+                        cudaStream_t s) {
+    if (opts && (opts->flags & PF_SORT_WEIGHTS))
+        return resample_sorted_weights(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, opts, s);
+    return resample_core(scheme, logw, ld, N, P, seed, first_filter, B, anc, ld_anc, opts, s);
+}
+
 // NS-3d: binary64 log-weights -> t = fl32(logw - lmax) in a slot-1 pool block -> the float32
 // path on t (every dispatch of resample_impl applies) -> lse += lmax
 pf_status resample_f64_impl(int scheme, const double* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
@@ -294,7 +358,8 @@ pf_status resample_f64_impl(int scheme, const double* logw, int64_t ld, int32_t 
     if (!logw || !anc) return PF_ERR_INVALID_ARG;
     if (scheme < PF_MULTINOMIAL || scheme > PF_METROPOLIS) return PF_ERR_INVALID_ARG;
     if (N < 1 || P < 1 || B < 0 || ld < P || ld_anc < P) return PF_ERR_INVALID_ARG;
-    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORTED)) != 0) return PF_ERR_UNSUPPORTED;
+    if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORTED | PF_SORT_WEIGHTS)) != 0)
+        return PF_ERR_UNSUPPORTED;
     if (opts && (opts->flags & PF_SORTED) && scheme != PF_MULTINOMIAL) return PF_ERR_UNSUPPORTED;
     void* ws = nullptr;
     pf_status st = pool_get(pf::f64_ws_bytes(N, P), s, &ws, 1);

@@ -205,4 +205,19 @@ cudaError_t launch_shift64(const double* logw, int64_t ld, int32_t N, int32_t P,
 cudaError_t launch_lse64(const unsigned long long* key, int32_t N, double* lse, cudaStream_t s,
                          uint64_t* launches);
 
+// pf_wsort.cu: pre-sorted weights (PF_SORT_WEIGHTS, NS-17).  ws holds wsort_ws_bytes(N, P, normw).
+struct WsortBufs {
+    float* y;          // [N][ldk] log-weights sorted in descending order
+    int32_t* sigma;    // [N][ldk] original index of each sorted position
+    int64_t ldk;
+    int32_t* b;        // [N][ldk] ancestors in sorted space (written by the float path)
+    int32_t* fstatus;  // [N] filter status (written by the float path)
+    float* vs;         // [N][P] normalised weights in sorted order (nullable)
+};
+size_t wsort_ws_bytes(int32_t N, int32_t P, bool normw);
+cudaError_t launch_wsort(const float* logw, int64_t ld, int32_t N, int32_t P, void* ws, bool normw, WsortBufs* out,
+                         cudaStream_t s, uint64_t* launches);
+cudaError_t launch_unsort(const WsortBufs& w, int32_t N, int32_t P, int32_t* anc, int64_t ld_anc, float* normw,
+                          cudaStream_t s, uint64_t* launches);
+
 }  // namespace pf
