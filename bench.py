@@ -503,6 +503,24 @@ def run_ours(args):
         del logw64
         extras["f64_logw"] = f64
 
+        # the paper's pre-sorted weight series (PF_SORT_WEIGHTS, NS-17): sort + resample
+        presorted = {}
+        for sch in ("multinomial", "stratified", "systematic"):
+            def call_sorted():
+                pf.pf_resample_batched(sch, logw, seed, first_filter=first, ancestors=anc, flags=pf.PF_SORT_WEIGHTS,
+                                       stream=stream)
+            call_sorted()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                call_sorted()
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            sms = a0.elapsed_time(a1) / reps
+            presorted[sch] = {"ms": round(sms, 4), "particles_per_s": N * P / (sms / 1e3)}
+        extras["resample_presorted_weights"] = presorted
+
         # C1 (BASELINE configs[0]): single resampling of P = 16, latency per call with the calls
         # captured in a CUDA graph (device time, no host overhead on the timeline)
         from tools.sweep import time_calls

@@ -28,6 +28,7 @@ constexpr int kRTile = kRT * kRI;     // 4096 items per tile
 constexpr int kRadixBits = 4;
 constexpr int kDigits = 1 << kRadixBits;
 constexpr int kPasses = 32 / kRadixBits;
+constexpr int kSortSmem = (kDigits * kRT + 2 * kRTile) * 4;  // counters + the tile's keys and values
 
 // descending order key: equal floats (+0 == -0) get equal keys; -inf sorts last among numbers
 __device__ __forceinline__ uint32_t sort_key(float f) {
@@ -165,22 +166,15 @@ __global__ void __launch_bounds__(kRT) k_rscan(uint32_t* H, int32_t T) {
     }
 }
 
-template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kRT) k_rscatter(SortArgs a) {
-    const int64_t n = blockIdx.x / a.T;
-    const int tile = static_cast<int>(blockIdx.x % a.T);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t k[kRI];
-    int32_t v[kRI];
-    const int cnt = load_items<FIRST>(a, n, tile, k, v);
-    uint64_t lo, hi;
-    count_digits(k, cnt, a.shift, lo, hi);
-    __shared__ uint32_t s_cnt[kDigits * kRT];  // (digit, thread) order
-    __shared__ uint32_t s_w[kRT / 32];
+// s_cnt[d * kRT + t] <- number of items of digit d in threads < t plus in digits < d over the
+// whole tile: the CTA-wide exclusive scan of the per-thread digit counts in (digit, thread)
+// order, i.e. the position in the tile's stable digit order of thread t's first digit-d item
+__device__ __forceinline__ void tile_digit_scan(uint64_t lo, uint64_t hi, uint32_t* s_cnt, uint32_t* s_w, int tid) {
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int d = 0; d < kDigits; ++d) s_cnt[d * kRT + tid] = field(lo, hi, d);
     __syncthreads();
-    // CTA exclusive scan over the 4096 counters: thread t owns entries [16t, 16t + 16)
+    // thread t owns the entries [16t, 16t + 16) of the flat (digit, thread) array
     uint32_t run[kRI];
     uint32_t sum = 0;
 #pragma unroll
@@ -204,25 +198,94 @@ __global__ void __launch_bounds__(kRT) k_rscatter(SortArgs a) {
 #pragma unroll
     for (int j = 0; j < kRI; ++j) s_cnt[tid * kRI + j] = excl + run[j];
     __syncthreads();
-    // position of this thread's first digit-d item: the filter's digit-d offset for this tile
-    // (H, scanned) + its rank among the tile's digit-d items
-    uint32_t base[kDigits];
+}
+
+// Filters of P <= 4096 (one tile): all eight passes in shared memory, one launch, one CTA per
+// filter; writes the sorted weights and sigma like the last multi-tile pass.
+__global__ void __launch_bounds__(kRT) k_rsort_tile(SortArgs a) {
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    uint32_t* s_cnt = s_dyn;                                       // kDigits * kRT
+    uint32_t* s_k = s_dyn + kDigits * kRT;                         // kRTile
+    int32_t* s_v = reinterpret_cast<int32_t*>(s_k + kRTile);       // kRTile
+    __shared__ uint32_t s_w[kRT / 32];
+    const int64_t n = blockIdx.x;
+    const int tid = threadIdx.x;
+    uint32_t k[kRI];
+    int32_t v[kRI];
+    const int cnt = load_items<true>(a, n, 0, k, v);
+    for (int pass = 0; pass < kPasses; ++pass) {
+        const int shift = pass * kRadixBits;
+        uint64_t lo, hi;
+        count_digits(k, cnt, shift, lo, hi);
+        tile_digit_scan(lo, hi, s_cnt, s_w, tid);
 #pragma unroll
-    for (int d = 0; d < kDigits; ++d)
-        base[d] = a.H[(n * kDigits + d) * a.T + tile] + s_cnt[d * kRT + tid] - s_cnt[d * kRT];
+        for (int j = 0; j < kRI; ++j) {
+            if (j < cnt) {
+                const uint32_t d = (k[j] >> shift) & (kDigits - 1);
+                const uint32_t pos = s_cnt[d * kRT + tid]++;
+                s_k[pos] = k[j];
+                s_v[pos] = v[j];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kRI; ++j) {
+            if (j < cnt) {
+                k[j] = s_k[tid * kRI + j];
+                v[j] = s_v[tid * kRI + j];
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) {
+        if (j < cnt) {
+            const int64_t o = n * a.ldk + tid * kRI + j;
+            a.kout[o] = __float_as_uint(key_value(k[j]));
+            a.vout[o] = v[j];
+        }
+    }
+}
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kRT) k_rscatter(SortArgs a) {
+    const int64_t n = blockIdx.x / a.T;
+    const int tile = static_cast<int>(blockIdx.x % a.T);
+    const int tid = threadIdx.x;
+    uint32_t k[kRI];
+    int32_t v[kRI];
+    const int cnt = load_items<FIRST>(a, n, tile, k, v);
+    uint64_t lo, hi;
+    count_digits(k, cnt, a.shift, lo, hi);
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    uint32_t* s_cnt = s_dyn;                                  // (digit, thread) order
+    uint32_t* s_k = s_dyn + kDigits * kRT;                    // the tile in digit order
+    int32_t* s_v = reinterpret_cast<int32_t*>(s_k + kRTile);
+    __shared__ uint32_t s_w[kRT / 32];
+    __shared__ int64_t s_goff[kDigits];
+    tile_digit_scan(lo, hi, s_cnt, s_w, tid);
+    // a tile item at digit-order position p goes to the filter's position H[d][tile] + p - start[d]
+    if (tid < kDigits)
+        s_goff[tid] = static_cast<int64_t>(a.H[(n * kDigits + tid) * a.T + tile]) - s_cnt[tid * kRT];
     __syncthreads();
-#pragma unroll
-    for (int d = 0; d < kDigits; ++d) s_cnt[d * kRT + tid] = base[d];
-    __syncwarp();
+    // stable local sort of the tile by the digit (thread order = index order), in shared memory
 #pragma unroll
     for (int j = 0; j < kRI; ++j) {
         if (j < cnt) {
             const uint32_t d = (k[j] >> a.shift) & (kDigits - 1);
             const uint32_t pos = s_cnt[d * kRT + tid]++;  // column of this thread: no conflicts
-            const int64_t o = n * a.ldk + pos;
-            a.kout[o] = LAST ? __float_as_uint(key_value(k[j])) : k[j];
-            a.vout[o] = v[j];
+            s_k[pos] = k[j];
+            s_v[pos] = v[j];
         }
+    }
+    __syncthreads();
+    // coalesced stores: consecutive positions of one digit are consecutive in the filter
+    const int tc = static_cast<int>(min(int64_t{kRTile}, static_cast<int64_t>(a.P) - static_cast<int64_t>(tile) * kRTile));
+    for (int p = tid; p < tc; p += kRT) {
+        const uint32_t key = s_k[p];
+        const int64_t o = n * a.ldk + s_goff[(key >> a.shift) & (kDigits - 1)] + p;
+        a.kout[o] = LAST ? __float_as_uint(key_value(key)) : key;
+        a.vout[o] = s_v[p];
     }
 }
 
@@ -271,7 +334,28 @@ cudaError_t launch_wsort(const float* logw, int64_t ld, int32_t N, int32_t P, vo
                       : nullptr;
     SortArgs a{logw, ld, N, P, T, ldk, nullptr, nullptr, nullptr, nullptr, H, 0};
     const unsigned grid = static_cast<unsigned>(static_cast<int64_t>(N) * T);
-    for (int pass = 0; pass < kPasses; ++pass) {
+    {
+        // dynamic shared memory above 48 KB (per device; idempotent, so a racing first call on
+        // one device just sets the same values twice)
+        static std::atomic<int> done[kMaxDevices];
+        std::atomic<int>& d = done[current_device()];
+        if (!d.load(std::memory_order_relaxed)) {
+            cudaFuncSetAttribute(k_rsort_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+            cudaFuncSetAttribute(k_rscatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+            cudaFuncSetAttribute(k_rscatter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+            cudaFuncSetAttribute(k_rscatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+            d.store(1, std::memory_order_relaxed);
+        }
+    }
+    for (int pass = 0; pass < kPasses && T == 1; ++pass) {  // one tile: a single launch
+        a.kout = kB;
+        a.vout = vB;
+        ProfScope ps_("k_rsort_tile", s);
+        k_rsort_tile<<<static_cast<unsigned>(N), kRT, kSortSmem, s>>>(a);
+        ++*launches;
+        break;
+    }
+    for (int pass = 0; pass < kPasses && T > 1; ++pass) {
         a.shift = pass * kRadixBits;
         const bool first = pass == 0, last = pass == kPasses - 1;
         a.kin = (pass & 1) ? kA : kB;
@@ -289,9 +373,9 @@ cudaError_t launch_wsort(const float* logw, int64_t ld, int32_t N, int32_t P, vo
         }
         {
             ProfScope ps_("k_rscatter", s);
-            if (first) k_rscatter<true, false><<<grid, kRT, 0, s>>>(a);
-            else if (last) k_rscatter<false, true><<<grid, kRT, 0, s>>>(a);
-            else k_rscatter<false, false><<<grid, kRT, 0, s>>>(a);
+            if (first) k_rscatter<true, false><<<grid, kRT, kSortSmem, s>>>(a);
+            else if (last) k_rscatter<false, true><<<grid, kRT, kSortSmem, s>>>(a);
+            else k_rscatter<false, false><<<grid, kRT, kSortSmem, s>>>(a);
         }
         *launches += 3;
     }
