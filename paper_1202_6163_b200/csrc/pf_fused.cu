@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "pf_device.cuh"
@@ -785,9 +786,11 @@ __device__ __forceinline__ uint64_t packed_of(int32_t o, bool real) {
     return (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && real) ? 1ull : 0ull);
 }
 
-// this thread's 16 offspring of the sub-tile at t0 (rows of 4, natural order), 0 past c1
+// this thread's FI offspring of the sub-tile at t0 (rows of 4, natural order), 0 past c1
+template <int FI>
 __device__ __forceinline__ void coop_load_o(const int32_t* orow, int64_t t0, int64_t c1, int tid, int vec,
-                                            int32_t ov[kFI]) {
+                                            int32_t* ov) {
+    constexpr int kFR = FI / 4;
 #pragma unroll
     for (int j = 0; j < kFR; ++j) {
         const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
@@ -803,9 +806,12 @@ __device__ __forceinline__ void coop_load_o(const int32_t* orow, int64_t t0, int
 
 // block exclusive scan of the packed values of a sub-tile: pex[j] = this lane's offset in row j's
 // warp segment, s_wt[j][warp] = the (row, warp) segment offset, *total = the sub-tile's total
-__device__ __forceinline__ void coop_packed_scan(const int32_t ov[kFI], int64_t t0, int64_t c1, int tid, int warp,
-                                                 int lane, uint64_t (*s_wt)[kFW], uint64_t* s_u64, uint64_t pex[kFR],
+template <int FI>
+__device__ __forceinline__ void coop_packed_scan(const int32_t* ov, int64_t t0, int64_t c1, int tid, int warp,
+                                                 int lane, uint64_t (*s_wt)[kFW], uint64_t* s_u64, uint64_t* pex,
                                                  uint64_t* total) {
+    constexpr int kFR = FI / 4;
+    constexpr int kTPL = kFR * kFW / 32;
 #pragma unroll
     for (int j = 0; j < kFR; ++j) {
         uint64_t loc = 0;
@@ -841,8 +847,15 @@ __device__ __forceinline__ void coop_packed_scan(const int32_t ov[kFI], int64_t 
 }
 
 // PERM: 0 ancestors (+ offspring), 1 + the canonical permutation (offspring required)
-template <int SCHEME, bool SUMS, int PERM>
+template <int SCHEME, bool SUMS, int PERM, int FI>
 __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
+    // FI particles per thread: sub-tiles of kPP = 512 x FI particles (16: 8192, 8: 4096, so that
+    // filters of 2^18..2^20 spread over 64..256 CTAs instead of 32..128)
+    constexpr int kFI = FI;
+    constexpr int kFR = FI / 4;
+    constexpr int kPP = kFT * FI;
+    constexpr int kTPL = kFR * kFW / 32;
+    static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32 (row, warp) totals");
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];
@@ -1131,7 +1144,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             uint64_t ploc = 0;
             for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
                 int32_t ov[kFI];
-                coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+                coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
 #pragma unroll
                 for (int t = 0; t < kFI; ++t) ploc += packed_of(ov[t], t0 + (t >> 2) * (kFT * 4) + tid * 4 + (t & 3) < c1);
             }
@@ -1156,9 +1169,9 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 uint64_t run0 = s_u64[3];
                 for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
                     int32_t ov[kFI];
-                    coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+                    coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
                     uint64_t pex[kFR], stot;
-                    coop_packed_scan(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
 #pragma unroll
                     for (int j = 0; j < kFR; ++j) {
                         uint64_t run = run0 + s_wt[j][warp] + pex[j];
@@ -1184,9 +1197,9 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 int32_t* s_head = &s_buf[0][0];
                 for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
                     int32_t ov[kFI];
-                    coop_load_o(orow, t0, c1, tid, a.anc_vec, ov);
+                    coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
                     uint64_t pex[kFR], stot;
-                    coop_packed_scan(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
                     const uint32_t XS = static_cast<uint32_t>(run0 >> 31);          // first extras rank
                     const uint32_t XT = static_cast<uint32_t>((run0 + stot) >> 31) - XS;
                     const int32_t idbase = static_cast<int32_t>(t0) + tid * 4;
@@ -1782,12 +1795,12 @@ size_t coop_scratch_bytes(int32_t P) {
     return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(P) * 4 + 256;
 }
 
-template <int SCHEME, bool SUMS, int PERM>
+template <int SCHEME, bool SUMS, int PERM, int FI>
 int coop_occupancy() {
     static std::atomic<int> per_sm[kMaxDevices];
     return cached_per_device(per_sm, [] {
         int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_coop_sorted<SCHEME, SUMS, PERM>, kFT, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_coop_sorted<SCHEME, SUMS, PERM, FI>, kFT, 0) !=
                 cudaSuccess ||
             o < 1) {
             cudaGetLastError();
@@ -1797,18 +1810,38 @@ int coop_occupancy() {
     });
 }
 
-template <int SCHEME, bool SUMS, int PERM>
-cudaError_t launch_coop_t(CoopArgs& a, cudaStream_t s) {
-    int G = std::min(device_sms() * coop_occupancy<SCHEME, SUMS, PERM>(), 4096);
-    // chunks are whole 8192-particle sub-tiles; never more CTAs than sub-tiles
-    const int64_t tiles = (static_cast<int64_t>(a.P) + kPP - 1) / kPP;
+// particles per thread of the cooperative kernel: 8 (4096-particle sub-tiles) while the filter
+// has no more 4096-tiles than co-resident CTAs, so that every CTA holds one short sub-tile; 16
+// above (fewer, longer sub-tiles amortise the per-sub-tile barriers).  PF_COOP_FI=8|16 forces one.
+int coop_fi(int32_t P, int g_max) {
+    static const int forced = [] {
+        const char* e = std::getenv("PF_COOP_FI");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 8 || forced == 16) return forced;
+    return (static_cast<int64_t>(P) + kFT * 8 - 1) / (kFT * 8) <= g_max ? 8 : 16;
+}
+
+template <int SCHEME, bool SUMS, int PERM, int FI>
+cudaError_t launch_coop_fi(CoopArgs& a, cudaStream_t s) {
+    constexpr int64_t kSub = static_cast<int64_t>(kFT) * FI;
+    int G = std::min(device_sms() * coop_occupancy<SCHEME, SUMS, PERM, FI>(), 4096);
+    // chunks are whole sub-tiles; never more CTAs than sub-tiles
+    const int64_t tiles = (static_cast<int64_t>(a.P) + kSub - 1) / kSub;
     G = static_cast<int>(std::min<int64_t>(G, tiles));
     const int64_t per = (tiles + G - 1) / G;
-    a.CH = per * kPP;
+    a.CH = per * kSub;
     G = static_cast<int>((static_cast<int64_t>(a.P) + a.CH - 1) / a.CH);
     void* args[] = {&a};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_coop_sorted<SCHEME, SUMS, PERM>), dim3(G), dim3(kFT),
-                                       args, 0, s);
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_coop_sorted<SCHEME, SUMS, PERM, FI>), dim3(G),
+                                       dim3(kFT), args, 0, s);
+}
+
+template <int SCHEME, bool SUMS, int PERM>
+cudaError_t launch_coop_t(CoopArgs& a, cudaStream_t s) {
+    const int g8 = std::min(device_sms() * coop_occupancy<SCHEME, SUMS, PERM, 8>(), 4096);
+    return coop_fi(a.P, g8) == 8 ? launch_coop_fi<SCHEME, SUMS, PERM, 8>(a, s)
+                                 : launch_coop_fi<SCHEME, SUMS, PERM, 16>(a, s);
 }
 
 template <int PERM>
