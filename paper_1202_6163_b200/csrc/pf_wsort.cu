@@ -106,13 +106,42 @@ __device__ __forceinline__ uint32_t field(uint64_t lo, uint64_t hi, int d) {
     return static_cast<uint32_t>(((d < 8) ? (lo >> (8 * d)) : (hi >> (8 * (d - 8)))) & 0xFFu);
 }
 
+// the histogram does not depend on the order of the items: coalesced striped loads (float4 /
+// uint4 where the rows allow), 16 items per thread
 template <bool FIRST>
 __global__ void __launch_bounds__(kRT) k_rhist(SortArgs a) {
     const int64_t n = blockIdx.x / a.T;
     const int tile = static_cast<int>(blockIdx.x % a.T);
+    const int64_t t0 = static_cast<int64_t>(tile) * kRTile;
+    const int tc = static_cast<int>(min(int64_t{kRTile}, static_cast<int64_t>(a.P) - t0));
     uint32_t k[kRI];
-    int32_t v[kRI];
-    const int cnt = load_items<FIRST>(a, n, tile, k, v);
+    int cnt = 0;
+    const bool vec = FIRST ? ((reinterpret_cast<uintptr_t>(a.logw) & 15) == 0 && (a.ld & 3) == 0) : true;
+    if (vec && tc == kRTile) {
+#pragma unroll
+        for (int q = 0; q < kRI / 4; ++q) {
+            const int64_t i = t0 + (q * kRT + threadIdx.x) * 4;
+            if (FIRST) {
+                const float4 f = __ldcs(reinterpret_cast<const float4*>(a.logw + n * a.ld + i));
+                k[4 * q] = sort_key(f.x); k[4 * q + 1] = sort_key(f.y);
+                k[4 * q + 2] = sort_key(f.z); k[4 * q + 3] = sort_key(f.w);
+            } else {
+                const uint4 u = *reinterpret_cast<const uint4*>(a.kin + n * a.ldk + i);
+                k[4 * q] = u.x; k[4 * q + 1] = u.y; k[4 * q + 2] = u.z; k[4 * q + 3] = u.w;
+            }
+        }
+        cnt = kRI;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRI; ++j) {
+            const int r = j * kRT + threadIdx.x;  // striped
+            k[j] = 0;
+            if (r < tc) {
+                k[j] = FIRST ? sort_key(a.logw[n * a.ld + t0 + r]) : a.kin[n * a.ldk + t0 + r];
+                cnt = j + 1;
+            }
+        }
+    }
     uint64_t lo, hi;
     count_digits(k, cnt, a.shift, lo, hi);
     __shared__ uint32_t s_c[kDigits];
