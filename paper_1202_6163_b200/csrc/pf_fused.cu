@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
     __shared__ uint64_t s_off, s_tot, s_Qtot;
     __shared__ double s_S, s_S2;
     __shared__ uint32_t s_klo;
+    __shared__ uint64_t s_rho;
+    __shared__ double s_zA, s_zBc;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int c = static_cast<int>(cluster.block_rank());
@@ -472,6 +474,14 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 s_Qtot = tot;
                 s_S = Sr;
                 s_S2 = S2r;
+                // the filter's position constants, once per CTA (not per thread: a Philox call
+                // and two double divisions on the FP64 pipe by 512 threads)
+                const uint64_t rho =
+                    (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+                s_rho = rho;
+                // A = 2^64 / (D Q), Bc = rho / D  (the double estimate of k*)
+                s_zA = 0x1p64 / (static_cast<double>(a.D) * static_cast<double>(tot));
+                s_zBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
             }
         }
         __syncthreads();
@@ -482,10 +492,9 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         z.key = a.key;
         z.filt = filt;
         z.P = a.P;
-        z.rho = (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
-        // A = 2^64 / (D Q), Bc = rho / D  (the double estimate of k*)
-        z.A = 0x1p64 / (static_cast<double>(z.D) * static_cast<double>(z.Qtot));
-        z.Bc = (SCHEME == 3) ? static_cast<double>(z.rho) / static_cast<double>(z.D) : 0.0;
+        z.rho = s_rho;
+        z.A = s_zA;
+        z.Bc = s_zBc;
         if (c == 0 && tid == 0) {
             if (a.lse_out) a.lse_out[n] = static_cast<double>(lm) + log(s_S);
             if (a.ess_out) a.ess_out[n] = s_S * s_S / s_S2;
