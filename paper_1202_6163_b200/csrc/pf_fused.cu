@@ -876,6 +876,8 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     __shared__ uint64_t s_u64[4];
     __shared__ uint32_t s_prevE;
     __shared__ int32_t s_wmax[kFW];
+    __shared__ uint64_t s_crho;
+    __shared__ double s_cA, s_cBc;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
@@ -996,6 +998,12 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             if (lane == 0) {
                 s_u64[0] = off;
                 s_u64[1] = all;
+                // the filter's position constants, once per CTA (as in k_fused_sorted)
+                const uint64_t rho =
+                    (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+                s_crho = rho;
+                s_cA = 0x1p64 / (static_cast<double>(a.D) * static_cast<double>(all));
+                s_cBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
                 if (SUMS && c == 0) {
                     double S = 0.0, S2 = 0.0;
                     for (int r = 0; r < G; ++r) { S += __ldcg(a.g_sw + r); S2 += __ldcg(a.g_sw2 + r); }
@@ -1012,9 +1020,9 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         z.key = a.key;
         z.filt = filt;
         z.P = a.P;
-        z.rho = (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
-        z.A = 0x1p64 / (static_cast<double>(z.D) * static_cast<double>(z.Qtot));
-        z.Bc = (SCHEME == 3) ? static_cast<double>(z.rho) / static_cast<double>(z.D) : 0.0;
+        z.rho = s_crho;
+        z.A = s_cA;
+        z.Bc = s_cBc;
         uint64_t carry = s_u64[0];
         if (tid == 0) s_prevE = count_below<SCHEME>(z, carry);
         // ---------------- C: sub-tiles in order
