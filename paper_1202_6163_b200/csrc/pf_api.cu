@@ -119,6 +119,44 @@ bool medium_preferred(int scheme, int32_t N, int32_t P) {
     return false;
 }
 
+// one launch per batch: cluster-per-filter kernel (ancestors, offspring, permutation and the
+// state gather), no workspace except the permutation when the state is gathered without
+// permuted_out (pf_fused.cu).  logw64 non-null: the binary64 instantiation (NS-3d), P <= 65536.
+pf_status fused_branch(int scheme, const float* logw, const double* logw64, int64_t ld, int32_t N, int32_t P,
+                       uint64_t seed, uint32_t first_filter, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
+                       cudaStream_t s) {
+    double* lse = opts ? opts->lse_out : nullptr;
+    double* ess = opts ? opts->ess_out : nullptr;
+    float* normw = opts ? opts->normw_out : nullptr;
+    int32_t* status_out = opts ? opts->status_out : nullptr;
+    int32_t* offspring_out = opts ? opts->offspring_out : nullptr;
+    int32_t* permuted_out = opts ? opts->permuted_out : nullptr;
+    void* state = opts ? opts->state : nullptr;
+    const int64_t x_row = opts ? opts->state_row_bytes : 0, x_ld = opts ? opts->state_ld_bytes : 0;
+    const int64_t x_fld = opts ? opts->state_filter_ld_bytes : 0;
+    // The cluster kernel gathers the state itself when the batch spans the GPU; a batch of few
+    // filters (one cluster each) would copy its rows through a handful of SMs, so there the
+    // permutation is fused and the gather runs as its own full-GPU kernel.
+    const bool fuse_gather = state && pf::fused_gather_supported(state, x_row, x_ld, x_fld) &&
+                             static_cast<int64_t>(N) * pf::fused_cluster_ctas(P) >= pf::sm_count();
+    int32_t* perm = permuted_out;
+    void* fstate = fuse_gather ? state : nullptr;
+    if (state && !perm) {
+        void* p = nullptr;
+        const pf_status st = get_workspace(opts, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4, s, &p);
+        if (st != PF_OK) return st;
+        perm = static_cast<int32_t*>(p);
+    }
+    uint64_t nl = 0;
+    cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse, ess, normw,
+                                            status_out, offspring_out, perm, fstate, x_row, x_ld, x_fld, s, &nl,
+                                            logw64);
+    if (e == cudaSuccess && state && !fstate)
+        e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
 pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
                         cudaStream_t s) {
@@ -158,32 +196,8 @@ pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
-    // The cluster kernel gathers the state itself when the batch spans the GPU; a batch of few
-    // filters (one cluster each) would copy its rows through a handful of SMs, so there the
-    // permutation is fused and the gather runs as its own full-GPU kernel.
-    const bool fuse_gather = state && pf::fused_gather_supported(state, x_row, x_ld, x_fld) &&
-                             static_cast<int64_t>(N) * pf::fused_cluster_ctas(P) >= pf::sm_count();
-    if (!no_fusion && pf::fused_supported(scheme, N, P)) {
-        // one launch per batch: cluster-per-filter kernel (ancestors, offspring, permutation and
-        // the state gather), no workspace except the permutation when the state is gathered
-        // without permuted_out (pf_fused.cu)
-        int32_t* perm = permuted_out;
-        void* fstate = fuse_gather ? state : nullptr;
-        if (state && !perm) {
-            void* p = nullptr;
-            const pf_status st = get_workspace(opts, static_cast<size_t>(N) * static_cast<size_t>(ld_anc) * 4, s, &p);
-            if (st != PF_OK) return st;
-            perm = static_cast<int32_t*>(p);
-        }
-        uint64_t nl = 0;
-        cudaError_t e = pf::launch_fused_sorted(scheme, logw, ld, N, P, seed, first_filter, anc, ld_anc, lse, ess,
-                                                normw, status_out, offspring_out, perm, fstate, x_row, x_ld, x_fld,
-                                                s, &nl);
-        if (e == cudaSuccess && state && !fstate)
-            e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_anc, s, &nl);
-        g_launches += nl;
-        return cuda_status(e);
-    }
+    if (!no_fusion && pf::fused_supported(scheme, N, P))
+        return fused_branch(scheme, logw, nullptr, ld, N, P, seed, first_filter, anc, ld_anc, opts, s);
     if ((permuted_out || state) && !no_fusion && !normw && pf::coop_supported(scheme, N, P)) {
         // large filters, few of them: the cooperative kernel writes the permutation too (and gathers
         // the state when the rows allow it); scratch = [coop scratch + free list | offspring | perm]
@@ -361,6 +375,16 @@ pf_status resample_f64_impl(int scheme, const double* logw, int64_t ld, int32_t 
     if (opts && (opts->flags & ~static_cast<uint32_t>(PF_NO_FUSION | PF_SORTED | PF_SORT_WEIGHTS)) != 0)
         return PF_ERR_UNSUPPORTED;
     if (opts && (opts->flags & PF_SORTED) && scheme != PF_MULTINOMIAL) return PF_ERR_UNSUPPORTED;
+    const uint32_t fl = opts ? opts->flags : 0u;
+    void* state = opts ? opts->state : nullptr;
+    if (state && (opts->state_row_bytes < 1 || opts->state_ld_bytes < opts->state_row_bytes ||
+                  (N > 1 && opts->state_filter_ld_bytes < opts->state_ld_bytes * static_cast<int64_t>(P))))
+        return PF_ERR_INVALID_ARG;
+    // stratified / systematic batches of 4097..65536-particle filters: the cluster kernel reads the
+    // doubles itself (max, then t_i = fl32(logw_i - lmax) from a second, L2-resident read)
+    if (!(fl & (PF_NO_FUSION | PF_SORT_WEIGHTS)) && !g_no_fusion.load() &&
+        (scheme == PF_STRATIFIED || scheme == PF_SYSTEMATIC) && P > 4096 && P <= pf::kFusedF64MaxP)
+        return fused_branch(scheme, nullptr, logw, ld, N, P, seed, first_filter, anc, ld_anc, opts, s);
     void* ws = nullptr;
     pf_status st = pool_get(pf::f64_ws_bytes(N, P), s, &ws, 1);
     if (st != PF_OK) return st;

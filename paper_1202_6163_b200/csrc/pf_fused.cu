@@ -52,7 +52,6 @@ constexpr int kFI = 16;            // particles per thread
 constexpr int kFR = kFI / 4;       // 4 float4 rows
 constexpr int kPP = kFT * kFI;     // particles per CTA (max): 8192
 constexpr int kChunk = 256;        // slots per warp max-scan pass (8 per lane)
-constexpr int kTPL = kFR * kFW / 32;  // (row, warp) totals per lane in the phase-B scan
 constexpr int kXS = kFW * kChunk;   // slots (ranks) per CTA-wide expansion chunk: 8 per thread
 static_assert(kXS == 8 * kFT, "CTA-wide expansion assumes 8 slots per thread");
 static_assert(kFW <= 32, "the cross-warp max-scan reads one warp total per lane");
@@ -61,6 +60,7 @@ static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32
 struct Exchange {
     float m;
     int bad;
+    double m64;  // binary64 input (NS-3d): the CTA's max of the doubles
     uint64_t tot;
     double sw, sw2;
     uint64_t ptot;  // packed (extras << 31 | free) total of the CTA (phase D)
@@ -68,6 +68,7 @@ struct Exchange {
 
 struct FusedArgs {
     const float* logw;
+    const double* logw64;  // F64 instantiations: binary64 log-weights (NS-3d), same ld
     int64_t ld;
     int32_t N, P, CL, PP;
     uint64_t D;
@@ -255,7 +256,7 @@ __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32
 }
 
 // PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
-template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
 __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
     // geometry of this instantiation: FT threads x FI particles per thread (FT = 512, FI = 16:
     // 8192 particles per CTA, clusters of <= 8; FT = 1024, FI = 16: 16384 per CTA, clusters of
@@ -281,6 +282,8 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
     __shared__ __align__(16) int32_t s_buf[kFW][kChunk];
     __shared__ int32_t s_wmax[kFW];
     __shared__ float s_lmax;
+    __shared__ double s_lmax64;
+    __shared__ double s_m64[kFW];
     __shared__ int s_bad;
     __shared__ uint64_t s_off, s_tot, s_Qtot;
     __shared__ double s_S, s_S2;
@@ -304,58 +307,121 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
 
         // ---------------- A: load + max
         float v[kFI];
+        const double* row64 = F64 ? a.logw64 + static_cast<int64_t>(n) * a.ld + p0 : nullptr;
+        if (F64) {
+            // NS-3d: the max and the NaN / +inf flag on the doubles; the shifted float32 weights
+            // are formed in phase B from a second (L2) read of the same rows
+            double m = -INFINITY;
+            int bad = 0;
 #pragma unroll
-        for (int j = 0; j < kFR; ++j) {
-            const int i0 = j * (kFT * 4) + tid * 4;
-            if (a.vec && i0 + 3 < np) {
-                const float4 t = __ldcs(reinterpret_cast<const float4*>(row + i0));
-                v[j * 4 + 0] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
-            } else {
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                double x[4];
+                if (a.vec && i0 + 3 < np) {
+                    const double2 t0 = __ldcg(reinterpret_cast<const double2*>(row64 + i0));
+                    const double2 t1 = __ldcg(reinterpret_cast<const double2*>(row64 + i0 + 2));
+                    x[0] = t0.x; x[1] = t0.y; x[2] = t1.x; x[3] = t1.y;
+                } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v[j * 4 + q] = (i0 + q < np) ? __ldcs(row + i0 + q) : -INFINITY;
+                    for (int q = 0; q < 4; ++q) x[q] = (i0 + q < np) ? __ldcg(row64 + i0 + q) : -INFINITY;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    bad |= (isnan(x[q]) || x[q] == INFINITY) ? 1 : 0;
+                    m = fmax(m, x[q]);
+                }
             }
-        }
-        float m = -INFINITY;
-        int bad = 0;
-#pragma unroll
-        for (int t = 0; t < kFI; ++t) {
-            bad |= (isnan(v[t]) || v[t] == INFINITY) ? 1 : 0;
-            m = fmaxf(m, v[t]);  // fmaxf ignores NaN; +inf makes the filter invalid anyway
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-            bad |= __shfl_xor_sync(kFull, bad, o);
-        }
-        if (lane == 0) { s_f[warp] = m; s_i[warp] = bad; }
-        __syncthreads();
-        if (warp == 0) {
-            float mm = (lane < kFW) ? s_f[lane] : -INFINITY;
-            int bb = (lane < kFW) ? s_i[lane] : 0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
-                bb |= __shfl_xor_sync(kFull, bb, o);
+                m = fmax(m, __shfl_xor_sync(kFull, m, o));
+                bad |= __shfl_xor_sync(kFull, bad, o);
             }
-            if (lane == 0) { s_x.m = mm; s_x.bad = bb; }
+            if (lane == 0) { s_m64[warp] = m; s_i[warp] = bad; }
+            __syncthreads();
+            if (warp == 0) {
+                double mm = (lane < kFW) ? s_m64[lane] : -INFINITY;
+                int bb = (lane < kFW) ? s_i[lane] : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mm = fmax(mm, __shfl_xor_sync(kFull, mm, o));
+                    bb |= __shfl_xor_sync(kFull, bb, o);
+                }
+                if (lane == 0) { s_x.m64 = mm; s_x.bad = bb; }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                if (a.vec && i0 + 3 < np) {
+                    const float4 t = __ldcs(reinterpret_cast<const float4*>(row + i0));
+                    v[j * 4 + 0] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[j * 4 + q] = (i0 + q < np) ? __ldcs(row + i0 + q) : -INFINITY;
+                }
+            }
+            float m = -INFINITY;
+            int bad = 0;
+#pragma unroll
+            for (int t = 0; t < kFI; ++t) {
+                bad |= (isnan(v[t]) || v[t] == INFINITY) ? 1 : 0;
+                m = fmaxf(m, v[t]);  // fmaxf ignores NaN; +inf makes the filter invalid anyway
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+                bad |= __shfl_xor_sync(kFull, bad, o);
+            }
+            if (lane == 0) { s_f[warp] = m; s_i[warp] = bad; }
+            __syncthreads();
+            if (warp == 0) {
+                float mm = (lane < kFW) ? s_f[lane] : -INFINITY;
+                int bb = (lane < kFW) ? s_i[lane] : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+                    bb |= __shfl_xor_sync(kFull, bb, o);
+                }
+                if (lane == 0) { s_x.m = mm; s_x.bad = bb; }
+            }
         }
         cluster_sync_publish(warp == 0 && lane == 0);  // #1 (s_x.m, s_x.bad)
         if (warp == 0) {
-            float gm = -INFINITY;
-            int gb = 0;
-            if (lane < CL) {
-                const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
-                gm = rx->m;
-                gb = rx->bad;
-            }
+            if (F64) {
+                double gm = -INFINITY;
+                int gb = 0;
+                if (lane < CL) {
+                    const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
+                    gm = rx->m64;
+                    gb = rx->bad;
+                }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
-                gb |= __shfl_xor_sync(kFull, gb, o);
-            }
-            if (lane == 0) {
-                s_lmax = gm;
-                s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+                for (int o = 16; o > 0; o >>= 1) {
+                    gm = fmax(gm, __shfl_xor_sync(kFull, gm, o));
+                    gb |= __shfl_xor_sync(kFull, gb, o);
+                }
+                if (lane == 0) {
+                    s_lmax64 = gm;
+                    s_lmax = 0.0f;  // the shifted weights' maximum is exactly 0 (NS-3d)
+                    s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+                }
+            } else {
+                float gm = -INFINITY;
+                int gb = 0;
+                if (lane < CL) {
+                    const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
+                    gm = rx->m;
+                    gb = rx->bad;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
+                    gb |= __shfl_xor_sync(kFull, gb, o);
+                }
+                if (lane == 0) {
+                    s_lmax = gm;
+                    s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+                }
             }
         }
         __syncthreads();
@@ -379,12 +445,33 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             continue;
         }
         const float lm = s_lmax;
+        if (F64) {
+            // NS-3d: t_i = fl32(logw_i - lmax) (binary64 subtraction, one rounding); padding -inf
+            const double lm64 = s_lmax64;
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                double x[4];
+                if (a.vec && i0 + 3 < np) {
+                    const double2 t0 = __ldcg(reinterpret_cast<const double2*>(row64 + i0));
+                    const double2 t1 = __ldcg(reinterpret_cast<const double2*>(row64 + i0 + 2));
+                    x[0] = t0.x; x[1] = t0.y; x[2] = t1.x; x[3] = t1.y;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) x[q] = (i0 + q < np) ? __ldcg(row64 + i0 + q) : -INFINITY;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[j * 4 + q] = __double2float_rn(__dsub_rn(x[q], lm64));
+            }
+        }
 #if PF_PREFETCH_NEXT
         // the next filter's log-weights of this CTA into L2 (one bulk prefetch), so its phase A
         // loads come from L2 instead of HBM
         if (tid == 0 && n + num_clusters < a.N && a.vec && (np & 3) == 0 && np > 0) {
-            const float* nrow = a.logw + static_cast<int64_t>(n + num_clusters) * a.ld + p0;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nrow), "r"(static_cast<uint32_t>(np) * 4u)
+            const int64_t off = static_cast<int64_t>(n + num_clusters) * a.ld + p0;
+            const void* nrow = F64 ? static_cast<const void*>(a.logw64 + off) : static_cast<const void*>(a.logw + off);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nrow),
+                         "r"(static_cast<uint32_t>(np) * (F64 ? 8u : 4u))
                          : "memory");
         }
 #endif
@@ -496,7 +583,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         z.A = s_zA;
         z.Bc = s_zBc;
         if (c == 0 && tid == 0) {
-            if (a.lse_out) a.lse_out[n] = static_cast<double>(lm) + log(s_S);
+            if (a.lse_out) a.lse_out[n] = (F64 ? s_lmax64 : static_cast<double>(lm)) + log(s_S);
             if (a.ess_out) a.ess_out[n] = s_S * s_S / s_S2;
             if (a.status_out) a.status_out[n] = 0;
         }
@@ -1713,12 +1800,12 @@ constexpr size_t fused_smem(int perm) {
     return perm ? static_cast<size_t>(FT * FI + (perm == 2 ? (FT / 32) * kChunk : 0)) * sizeof(int32_t) : 0;
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
 void fused_set_attributes() {
     // per-device function attributes: set once per device
     static std::atomic<int> attr_set[kMaxDevices];
     cached_per_device(attr_set, [] {
-        auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>;
+        auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT, FI, F64>;
         if (PERM)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(fused_smem<FT, FI>(PERM)));
@@ -1728,13 +1815,13 @@ void fused_set_attributes() {
     });
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
 int fused_max_clusters(int CL) {
     // occupancy of (kernel, cluster size) is a device constant: query once (host cost ~us);
     // -1 = a cluster of this size cannot be scheduled on this device (0 = not queried yet)
     static std::atomic<int> cached[kMaxCL + 1][kMaxDevices];
     return cached_per_device(cached[CL], [&] {
-        fused_set_attributes<SCHEME, SUMS, PERM, FT, FI>();
+        fused_set_attributes<SCHEME, SUMS, PERM, FT, FI, F64>();
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1747,7 +1834,7 @@ int fused_max_clusters(int CL) {
         cfg.numAttrs = 1;
         cfg.gridDim = dim3(CL, 1, 1);
         int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>, &cfg) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveClusters(&mc, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI, F64>, &cfg) != cudaSuccess ||
             mc < 1) {
             cudaGetLastError();
             mc = -1;
@@ -1756,10 +1843,10 @@ int fused_max_clusters(int CL) {
     });
 }
 
-template <int SCHEME, bool SUMS, int PERM, int FT, int FI>
+template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
 cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
-    fused_set_attributes<SCHEME, SUMS, PERM, FT, FI>();
-    const int max_clusters = fused_max_clusters<SCHEME, SUMS, PERM, FT, FI>(a.CL);
+    fused_set_attributes<SCHEME, SUMS, PERM, FT, FI, F64>();
+    const int max_clusters = fused_max_clusters<SCHEME, SUMS, PERM, FT, FI, F64>(a.CL);
     if (max_clusters < 1) return cudaErrorNotSupported;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1774,19 +1861,23 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     const int clusters = std::max(1, std::min(a.N, max_clusters));
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * a.CL), 1, 1);
-    return cudaLaunchKernelEx(&cfg, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI>, a);
+    return cudaLaunchKernelEx(&cfg, k_fused_sorted<SCHEME, SUMS, PERM, FT, FI, F64>, a);
 }
 
-template <int FT, int FI>
+template <int FT, int FI, bool F64 = false>
 cudaError_t launch_fused_ft(int scheme, int pm, const FusedArgs& a, cudaStream_t s) {
     if (scheme == 2) {
-        if (pm == 2) return a.sums ? launch_fused_t<2, true, 2, FT, FI>(a, s) : launch_fused_t<2, false, 2, FT, FI>(a, s);
-        if (pm == 1) return a.sums ? launch_fused_t<2, true, 1, FT, FI>(a, s) : launch_fused_t<2, false, 1, FT, FI>(a, s);
-        return a.sums ? launch_fused_t<2, true, 0, FT, FI>(a, s) : launch_fused_t<2, false, 0, FT, FI>(a, s);
+        if (pm == 2)
+            return a.sums ? launch_fused_t<2, true, 2, FT, FI, F64>(a, s) : launch_fused_t<2, false, 2, FT, FI, F64>(a, s);
+        if (pm == 1)
+            return a.sums ? launch_fused_t<2, true, 1, FT, FI, F64>(a, s) : launch_fused_t<2, false, 1, FT, FI, F64>(a, s);
+        return a.sums ? launch_fused_t<2, true, 0, FT, FI, F64>(a, s) : launch_fused_t<2, false, 0, FT, FI, F64>(a, s);
     }
-    if (pm == 2) return a.sums ? launch_fused_t<3, true, 2, FT, FI>(a, s) : launch_fused_t<3, false, 2, FT, FI>(a, s);
-    if (pm == 1) return a.sums ? launch_fused_t<3, true, 1, FT, FI>(a, s) : launch_fused_t<3, false, 1, FT, FI>(a, s);
-    return a.sums ? launch_fused_t<3, true, 0, FT, FI>(a, s) : launch_fused_t<3, false, 0, FT, FI>(a, s);
+    if (pm == 2)
+        return a.sums ? launch_fused_t<3, true, 2, FT, FI, F64>(a, s) : launch_fused_t<3, false, 2, FT, FI, F64>(a, s);
+    if (pm == 1)
+        return a.sums ? launch_fused_t<3, true, 1, FT, FI, F64>(a, s) : launch_fused_t<3, false, 1, FT, FI, F64>(a, s);
+    return a.sums ? launch_fused_t<3, true, 0, FT, FI, F64>(a, s) : launch_fused_t<3, false, 0, FT, FI, F64>(a, s);
 }
 
 // can a 16-CTA cluster of 1024-thread CTAs be scheduled (one per GPC)?  cached per device
@@ -2035,9 +2126,10 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
                                 int32_t* permuted, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
-                                cudaStream_t s, uint64_t* launches) {
+                                cudaStream_t s, uint64_t* launches, const double* logw64) {
     FusedArgs a{};
     a.logw = logw;
+    a.logw64 = logw64;
     a.ld = ld;
     a.N = N;
     a.P = P;
@@ -2052,7 +2144,8 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.key = make_key(seed);
     a.filt0 = first_filter;
     a.kfx = 61 - m;
-    a.vec = ((reinterpret_cast<uintptr_t>(logw) & 15) == 0 && ld % 4 == 0) ? 1 : 0;
+    a.vec = logw64 ? (((reinterpret_cast<uintptr_t>(logw64) & 15) == 0 && ld % 2 == 0) ? 1 : 0)
+                   : (((reinterpret_cast<uintptr_t>(logw) & 15) == 0 && ld % 4 == 0) ? 1 : 0);
     a.sums = (lse_out || ess_out || normw) ? 1 : 0;
     a.anc = anc;
     a.ld_anc = ld_anc;
@@ -2071,7 +2164,12 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     ProfScope ps_("k_fused_sorted", s);
     cudaError_t e;
     const int pm = a.X ? 2 : (a.perm ? 1 : 0);
-    e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
+    if (logw64) {
+        if (FT != 512) return cudaErrorNotSupported;  // binary64 fused for P <= 65536 only (f64_fused_supported)
+        e = launch_fused_ft<512, 16, true>(scheme, pm, a, s);
+    } else {
+        e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
+    }
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

@@ -157,7 +157,7 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
                                 int32_t* permuted, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
-                                cudaStream_t s, uint64_t* launches);
+                                cudaStream_t s, uint64_t* launches, const double* logw64 = nullptr);
 
 // One-warp-per-filter kernel for P <= 256, every scheme (pf_fused.cu).
 bool small_supported(int32_t P);
@@ -200,6 +200,7 @@ cudaError_t launch_mig_unpack(void* X, int64_t row_bytes, int64_t ld, int32_t Pl
 // pf_f64.cu: binary64 log-weights (NS-3d).  ws holds f64_ws_bytes(N, P): t [N][ldt] float
 // (ldt = P rounded up to 4), then the per-filter max keys (u64) and bad flags (i32).
 size_t f64_ws_bytes(int32_t N, int32_t P);
+constexpr int32_t kFusedF64MaxP = 65536;  // binary64 instantiation of the cluster kernel: 8 x 8192
 cudaError_t launch_shift64(const double* logw, int64_t ld, int32_t N, int32_t P, void* ws, float** t_out,
                            int64_t* ldt_out, unsigned long long** key_out, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_lse64(const unsigned long long* key, int32_t N, double* lse, cudaStream_t s,

@@ -129,12 +129,13 @@ def test_f64_batched_paths(pf, dev, orc, scheme, fusion):
 @pytest.mark.parametrize("scheme", ["systematic", "stratified", "multinomial"])
 def test_f64_permutation_and_state(pf, dev, orc, scheme):
     """offspring_out, permuted_out and the fused in-place state gather with binary64 weights
-    (the cluster kernel's batch, the cooperative kernel's single large filter, the
+    (the pre-pass + cluster kernel at P = 4096, the binary64 cluster kernel itself at 8192 and
+    65536 (gather fused / separate), the cooperative kernel's single large filter, the
     multi-launch path for multinomial)."""
     import torch
 
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    for N, P in ((2 * sms, 4096), (1, 300000)):
+    for N, P in ((2 * sms, 4096), (2 * sms, 8192), (5, 65536), (1, 300000)):
         x = pfinputs.gaussian_logw_f64(P, 1.0, offset=-1e7, seed=N, N=N)
         X = np.stack([pfinputs.state_matrix(P, 16, seed=n) for n in range(N)])
         gX = _gpu(X, dev)
