@@ -276,6 +276,20 @@ pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, in
     if (st != PF_OK) return st;
     const pf::Ws ws = pf::carve(base, L);
     uint64_t nl = 0;
+    if (!no_fusion && scheme == PF_MULTINOMIAL && !sorted_multi && pf::buckets_fused_supported(P)) {
+        // one cluster-kernel launch writes Q, the totals, the status, the side outputs and the
+        // bucket index (the rho = 0 systematic positions); then the per-slot searches
+        cudaError_t e = pf::launch_fused_sorted(pf::kFusedBuckets, logw, ld, N, P, seed, first_filter, ws.bidx, L.ldb,
+                                                lse, ess, normw, ws.fstatus, nullptr, nullptr, nullptr, 0, 0, 0, s, &nl,
+                                                nullptr, ws.Q, L.ldq, ws.Qtot);
+        if (e == cudaSuccess) e = pf::launch_bsearch_buckets(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl);
+        if (e == cudaSuccess && status_out)
+            e = cudaMemcpyAsync(status_out, ws.fstatus, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s);
+        if (offspring_out && e == cudaSuccess)
+            e = pf::launch_offspring(anc, ld_anc, N, P, offspring_out, ld_anc, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
     if (sorted_multi && e == cudaSuccess)  // spacings do not depend on the weights: first
         e = pf::launch_sorted_multinomial(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl, true);

@@ -66,8 +66,16 @@ struct Exchange {
     uint64_t ptot;  // packed (extras << 31 | free) total of the CTA (phase D)
 };
 
+// SCHEME value of the cluster kernel's multinomial bucket mode: the systematic machinery with
+// rho = 0 (positions b 2^64 / P, P a power of two) gives the bucket index of the multinomial
+// search, idx[b] = min{i : Q_i > floor(b Q / P)} (pf_kernels.cu ModeBuckets), and Q is written
+constexpr int kBuckets = 5;
+
 struct FusedArgs {
     const float* logw;
+    uint64_t* Qout;      // kBuckets: Q [N][ldq] and the filter totals
+    int64_t ldq;
+    uint64_t* Qtot_out;
     const double* logw64;  // F64 instantiations: binary64 log-weights (NS-3d), same ld
     int64_t ld;
     int32_t N, P, CL, PP;
@@ -610,10 +618,31 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         uint32_t E[kFI];
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
-            count_row<SCHEME>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
+            count_row<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
+            if (SCHEME == kBuckets) {
+                // the multinomial's search structure: Q_i of every particle (u64, 2 x 16-byte stores)
+                uint64_t r = O + s_wt[j][warp] + ex[j];
+                uint64_t q4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    r += quantise(v[j * 4 + q], a.kfx);
+                    q4[q] = r;
+                }
+                const int i0 = j * (kFT * 4) + tid * 4;
+                uint64_t* qrow = a.Qout + static_cast<int64_t>(n) * a.ldq + p0 + i0;
+                if (i0 + 3 < np) {
+                    reinterpret_cast<ulonglong2*>(qrow)[0] = make_ulonglong2(q4[0], q4[1]);
+                    reinterpret_cast<ulonglong2*>(qrow)[1] = make_ulonglong2(q4[2], q4[3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (i0 + q < np) qrow[q] = q4[q];
+                }
+            }
             if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
         }
-        if (tid == 0) s_klo = count_below<SCHEME>(z, O);
+        if (tid == 0) s_klo = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O);
+        if (SCHEME == kBuckets && c == 0 && tid == 0) a.Qtot_out[n] = z.Qtot;
         __syncthreads();
         const uint32_t k_lo = s_klo;
         // E_{i-1} of the first particle of each 4-chunk (natural order: row j, warp, lane, q);
@@ -1866,6 +1895,10 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
 
 template <int FT, int FI, bool F64 = false>
 cudaError_t launch_fused_ft(int scheme, int pm, const FusedArgs& a, cudaStream_t s) {
+    if constexpr (FT == 512 && !F64) {
+        if (scheme == kBuckets)
+            return a.sums ? launch_fused_t<kBuckets, true, 0, FT, FI>(a, s) : launch_fused_t<kBuckets, false, 0, FT, FI>(a, s);
+    }
     if (scheme == 2) {
         if (pm == 2)
             return a.sums ? launch_fused_t<2, true, 2, FT, FI, F64>(a, s) : launch_fused_t<2, false, 2, FT, FI, F64>(a, s);
@@ -2115,6 +2148,11 @@ int fused_cluster_ctas(int32_t P) {
 // P <= 65536: any batch.  65536 < P <= 262144 (clusters of 5..16 CTAs of 1024 threads): only
 // batches that span the GPU; a single big cluster per filter runs on <= 16 SMs, where the
 // cooperative kernel uses all of them (C4: 55.7 vs 62.6 us per PF step).
+// multinomial: the bucket index + Q from one cluster-kernel launch (kBuckets), then the per-slot
+// searches; P a power of two (the buckets are then the rho = 0 systematic positions) above the
+// sizes the CTA-per-filter kernel takes
+bool buckets_fused_supported(int32_t P) { return P > 4096 && P <= 8 * 512 * kFI && (P & (P - 1)) == 0; }
+
 bool fused_supported(int scheme, int32_t N, int32_t P) {
     if (!(scheme == 2 || scheme == 3) || P < 1) return false;
     if (P <= 8 * 512 * kFI) return true;
@@ -2126,10 +2164,14 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
                                 int32_t* permuted, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
-                                cudaStream_t s, uint64_t* launches, const double* logw64) {
+                                cudaStream_t s, uint64_t* launches, const double* logw64, uint64_t* Qout,
+                                int64_t ldq, uint64_t* Qtot_out) {
     FusedArgs a{};
     a.logw = logw;
     a.logw64 = logw64;
+    a.Qout = Qout;
+    a.ldq = ldq;
+    a.Qtot_out = Qtot_out;
     a.ld = ld;
     a.N = N;
     a.P = P;

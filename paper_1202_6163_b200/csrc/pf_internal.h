@@ -157,7 +157,14 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
                                 uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                 double* ess_out, float* normw, int32_t* status_out, int32_t* offspring,
                                 int32_t* permuted, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
-                                cudaStream_t s, uint64_t* launches, const double* logw64 = nullptr);
+                                cudaStream_t s, uint64_t* launches, const double* logw64 = nullptr,
+                                uint64_t* Qout = nullptr, int64_t ldq = 0, uint64_t* Qtot_out = nullptr);
+// scheme id of launch_fused_sorted's multinomial bucket mode (Q + bucket index, pf_fused.cu)
+constexpr int kFusedBuckets = 5;
+bool buckets_fused_supported(int32_t P);
+cudaError_t launch_bsearch_buckets(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                                   uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                                   uint64_t* launches);
 
 // One-warp-per-filter kernel for P <= 256, every scheme (pf_fused.cu).
 bool small_supported(int32_t P);

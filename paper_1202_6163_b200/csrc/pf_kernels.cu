@@ -1935,6 +1935,21 @@ static uint64_t stratum_width(int32_t P) {
     return UINT64_MAX / static_cast<uint64_t>(P);
 }
 
+// the multinomial's per-slot searches against Q and the bucket index (ws.Q, ws.bidx, ws.Qtot,
+// ws.fstatus written by k_merge<ModeBuckets> after the scan, or by the cluster kernel's bucket mode)
+cudaError_t launch_bsearch_buckets(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
+                                   uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
+                                   uint64_t* launches) {
+    const int lgNB = ceil_log2(P);
+    {
+        ProfScope ps_("k_bsearch", s);
+        k_bsearch_buckets<<<static_cast<unsigned>(grid_for(static_cast<int64_t>(N) * cdiv(P, 8), 8)), kThreads, 0,
+                            s>>>(N, P, ws, L.ldq, L.ldb, lgNB, make_key(seed), first_filter, anc, ld_anc);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
 cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,
                           uint32_t first_filter, int32_t* anc, int64_t ld_anc, cudaStream_t s,
                           uint64_t* launches) {
@@ -1951,11 +1966,7 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
                                                                                                         chunk);
         }
         ++*launches;
-        {
-            ProfScope ps_("k_bsearch", s);
-            k_bsearch_buckets<<<static_cast<unsigned>(grid_for(static_cast<int64_t>(N) * cdiv(P, 8), 8)), kThreads, 0,
-                                s>>>(N, P, ws, L.ldq, L.ldb, lgNB, key, first_filter, anc, ld_anc);
-        }
+        return launch_bsearch_buckets(N, P, L, ws, seed, first_filter, anc, ld_anc, s, launches);
     } else {
         const int64_t chunk = merge_chunk(N, P);
         const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
