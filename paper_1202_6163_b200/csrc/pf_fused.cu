@@ -67,14 +67,16 @@ struct Exchange {
 };
 
 // SCHEME value of the cluster kernel's multinomial bucket mode: the systematic machinery with
-// rho = 0 (positions b 2^64 / P, P a power of two) gives the bucket index of the multinomial
-// search, idx[b] = min{i : Q_i > floor(b Q / P)} (pf_kernels.cu ModeBuckets), and Q is written
+// rho = 0 over NB = 2^ceil(log2 P) slots at b 2^(64 - m) gives the bucket index of the
+// multinomial search, idx[b] = min{i : Q_i > floor(b Q / NB)} (pf_kernels.cu ModeBuckets), and
+// Q is written
 constexpr int kBuckets = 5;
 
 struct FusedArgs {
     const float* logw;
     uint64_t* Qout;      // kBuckets: Q [N][ldq] and the filter totals
     int64_t ldq;
+    int32_t S;           // kBuckets: bucket count NB = 2^ceil(log2 P) (the slots of the expansion)
     uint64_t* Qtot_out;
     const double* logw64;  // F64 instantiations: binary64 log-weights (NS-3d), same ld
     int64_t ld;
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         z.Qtot = s_Qtot;
         z.key = a.key;
         z.filt = filt;
-        z.P = a.P;
+        z.P = (SCHEME == kBuckets) ? a.S : a.P;  // slots: the P resampled particles, or the NB buckets
         z.rho = s_rho;
         z.A = s_zA;
         z.Bc = s_zBc;
@@ -2148,10 +2150,10 @@ int fused_cluster_ctas(int32_t P) {
 // P <= 65536: any batch.  65536 < P <= 262144 (clusters of 5..16 CTAs of 1024 threads): only
 // batches that span the GPU; a single big cluster per filter runs on <= 16 SMs, where the
 // cooperative kernel uses all of them (C4: 55.7 vs 62.6 us per PF step).
-// multinomial: the bucket index + Q from one cluster-kernel launch (kBuckets), then the per-slot
-// searches; P a power of two (the buckets are then the rho = 0 systematic positions) above the
-// sizes the CTA-per-filter kernel takes
-bool buckets_fused_supported(int32_t P) { return P > 4096 && P <= 8 * 512 * kFI && (P & (P - 1)) == 0; }
+// multinomial: the bucket index + Q from one cluster-kernel launch (kBuckets: the rho = 0
+// systematic machinery over NB = 2^ceil(log2 P) slots of width 2^(64 - m)), then the per-slot
+// searches; above the sizes the CTA-per-filter kernel takes
+bool buckets_fused_supported(int32_t P) { return P > 4096 && P <= 8 * 512 * kFI; }
 
 bool fused_supported(int scheme, int32_t N, int32_t P) {
     if (!(scheme == 2 || scheme == 3) || P < 1) return false;
@@ -2183,6 +2185,12 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.PP = static_cast<int32_t>(pp);
     const int m = ceil_log2(P);
     a.D = (P <= 1) ? 0 : (((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P)));
+    a.S = P;
+    if (scheme == kBuckets) {
+        // NB = 2^m equal buckets of the 64-bit uniform: positions b 2^(64-m) (ModeBuckets)
+        a.S = 1 << m;
+        a.D = uint64_t{1} << (64 - m);
+    }
     a.key = make_key(seed);
     a.filt0 = first_filter;
     a.kfx = 61 - m;

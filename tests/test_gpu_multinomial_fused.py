@@ -1,6 +1,6 @@
 """GPU parity of the multinomial's one-launch search structure (the cluster kernel's bucket
 mode: Q, totals, status, side outputs and the bucket index in one launch, then the per-slot
-searches) against the oracle, for power-of-two filters of 8192..65536 particles: batches with
+searches) against the oracle, for filters of 4097..65536 particles (power-of-two and not): batches with
 invalid filters, -inf runs, side outputs, status, offspring and an explicit workspace; the
 multi-launch path (PF_NO_FUSION) gives the same ancestors."""
 from __future__ import annotations
@@ -36,7 +36,8 @@ def dev():
     return torch.device("cuda:0")
 
 
-@pytest.mark.parametrize("N,P", [(1, 8192), (40, 16384), (300, 8192), (7, 65536), (1, 65536)])
+@pytest.mark.parametrize("N,P", [(1, 8192), (40, 16384), (300, 8192), (7, 65536), (1, 65536), (1, 4097),
+                                 (20, 12289), (9, 50001), (200, 40000)])
 def test_multinomial_bucket_mode(pf, dev, orc, N, P):
     import torch
 
