@@ -290,6 +290,24 @@ pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, in
         g_launches += nl;
         return cuda_status(e);
     }
+    if (!no_fusion && scheme == PF_MULTINOMIAL && !sorted_multi && !normw && !(opts && opts->workspace) &&
+        pf::coop_supported(PF_SYSTEMATIC, N, P)) {
+        // large filters, few of them: the cooperative kernel's bucket mode (Q, totals, status, lse /
+        // ESS and the bucket index in one launch), then the per-slot searches
+        void* sc = nullptr;
+        pf_status st2 = pool_get(pf::coop_scratch_bytes(P), s, &sc, 3);
+        if (st2 != PF_OK) return st2;
+        cudaError_t e = pf::launch_coop_sorted(pf::kFusedBuckets, logw, ld, N, P, seed, first_filter, ws.bidx, L.ldb,
+                                               lse, ess, ws.fstatus, nullptr, nullptr, nullptr, 0, 0, 0, sc, s, &nl,
+                                               ws.Q, L.ldq, ws.Qtot);
+        if (e == cudaSuccess) e = pf::launch_bsearch_buckets(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl);
+        if (e == cudaSuccess && status_out)
+            e = cudaMemcpyAsync(status_out, ws.fstatus, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s);
+        if (offspring_out && e == cudaSuccess)
+            e = pf::launch_offspring(anc, ld_anc, N, P, offspring_out, ld_anc, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
     if (sorted_multi && e == cudaSuccess)  // spacings do not depend on the weights: first
         e = pf::launch_sorted_multinomial(N, P, L, ws, seed, first_filter, anc, ld_anc, s, &nl, true);

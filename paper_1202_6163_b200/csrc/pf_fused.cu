@@ -899,6 +899,10 @@ struct CoopArgs {
     int32_t* off;  // offspring out (row stride ld_anc), nullable (required with PERM)
     int32_t* perm;  // canonical permutation out (row stride ld_anc), PERM
     int32_t* freelist;  // scratch [P]: the filter's free slots in rank order (PERM)
+    uint64_t* Qout;     // kBuckets: Q [N][ldq], the totals, and the bucket count S
+    int64_t ldq;
+    uint64_t* Qtot_out;
+    int32_t S;
     uint64_t* g_ptot;   // scratch [G]: packed (extras, free) totals of the chunks (PERM)
     // scratch (device): [G] per-CTA values
     float* g_max;
@@ -1129,6 +1133,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     if (a.ess_out) a.ess_out[n] = S * S / S2;
                 }
                 if (c == 0 && a.status_out) a.status_out[n] = 0;
+                if (SCHEME == kBuckets && c == 0) a.Qtot_out[n] = all;
             }
         }
         __syncthreads();
@@ -1137,12 +1142,12 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         z.Qtot = s_u64[1];
         z.key = a.key;
         z.filt = filt;
-        z.P = a.P;
+        z.P = (SCHEME == kBuckets) ? a.S : a.P;  // slots: the particles, or the NB buckets
         z.rho = s_crho;
         z.A = s_cA;
         z.Bc = s_cBc;
         uint64_t carry = s_u64[0];
-        if (tid == 0) s_prevE = count_below<SCHEME>(z, carry);
+        if (tid == 0) s_prevE = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, carry);
         // ---------------- C: sub-tiles in order
         for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
             float v[kFI];
@@ -1196,7 +1201,28 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             uint32_t E[kFI];
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
-                count_row<SCHEME>(z, carry + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
+                count_row<(SCHEME == kBuckets ? 3 : SCHEME)>(z, carry + s_wt[j][warp] + ex[j], v + j * 4, a.kfx,
+                                                             E + j * 4);
+                if (SCHEME == kBuckets) {
+                    // the multinomial's search structure: Q_i of every particle of the sub-tile
+                    uint64_t r = carry + s_wt[j][warp] + ex[j];
+                    const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
+                    uint64_t* qrow = a.Qout + static_cast<int64_t>(n) * a.ldq + i0;
+                    uint64_t q4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        r += quantise(v[j * 4 + q], a.kfx);
+                        q4[q] = r;
+                    }
+                    if (i0 + 3 < c1) {
+                        reinterpret_cast<ulonglong2*>(qrow)[0] = make_ulonglong2(q4[0], q4[1]);
+                        reinterpret_cast<ulonglong2*>(qrow)[1] = make_ulonglong2(q4[2], q4[3]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (i0 + q < c1) qrow[q] = q4[q];
+                    }
+                }
                 if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
             }
             __syncthreads();
@@ -1989,6 +2015,10 @@ cudaError_t launch_coop_t(CoopArgs& a, cudaStream_t s) {
 
 template <int PERM>
 cudaError_t launch_coop_p(int scheme, bool sums, CoopArgs& a, cudaStream_t s) {
+    if constexpr (PERM == 0) {
+        if (scheme == kBuckets)
+            return sums ? launch_coop_t<kBuckets, true, 0>(a, s) : launch_coop_t<kBuckets, false, 0>(a, s);
+    }
     if (scheme == 2) return sums ? launch_coop_t<2, true, PERM>(a, s) : launch_coop_t<2, false, PERM>(a, s);
     return sums ? launch_coop_t<3, true, PERM>(a, s) : launch_coop_t<3, false, PERM>(a, s);
 }
@@ -1997,7 +2027,7 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
                                uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                double* ess_out, int32_t* status_out, int32_t* offspring, int32_t* permuted,
                                void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld, void* scratch,
-                               cudaStream_t s, uint64_t* launches) {
+                               cudaStream_t s, uint64_t* launches, uint64_t* Qout, int64_t ldq, uint64_t* Qtot_out) {
     CoopArgs a{};
     const bool sums = lse_out || ess_out;
     a.logw = logw;
@@ -2006,6 +2036,14 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     a.P = P;
     const int m = ceil_log2(P);
     a.D = ((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P));
+    a.S = P;
+    a.Qout = Qout;
+    a.ldq = ldq;
+    a.Qtot_out = Qtot_out;
+    if (scheme == kBuckets) {  // NB = 2^m bucket boundaries b 2^(64-m) as the slots (ModeBuckets)
+        a.S = 1 << m;
+        a.D = uint64_t{1} << (64 - m);
+    }
     a.key = make_key(seed);
     a.filt0 = first_filter;
     a.kfx = 61 - m;

@@ -189,7 +189,8 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
                                uint32_t first_filter, int32_t* anc, int64_t ld_anc, double* lse_out,
                                double* ess_out, int32_t* status_out, int32_t* offspring, int32_t* permuted,
                                void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld, void* scratch,
-                               cudaStream_t s, uint64_t* launches);
+                               cudaStream_t s, uint64_t* launches, uint64_t* Qout = nullptr, int64_t ldq = 0,
+                               uint64_t* Qtot_out = nullptr);
 
 // Cross-GPU particle migration of a sharded filter (pf_migrate.cu; include/pf.h 4a-4d).
 size_t mig_plan_bytes(int32_t Pl);  // the tiles' prefixes of extras / free slots

@@ -69,3 +69,36 @@ def test_multinomial_bucket_mode(pf, dev, orc, N, P):
             assert np.all(np.abs(v[n] - wv) <= 1e-6 * np.maximum(np.abs(wv), 1e-30))
         else:
             assert math.isnan(lse[n])
+
+
+@pytest.mark.parametrize("P", [65537, 1 << 18, (1 << 20) + 3, 1 << 22])
+def test_multinomial_cooperative_bucket_mode(pf, dev, orc, P):
+    """Single large filters: the cooperative kernel's bucket mode (Q, totals, status, lse / ESS
+    and the bucket index in one launch) + the per-slot searches; an all -inf filter and a NaN."""
+    import torch
+
+    for case in ("ok", "neg_inf", "nan"):
+        x = pfinputs.with_neg_inf_runs(pfinputs.gaussian_logw(P, 2.0, seed=P))
+        if case == "neg_inf":
+            x[:] = -np.inf
+        elif case == "nan":
+            x[P // 3] = np.nan
+        g = torch.from_numpy(x).to(dev)
+        st = torch.empty(1, dtype=torch.int32, device=dev)
+        lse = torch.empty(1, dtype=torch.float64, device=dev)
+        ess = torch.empty(1, dtype=torch.float64, device=dev)
+        off = torch.empty(P, dtype=torch.int32, device=dev)
+        a = pf.pf_resample_ex("multinomial", g, 5, filter_index=9, status_out=st, lse_out=lse, ess_out=ess,
+                              offspring_out=off)
+        a2 = pf.pf_resample_ex("multinomial", g, 5, filter_index=9, flags=pf.PF_NO_FUSION)
+        torch.cuda.synchronize()
+        wst, want, wlse, _, wess = orc.resample("multinomial", x, 5, filter_index=9, side=True)
+        assert int(st.item()) == wst
+        assert np.array_equal(a.cpu().numpy(), want), (P, case)
+        assert np.array_equal(a2.cpu().numpy(), want)
+        assert np.array_equal(off.cpu().numpy(), orc.ancestors_to_offspring(want))
+        if wst == 0:
+            assert abs(lse.item() - wlse) <= 1e-6 * max(1.0, abs(wlse))
+            assert abs(ess.item() - wess) <= 1e-6 * wess
+        else:
+            assert math.isnan(lse.item())
