@@ -167,3 +167,19 @@ def test_f64_argument_errors(pf, dev):
     assert lib.pf_resample_batched_f64(3, x.data_ptr(), 4, 2, 8, 1, 0, 0, a.data_ptr(), 8, None,
                                        None) == 1
     assert pf.pf_launch_count() == n0
+
+
+@pytest.mark.parametrize("scheme", ["systematic", "stratified", "multinomial"])
+def test_f64_bench_size_sampled(pf, dev, orc, scheme):
+    """The bench's binary64 extras at full C3 size (1024 filters x 2^16, offset -1e7, the
+    binary64 cluster kernel for systematic / stratified, the pre-pass + bucket mode for
+    multinomial): sampled filters against the oracle."""
+    import torch
+
+    N, P = 1024, 1 << 16
+    x = pfinputs.gaussian_logw_torch(P, 1.0, 77, N, dev).double() - 1e7
+    a = pf.pf_resample_batched(scheme, x, 2026, first_filter=5)
+    torch.cuda.synchronize()
+    for n in (0, 511, 1023):
+        xn = x[n].cpu().numpy()
+        assert np.array_equal(a[n].cpu().numpy(), orc.resample_f64(scheme, xn, 2026, filter_index=5 + n)[1]), n
