@@ -170,8 +170,11 @@ pf_status pf_resample_batched(pf_scheme scheme, const float* logw, int64_t ld_lo
  * = lmax + ln sum_i w_i keeps the binary64 maximum.  Use it when the log-weights carry a
  * large common offset (an accumulated log-likelihood) that float32 would round away.  The
  * shifted weights (4 B per particle + 12 B per filter) always come from the library pool
- * (pf_opts.workspace, when given, serves the float path only).  Two extra launches (max,
- * shift) before the float path, one after it when lse_out is set.
+ * (pf_opts.workspace, when given, serves the float path only).  Stratified / systematic
+ * filters of 4097..65536 particles (no PF_NO_FUSION / PF_SORT_WEIGHTS) run in one launch of
+ * the cluster kernel's binary64 instantiation, which reads the doubles itself; every other
+ * call takes two extra launches (max, shift) before the float path and one after it when
+ * lse_out is set.  Results are identical either way.
  */
 pf_status pf_resample_ex_f64(pf_scheme scheme, const double* logw, int32_t P, uint64_t seed, int32_t B,
                              int32_t* ancestors, const pf_opts* opts, pf_stream_t stream);
