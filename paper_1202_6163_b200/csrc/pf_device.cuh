@@ -206,6 +206,31 @@ __device__ __forceinline__ uint64_t spacing_from_word(uint32_t r) {
     return static_cast<uint64_t>(__dmul_rn(E, 16777216.0)) + 1ull;
 }
 
+// floor(a * b / d) with the per-(b, d) constants ratio = b / d and inv_d = 1 / d precomputed
+// (double): the same estimate + two coarse corrections + exact 128-bit fix-up as
+// muldiv_floor below, without a double division per call
+__device__ __forceinline__ uint64_t muldiv_floor_pre(uint64_t a, uint64_t b, uint64_t d, double ratio, double inv_d) {
+    const uint64_t plo = a * b, phi = __umul64hi(a, b);
+    uint64_t q = static_cast<uint64_t>(__dmul_rn(static_cast<double>(a), ratio));
+    for (int it = 0; it < 2; ++it) {
+        const uint64_t tlo = q * d, thi = __umul64hi(q, d);
+        const uint64_t rlo = plo - tlo;
+        const int64_t rhi = static_cast<int64_t>(phi - thi - (plo < tlo ? 1ull : 0ull));
+        const double rd = __dadd_rn(__dmul_rn(static_cast<double>(rhi), 18446744073709551616.0),
+                                    static_cast<double>(rlo));
+        const double dq = floor(__dmul_rn(rd, inv_d));
+        q = static_cast<uint64_t>(static_cast<int64_t>(q) + static_cast<int64_t>(dq));
+    }
+    for (int it = 0; it < 3; ++it) {
+        const uint64_t tlo = q * d, thi = __umul64hi(q, d);
+        if (thi > phi || (thi == phi && tlo > plo)) { --q; continue; }
+        const uint64_t ulo = tlo + d, uhi = thi + (ulo < tlo ? 1ull : 0ull);
+        if (uhi < phi || (uhi == phi && ulo <= plo)) { ++q; continue; }
+        break;
+    }
+    return q;
+}
+
 // floor(a * b / d) for a < d (so the quotient is < b), exact: double estimate,
 // then two exact 128-bit corrections.
 __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t b, uint64_t d) {

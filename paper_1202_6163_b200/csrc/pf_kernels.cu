@@ -583,6 +583,7 @@ struct SpacCtx {
     uint64_t Qtot, GP;
     const uint64_t* Q;
     const uint64_t* G;
+    double ratio, inv_d;  // Q / G_P and 1 / G_P (estimates only; the division is exact)
 };
 
 // a6 merge: slot k's position is x_k = floor(G_k Q / G_P) (exact 128/64 division);
@@ -601,11 +602,15 @@ struct ModeSpacings {
 
     using Ctx = SpacCtx;
     __device__ Ctx ctx(int n) const {
-        return {n, Qtot[n], Gtot[n], Q + static_cast<int64_t>(n) * ldq, G + static_cast<int64_t>(n) * ldg};
+        const uint64_t qt = Qtot[n], gp = Gtot[n];
+        return {n, qt, gp, Q + static_cast<int64_t>(n) * ldq, G + static_cast<int64_t>(n) * ldg,
+                __ddiv_rn(static_cast<double>(qt), static_cast<double>(gp)), __drcp_rn(static_cast<double>(gp))};
     }
     __device__ bool valid(int n) const { return fstatus[n] == 0; }
     __device__ int64_t nA(const Ctx&) const { return P; }
-    __device__ uint64_t x(const Ctx& c, int64_t k) const { return muldiv_floor(__ldg(c.G + k), c.Qtot, c.GP); }
+    __device__ uint64_t x(const Ctx& c, int64_t k) const {
+        return muldiv_floor_pre(__ldg(c.G + k), c.Qtot, c.GP, c.ratio, c.inv_d);
+    }
     __device__ uint64_t b(const Ctx& c, int64_t i) const { return __ldg(c.Q + i); }
     __device__ void fill_a(const Ctx& c, int64_t ka0, int na, uint64_t* s) const {
         for (int t = threadIdx.x; t < na; t += kThreads) s[t] = x(c, ka0 + t);
