@@ -2191,7 +2191,7 @@ int fused_cluster_ctas(int32_t P) {
 // multinomial: the bucket index + Q from one cluster-kernel launch (kBuckets: the rho = 0
 // systematic machinery over NB = 2^ceil(log2 P) slots of width 2^(64 - m)), then the per-slot
 // searches; above the sizes the CTA-per-filter kernel takes
-bool buckets_fused_supported(int32_t P) { return P > 4096 && P <= 8 * 512 * kFI; }
+bool buckets_fused_supported(int32_t P) { return P > 2048 && P <= 8 * 512 * kFI; }
 
 bool fused_supported(int scheme, int32_t N, int32_t P) {
     if (!(scheme == 2 || scheme == 3) || P < 1) return false;

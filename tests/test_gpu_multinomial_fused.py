@@ -37,7 +37,7 @@ def dev():
 
 
 @pytest.mark.parametrize("N,P", [(1, 8192), (40, 16384), (300, 8192), (7, 65536), (1, 65536), (1, 4097),
-                                 (20, 12289), (9, 50001), (200, 40000)])
+                                 (20, 12289), (9, 50001), (200, 40000), (300, 3000), (200, 4096)])
 def test_multinomial_bucket_mode(pf, dev, orc, N, P):
     import torch
 
