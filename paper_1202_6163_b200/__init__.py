@@ -17,6 +17,9 @@ import os
 
 from ._build import LIB as _LIB_PATH
 
+# diagnostics only (tools/variants.py A/B builds): another build of the same library
+_LIB_PATH = os.environ.get("PF_LIB_OVERRIDE", _LIB_PATH)
+
 PF_MULTINOMIAL, PF_STRATIFIED, PF_SYSTEMATIC, PF_METROPOLIS = 1, 2, 3, 4
 SCHEMES = {"multinomial": 1, "stratified": 2, "systematic": 3, "metropolis": 4}
 PF_FILTER_OK, PF_FILTER_INVALID_WEIGHTS = 0, 1

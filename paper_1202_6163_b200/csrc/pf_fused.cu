@@ -29,6 +29,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cfloat>
+#include <type_traits>
 #include <cstdlib>
 #include <cmath>
 
@@ -236,6 +238,35 @@ __device__ __forceinline__ void cluster_sync_publish(bool publisher) {
 #define PF_COPY_U 4
 #endif
 constexpr int kCopyU = PF_COPY_U;
+// Deferred state copy (max-ahead instantiations with the gather): every warp keeps the (free
+// slot, owner) pairs it produced in phase D in a private ring and copies their rows in "ticks"
+// spread over the NEXT filter's phases: a tick stores the rows staged by the previous tick
+// (cp.async, 16 bytes per lane, into shared memory: no registers held while in flight) and
+// stages the next kCU x (32 / chunks-per-row) rows.  The copy's memory latency hides under
+// the compute of the following phases instead of stalling the warp at the end of phase D.
+#ifndef PF_COPY_CU
+#define PF_COPY_CU 3
+#endif
+#ifndef PF_COPY_CU256
+#define PF_COPY_CU256 8
+#endif
+// chunks per lane per tick: 256-thread CTAs with the gather run 3 per SM (85 registers, room
+// for larger staged batches)
+template <int FT>
+__host__ __device__ constexpr int copy_cu() {
+    return FT == 256 ? PF_COPY_CU256 : PF_COPY_CU;
+}
+// the deferred copy runs in the systematic instantiations (stratified's per-particle Philox in
+// phase C leaves no registers for the ticks: its step was 1.96 -> 2.40 ms with them)
+template <int SCHEME, int PERM, int FT, bool F64>
+__host__ __device__ constexpr bool fused_deferred_copy() {
+    return FT <= 512 && !F64 && PERM == 2 && SCHEME == 3;
+}
+template <int FT, int PERM>
+__host__ __device__ constexpr int fused_min_blocks() {
+    return (FT == 256 && PERM == 2) ? 3 : 1024 / FT;
+}
+constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner), P <= 65536
 #ifndef PF_PREFETCH_NEXT
 #define PF_PREFETCH_NEXT 1
 #endif
@@ -265,9 +296,60 @@ __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32
                __ldcg(reinterpret_cast<const int4*>(Xf + (static_cast<uint32_t>(owner[p]) * xld + ch))));
 }
 
+// Max-ahead mode (512-thread float32 instantiations): the CTA's slice of the NEXT filter's
+// log-weights arrives in shared memory by one bulk asynchronous copy (cp.async.bulk, mbarrier
+// completion) issued as soon as the current filter's values are in registers; its CTA maximum
+// is formed during phase B and travels with the scan totals at the cluster exchange, so a
+// filter needs one cluster barrier without the permutation (was two) and two with it (was
+// four: the free-slot lists are built before the packed totals are exchanged).  The exchange
+// words are double-buffered by filter parity, which makes one barrier per filter enough.
+template <int FT, bool F64>
+__host__ __device__ constexpr bool fused_max_ahead() {
+    return FT <= 512 && !F64;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
+            smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one thread: bytes (a multiple of 16, 16-byte aligned ends) from global src into shared dst,
+// completion counted on bar (the caller waits on the barrier's current phase)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
 // PERM: 0 ancestors (+ offspring) only, 1 + canonical permutation, 2 + in-place state gather
 template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
-__global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
+__global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_sorted(FusedArgs a) {
     // geometry of this instantiation: FT threads x FI particles per thread (FT = 512, FI = 16:
     // 8192 particles per CTA, clusters of <= 8; FT = 1024, FI = 16: 16384 per CTA, clusters of
     // <= 16 for 65536 < P <= 262144)
@@ -278,10 +360,20 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
     constexpr int kPP = FT * FI;
     constexpr int kTPL = kFR * kFW / 32;
     constexpr int kXS = kFW * kChunk;
+    constexpr bool MA = fused_max_ahead<FT, F64>();
+    constexpr int kCU = copy_cu<FT>();
     static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
-    extern __shared__ __align__(16) int32_t s_fs[];  // PERM: this CTA's free-slot list (kPP entries)
-    int32_t* s_pslot = s_fs + kPP;                    // PERM == 2: free slot of each extras rank of a chunk
-    __shared__ Exchange s_x;
+    extern __shared__ __align__(16) int32_t s_dyn[];
+    float* s_lw = reinterpret_cast<float*>(s_dyn);  // MA: this CTA's slice of the next filter's log-weights
+    // PERM: this CTA's free-slot list (kPP entries; 16-bit slots in the max-ahead mode, P <= 65536)
+    using FsT = std::conditional_t<MA, uint16_t, int32_t>;
+    constexpr bool DC = fused_deferred_copy<SCHEME, PERM, FT, F64>();  // deferred, asynchronous state copy
+    FsT* s_fs = reinterpret_cast<FsT*>(s_dyn + (MA ? kPP : 0));
+    int32_t* s_pslot = reinterpret_cast<int32_t*>(s_fs + kPP);  // PERM == 2 (not DC): free slot per extras rank
+    uint32_t* s_ring = reinterpret_cast<uint32_t*>(s_fs + kPP);  // DC: kFW rings of kRQ pairs
+    int4* s_stage = reinterpret_cast<int4*>(s_ring + kFW * kRQ); // DC: kFW x kCU x 32 staged chunks
+    __shared__ Exchange s_xx[2];                    // MA: double-buffered by filter parity
+    __shared__ uint64_t s_mbar;
     __shared__ uint32_t s_rf[kMaxCL + 1];
     __shared__ uint64_t s_poff;
     __shared__ float s_f[kFW];
@@ -307,18 +399,185 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int num_clusters = gridDim.x / CL;
     const int cid = blockIdx.x / CL;
+    // this CTA's particle range is the same for every filter
+    const int64_t p0 = static_cast<int64_t>(c) * a.PP;
+    const int64_t p1 = min(static_cast<int64_t>(a.P), p0 + a.PP);
+    const int np = static_cast<int>(max(int64_t{0}, p1 - p0));
 
-    for (int n = cid; n < a.N; n += num_clusters) {
-        const int64_t p0 = static_cast<int64_t>(c) * a.PP;
-        const int64_t p1 = min(static_cast<int64_t>(a.P), p0 + a.PP);
-        const int np = static_cast<int>(max(int64_t{0}, p1 - p0));
+    // ---- MA helpers: the next filter's slice into s_lw, its CTA max / invalid flag from s_lw
+    const bool lw_bulk = MA && a.vec && np > 0 && (np & 3) == 0;
+    uint32_t lw_phase = 0;
+    auto lw_issue = [&](int nn) {  // all threads, after a barrier that ends every read of s_lw
+        const float* src = a.logw + static_cast<int64_t>(nn) * a.ld + p0;
+        if (lw_bulk) {
+            if (tid == 0) bulk_g2s(s_lw, src, static_cast<uint32_t>(np) * 4u, &s_mbar);
+        } else {
+            for (int i = tid; i < np; i += kFT) s_lw[i] = __ldcs(src + i);
+        }
+    };
+    auto lw_wait = [&]() {  // all threads
+        if (lw_bulk) {
+            mbar_wait(&s_mbar, lw_phase);
+            lw_phase ^= 1u;
+        } else {
+            __syncthreads();
+        }
+    };
+    // CTA partials of max / invalid flag of the slice in s_lw into s_f / s_i (the caller
+    // synchronises before warp 0 reads them)
+    auto lw_partials = [&]() {
+        float m = -INFINITY;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < kFR; ++j) {
+            const int i0 = j * (kFT * 4) + tid * 4;
+            float x[4];
+            if (i0 + 3 < np) {
+                const float4 t = *reinterpret_cast<const float4*>(s_lw + i0);
+                x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) x[q] = (i0 + q < np) ? s_lw[i0 + q] : -INFINITY;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bad |= !(x[q] <= FLT_MAX);  // NaN or +inf
+                m = fmaxf(m, x[q]);
+            }
+        }
+        int b = bad ? 1 : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+            b |= __shfl_xor_sync(kFull, b, o);
+        }
+        if (lane == 0) { s_f[warp] = m; s_i[warp] = b; }
+    };
+    // warp 0 after the barrier that follows lw_partials: CTA max / flag into the exchange
+    auto lw_cta_reduce = [&](Exchange& x) {
+        float mm = (lane < kFW) ? s_f[lane] : -INFINITY;
+        int bb = (lane < kFW) ? s_i[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mm = fmaxf(mm, __shfl_xor_sync(kFull, mm, o));
+            bb |= __shfl_xor_sync(kFull, bb, o);
+        }
+        if (lane == 0) { x.m = mm; x.bad = bb; }
+    };
+    // warp 0 after the cluster barrier: the filter maximum / invalid flag from every CTA's exchange
+    auto lw_cluster_reduce = [&](int xb) {
+        float gm = -INFINITY;
+        int gb = 0;
+        if (lane < CL) {
+            const Exchange* rx = cluster.map_shared_rank(&s_xx[xb], lane);
+            gm = rx->m;
+            gb = rx->bad;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
+            gb |= __shfl_xor_sync(kFull, gb, o);
+        }
+        if (lane == 0) {
+            s_lmax = gm;
+            s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+        }
+    };
+    // ---- DC: this warp's ring of (slot, owner) pairs of filter rq_n and its staged batch
+    uint32_t rq_head = 0, rq_tail = 0, rq_nb = 0;  // pairs stored, produced, staged (in flight)
+    int rq_n = 0;
+    const int cxl = a.xlg;
+    const int rstep = 32 >> cxl;                          // rows per warp instruction
+    const uint32_t cch = static_cast<uint32_t>(lane & ((1 << cxl) - 1)) * 16u;  // this lane's chunk
+    const uint32_t csub = static_cast<uint32_t>(lane >> cxl);                   // this lane's row
+    const uint32_t cxld = static_cast<uint32_t>(a.xld);
+    uint32_t* const ring = s_ring + warp * kRQ;
+    int4* const stage = s_stage + warp * (kCU * 32);
+    // a tick: wait for the batch staged by the previous tick (each lane reads back only its own
+    // chunks, so the lane's cp.async wait is all it needs), store its rows to their free slots,
+    // then stage the next batch of the ring.  Whole warp, uniform.
+    auto tick = [&]() {
+        if constexpr (DC) {
+            if (rq_nb) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                char* Xf = a.X + static_cast<int64_t>(rq_n) * a.xfld;
+#pragma unroll
+                for (int u = 0; u < kCU; ++u) {
+                    const uint32_t k = static_cast<uint32_t>(u * rstep) + csub;
+                    if (k < rq_nb) {
+                        const uint32_t e = ring[(rq_head + k) & (kRQ - 1)];
+                        __stcg(reinterpret_cast<int4*>(Xf + ((e >> 16) * cxld + cch)), stage[u * 32 + lane]);
+                    }
+                }
+                rq_head += rq_nb;
+                rq_nb = 0;
+            }
+            const uint32_t avail = rq_tail - rq_head;
+            if (avail) {
+                rq_nb = min(avail, static_cast<uint32_t>(kCU * rstep));
+                const char* Xf = a.X + static_cast<int64_t>(rq_n) * a.xfld;
+#pragma unroll
+                for (int u = 0; u < kCU; ++u) {
+                    const uint32_t k = static_cast<uint32_t>(u * rstep) + csub;
+                    if (k < rq_nb) {
+                        const uint32_t e = ring[(rq_head + k) & (kRQ - 1)];
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stage + u * 32 + lane)),
+                                     "l"(Xf + ((e & 0xFFFFu) * cxld + cch))
+                                     : "memory");
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
+    };
+    auto drain_all = [&]() {
+        if constexpr (DC) {
+            while (rq_nb || rq_tail != rq_head) tick();
+        }
+    };
+    int it = 0;
+    if (MA) {
+        if (tid == 0) mbar_init(&s_mbar);
+        __syncthreads();
+        if (cid < a.N) {
+            // prologue: the first filter's slice, its maximum through one cluster exchange
+            lw_issue(cid);
+            lw_wait();
+            lw_partials();
+            __syncthreads();
+            if (warp == 0) lw_cta_reduce(s_xx[1]);
+            cluster_sync_publish(warp == 0 && lane == 0);
+            if (warp == 0) lw_cluster_reduce(1);
+            __syncthreads();
+        }
+    }
+
+    for (int n = cid; n < a.N; n += num_clusters, ++it) {
+        const int xb = MA ? (it & 1) : 0;
+        Exchange& s_x = s_xx[xb];
         const float* row = a.logw + static_cast<int64_t>(n) * a.ld + p0;
         const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+        const bool has_next = n + num_clusters < a.N;
 
         // ---------------- A: load + max
         float v[kFI];
         const double* row64 = F64 ? a.logw64 + static_cast<int64_t>(n) * a.ld + p0 : nullptr;
-        if (F64) {
+        if (MA) {
+            // the values arrived in shared memory during the previous filter (or the prologue),
+            // and its maximum / flag came with the previous exchange
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                if (i0 + 3 < np) {
+                    const float4 t = *reinterpret_cast<const float4*>(s_lw + i0);
+                    v[j * 4 + 0] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[j * 4 + q] = (i0 + q < np) ? s_lw[i0 + q] : -INFINITY;
+                }
+            }
+            tick();
+        } else if (F64) {
             // NS-3d: the max and the NaN / +inf flag on the doubles; the shifted float32 weights
             // are formed in phase B from a second (L2) read of the same rows
             double m = -INFINITY;
@@ -395,46 +654,37 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 if (lane == 0) { s_x.m = mm; s_x.bad = bb; }
             }
         }
-        cluster_sync_publish(warp == 0 && lane == 0);  // #1 (s_x.m, s_x.bad)
-        if (warp == 0) {
-            if (F64) {
-                double gm = -INFINITY;
-                int gb = 0;
-                if (lane < CL) {
-                    const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
-                    gm = rx->m64;
-                    gb = rx->bad;
-                }
+        if (MA) {
+            __syncthreads();  // every read of s_lw, s_lmax and s_bad of this filter is done
+            if (has_next) lw_issue(n + num_clusters);
+        } else {
+            cluster_sync_publish(warp == 0 && lane == 0);  // #1 (s_x.m, s_x.bad)
+            if (warp == 0) {
+                if (F64) {
+                    double gm = -INFINITY;
+                    int gb = 0;
+                    if (lane < CL) {
+                        const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
+                        gm = rx->m64;
+                        gb = rx->bad;
+                    }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    gm = fmax(gm, __shfl_xor_sync(kFull, gm, o));
-                    gb |= __shfl_xor_sync(kFull, gb, o);
-                }
-                if (lane == 0) {
-                    s_lmax64 = gm;
-                    s_lmax = 0.0f;  // the shifted weights' maximum is exactly 0 (NS-3d)
-                    s_bad = (gb || gm == -INFINITY) ? 1 : 0;
-                }
-            } else {
-                float gm = -INFINITY;
-                int gb = 0;
-                if (lane < CL) {
-                    const Exchange* rx = cluster.map_shared_rank(&s_x, lane);
-                    gm = rx->m;
-                    gb = rx->bad;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    gm = fmaxf(gm, __shfl_xor_sync(kFull, gm, o));
-                    gb |= __shfl_xor_sync(kFull, gb, o);
-                }
-                if (lane == 0) {
-                    s_lmax = gm;
-                    s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+                    for (int o = 16; o > 0; o >>= 1) {
+                        gm = fmax(gm, __shfl_xor_sync(kFull, gm, o));
+                        gb |= __shfl_xor_sync(kFull, gb, o);
+                    }
+                    if (lane == 0) {
+                        s_lmax64 = gm;
+                        s_lmax = 0.0f;  // the shifted weights' maximum is exactly 0 (NS-3d)
+                        s_bad = (gb || gm == -INFINITY) ? 1 : 0;
+                    }
+                } else {
+                    lw_cluster_reduce(xb);
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
+        const float lm = s_lmax;
         if (s_bad) {
             // NS-1: invalid filter -> identity ancestors, NaN side outputs
             int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
@@ -451,10 +701,22 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 if (a.ess_out) a.ess_out[n] = NAN;
                 if (a.status_out) a.status_out[n] = 1;
             }
-            cluster_sync_publish(false);  // remote readers of s_x are done before the next filter writes it
+            if (MA) {
+                // the next filter's maximum still travels through this filter's exchange
+                if (has_next) {
+                    lw_wait();
+                    lw_partials();
+                }
+                __syncthreads();
+                if (warp == 0 && has_next) lw_cta_reduce(s_x);
+                cluster_sync_publish(warp == 0 && lane == 0);
+                if (warp == 0 && has_next) lw_cluster_reduce(xb);
+                __syncthreads();
+            } else {
+                cluster_sync_publish(false);  // remote readers of s_x are done before the next filter writes it
+            }
             continue;
         }
-        const float lm = s_lmax;
         if (F64) {
             // NS-3d: t_i = fl32(logw_i - lmax) (binary64 subtraction, one rounding); padding -inf
             const double lm64 = s_lmax64;
@@ -476,8 +738,8 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         }
 #if PF_PREFETCH_NEXT
         // the next filter's log-weights of this CTA into L2 (one bulk prefetch), so its phase A
-        // loads come from L2 instead of HBM
-        if (tid == 0 && n + num_clusters < a.N && a.vec && (np & 3) == 0 && np > 0) {
+        // loads come from L2 instead of HBM (the max-ahead mode copies them to shared memory)
+        if (!MA && tid == 0 && has_next && a.vec && (np & 3) == 0 && np > 0) {
             const int64_t off = static_cast<int64_t>(n + num_clusters) * a.ld + p0;
             const void* nrow = F64 ? static_cast<const void*>(a.logw64 + off) : static_cast<const void*>(a.logw + off);
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nrow),
@@ -506,11 +768,18 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             ex[j] = incl - loc;
             const uint64_t wt = __shfl_sync(kFull, incl, 31);
             if (lane == 0) s_wt[j][warp] = wt;
+            tick();
         }
         if (SUMS) {
             sw = warp_sum_f64(sw);
             sw2 = warp_sum_f64(sw2);
             if (lane == 0) { s_d[0][warp] = sw; s_d[1][warp] = sw2; }
+        }
+        if (MA && has_next) {
+            // the next filter's slice has landed (issued at the top of this filter)
+            lw_wait();
+            lw_partials();
+            tick();
         }
         __syncthreads();
         if (warp == 0) {
@@ -546,8 +815,9 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 s_x.sw = A;
                 s_x.sw2 = Bv;
             }
+            if (MA && has_next) lw_cta_reduce(s_x);
         }
-        cluster_sync_publish(warp == 0);  // #2 (s_wt, s_x.tot / sw / sw2, s_tot)
+        cluster_sync_publish(warp == 0);  // #2 (s_wt, s_x.tot / sw / sw2, s_tot; MA: next max)
         if (warp == 0) {
             uint64_t tot = 0, off = 0;
             double S = 0.0, S2 = 0.0;
@@ -580,6 +850,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 s_zA = 0x1p64 / (static_cast<double>(a.D) * static_cast<double>(tot));
                 s_zBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
             }
+            if (MA && has_next) lw_cluster_reduce(xb);  // the next filter's lmax / flag
         }
         __syncthreads();
         const uint64_t O = s_off;
@@ -615,7 +886,6 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             __syncthreads();
             continue;
         }
-
         // ---------------- C: E_i = c(Q_i), heads, max-scan
         uint32_t E[kFI];
 #pragma unroll
@@ -642,6 +912,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 }
             }
             if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
+            tick();
         }
         if (tid == 0) s_klo = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O);
         if (SCHEME == kBuckets && c == 0 && tid == 0) a.Qtot_out[n] = z.Qtot;
@@ -713,6 +984,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                     for (int t = 0; t < 8; ++t)
                         if (k0 + t >= k_lo && k0 + t < K1) arow[k0 + t] = h[t];
                 }
+                tick();
             }
         }
         if (PERM) {
@@ -727,6 +999,10 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
             }
             uint32_t* const O4 = E;  // O4[j * 4 + q] = o of particle (j, q)
             uint64_t pex[kFR];
+            if (DC) {
+                drain_all();  // the ring now takes this filter's pairs
+                rq_n = n;
+            }
             __syncthreads();  // s_wt is reused
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
@@ -762,7 +1038,44 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 }
                 if (lane == 31) s_x.ptot = incl;
             }
-            cluster_sync_publish(warp == 0);  // #3 packed CTA totals (s_wt, s_x.ptot) published
+            int32_t* prow = a.perm + static_cast<int64_t>(n) * a.ld_anc;
+            // survivors keep their slot: the identity over the CTA's range (aligned vector stores;
+            // the free slots are overwritten by their owners after the next cluster barrier)
+            if (a.perm) {
+#pragma unroll
+                for (int j = 0; j < kFR; ++j) {
+                    const int i0 = j * (kFT * 4) + tid * 4;
+                    const int32_t id0 = static_cast<int32_t>(p0) + i0;
+                    if (a.anc_vec && i0 + 3 < np) {
+                        __stcg(reinterpret_cast<int4*>(prow + p0 + i0), make_int4(id0, id0 + 1, id0 + 2, id0 + 3));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (i0 + q < np) prow[p0 + i0 + q] = id0 + q;
+                    }
+                }
+            }
+            uint64_t poff;
+            if (MA) {
+                // the CTA's free-slot list (local free ranks) before the exchange, so one cluster
+                // barrier publishes both the packed totals and the lists
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < kFR; ++j) {
+                    uint64_t run = s_wt[j][warp] + pex[j];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = j * (kFT * 4) + tid * 4 + q;
+                        const uint32_t o = O4[j * 4 + q];
+                        if (o == 0 && i < np) s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull)] = static_cast<FsT>(p0 + i);
+                        run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
+                    }
+                }
+                __syncthreads();
+                cluster_sync_publish(tid == 0);  // #3 packed totals and free-slot lists published
+            } else {
+                cluster_sync_publish(warp == 0);  // #3 packed CTA totals (s_wt, s_x.ptot) published
+            }
             if (warp == 0) {
                 uint64_t pt = 0;
                 if (lane < CL) pt = cluster.map_shared_rank(&s_x, lane)->ptot;
@@ -778,26 +1091,23 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                 if (lane == c) s_poff = excl;
             }
             __syncthreads();
-            const uint64_t poff = s_poff;
-            const uint32_t rf_c = s_rf[c];
-            int32_t* prow = a.perm + static_cast<int64_t>(n) * a.ld_anc;
+            poff = s_poff;
+            if (!MA) {
+                const uint32_t rf_c = s_rf[c];
 #pragma unroll
-            for (int j = 0; j < kFR; ++j) {
-                uint64_t run = poff + s_wt[j][warp] + pex[j];
+                for (int j = 0; j < kFR; ++j) {
+                    uint64_t run = poff + s_wt[j][warp] + pex[j];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int i = j * (kFT * 4) + tid * 4 + q;
-                    const uint32_t o = O4[j * 4 + q];
-                    if (i < np) {
-                        if (o > 0) {
-                            if (a.perm) prow[p0 + i] = static_cast<int32_t>(p0 + i);
-                        } else s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull) - rf_c] = static_cast<int32_t>(p0 + i);
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = j * (kFT * 4) + tid * 4 + q;
+                        const uint32_t o = O4[j * 4 + q];
+                        if (o == 0 && i < np) s_fs[static_cast<uint32_t>(run & 0x7FFFFFFFull) - rf_c] = static_cast<FsT>(p0 + i);
+                        run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
                     }
-                    run += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && i < np) ? 1ull : 0ull);
                 }
+                __syncthreads();
+                cluster_sync_publish(tid == 0);  // #4 every CTA's free-slot list complete
             }
-            __syncthreads();
-            cluster_sync_publish(tid == 0);  // #4 every CTA's free-slot list complete
             // Survivors' extra copies, CTA-wide: the CTA's extras ranks are [XC0, XC0 + XC).  Per
             // 8192-rank chunk: heads[first extras rank of i] = i, CTA max-scan gives the owner of
             // every rank r; the r-th global free slot (this CTA's list or a peer's, DSMEM) gets it.
@@ -823,13 +1133,20 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                     int32_t h[8];
                     cta_max_scan8<kFW>(s_head, s_wmax, h, carry, tid, warp, lane);
                     const uint32_t r0 = c0 + 8 * tid;
+                    // this warp's pairs of the chunk: extras ranks [c0 + 256 warp, ...) of XC
+                    const int64_t wfirst = static_cast<int64_t>(c0) + 256 * warp;
+                    const int npairs = static_cast<int>(
+                        min(int64_t{256}, max(int64_t{0}, static_cast<int64_t>(XC) - wfirst)));
+                    if (DC) {
+                        while (rq_tail + static_cast<uint32_t>(npairs) - rq_head > static_cast<uint32_t>(kRQ)) tick();
+                    }
                     if (r0 < XC) {
                         uint32_t R = XC0 + r0;  // global free rank of this thread's first extra
                         int cc = 0;
 #pragma unroll
                         for (int q2 = 1; q2 < kMaxCL; ++q2) cc += (q2 < CL && s_rf[q2] <= R) ? 1 : 0;
                         uint32_t rb = s_rf[cc], nxt = s_rf[cc + 1];
-                        const int32_t* rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
+                        const FsT* rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
 #pragma unroll
                         for (int t = 0; t < 8; ++t) {
                             if (r0 + t < XC) {
@@ -839,23 +1156,28 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
                                     nxt = s_rf[cc + 1];
                                     rfs = (cc == c) ? s_fs : cluster.map_shared_rank(s_fs, cc);
                                 }
-                                const int32_t slot = rfs[R - rb];
+                                const int32_t slot = static_cast<int32_t>(rfs[R - rb]);
                                 prow[slot] = h[t];
-                                if (PERM == 2) s_pslot[8 * tid + t] = slot;
+                                if (DC)
+                                    ring[(rq_tail + 8 * lane + t) & (kRQ - 1)] =
+                                        (static_cast<uint32_t>(slot) << 16) | static_cast<uint32_t>(h[t]);
+                                else if (PERM == 2)
+                                    s_pslot[8 * tid + t] = slot;
                                 ++R;
                             }
                         }
                     }
-                    if (PERM == 2) {
+                    if (DC) {
+                        __syncwarp();  // the ring entries are read by other lanes of the warp
+                        rq_tail += static_cast<uint32_t>(npairs);
+                        tick();
+                    } else if (PERM == 2) {
                         // a10 fused (NS-16): X[free slot] <- X[owner] for this warp's (slot, owner)
                         // pairs; reads touch survivor rows only, writes free rows only
                         int4* hh = reinterpret_cast<int4*>(s_head);
                         hh[2 * tid] = make_int4(h[0], h[1], h[2], h[3]);
                         hh[2 * tid + 1] = make_int4(h[4], h[5], h[6], h[7]);
                         __syncwarp();
-                        const int64_t wfirst = static_cast<int64_t>(c0) + 256 * warp;
-                        const int npairs = static_cast<int>(
-                            min(int64_t{256}, max(int64_t{0}, static_cast<int64_t>(XC) - wfirst)));
                         copy_rows_warp(a, n, s_head + 256 * warp, s_pslot + 256 * warp, npairs, lane);
                         __syncwarp();
                     }
@@ -866,6 +1188,7 @@ __global__ void __launch_bounds__(FT, 1024 / FT) k_fused_sorted(FusedArgs a) {
         // thread reads any more in this filter, and its first barrier follows its loads, so warps
         // that finish their copies early start the next filter's loads under the stragglers' copies
     }
+    drain_all();
     cluster.sync();  // keep this CTA's shared memory alive for remote readers
 }
 
@@ -1852,9 +2175,19 @@ __global__ void __launch_bounds__(kMedT) k_medium(SmallArgs a) {
 
 int device_sms() { return sm_count(); }
 
-template <int FT, int FI>
-constexpr size_t fused_smem(int perm) {
-    return perm ? static_cast<size_t>(FT * FI + (perm == 2 ? (FT / 32) * kChunk : 0)) * sizeof(int32_t) : 0;
+template <int SCHEME, int PERM, int FT, int FI, bool F64 = false>
+constexpr size_t fused_smem() {
+    // max-ahead: [the next filter's log-weight slice, float] [PERM: free-slot list, u16]
+    //            [deferred copy: kFW pair rings of kRQ u32, kFW x kCU x 32 staged 16-byte chunks |
+    //             PERM 2 otherwise: free slot per extras rank of a chunk, int32]
+    // otherwise: [PERM: free-slot list, int32] [PERM 2: free slot per extras rank of a chunk]
+    constexpr size_t pslot = (PERM == 2) ? static_cast<size_t>(FT / 32) * kChunk * 4 : 0;
+    return fused_max_ahead<FT, F64>()
+               ? static_cast<size_t>(FT * FI) * 4 + (PERM ? static_cast<size_t>(FT * FI) * 2 : 0) +
+                     (fused_deferred_copy<SCHEME, PERM, FT, F64>()
+                          ? static_cast<size_t>(FT / 32) * (kRQ * 4 + copy_cu<FT>() * 32 * 16)
+                          : pslot)
+               : (PERM ? static_cast<size_t>(FT * FI) * 4 + pslot : 0);
 }
 
 template <int SCHEME, bool SUMS, int PERM, int FT, int FI, bool F64 = false>
@@ -1863,9 +2196,9 @@ void fused_set_attributes() {
     static std::atomic<int> attr_set[kMaxDevices];
     cached_per_device(attr_set, [] {
         auto kern = k_fused_sorted<SCHEME, SUMS, PERM, FT, FI, F64>;
-        if (PERM)
+        if (fused_smem<SCHEME, PERM, FT, FI, F64>() > 0)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(fused_smem<FT, FI>(PERM)));
+                                 static_cast<int>(fused_smem<SCHEME, PERM, FT, FI, F64>()));
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaGetLastError();
         return 1;
@@ -1886,7 +2219,7 @@ int fused_max_clusters(int CL) {
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.blockDim = dim3(FT, 1, 1);
-        cfg.dynamicSmemBytes = fused_smem<FT, FI>(PERM);
+        cfg.dynamicSmemBytes = fused_smem<SCHEME, PERM, FT, FI, F64>();
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cfg.gridDim = dim3(CL, 1, 1);
@@ -1912,7 +2245,7 @@ cudaError_t launch_fused_t(const FusedArgs& a, cudaStream_t s) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(FT, 1, 1);
-    cfg.dynamicSmemBytes = fused_smem<FT, FI>(PERM);
+    cfg.dynamicSmemBytes = fused_smem<SCHEME, PERM, FT, FI, F64>();
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -2215,8 +2548,15 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.ld = ld;
     a.N = N;
     a.P = P;
-    // geometry: 512 threads (8192 particles per CTA) up to 8 CTAs, else 1024 threads (16384)
-    const int FT = (P <= 8 * 512 * kFI) ? 512 : 1024;
+    // geometry: 512 threads (8192 particles per CTA) up to 8 CTAs, else 1024 threads (16384);
+    // PF_FUSED_FT=256 (experiment): 256 threads (4096 per CTA), clusters of up to 16
+    static const int ft_env = [] {
+        const char* e = std::getenv("PF_FUSED_FT");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int FT = (ft_env == 256 && !logw64 && P <= 16 * 256 * kFI && scheme != kBuckets)
+                       ? 256
+                       : ((P <= 8 * 512 * kFI) ? 512 : 1024);
     a.CL = static_cast<int32_t>((P + FT * kFI - 1) / (FT * kFI));
     int64_t pp = (P + a.CL - 1) / a.CL;
     pp = (pp + 3) / 4 * 4;
@@ -2256,7 +2596,9 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
         if (FT != 512) return cudaErrorNotSupported;  // binary64 fused for P <= 65536 only (f64_fused_supported)
         e = launch_fused_ft<512, 16, true>(scheme, pm, a, s);
     } else {
-        e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
+        e = (FT == 256)   ? launch_fused_ft<256, 16>(scheme, pm, a, s)
+            : (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s)
+                          : launch_fused_ft<1024, 16>(scheme, pm, a, s);
     }
     ++*launches;
     if (e != cudaSuccess) return e;

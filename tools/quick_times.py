@@ -19,6 +19,27 @@ def main():
     from tools.sweep import time_calls
 
     dev = torch.device("cuda:0")
+    if "--c3" in sys.argv:
+        # the C3 batch (1024 x 2^16, sigma^2 = 1 unless --var) by output set: resample only,
+        # + offspring, + permutation, + in-place gather of a D = 16 state (the bench step)
+        var = float(sys.argv[sys.argv.index("--var") + 1]) if "--var" in sys.argv else 1.0
+        N, P = 1024, 1 << 16
+        x = pfinputs.gaussian_logw_torch(P, var, pfinputs.BASE_SEED, N, dev)
+        anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+        off = torch.empty_like(anc)
+        pm = torch.empty_like(anc)
+        X = torch.randn((N, P, 16), device=dev)
+        for scheme in ("systematic", "stratified", "multinomial"):
+            for name, kw in (("anc", {}), ("off", {"offspring_out": off}),
+                             ("perm", {"offspring_out": off, "permuted_out": pm}),
+                             ("step", {"offspring_out": off, "permuted_out": pm, "state": X})):
+                if scheme == "multinomial" and name != "anc":
+                    continue
+                ms = time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, ancestors=anc, **kw), 5, dev)
+                print(json.dumps({"c3": scheme, "var": var, "outputs": name, "ms": round(ms, 4),
+                                  "particles_per_s": N * P / (ms / 1e3)}))
+                sys.stdout.flush()
+        return
     if "--small" in sys.argv:
         for P in (16, 64, 256):
             for scheme in ("systematic", "multinomial", "metropolis"):
