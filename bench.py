@@ -145,7 +145,12 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- GPU arm
 def run_c5(args):
     """Giant filter: P_global = 2^25 x world, contiguous shards, NCCL all_reduce / all_gather
-    between the shard stages (paper_1202_6163_b200.shard)."""
+    between the shard stages (paper_1202_6163_b200.shard).  The line carries the dominant
+    kernel's roofline (library-stated algorithmic bytes over its live CUDA-event time), the
+    per-collective device times of a traced pass, the oracle's single-core rate on a bounded
+    sample (cpu_baseline) and an end-to-end rate with the log-weight shard copied in from pinned
+    host memory and the rank's ancestors copied out every step (e2e)."""
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -174,11 +179,11 @@ def run_c5(args):
         gen = torch.Generator(device=dev).manual_seed(pfinputs.BASE_SEED + rank)
         X = torch.randn((Pl, args.migrate), device=dev, generator=gen)
 
-    def step():
-        anc, info = resample_sharded(scheme, logw, P_global, seed, B=B, comm=comm, assemble=False, flags=flags)
+    def step(lw=logw):
+        anc, info = resample_sharded(scheme, lw, P_global, seed, B=B, comm=comm, assemble=False, flags=flags)
         if X is not None:  # cross-GPU particle migration of the state rows (include/pf.h 4a-4d)
             migrate_sharded(X, anc, info, comm=comm)
-        return anc
+        return anc, info
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -202,6 +207,106 @@ def run_c5(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     clocks = sampler.stop()
+
+    # ---------------- traced pass: per-kernel and per-collective device times (same stream)
+    kprof = min(args.steps, 5)
+    if world > 1:
+        comm.timing = True
+    pf.pf_profile_enable(True)
+    for _ in range(kprof):
+        step()
+    kt = pf.pf_profile_collect()
+    pf.pf_profile_enable(False)
+    coll = comm.collect_times() if world > 1 else {}
+    if world > 1:
+        comm.timing = False
+    hbm, peak_src = peaks()
+    kernels = {}
+    for name, (cnt, tot, alg_sum, _row) in kt.items():
+        ent = {"launches_per_step": cnt / kprof, "avg_ms": tot / max(cnt, 1)}
+        if alg_sum > 0:
+            ent["alg_bytes"] = int(alg_sum / max(cnt, 1))
+            ent["gbs"] = ent["alg_bytes"] / (ent["avg_ms"] / 1e3) / 1e9
+            ent["frac_hbm"] = ent["gbs"] / hbm
+        kernels[name] = ent
+    roofline = None
+    stated = {k: v for k, v in kernels.items() if "frac_hbm" in v}
+    if stated:
+        dom = max(stated, key=lambda k: stated[k]["avg_ms"] * stated[k]["launches_per_step"])
+        d = stated[dom]
+        step_kernel_ms = sum(v["avg_ms"] * v["launches_per_step"] for v in kernels.values())
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(d["gbs"], 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(d["frac_hbm"], 4), "traffic": None, "alg_bytes_per_launch": d["alg_bytes"],
+                    "avg_ms": round(d["avg_ms"], 5),
+                    "share_of_step": round(d["avg_ms"] * d["launches_per_step"] / max(step_kernel_ms, 1e-9), 3),
+                    "peak_source": peak_src}
+    collectives = {k: {"calls_per_step": c / kprof, "ms_per_step": round(m / kprof, 4),
+                       "bytes_per_step": int(b / kprof)} for k, (c, m, b) in coll.items()}
+
+    # ---------------- e2e: pinned host shard in, the rank's ancestor slots out, every step
+    host_logw = logw.cpu().pin_memory()
+    dev_logw = torch.empty_like(logw)
+    out_host = torch.empty(max(Pl, 1), dtype=torch.int32).pin_memory()
+    h2d = Pl * 4
+    d2h_total = 0
+
+    def e2e_step():
+        nonlocal d2h_total
+        dev_logw.copy_(host_logw, non_blocking=True)
+        anc, info = step(dev_logw)
+        if scheme == "metropolis":
+            a, b = 0, Pl
+        else:
+            a, b = (int(v) for v in info["slot_range_dev"].tolist())  # device -> host: the rank's slot range
+        n = b - a
+        if n > out_host.numel():
+            return anc
+        out_host[:n].copy_(anc[a:b], non_blocking=True)
+        d2h_total += n * 4 + (0 if scheme == "metropolis" else 16)
+        return anc
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    d2h_total = 0
+    if world > 1:
+        dist.barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    f1.record()
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": P_global * args.steps / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": int(d2h_total / args.steps),
+           "note": "rank's pinned host log-weight shard -> H2D -> sharded resample -> D2H of the rank's "
+                   "ancestor slots (slot range read back first)"}
+
+    # ---------------- oracle on one host core over a bounded sample (one 2^22-particle filter)
+    cpu = None
+    if rank == 0 and not args.no_extras:
+        import oracle
+
+        oracle.build()
+        Ps = 1 << 22
+        xs = pfinputs.gaussian_logw(Ps, args.var, pfinputs.BASE_SEED)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            if flags:
+                oracle.resample_sorted_multinomial(xs, seed)
+            else:
+                oracle.resample(scheme, xs, seed, B=B)
+            reps += 1
+            if time.perf_counter() - t0 > 10.0 or reps >= 20:
+                break
+        el = time.perf_counter() - t0
+        cpu = {"value": Ps * reps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{reps} resampling(s) of one 2^22-particle filter of the same law (sigma^2={args.var}, "
+                         f"{scheme}{' sorted a6' if flags else ''}{f', B={B}' if B else ''}) on one host thread"}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": P_global * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
@@ -216,8 +321,10 @@ def run_c5(args):
                                       + (" + all_gather(weights)" if scheme == "metropolis" else "")
                                       + (" + all_gather(spacing totals)" if flags else "")
                                       + (" + all_gather(counts) + all_to_all(extra rows)" if args.migrate else ""),
+                       "process_group_ranks": dist.get_world_size() if world > 1 else 1,
                        "l2": "inputs larger than L2 (logw 128 MiB/GPU, Q 256 MiB/GPU)"},
-            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clocks,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "kernels": kernels, "collectives": collectives,
         }))
     if world > 1:
         dist.destroy_process_group()
@@ -285,8 +392,6 @@ def run_ours(args):
     import pfinputs
 
     world, rank, local = dist_env()
-    if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -373,42 +478,26 @@ def run_ours(args):
     pf.pf_profile_enable(False)
     torch.cuda.synchronize(dev)
 
-    # algorithmic bytes per launch of each kernel of the step
-    o = off
-    survivors = int((o > 0).sum().item())
-    free = N * P - survivors
-    row = args.D * 4
-    NP = N * P
-    alg = {
-        "k_max": 4 * NP,
-        "k_scan": 12 * NP,
-        "k_merge": 12 * NP,
-        "k_bsearch": 12 * NP,
-        "k_mexp_vec": 8 * NP,
-        "k_mexp": 8 * NP,
-        "k_metro": 8 * NP,
-        "k_hist": 8 * NP,
-        "k_pscan": 12 * NP,
-        "k_push": 8 * NP + 8 * free,
-        # logw in; ancestors, offspring, permutation out; moved state rows read + written
-        "k_fused_sorted": 16 * NP + 2 * row * free,
-        "k_coop_sorted": 12 * NP,
-        "k_gather_inplace": 4 * NP + 2 * row * free,
-    }
+    # algorithmic bytes per launch of each kernel of the step, as the library states them for
+    # what each launch was asked to read and write (pf_kernel_time.alg_bytes), plus one read and
+    # one write per state row the gather moved (pf_kernel_time.row_bytes x moved rows)
+    survivors = int((off > 0).sum().item())
+    moved = N * P - survivors  # rows the in-place gather rewrites (the free slots)
     hbm, peak_src = peaks()
     kernels = {}
-    for name, (cnt, tot) in kt.items():
+    for name, (cnt, tot, alg_sum, row_sum) in kt.items():
         per = tot / max(cnt, 1)
         ent = {"launches_per_step": cnt / kprof_steps, "avg_ms": per}
-        if name in alg:
-            ent["alg_bytes"] = alg[name]
-            ent["gbs"] = alg[name] / (per / 1e3) / 1e9
+        if alg_sum > 0:
+            alg_launch = (alg_sum + row_sum * moved) / max(cnt, 1)
+            ent["alg_bytes"] = int(alg_launch)
+            ent["gbs"] = alg_launch / (per / 1e3) / 1e9
             ent["frac_hbm"] = ent["gbs"] / hbm
         kernels[name] = ent
     # committed ncu evidence (DRAM traffic and warp instructions per launch) for this workload
     evidence = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_kernel_evidence.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "kernel_evidence.json")) as f:
             evidence = json.load(f).get(f"{args.workload}/{scheme}", {})
     except Exception:
         evidence = {}
@@ -617,6 +706,7 @@ def run_ours(args):
                                   + f", in-place gather of a D={args.D} f32 state",
                        "filters_per_gpu": N, "P": P, "var": args.var, "scheme": scheme, "D": args.D,
                        "global_filters": N * world, "parallelism": f"filter-sharded x{world} (no collective)",
+                       "process_group_ranks": dist.get_world_size() if world > 1 else 1,
                        "l2": ("L2 flushed (512 MiB write) before every timed step; steps timed one by one"
                               if flush_l2 else "inputs larger than L2 (logw N*P*4 B, state N*P*D*4 B), no flush")},
             "roofline": roofline,
@@ -625,7 +715,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "kernels": kernels,
-            "stage_survivor_fraction": survivors / NP,
+            "stage_survivor_fraction": survivors / (N * P),
             "extras": extras,
         }
         print(json.dumps(out))
@@ -729,8 +819,30 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: launch N ranks of this same command
+    line through torch.distributed.run on 127.0.0.1 (one process per GPU), so that a multi-GPU
+    request never silently measures one GPU.  Returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mismatched run",
+              file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "c5":

@@ -412,14 +412,21 @@ uint64_t pf_launch_count(void);
  * is bracketed by two CUDA events recorded on its own stream (the launching
  * stream, so the interval is that kernel's device duration).
  * pf_profile_collect waits for the recorded events, writes up to max_entries
- * aggregated {kernel name, launches, total milliseconds} records, clears the
- * record and returns the number of distinct kernels (or -1 on a CUDA error).
- * Not for use inside CUDA-graph capture.
+ * aggregated {kernel name, launches, total milliseconds, algorithmic bytes}
+ * records, clears the record and returns the number of distinct kernels (or -1
+ * on a CUDA error).  alg_bytes sums, over the kernel's launches, the HBM bytes
+ * each launch must move by what it was asked to read and write (inputs once,
+ * outputs once; 0 = not stated for that kernel); row_bytes sums the extra bytes
+ * per moved state row of launches that gather a state (2 x row bytes: one read,
+ * one write), which the caller multiplies by the rows that moved (data-
+ * dependent).  Not for use inside CUDA-graph capture.
  */
 typedef struct {
     char name[32];
     uint64_t launches;
     double total_ms;
+    uint64_t alg_bytes;
+    uint64_t row_bytes;
 } pf_kernel_time;
 void pf_profile_enable(int32_t on);
 int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries);

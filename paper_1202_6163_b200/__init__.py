@@ -615,7 +615,8 @@ def pf_status_string(status: int) -> str:
 
 
 class _KernelTime(ctypes.Structure):
-    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double),
+                ("alg_bytes", ctypes.c_uint64), ("row_bytes", ctypes.c_uint64)]
 
 
 def pf_profile_enable(on: bool = True) -> None:
@@ -624,12 +625,16 @@ def pf_profile_enable(on: bool = True) -> None:
 
 
 def pf_profile_collect() -> dict:
-    """{kernel name: (launches, total_ms)} since the last collect (waits for the events)."""
+    """{kernel name: (launches, total_ms, alg_bytes, row_bytes)} since the last collect (waits for
+    the events).  alg_bytes: summed algorithmic HBM bytes of those launches as stated by the
+    library (0 = not stated); row_bytes: summed bytes per moved state row (multiply by the rows
+    the gather moved)."""
     buf = (_KernelTime * 64)()
     n = lib().pf_profile_collect(buf, 64)
     if n < 0:
         raise PfError("pf_profile_collect: CUDA error")
-    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(n, 64))}
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms), int(buf[i].alg_bytes),
+                                   int(buf[i].row_bytes)) for i in range(min(n, 64))}
 
 
 def pf_set_fusion(on: bool = True) -> None:

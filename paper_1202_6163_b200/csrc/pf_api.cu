@@ -70,6 +70,7 @@ pf_status get_workspace(const pf_opts* opts, size_t bytes, cudaStream_t s, void*
 struct ProfRecord {
     const char* name;
     cudaEvent_t start, stop;
+    uint64_t alg_bytes, row_bytes;
 };
 std::atomic<bool> g_prof_on{false};
 std::mutex g_prof_mu;
@@ -438,10 +439,10 @@ pf_status resample_f64_impl(int scheme, const double* logw, int64_t ld, int32_t 
 }  // namespace
 
 namespace pf {
-ProfScope::ProfScope(const char* name, cudaStream_t s) : slot(-1), stream(s) {
+ProfScope::ProfScope(const char* name, cudaStream_t s, uint64_t alg_bytes, uint64_t row_bytes) : slot(-1), stream(s) {
     if (!g_prof_on.load(std::memory_order_relaxed)) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    ProfRecord r{name, prof_event(), prof_event()};
+    ProfRecord r{name, prof_event(), prof_event(), alg_bytes, row_bytes};
     cudaEventRecord(r.start, s);
     prof_records().push_back(r);
     slot = static_cast<int>(prof_records().size()) - 1;
@@ -461,7 +462,13 @@ void pf_set_fusion(int32_t on) { g_no_fusion.store(on == 0); }
 
 int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    std::vector<std::pair<std::string, std::pair<uint64_t, double>>> agg;
+    struct Agg {
+        std::string name;
+        uint64_t launches;
+        double ms;
+        uint64_t alg_bytes, row_bytes;
+    };
+    std::vector<Agg> agg;
     int32_t rc = 0;
     for (auto& r : prof_records()) {
         float ms = 0.0f;
@@ -469,12 +476,14 @@ int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries) {
             rc = -1;
         bool found = false;
         for (auto& a : agg)
-            if (a.first == r.name) {
-                a.second.first += 1;
-                a.second.second += ms;
+            if (a.name == r.name) {
+                a.launches += 1;
+                a.ms += ms;
+                a.alg_bytes += r.alg_bytes;
+                a.row_bytes += r.row_bytes;
                 found = true;
             }
-        if (!found) agg.push_back({r.name, {1, static_cast<double>(ms)}});
+        if (!found) agg.push_back({r.name, 1, static_cast<double>(ms), r.alg_bytes, r.row_bytes});
         prof_free_events().push_back(r.start);
         prof_free_events().push_back(r.stop);
     }
@@ -484,9 +493,11 @@ int32_t pf_profile_collect(pf_kernel_time* out, int32_t max_entries) {
     for (auto& a : agg) {
         if (n >= max_entries) break;
         std::memset(out[n].name, 0, sizeof(out[n].name));
-        std::strncpy(out[n].name, a.first.c_str(), sizeof(out[n].name) - 1);
-        out[n].launches = a.second.first;
-        out[n].total_ms = a.second.second;
+        std::strncpy(out[n].name, a.name.c_str(), sizeof(out[n].name) - 1);
+        out[n].launches = a.launches;
+        out[n].total_ms = a.ms;
+        out[n].alg_bytes = a.alg_bytes;
+        out[n].row_bytes = a.row_bytes;
         ++n;
     }
     return static_cast<int32_t>(agg.size());

@@ -133,12 +133,12 @@ cudaError_t launch_shift64(const double* logw, int64_t ld, int32_t N, int32_t P,
     const unsigned grid = static_cast<unsigned>(static_cast<int64_t>(N) * cpf);
     const bool vec = (reinterpret_cast<uintptr_t>(logw) & 15) == 0 && (ld % 2 == 0);
     {
-        ProfScope ps_("k_max64", s);
+        ProfScope ps_("k_max64", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
         if (vec) k_max64<true><<<grid, kT64, 0, s>>>(logw, ld, P, cpf, key, bad);
         else k_max64<false><<<grid, kT64, 0, s>>>(logw, ld, P, cpf, key, bad);
     }
     {
-        ProfScope ps_("k_shift64", s);
+        ProfScope ps_("k_shift64", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 12u);
         if (vec) k_shift64<true><<<grid, kT64, 0, s>>>(logw, ld, P, cpf, key, bad, t, ldt);
         else k_shift64<false><<<grid, kT64, 0, s>>>(logw, ld, P, cpf, key, bad, t, ldt);
     }

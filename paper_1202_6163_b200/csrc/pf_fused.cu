@@ -2401,7 +2401,10 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     a.g_sw2 = reinterpret_cast<double*>(sc + 4096 * 24);
     a.g_ptot = reinterpret_cast<uint64_t*>(sc + 4096 * 32);
     a.freelist = reinterpret_cast<int32_t*>(sc + 4096 * 40);
-    ProfScope ps_("k_coop_sorted", s);
+    const uint64_t NP = static_cast<uint64_t>(N) * static_cast<uint64_t>(P);
+    const uint64_t alg = NP * 4u * (1u + (scheme != kBuckets ? 1u : 0u) + (offspring ? 1u : 0u) + (permuted ? 1u : 0u)) +
+                         (scheme == kBuckets ? NP * 8u + static_cast<uint64_t>(N) * static_cast<uint64_t>(a.S) * 4u : 0u);
+    ProfScope ps_("k_coop_sorted", s, alg);
     if (X) return cudaErrorNotSupported;  // the state gather runs as its own kernel (pf_api.cu)
     cudaError_t e = permuted ? launch_coop_p<1>(scheme, sums, a, s) : launch_coop_p<0>(scheme, sums, a, s);
     ++*launches;
@@ -2437,7 +2440,8 @@ cudaError_t launch_small(int scheme, bool sorted, const float* logw, int64_t ld,
     a.off = offspring;
     const unsigned grid = static_cast<unsigned>((static_cast<int64_t>(N) + kSmallWarps - 1) / kSmallWarps);
     {
-        ProfScope ps_("k_small", s);
+        ProfScope ps_("k_small", s,
+                      static_cast<uint64_t>(N) * P * 4u * (2u + (offspring ? 1u : 0u) + (normw ? 1u : 0u)));
         k_small<<<grid, kSmallWarps * 32, 0, s>>>(a);
     }
     ++*launches;
@@ -2468,7 +2472,8 @@ cudaError_t launch_medium_t(const SmallArgs& a, size_t smem, cudaStream_t s, uin
     });
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.N, static_cast<int64_t>(device_sms()) * occ));
     {
-        ProfScope ps_("k_medium", s);
+        ProfScope ps_("k_medium", s,
+                      static_cast<uint64_t>(a.N) * a.P * 4u * (2u + (a.off ? 1u : 0u) + (a.normw ? 1u : 0u)));
         k_medium<T><<<grid, T, smem, s>>>(a);
     }
     ++*launches;
@@ -2589,7 +2594,14 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.xfld = x_fld;
     a.xlg = 0;
     while ((int64_t{16} << a.xlg) < x_row_bytes) ++a.xlg;
-    ProfScope ps_("k_fused_sorted", s);
+    // algorithmic bytes: log-weights once, each requested output once (bucket mode: Q and the
+    // bucket index), plus one read and one write per moved state row
+    const uint64_t NP = static_cast<uint64_t>(N) * static_cast<uint64_t>(P);
+    const uint64_t alg = NP * (logw64 ? 8u : 4u) +
+                         NP * 4u * ((scheme != kBuckets ? 1u : 0u) + (offspring ? 1u : 0u) + (permuted ? 1u : 0u) +
+                                    (normw ? 1u : 0u)) +
+                         (scheme == kBuckets ? NP * 8u + static_cast<uint64_t>(N) * static_cast<uint64_t>(a.S) * 4u : 0u);
+    ProfScope ps_("k_fused_sorted", s, alg, X ? 2u * static_cast<uint64_t>(x_row_bytes) : 0u);
     cudaError_t e;
     const int pm = a.X ? 2 : (a.perm ? 1 : 0);
     if (logw64) {

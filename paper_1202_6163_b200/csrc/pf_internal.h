@@ -37,8 +37,12 @@ constexpr int kItems = 16;              // items per thread in scan / merge tile
 constexpr int kTile = kThreads * kItems;  // 4096 particles per scan tile
 
 // Per-kernel event tracing (pf_profile_enable); a no-op unless enabled.
+// alg_bytes: the launch's algorithmic HBM bytes known at launch (inputs read once, outputs
+// written once); row_bytes: the extra algorithmic bytes per moved state row (data-dependent:
+// the caller multiplies by the rows its gather moved).  Both are reported per kernel name by
+// pf_profile_collect, so a roofline is computed from what each launch actually moved.
 struct ProfScope {
-    ProfScope(const char* name, cudaStream_t s);
+    ProfScope(const char* name, cudaStream_t s, uint64_t alg_bytes = 0, uint64_t row_bytes = 0);
     ~ProfScope();
     int slot;
     cudaStream_t stream;

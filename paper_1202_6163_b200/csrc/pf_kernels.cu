@@ -1897,8 +1897,8 @@ cudaError_t launch_max(const float* logw, int64_t ld, int32_t N, int32_t P, cons
     chunk = (chunk + 3) / 4 * 4;
     const bool vec = aligned16(logw) && (ld % 4 == 0);
     const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
-    if (vec) { ProfScope ps_("k_max", s); k_max<true><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
-    else { ProfScope ps_("k_max", s); k_max<false><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
+    if (vec) { ProfScope ps_("k_max", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u); k_max<true><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
+    else { ProfScope ps_("k_max", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u); k_max<false><<<grid, kThreads, 0, s>>>(logw, ld, P, cpf, chunk, ws, status_out, lmax_out, bad_out); }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -1911,7 +1911,7 @@ cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, con
     if (N >= sm_count() && P <= (1 << 17)) {
         // a CTA per filter (no lookback): 2 CTAs per SM, persistent over the filters
         const unsigned g = static_cast<unsigned>(std::min<int64_t>(N, 2LL * sm_count()));
-        ProfScope ps_("k_scan", s);
+        ProfScope ps_("k_scan", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * (write_q ? 12u : 4u));
         if (vec) k_scan_cta<true><<<g, kScanCtaT, 0, s>>>(logw, ld, N, P, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out);
         else k_scan_cta<false><<<g, kScanCtaT, 0, s>>>(logw, ld, N, P, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out);
         ++*launches;
@@ -1919,9 +1919,9 @@ cudaError_t launch_scan(const float* logw, int64_t ld, int32_t N, int32_t P, con
     }
     const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * L.T));
     if (vec)
-        { ProfScope ps_("k_scan", s); k_scan<true><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
+        { ProfScope ps_("k_scan", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * (write_q ? 12u : 4u)); k_scan<true><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
     else
-        { ProfScope ps_("k_scan", s); k_scan<false><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
+        { ProfScope ps_("k_scan", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * (write_q ? 12u : 4u)); k_scan<false><<<grid, kThreads, 0, s>>>(logw, ld, P, L.T, kfx, ws, L.ldq, write_q ? 1 : 0, lse_out, ess_out); }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -1947,7 +1947,7 @@ cudaError_t launch_bsearch_buckets(int32_t N, int32_t P, const Layout& L, const 
                                    uint64_t* launches) {
     const int lgNB = ceil_log2(P);
     {
-        ProfScope ps_("k_bsearch", s);
+        ProfScope ps_("k_bsearch", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 12u);  // Q read once, ancestors written
         k_bsearch_buckets<<<static_cast<unsigned>(grid_for(static_cast<int64_t>(N) * cdiv(P, 8), 8)), kThreads, 0,
                             s>>>(N, P, ws, L.ldq, L.ldb, lgNB, make_key(seed), first_filter, anc, ld_anc);
     }
@@ -1966,7 +1966,7 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
         const int cpf = static_cast<int>(cdiv(static_cast<int64_t>(NB) + P, chunk));
         ModeBuckets md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, lgNB, NB, P, ws.bidx, L.ldb};
         {
-            ProfScope ps_("k_merge_buckets", s);
+            ProfScope ps_("k_merge_buckets", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u + static_cast<uint64_t>(N) * static_cast<uint64_t>(NB) * 4u);
             k_merge<ModeBuckets><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf,
                                                                                                         chunk);
         }
@@ -1978,10 +1978,10 @@ cudaError_t launch_search(int scheme, int32_t N, int32_t P, const Layout& L, con
         const dim3 grid(static_cast<unsigned>(static_cast<int64_t>(N) * cpf));
         if (scheme == 2) {
             ModeSorted<2> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
-            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<2>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
+            { ProfScope ps_("k_merge", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 12u); k_merge<ModeSorted<2>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
         } else {
             ModeSorted<3> md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, stratum_width(P), key, first_filter, P, anc, ld_anc};
-            { ProfScope ps_("k_merge", s); k_merge<ModeSorted<3>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
+            { ProfScope ps_("k_merge", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 12u); k_merge<ModeSorted<3>><<<grid, kThreads, 0, s>>>(md, cpf, chunk); }
         }
     }
     ++*launches;
@@ -1994,10 +1994,10 @@ cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t 
     const int64_t total = static_cast<int64_t>(N) * P;
     if (B > 0) {
         if (aligned16(logw) && ld % 4 == 0 && P % 4 == 0) {
-            { ProfScope ps_("k_mexp_vec", s); k_mexp_vec<<<static_cast<unsigned>(grid_for(total / 4)), kThreads, 0, s>>>(
+            { ProfScope ps_("k_mexp_vec", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u); k_mexp_vec<<<static_cast<unsigned>(grid_for(total / 4)), kThreads, 0, s>>>(
                 reinterpret_cast<const float4*>(logw), ld / 4, N, P / 4, ws, L.ldq / 4); }
         } else {
-            { ProfScope ps_("k_mexp", s); k_mexp<<<static_cast<unsigned>(grid_for(total)), kThreads, 0, s>>>(logw, ld, N, P, ws, L.ldq); }
+            { ProfScope ps_("k_mexp", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u); k_mexp<<<static_cast<unsigned>(grid_for(total)), kThreads, 0, s>>>(logw, ld, N, P, ws, L.ldq); }
         }
         ++*launches;
     }
@@ -2010,11 +2010,11 @@ cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t 
             cudaGetLastError();
             return 1;
         });
-        ProfScope ps_("k_metro", s);
+        ProfScope ps_("k_metro", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);  // w read once, ancestors written
         k_metro_fpc<<<static_cast<unsigned>(std::min<int64_t>(N, sm_count())), 1024, 0, s>>>(
             N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc);
     } else {
-        ProfScope ps_("k_metro", s);
+        ProfScope ps_("k_metro", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
         k_metro<<<static_cast<unsigned>(cdiv(total, kThreads)), kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed),
                                                                                first_filter, B, anc, ld_anc);
     }
@@ -2050,7 +2050,7 @@ cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int3
         });
         const int vec = ((reinterpret_cast<uintptr_t>(anc) & 15) == 0 && ld_anc % 4 == 0) ? 1 : 0;
         const unsigned g = static_cast<unsigned>(std::min<int64_t>(2LL * N, sm_count()));
-        ProfScope ps_("k_hist", s);
+        ProfScope ps_("k_hist", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
         k_hist_smem<<<g, kHistT, smem, s>>>(anc, ld_anc, N, P, o, ld_o, vec);
         ++*launches;
         return cudaPeekAtLastError();
@@ -2064,10 +2064,10 @@ cudaError_t launch_offspring(const int32_t* anc, int64_t ld_anc, int32_t N, int3
         const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
         const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
                                                                                      sm_count() * 8)));
-        ProfScope ps_("k_hist", s);
+        ProfScope ps_("k_hist", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
         k_hist_runs<<<g, kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o);
     } else {
-        ProfScope ps_("k_hist", s);
+        ProfScope ps_("k_hist", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
         k_hist<<<static_cast<unsigned>(grid_for(total, 16)), kThreads, 0, s>>>(anc, ld_anc, N, P, o, ld_o);
     }
     ++*launches;
@@ -2078,11 +2078,12 @@ cudaError_t launch_permute_from_offspring(const int32_t* o, int64_t ld_o, int32_
                                          const Ws& ws, int32_t* perm, int64_t ld_perm, cudaStream_t s,
                                          uint64_t* launches) {
     const int o_vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0 && ld_o % 4 == 0) ? 1 : 0;
-    { ProfScope ps_("k_pscan", s); k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, o, ld_o, o_vec, perm,
+    { ProfScope ps_("k_pscan", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 12u);  // o read, permutation (survivors) + free list written
+      k_pscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T), kThreads, 0, s>>>(P, L.T, ws, L.ldq, o, ld_o, o_vec, perm,
                                                                                      ld_perm); }
     ++*launches;
     {
-        ProfScope ps_("k_push", s);
+        ProfScope ps_("k_push", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);  // o and the free list read
         const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
         const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
                                                                                      sm_count() * 8)));
@@ -2115,13 +2116,13 @@ cudaError_t launch_gather_inplace(void* X, int64_t row_bytes, int64_t ld_bytes, 
         const int64_t nblk = static_cast<int64_t>(N) * cdiv(P, 128);
         const unsigned g2 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cdiv(nblk, kThreads / 32),
                                                                                       sm_count() * 8)));
-        ProfScope ps_("k_gather_inplace", s);
+        ProfScope ps_("k_gather_inplace", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u, 2u * static_cast<uint64_t>(row_bytes));
         k_gather_rows16<<<g2, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, static_cast<int>(cpr), perm,
                                                 ld_perm);
     }
-    else if (ch == 16) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
-    else if (ch == 4) { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<4><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
-    else { ProfScope ps_("k_gather_inplace", s); k_gather_inplace<1><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    else if (ch == 16) { ProfScope ps_("k_gather_inplace", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u, 2u * static_cast<uint64_t>(row_bytes)); k_gather_inplace<16><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    else if (ch == 4) { ProfScope ps_("k_gather_inplace", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u, 2u * static_cast<uint64_t>(row_bytes)); k_gather_inplace<4><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
+    else { ProfScope ps_("k_gather_inplace", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 4u, 2u * static_cast<uint64_t>(row_bytes)); k_gather_inplace<1><<<grid, kThreads, 0, s>>>(x, ld_bytes, ld_filter_bytes, N, P, cpr, perm, ld_perm); }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -2137,9 +2138,9 @@ cudaError_t launch_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t
     const int64_t cpr = row_bytes / ch;
     const int64_t total = static_cast<int64_t>(P) * cpr;
     const unsigned grid = static_cast<unsigned>(grid_for(total, 16));
-    if (ch == 16) { ProfScope ps_("k_gather_out", s); k_gather_out<16><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
-    else if (ch == 4) { ProfScope ps_("k_gather_out", s); k_gather_out<4><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
-    else { ProfScope ps_("k_gather_out", s); k_gather_out<1><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    if (ch == 16) { ProfScope ps_("k_gather_out", s, static_cast<uint64_t>(P) * (4u + 2u * static_cast<uint64_t>(row_bytes))); k_gather_out<16><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    else if (ch == 4) { ProfScope ps_("k_gather_out", s, static_cast<uint64_t>(P) * (4u + 2u * static_cast<uint64_t>(row_bytes))); k_gather_out<4><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
+    else { ProfScope ps_("k_gather_out", s, static_cast<uint64_t>(P) * (4u + 2u * static_cast<uint64_t>(row_bytes))); k_gather_out<1><<<grid, kThreads, 0, s>>>(x, y, ld_x, ld_y, P, cpr, anc); }
     ++*launches;
     return cudaPeekAtLastError();
 }
@@ -2160,7 +2161,7 @@ cudaError_t launch_shard_search(int scheme, const uint64_t* Q, int32_t Pl, int64
     }
     ++*launches;
     if (scheme == 1) {
-        ProfScope ps_("k_shard_multinomial", s);
+        ProfScope ps_("k_shard_multinomial", s, static_cast<uint64_t>(Pl) * 12u);
         k_shard_multinomial<<<static_cast<unsigned>(grid_for((P_global + 1) / 2, 8)), kThreads, 0, s>>>(
             Q, Pl, p0, P_global, dctx, key, filt, anc);
         ++*launches;
@@ -2170,11 +2171,11 @@ cudaError_t launch_shard_search(int scheme, const uint64_t* Q, int32_t Pl, int64
     const int cpf = static_cast<int>(cdiv(P_global + Pl, chunk));
     if (scheme == 2) {
         ModeShard<2> md{Q, dctx, D, key, filt, Pl, p0, anc};
-        ProfScope ps_("k_merge", s);
+        ProfScope ps_("k_merge", s, static_cast<uint64_t>(Pl) * 12u);  // Q read, ~Pl slots written
         k_merge<ModeShard<2>><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
     } else {
         ModeShard<3> md{Q, dctx, D, key, filt, Pl, p0, anc};
-        ProfScope ps_("k_merge", s);
+        ProfScope ps_("k_merge", s, static_cast<uint64_t>(Pl) * 12u);
         k_merge<ModeShard<3>><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
     }
     ++*launches;
@@ -2183,7 +2184,7 @@ cudaError_t launch_shard_search(int scheme, const uint64_t* Q, int32_t Pl, int64
 
 cudaError_t launch_shard_weights(const float* logw, int32_t Pl, const float* gmax, float* w, cudaStream_t s,
                                  uint64_t* launches) {
-    ProfScope ps_("k_shard_weights", s);
+    ProfScope ps_("k_shard_weights", s, static_cast<uint64_t>(Pl) * 8u);
     k_shard_weights<<<static_cast<unsigned>(grid_for(Pl)), kThreads, 0, s>>>(logw, Pl, gmax, w);
     ++*launches;
     return cudaPeekAtLastError();
@@ -2192,7 +2193,7 @@ cudaError_t launch_shard_weights(const float* logw, int32_t Pl, const float* gma
 cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, int32_t nslots, uint64_t seed,
                                int32_t B, uint32_t filt, const float* gmax, const int32_t* gbad, int32_t* anc,
                                cudaStream_t s, uint64_t* launches) {
-    ProfScope ps_("k_metro_slots", s);
+    ProfScope ps_("k_metro_slots", s, static_cast<uint64_t>(nslots) * 8u);
     k_metro_slots<<<static_cast<unsigned>(cdiv(nslots, kThreads)), kThreads, 0, s>>>(w, P_global, slot0, nslots,
                                                                                      make_key(seed), filt, B, gmax,
                                                                                      gbad, anc);
@@ -2271,7 +2272,7 @@ cudaError_t launch_shard_search_sorted(const uint64_t* Q, int32_t Pl, int64_t p0
     const int cpf = static_cast<int>(cdiv(P_global + Pl, chunk));
     ModeShardSpacings md{Q, dctx, G, Pl, p0, anc};
     {
-        ProfScope ps_("k_merge", s);
+        ProfScope ps_("k_merge", s, static_cast<uint64_t>(Pl) * 20u);  // Q and G read, ~Pl slots written
         k_merge<ModeShardSpacings><<<static_cast<unsigned>(cpf), kThreads, 0, s>>>(md, cpf, chunk);
     }
     ++*launches;
@@ -2283,7 +2284,7 @@ cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, con
                                       uint64_t* launches, bool spacings_only) {
     const Key key = make_key(seed);
     if (spacings_only) {
-        ProfScope ps_("k_gscan", s);
+        ProfScope ps_("k_gscan", s, (static_cast<uint64_t>(N) * static_cast<uint64_t>(P) + N) * 8u);  // G_0..G_P written
         k_gscan<<<static_cast<unsigned>(static_cast<int64_t>(N) * L.T2), kThreads, 0, s>>>(P, L.T2, ws, L.ldg, key,
                                                                                           first_filter);
         ++*launches;
@@ -2293,7 +2294,7 @@ cudaError_t launch_sorted_multinomial(int32_t N, int32_t P, const Layout& L, con
     const int cpf = static_cast<int>(cdiv(2 * static_cast<int64_t>(P), chunk));
     ModeSpacings md{ws.Q, L.ldq, ws.Qtot, ws.fstatus, ws.G, L.ldg, ws.Gtot, P, anc, ld_anc};
     {
-        ProfScope ps_("k_merge_spacings", s);
+        ProfScope ps_("k_merge_spacings", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 20u);  // Q and G read, ancestors written
         k_merge<ModeSpacings><<<static_cast<unsigned>(static_cast<int64_t>(N) * cpf), kThreads, 0, s>>>(md, cpf,
                                                                                                      chunk);
     }

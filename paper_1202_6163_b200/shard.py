@@ -45,26 +45,69 @@ def shard_range(P_global: int, world: int, rank: int):
     return p0, min(P_global, p0 + per) - p0
 
 
-class TorchComm:
-    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+def check_shards(P_global: int, world: int):
+    """Every rank must hold at least one particle (the exchange steps assume it).  Evaluated from
+    (P_global, world) alone, so every rank reaches the same verdict before any collective: a bad
+    configuration raises on all ranks instead of leaving the others waiting in a collective."""
+    if world < 1 or P_global < 1:
+        raise ValueError(f"P_global={P_global}, world={world}")
+    per = -(-P_global // world)
+    if (world - 1) * per >= P_global:
+        raise ValueError(f"P_global={P_global} over {world} ranks leaves ranks without particles "
+                         f"(contiguous shards of {per}); use at most {-(-P_global // per)} ranks or a larger filter")
 
-    def __init__(self, group=None):
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU).
+
+    With ``timing=True`` (CUDA tensors) every collective is bracketed by CUDA events on the
+    current stream, so ``collect_times()`` reports each kind's device time as the stream sees it
+    (the NCCL kernel plus its wait): {name: (calls, total_ms, bytes)}."""
+
+    def __init__(self, group=None, timing: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.timing = timing
+        self._ev = []
+
+    def _timed(self, name, nbytes, fn):
+        if not self.timing:
+            return fn()
+        import torch
+
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        self._ev.append((name, a, b, nbytes))
+        return r
+
+    def collect_times(self):
+        import torch
+
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b, nb in self._ev:
+            c, ms, by = out.get(name, (0, 0.0, 0))
+            out[name] = (c + 1, ms + a.elapsed_time(b), by + nb)
+        self._ev = []
+        return out
 
     def all_reduce_max(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        self._timed("all_reduce_max", t.numel() * t.element_size(),
+                    lambda: self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group))
         return t
 
     def all_gather_cat(self, t):
         import torch
 
         out = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(out, t, group=self.group)
+        self._timed("all_gather", t.numel() * t.element_size() * self.world,
+                    lambda: self.dist.all_gather(out, t, group=self.group))
         return torch.cat(out)
 
     def reduce_scatter_sum(self, t):
@@ -77,7 +120,8 @@ class TorchComm:
             self.dist.all_reduce(t, group=self.group)
             out.copy_(t[self.rank * n:(self.rank + 1) * n])
         else:
-            self.dist.reduce_scatter_tensor(out, t, group=self.group)
+            self._timed("reduce_scatter", t.numel() * t.element_size(),
+                        lambda: self.dist.reduce_scatter_tensor(out, t, group=self.group))
         return out
 
     def all_to_all_v(self, t, send_splits, recv_splits):
@@ -85,15 +129,27 @@ class TorchComm:
         import torch
 
         out = torch.empty((sum(recv_splits),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=list(recv_splits),
-                                    input_split_sizes=list(send_splits), group=self.group)
+        row = math.prod(t.shape[1:]) * t.element_size()
+        self._timed("all_to_all", row * (sum(recv_splits) + sum(send_splits)),
+                    lambda: self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=list(recv_splits),
+                                                        input_split_sizes=list(send_splits), group=self.group))
         return out
+
+    def broadcast_(self, t, src: int):
+        """t (contiguous) from rank ``src`` to every rank, in place."""
+        self._timed("broadcast", t.numel() * t.element_size(),
+                    lambda: self.dist.broadcast(t, src=self.dist.get_global_rank(self.group, src) if self.group
+                                                else src, group=self.group))
+        return t
 
 
 class SingleComm:
     """World of one (no communication): the sharded path on a single GPU."""
 
     rank, world = 0, 1
+
+    def collect_times(self):
+        return {}
 
     def all_reduce_max(self, t):
         return t
@@ -105,6 +161,9 @@ class SingleComm:
         return t
 
     def all_to_all_v(self, t, send_splits, recv_splits):
+        return t
+
+    def broadcast_(self, t, src: int):
         return t
 
 
@@ -158,9 +217,16 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
 
     logw_local: this rank's contiguous shard (``shard_range(P_global, world, rank)``).
     Returns (ancestors, info): with ``assemble`` the full int32 [P_global] ancestor
-    vector on every rank (all_reduce MAX of per-rank slot writes / all_gather of
-    Metropolis chains); otherwise this rank's slots only (Metropolis: slots
-    [p0, p0 + Pl); prefix-sum schemes: entries [k_lo, k_hi) of a [P_global] buffer).
+    vector on every rank (each rank's contiguous slot range broadcast from it: P_global x 4
+    bytes received per rank; the unsorted multinomial, whose slots scatter over the filter,
+    all-reduces the vector; Metropolis all-gathers the chains); otherwise this rank's slots
+    only (Metropolis: slots [p0, p0 + Pl); prefix-sum schemes: entries [k_lo, k_hi) of a
+    [P_global] buffer).
+
+    Errors never strand the other ranks in a collective: a configuration that leaves a rank
+    without particles raises on every rank before any exchange (``check_shards``); a shard of
+    the wrong size is replaced by a NaN shard of the right size (so every rank computes the
+    NS-1 invalid result through the same exchanges) and then raises on its own rank.
     """
     import torch
 
@@ -169,11 +235,12 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     scheme_id = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
     is_sorted = _sorted(scheme_id, flags)
     world, rank = comm.world, comm.rank
+    check_shards(P_global, world)
     p0, Pl = shard_range(P_global, world, rank)
-    if logw_local.shape[0] != Pl:
-        raise ValueError(f"rank {rank}: shard has {logw_local.shape[0]} particles, expected {Pl}")
-    if Pl < 1:
-        raise ValueError("every rank needs at least one particle")
+    shape_err = None
+    if logw_local.dim() != 1 or logw_local.shape[0] != Pl:
+        shape_err = f"rank {rank}: shard has shape {tuple(logw_local.shape)}, expected ({Pl},)"
+        logw_local = torch.full((Pl,), float("nan"), dtype=logw_local.dtype, device=logw_local.device)
     lmax, bad = stages.max(logw_local)
     gmax = comm.all_reduce_max(lmax.clone())
     gbad = comm.all_reduce_max(bad.clone())
@@ -188,11 +255,14 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
         anc_local = stages.metropolis(w_full, p0, Pl, seed, B, filter_index, gmax, gbad)
         info["slot_range"] = (p0, p0 + Pl)
         if not assemble:
+            _raise_if(shape_err)
             return anc_local, info
         per_anc = anc_local
         if Pl < per:
             per_anc = torch.cat([anc_local, torch.zeros(per - Pl, dtype=anc_local.dtype, device=anc_local.device)])
-        return comm.all_gather_cat(per_anc)[:P_global].contiguous(), info
+        out = comm.all_gather_cat(per_anc)[:P_global].contiguous()
+        _raise_if(shape_err)
+        return out, info
     Q, total, wsum = stages.scan(logw_local, P_global, gmax)
     totals = comm.all_gather_cat(total)
     wsums = comm.all_gather_cat(wsum)
@@ -206,8 +276,30 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
     info["slot_range_dev"] = rng
     info["lse"] = (gmax, wsums)  # lse = gmax + ln(sum wsums) (NS-13), left on the device
     if not assemble:
+        _raise_if(shape_err)
         return anc, info
-    return comm.all_reduce_max(anc), info
+    if scheme_id == 1 and not is_sorted:
+        # the unsorted multinomial's slots scatter over the whole filter
+        out = comm.all_reduce_max(anc)
+    else:
+        # contiguous slot ranges: each rank's slice broadcast from it (an invalid filter's
+        # identity was written over every rank's own particle range)
+        rngs = comm.all_gather_cat(rng).cpu().view(-1, 2).tolist()
+        invalid = bool(int(gbad.max().item()) != 0 or float(gmax.max().item()) == float("-inf"))
+        for g in range(world):
+            a, b = shard_range(P_global, world, g) if invalid else rngs[g]
+            if invalid:
+                b = a + b
+            if b > a:
+                comm.broadcast_(anc[a:b], g)
+        out = anc
+    _raise_if(shape_err)
+    return out, info
+
+
+def _raise_if(msg):
+    if msg:
+        raise ValueError(msg)
 
 
 def _overlap(a0, a1, b0, b1):

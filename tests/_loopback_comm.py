@@ -40,6 +40,12 @@ class LoopbackComm:
         s = torch.stack(self._exchange(t)).sum(dim=0).to(t.dtype)
         return s[self.rank * n:(self.rank + 1) * n].contiguous()
 
+    def broadcast_(self, t, src: int):
+        got = self._exchange(t)
+        if self.rank != src:
+            t.copy_(got[src])
+        return t
+
     def all_to_all_v(self, t, send_splits, recv_splits):
         got = self._exchange((t, list(send_splits)))
         parts = []

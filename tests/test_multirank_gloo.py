@@ -14,6 +14,7 @@
 """
 from __future__ import annotations
 
+import json
 import os
 import socket
 import sys
@@ -123,3 +124,46 @@ def test_two_rank_giant_filter_and_batches(tmp_path):
     xs = pfinputs.gaussian_logw(500, 1.0, seed=11, N=3 * world)
     _, want = oracle.resample_batched("stratified", xs, 99, first_filter=0)
     assert np.array_equal(np.load(os.path.join(tmp_path, "batched.npy")), want)
+
+
+def _worker_errors(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    import pfinputs
+    from paper_1202_6163_b200.shard import TorchComm, resample_sharded, shard_range
+    from tests._cpu_shard_stages import CpuOracleStages
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm, stages = TorchComm(), CpuOracleStages()
+    res = {}
+    # a wrong-size shard on rank 1: every rank finishes the exchanges (the filter is NS-1 invalid
+    # everywhere), rank 1 raises, rank 0 holds the identity
+    P = 600
+    x = pfinputs.gaussian_logw(P, 1.0, seed=3)
+    for scheme in ("systematic", "metropolis"):
+        p0, Pl = shard_range(P, world, rank)
+        mine = x[p0:p0 + Pl - (5 if rank == 1 else 0)].copy()
+        try:
+            anc, _ = resample_sharded(scheme, torch.from_numpy(mine), P, 4, B=3, comm=comm, stages=stages)
+            res[scheme] = ("ok", anc.numpy().tolist())
+        except ValueError as e:
+            res[scheme] = ("error", str(e))
+    # a configuration that leaves a rank without particles raises on every rank, before any collective
+    try:
+        resample_sharded("systematic", torch.zeros(1), 1, 4, comm=comm, stages=stages)
+        res["empty"] = ("ok", None)
+    except ValueError as e:
+        res["empty"] = ("error", str(e))
+    dist.barrier()  # both ranks are still in step
+    np.save(os.path.join(outdir, f"err_{rank}.npy"), np.array([json.dumps(res)]))
+    dist.destroy_process_group()
+
+
+def test_two_rank_errors_do_not_hang(tmp_path):
+    world = 2
+    mp.spawn(_worker_errors, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    r0 = json.loads(str(np.load(os.path.join(tmp_path, "err_0.npy"))[0]))
+    r1 = json.loads(str(np.load(os.path.join(tmp_path, "err_1.npy"))[0]))
+    for scheme in ("systematic", "metropolis"):
+        assert r1[scheme][0] == "error" and "shape" in r1[scheme][1]
+        assert r0[scheme][0] == "ok" and r0[scheme][1] == list(range(600))  # NS-1: identity
+    assert r0["empty"][0] == "error" and r1["empty"][0] == "error"

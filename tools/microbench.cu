@@ -9,6 +9,10 @@
 //  rand4_l2 : warp-wide random 4-byte loads from 256 KiB windows (L2-resident):
 //             the Metropolis proposal pattern, loads per second
 //  rand4_smem: the same from shared memory (upper bound for smem-resident w)
+//  l2_stream: float4 reads (ld.global.cg) of an L2-resident buffer, repeated (L2 read bandwidth:
+//             the roofline denominator of the L2-resident C2 working set)
+//  l2_sector: random 32-byte sector reads of an L2-resident buffer (the random-sector rate that
+//             bounds the multinomial bucket searches and the Metropolis proposals)
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -67,6 +71,33 @@ __global__ void k_rand4(const float* __restrict__ w, int64_t nwin, int steps, fl
         for (int t = 0; t < 8; ++t) { s = s * 1664525u + 1013904223u; x[t] = __ldg(win + (s >> 16)); }
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc += x[t];
+    }
+    if (acc == 12345.f) out[0] = acc;
+}
+
+__global__ void k_l2_stream(const float4* __restrict__ a, int64_t n4, int reps, float* out) {
+    float acc = 0.f;
+    for (int r = 0; r < reps; ++r)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(a + i);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    if (acc == 12345.f) out[0] = acc;
+}
+
+// each thread reads 8 independent random 32-byte sectors (two float4 each) per step
+__global__ void k_l2_sector(const float4* __restrict__ a, int64_t nsec, int steps, float* out) {
+    uint32_t s = hash32((uint32_t)(blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 7u);
+    float acc = 0.f;
+    for (int b = 0; b < steps; ++b) {
+        float4 x[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            s = s * 1664525u + 1013904223u;
+            x[t] = __ldcg(a + 2 * (int64_t)(hash32(s) % (uint32_t)nsec));
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc += x[t].x;
     }
     if (acc == 12345.f) out[0] = acc;
 }
@@ -150,6 +181,29 @@ int main() {
         CK(cudaEventSynchronize(e1));
         cudaEventElapsedTime(&ms, e0, e1);
         printf("{\"bench\":\"rand4_smem\",\"loads_per_s\":%.3e}\n", (double)blocks * threads * steps * 4 / (ms * 1e-3));
+    }
+    // ---- L2: 32 MiB resident buffer
+    {
+        const int64_t n4 = (int64_t(32) << 20) / 16;
+        const int reps = 20;
+        k_l2_stream<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(b), n4, 2, out);
+        cudaEventRecord(e0);
+        k_l2_stream<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(b), n4, reps, out);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("{\"bench\":\"l2_stream\",\"MiB\":32,\"GBs\":%.1f}\n", (double)n4 * 16 * reps / (ms * 1e-3) / 1e9);
+        const int64_t nsec = (int64_t(32) << 20) / 32;
+        const int steps = 64;
+        k_l2_sector<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(b), nsec, 4, out);
+        cudaEventRecord(e0);
+        k_l2_sector<<<sms * 8, 256>>>(reinterpret_cast<const float4*>(b), nsec, steps, out);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double sectors = (double)sms * 8 * 256 * steps * 8;
+        printf("{\"bench\":\"l2_random_sector\",\"MiB\":32,\"sectors_per_s\":%.3e,\"GBs_32B\":%.1f}\n",
+               sectors / (ms * 1e-3), sectors * 32 / (ms * 1e-3) / 1e9);
     }
     return 0;
 }

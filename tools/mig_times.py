@@ -54,7 +54,7 @@ def main():
     torch.cuda.synchronize()
     tr = pf.pf_profile_collect()
     pf.pf_profile_enable(False)
-    for k, (n, ms) in sorted(tr.items(), key=lambda kv: -kv[1][1]):
+    for k, (n, ms, *_) in sorted(tr.items(), key=lambda kv: -kv[1][1]):
         print(json.dumps({"kernel": k, "launches_per_step": n / a.reps, "ms_per_step": ms / a.reps}))
 
 

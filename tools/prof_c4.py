@@ -27,7 +27,7 @@ def main():
     kt = pf.pf_profile_collect()
     pf.pf_profile_enable(False)
     torch.cuda.synchronize()
-    out = {k: {"launches_per_step": c / 50, "us_per_step": 1e3 * t / 50} for k, (c, t) in kt.items()}
+    out = {k: {"launches_per_step": c / 50, "us_per_step": 1e3 * t / 50} for k, (c, t, *_) in kt.items()}
     print(json.dumps({"P": P, "kernels": out, "sum_us": sum(v["us_per_step"] for v in out.values())}))
 
 
