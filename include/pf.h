@@ -31,8 +31,14 @@
  *    (oracle/pfo.c) and independent of launch configuration and GPU count.
  *  - Workspace: by default the library uses its own pool keyed by (device,
  *    stream), grown on demand outside steady state ("pooled memory").
- *    Concurrent calls must use different streams or explicit workspaces.
- *  - Thread safety: distinct streams may be driven from distinct host threads.
+ *    The device is the CURRENT device (cudaGetDevice) of the calling thread:
+ *    make it the device of the buffers and of the stream (the Python binding
+ *    does so around every call).
+ *  - Thread safety: concurrent calls are safe on distinct streams.  Calls that
+ *    share a stream from several host threads must be serialised by the caller,
+ *    even with explicit workspaces: the binary64 shift buffer, PF_SORT_WEIGHTS,
+ *    pf_permute*, pf_gather_state* and every pf_shard_* stage always draw
+ *    scratch from the (device, stream) pool.
  */
 #ifndef PF_H
 #define PF_H
@@ -351,7 +357,7 @@ pf_status pf_metropolis_from_weights(const float* w_full, int64_t P_global, int6
 pf_status pf_shard_offspring(const int32_t* anc, int64_t n_anc, const int64_t* d_slot_range, int64_t win0,
                              int32_t Pw, const float* d_gmax, const int32_t* d_gbad, int32_t* offspring,
                              pf_stream_t stream);
-/* Bytes of the migration plan of a shard of Pl particles (16 per 2048-particle tile). */
+/* Bytes of the migration plan of a shard of Pl particles (24 per 2048-particle tile + 8). */
 size_t pf_shard_migration_plan_bytes(int32_t Pl);
 /* d_counts[0] = E = sum_i max(o_i - 1, 0), d_counts[1] = F = #{i : o_i = 0} (device int64);
  * plan (device, caller-owned, 8-byte aligned, >= pf_shard_migration_plan_bytes(Pl)) receives
@@ -397,8 +403,10 @@ pf_status pf_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* 
 
 /*
  * Host helper: minimum B with lambda^B <= eps (alpha+beta)/max(alpha,beta)
- * (Eq. (4)-(5)), alpha = (1 - w_max)/(P w_max) (Eq. (2)), beta = 1/P.  Returns 0 if
- * B = 0 already satisfies Eq. (4), -1 on invalid arguments.  Host-only, no GPU.
+ * (Eq. (4)-(5)), alpha = (1 - w_max)/(P w_max) (Eq. (2)), beta = 1/P.  Returns at least 1
+ * (a resampler takes at least one step: 1 when Eq. (4) holds already or lambda <= 0;
+ * DESIGN R-22), -1 on invalid arguments: P < 1, eps <= 0, w_max outside [1/P, 1] (a maximum
+ * of P normalised weights is >= 1/P), or a B beyond INT32_MAX.  Host-only, no GPU.
  */
 int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps);
 

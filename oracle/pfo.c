@@ -590,15 +590,20 @@ void pfo_gather_out(const void* X, void* Y, int64_t row_bytes, int64_t ld_x, int
 /* ------------------------------------------------------------------------ */
 /* P:142-186 two-state chain, Eq. (2) alpha, beta = 1/P, Eq. (5).           */
 /* ------------------------------------------------------------------------ */
+/* Readings (R-22): B >= 1 (B = max(1, ceil(Eq. (5)))); w_max < 1/P
+ * lies outside Eq. (2)'s domain and a B beyond int32 is not representable:
+ * both return -1. */
 int32_t pfo_metropolis_required_B(int64_t P, double w_max, double eps)
 {
     double beta = 1.0 / (double)P;
+    if (w_max * (double)P < 1.0 - 1e-12) return -1;            /* w_max >= 1/P */
     double alpha = (1.0 - w_max) / ((double)P * w_max);         /* Eq. (2) */
     double lambda = 1.0 - alpha - beta;
     double mx = alpha > beta ? alpha : beta;
     double target = eps * (alpha + beta) / mx;                  /* Eq. (4) */
-    if (target >= 1.0) return 0;
+    if (target >= 1.0) return 1;                                /* S:250 clamp */
     if (lambda <= 0.0) return 1;
-    double B = log(target) / log(lambda);                       /* Eq. (5) */
-    return (int32_t)ceil(B);
+    double B = ceil(log(target) / log(lambda));                 /* Eq. (5) */
+    if (B > 2147483647.0) return -1;
+    return B < 1.0 ? 1 : (int32_t)B;
 }

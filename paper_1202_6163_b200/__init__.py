@@ -158,6 +158,41 @@ def _need_cuda(t, dtype, name):
         raise PfError(f"{name} must be {dtype}, got {t.dtype}")
 
 
+def _same_device(t, ref, name):
+    if t.device != ref.device:
+        raise PfError(f"{name} is on {t.device}, logw on {ref.device}: every buffer of a call must be on one device")
+
+
+def _need_vec(t, dtype, name, ref, n):
+    """A caller buffer the library writes n elements of, densely: right dtype, same device as
+    logw, contiguous, at least n elements (the C ABI cannot see tensor sizes)."""
+    _need_cuda(t, dtype, name)
+    _same_device(t, ref, name)
+    if not t.is_contiguous():
+        raise PfError(f"{name} must be contiguous")
+    if t.numel() < n:
+        raise PfError(f"{name} has {t.numel()} elements, the call writes {n}")
+
+
+def _need_rows(t, dtype, name, ref, N, P, ld=None):
+    """A caller [N, P] int32 buffer written with row stride ld (the ancestors' stride)."""
+    _need_cuda(t, dtype, name)
+    _same_device(t, ref, name)
+    if t.dim() != 2 or t.shape[0] < N or t.shape[1] < P or t.stride(1) != 1:
+        raise PfError(f"{name} must be a row-contiguous [>= {N}, >= {P}] tensor, got {tuple(t.shape)}")
+    if ld is not None and t.stride(0) != ld:
+        raise PfError(f"{name} must have the ancestors' row stride {ld}, got {t.stride(0)}")
+
+
+def _need_state(X, ref, N, P, batched):
+    _same_device(X, ref, "state")
+    if batched:
+        if X.dim() < 2 or X.shape[0] < N or X.shape[1] < P:
+            raise PfError(f"state must be [>= {N}, >= {P}, ...], got {tuple(X.shape)}")
+    elif X.dim() < 1 or X.shape[0] < P:
+        raise PfError(f"state must have >= {P} rows, got {tuple(X.shape)}")
+
+
 def _rows(t, name):
     """(ptr, ld) of a 1-D contiguous or 2-D row-strided tensor."""
     if t.dim() == 1:
@@ -224,25 +259,23 @@ def pf_resample_ex(scheme, logw, seed: int, B: int = 0, ancestors=None, filter_i
     P = logw.shape[0]
     if ancestors is None:
         ancestors = torch.empty(P, dtype=torch.int32, device=logw.device)
-    _need_cuda(ancestors, torch.int32, "ancestors")
+    _need_vec(ancestors, torch.int32, "ancestors", logw, P)
     opts = _Opts(filter_index=filter_index, flags=flags)
-    if lse_out is not None:
-        _need_cuda(lse_out, torch.float64, "lse_out"); opts.lse_out = lse_out.data_ptr()
-    if ess_out is not None:
-        _need_cuda(ess_out, torch.float64, "ess_out"); opts.ess_out = ess_out.data_ptr()
-    if normw_out is not None:
-        _need_cuda(normw_out, torch.float32, "normw_out"); opts.normw_out = normw_out.data_ptr()
-    if status_out is not None:
-        _need_cuda(status_out, torch.int32, "status_out"); opts.status_out = status_out.data_ptr()
-    if offspring_out is not None:
-        _need_cuda(offspring_out, torch.int32, "offspring_out"); opts.offspring_out = offspring_out.data_ptr()
-    if permuted_out is not None:
-        _need_cuda(permuted_out, torch.int32, "permuted_out"); opts.permuted_out = permuted_out.data_ptr()
+    for name, t, dt, n in (("lse_out", lse_out, torch.float64, 1), ("ess_out", ess_out, torch.float64, 1),
+                           ("normw_out", normw_out, torch.float32, P), ("status_out", status_out, torch.int32, 1),
+                           ("offspring_out", offspring_out, torch.int32, P),
+                           ("permuted_out", permuted_out, torch.int32, P)):
+        if t is not None:
+            _need_vec(t, dt, name, logw, n)
+            setattr(opts, name, t.data_ptr())
+    if state is not None:
+        _need_state(state, logw, 1, P, False)
     _set_state(opts, state, False)
     _set_workspace(opts, workspace)
     fn = "pf_resample_ex_f64" if f64 else "pf_resample_ex"
-    rc = getattr(lib(), fn)(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
-                            ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
+    with torch.cuda.device(logw.device):
+        rc = getattr(lib(), fn)(_scheme(scheme), logw.data_ptr(), P, seed & (2 ** 64 - 1), B,
+                                ancestors.data_ptr(), ctypes.byref(opts), _stream(logw, stream))
     _check(rc, fn)
     return ancestors
 
@@ -256,9 +289,10 @@ def _single(name, scheme):
         P = logw.shape[0]
         if ancestors is None:
             ancestors = torch.empty(P, dtype=torch.int32, device=logw.device)
-        _need_cuda(ancestors, torch.int32, "ancestors")
-        rc = getattr(lib(), name)(logw.data_ptr(), P, seed & (2 ** 64 - 1), B, ancestors.data_ptr(),
-                                  _stream(logw, stream))
+        _need_vec(ancestors, torch.int32, "ancestors", logw, P)
+        with torch.cuda.device(logw.device):
+            rc = getattr(lib(), name)(logw.data_ptr(), P, seed & (2 ** 64 - 1), B, ancestors.data_ptr(),
+                                      _stream(logw, stream))
         _check(rc, name)
         return ancestors
 
@@ -289,20 +323,26 @@ def pf_resample_batched(scheme, logw, seed: int, B: int = 0, first_filter: int =
     ptr, ld = _rows(logw, "logw")
     if ancestors is None:
         ancestors = torch.empty((N, P), dtype=torch.int32, device=logw.device)
-    _need_cuda(ancestors, torch.int32, "ancestors")
+    _need_rows(ancestors, torch.int32, "ancestors", logw, N, P)
     aptr, ald = _rows(ancestors, "ancestors")
     opts = _Opts(flags=flags)
-    for name, t, dt in (("lse_out", lse_out, torch.float64), ("ess_out", ess_out, torch.float64),
-                        ("normw_out", normw_out, torch.float32), ("status_out", status_out, torch.int32),
-                        ("offspring_out", offspring_out, torch.int32), ("permuted_out", permuted_out, torch.int32)):
+    for name, t, dt, n in (("lse_out", lse_out, torch.float64, N), ("ess_out", ess_out, torch.float64, N),
+                           ("normw_out", normw_out, torch.float32, N * P), ("status_out", status_out, torch.int32, N)):
         if t is not None:
-            _need_cuda(t, dt, name)
+            _need_vec(t, dt, name, logw, n)  # dense: [N] / [N, P]
             setattr(opts, name, t.data_ptr())
+    for name, t in (("offspring_out", offspring_out), ("permuted_out", permuted_out)):
+        if t is not None:
+            _need_rows(t, torch.int32, name, logw, N, P, ld=ald)  # written with the ancestors' row stride
+            setattr(opts, name, t.data_ptr())
+    if state is not None:
+        _need_state(state, logw, N, P, True)
     _set_state(opts, state, True)
     _set_workspace(opts, workspace)
     fn = "pf_resample_batched_f64" if f64 else "pf_resample_batched"
-    rc = getattr(lib(), fn)(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
-                            aptr, ald, ctypes.byref(opts), _stream(logw, stream))
+    with torch.cuda.device(logw.device):
+        rc = getattr(lib(), fn)(_scheme(scheme), ptr, ld, N, P, seed & (2 ** 64 - 1), first_filter, B,
+                                aptr, ald, ctypes.byref(opts), _stream(logw, stream))
     _check(rc, fn)
     return ancestors
 
@@ -324,20 +364,36 @@ def _set_workspace(opts, workspace):
 
 
 # ----------------------------------------------------------------------------- conversions
+def _pair_args(src, src_name, dst, dst_name):
+    """(N, P) of a [P] / [N, P] int32 source and a destination of the same shape and device."""
+    torch = _torch()
+    _need_cuda(src, torch.int32, src_name)
+    _need_cuda(dst, torch.int32, dst_name)
+    _same_device(dst, src, dst_name)
+    if src.dim() == 1:
+        _need_vec(dst, torch.int32, dst_name, src, src.shape[0])
+        return 1, src.shape[0]
+    if src.dim() != 2:
+        raise PfError(f"{src_name} must be [P] or [N, P]")
+    N, P = src.shape
+    _need_rows(dst, torch.int32, dst_name, src, N, P)
+    return N, P
+
+
 def pf_ancestors_to_offspring(anc, offspring=None, stream=None):
     """int32 [P] or [N, P] ancestors -> int32 offspring (NS-14)."""
     torch = _torch()
     _need_cuda(anc, torch.int32, "anc")
     if offspring is None:
         offspring = torch.empty_like(anc)
-    _need_cuda(offspring, torch.int32, "offspring")
-    if anc.dim() == 1:
-        rc = lib().pf_ancestors_to_offspring(anc.data_ptr(), anc.shape[0], offspring.data_ptr(), _stream(anc, stream))
-    else:
-        N, P = anc.shape
-        ap, ald = _rows(anc, "anc")
-        op, old = _rows(offspring, "offspring")
-        rc = lib().pf_ancestors_to_offspring_batched(ap, ald, N, P, op, old, _stream(anc, stream))
+    N, P = _pair_args(anc, "anc", offspring, "offspring")
+    with torch.cuda.device(anc.device):
+        if anc.dim() == 1:
+            rc = lib().pf_ancestors_to_offspring(anc.data_ptr(), P, offspring.data_ptr(), _stream(anc, stream))
+        else:
+            ap, ald = _rows(anc, "anc")
+            op, old = _rows(offspring, "offspring")
+            rc = lib().pf_ancestors_to_offspring_batched(ap, ald, N, P, op, old, _stream(anc, stream))
     _check(rc, "pf_ancestors_to_offspring")
     return offspring
 
@@ -348,14 +404,14 @@ def pf_permute(anc, permuted=None, stream=None):
     _need_cuda(anc, torch.int32, "anc")
     if permuted is None:
         permuted = torch.empty_like(anc)
-    _need_cuda(permuted, torch.int32, "permuted")
-    if anc.dim() == 1:
-        rc = lib().pf_permute(anc.data_ptr(), anc.shape[0], permuted.data_ptr(), _stream(anc, stream))
-    else:
-        N, P = anc.shape
-        ap, ald = _rows(anc, "anc")
-        pp, pld = _rows(permuted, "permuted")
-        rc = lib().pf_permute_batched(ap, ald, N, P, pp, pld, _stream(anc, stream))
+    N, P = _pair_args(anc, "anc", permuted, "permuted")
+    with torch.cuda.device(anc.device):
+        if anc.dim() == 1:
+            rc = lib().pf_permute(anc.data_ptr(), P, permuted.data_ptr(), _stream(anc, stream))
+        else:
+            ap, ald = _rows(anc, "anc")
+            pp, pld = _rows(permuted, "permuted")
+            rc = lib().pf_permute_batched(ap, ald, N, P, pp, pld, _stream(anc, stream))
     _check(rc, "pf_permute")
     return permuted
 
@@ -366,15 +422,14 @@ def pf_permute_offspring(offspring, permuted=None, stream=None):
     _need_cuda(offspring, torch.int32, "offspring")
     if permuted is None:
         permuted = torch.empty_like(offspring)
-    _need_cuda(permuted, torch.int32, "permuted")
-    if offspring.dim() == 1:
-        rc = lib().pf_permute_offspring(offspring.data_ptr(), offspring.shape[0], permuted.data_ptr(),
-                                        _stream(offspring, stream))
-    else:
-        N, P = offspring.shape
-        op, old = _rows(offspring, "offspring")
-        pp, pld = _rows(permuted, "permuted")
-        rc = lib().pf_permute_offspring_batched(op, old, N, P, pp, pld, _stream(offspring, stream))
+    N, P = _pair_args(offspring, "offspring", permuted, "permuted")
+    with torch.cuda.device(offspring.device):
+        if offspring.dim() == 1:
+            rc = lib().pf_permute_offspring(offspring.data_ptr(), P, permuted.data_ptr(), _stream(offspring, stream))
+        else:
+            op, old = _rows(offspring, "offspring")
+            pp, pld = _rows(permuted, "permuted")
+            rc = lib().pf_permute_offspring_batched(op, old, N, P, pp, pld, _stream(offspring, stream))
     _check(rc, "pf_permute_offspring")
     return permuted
 
@@ -386,13 +441,17 @@ def pf_gather_state(X, permuted, stream=None):
     _need_cuda(permuted, torch.int32, "permuted")
     if permuted.dim() == 1:
         P = permuted.shape[0]
+        _need_state(X, permuted, 1, P, False)
         row, ld, _ = _state_layout(X, False)
-        rc = lib().pf_gather_state(X.data_ptr(), row, ld, P, permuted.data_ptr(), _stream(X, stream))
+        with torch.cuda.device(X.device):
+            rc = lib().pf_gather_state(X.data_ptr(), row, ld, P, permuted.data_ptr(), _stream(X, stream))
     else:
         N, P = permuted.shape
+        _need_state(X, permuted, N, P, True)
         row, ld, ldf = _state_layout(X, True)
         pp, pld = _rows(permuted, "permuted")
-        rc = lib().pf_gather_state_batched(X.data_ptr(), row, ld, ldf, N, P, pp, pld, _stream(X, stream))
+        with torch.cuda.device(X.device):
+            rc = lib().pf_gather_state_batched(X.data_ptr(), row, ld, ldf, N, P, pp, pld, _stream(X, stream))
     _check(rc, "pf_gather_state")
     return X
 
@@ -401,15 +460,20 @@ def pf_gather_state_out(X, anc, Y=None, stream=None):
     """Out of place Y[i] <- X[anc[i]] for arbitrary ancestors."""
     torch = _torch()
     _need_cuda(anc, torch.int32, "anc")
+    if anc.dim() != 1 or not anc.is_contiguous():
+        raise PfError("anc must be a contiguous 1-D tensor")
     if Y is None:
         Y = torch.empty_like(X)
     P = anc.shape[0]
+    _need_state(X, anc, 1, P, False)
+    _need_state(Y, anc, 1, P, False)
     row, ldx, _ = _state_layout(X, False)
     rowy, ldy, _ = _state_layout(Y, False)
     if rowy != row:
         raise PfError("X and Y rows differ in size")
-    rc = lib().pf_gather_state_out(X.data_ptr(), Y.data_ptr(), row, ldx, ldy, P, anc.data_ptr(),
-                                   _stream(X, stream))
+    with torch.cuda.device(X.device):
+        rc = lib().pf_gather_state_out(X.data_ptr(), Y.data_ptr(), row, ldx, ldy, P, anc.data_ptr(),
+                                       _stream(X, stream))
     _check(rc, "pf_gather_state_out")
     return Y
 

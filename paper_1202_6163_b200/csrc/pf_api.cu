@@ -853,13 +853,16 @@ pf_status pf_lg_accumulate(const double* lse, int32_t P, float sigma_y, double* 
 
 int32_t pf_metropolis_required_B(int64_t P, double w_max, double eps) {
     if (P < 1 || !(w_max > 0.0) || w_max > 1.0 || !(eps > 0.0)) return -1;
+    // w_max >= 1/P: the maximum of P normalised weights (outside Eq. (2)'s domain otherwise)
+    if (w_max * static_cast<double>(P) < 1.0 - 1e-12) return -1;
     const double beta = 1.0 / static_cast<double>(P);
     const double alpha = (1.0 - w_max) / (static_cast<double>(P) * w_max);    // Eq. (2)
     const double lambda = 1.0 - alpha - beta;
     const double bound = eps * (alpha + beta) / (alpha > beta ? alpha : beta);  // Eq. (4)
-    if (bound >= 1.0) return 0;
-    if (lambda <= 0.0) return 1;
-    return static_cast<int32_t>(std::ceil(std::log(bound) / std::log(lambda)));  // Eq. (5)
+    if (bound >= 1.0 || lambda <= 0.0) return 1;  // at least one step (DESIGN R-22)
+    const double B = std::ceil(std::log(bound) / std::log(lambda));           // Eq. (5)
+    if (B > 2147483647.0) return -1;  // not representable (e.g. w_max -> 1 at P = 2^28)
+    return B < 1.0 ? 1 : static_cast<int32_t>(B);
 }
 
 const char* pf_status_string(pf_status s) {

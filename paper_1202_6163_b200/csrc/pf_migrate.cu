@@ -5,8 +5,8 @@
 // own extras (particle i repeated o_i - 1 times, ascending i) and fills its own free slots
 // (o_i = 0, ascending) from the rows the all-to-all delivers.  Both lists are built per
 // 2048-particle tile from a tile-level exclusive scan, then expanded item by item (one
-// 4/16-byte chunk of one row per thread), so the copies are coalesced on the packed side and
-// load-balanced whatever the offspring distribution.
+// 4/16-byte chunk of one row per thread), so the copies are coalesced on the packed side; the
+// pack side walks work items of 2048 extras ranks (a skewed tile is split over many CTAs).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -142,15 +142,18 @@ __global__ void __launch_bounds__(kThreads) k_mig_tile_counts(const int32_t* __r
 // One CTA: exclusive scans of tE and tF in place; totals into counts[0..1].  Thread t owns
 // kScanPer consecutive tiles of each round of 1024 * kScanPer (all loads issued at once).
 constexpr int kScanPer = 16;
+// The pack stage's work items: tile t's extras are cut into ceil(E_t / kMigTile) chunks of
+// kMigTile ranks; tC (ntiles + 1 entries) = their exclusive prefix, tC[ntiles] = the total.
 __global__ void __launch_bounds__(1024) k_mig_tile_scan(int64_t* __restrict__ tE, int64_t* __restrict__ tF,
-                                                        int64_t ntiles, int64_t* __restrict__ counts) {
-    __shared__ int64_t s_warp[2][32];
+                                                        int64_t* __restrict__ tC, int64_t ntiles,
+                                                        int64_t* __restrict__ counts) {
+    __shared__ int64_t s_warp[3][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t cE = 0, cF = 0;
+    int64_t cE = 0, cF = 0, cC = 0;
     for (int64_t r0 = 0; r0 < ntiles; r0 += 1024 * kScanPer) {
         const int64_t b = r0 + static_cast<int64_t>(threadIdx.x) * kScanPer;
         int64_t vE[kScanPer], vF[kScanPer];
-        int64_t sE = 0, sF = 0;
+        int64_t sE = 0, sF = 0, sC = 0;
 #pragma unroll
         for (int u = 0; u < kScanPer; ++u) {
             const bool in = b + u < ntiles;
@@ -158,49 +161,61 @@ __global__ void __launch_bounds__(1024) k_mig_tile_scan(int64_t* __restrict__ tE
             vF[u] = in ? tF[b + u] : 0;
             sE += vE[u];
             sF += vF[u];
+            sC += mig_cdiv(vE[u], kMigTile);
         }
-        int64_t iE = sE, iF = sF;
+        int64_t iE = sE, iF = sF, iC = sC;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int64_t a = __shfl_up_sync(kFullMask, iE, d), c = __shfl_up_sync(kFullMask, iF, d);
+            const int64_t k = __shfl_up_sync(kFullMask, iC, d);
             if (lane >= d) {
                 iE += a;
                 iF += c;
+                iC += k;
             }
         }
         if (lane == 31) {
             s_warp[0][warp] = iE;
             s_warp[1][warp] = iF;
+            s_warp[2][warp] = iC;
         }
         __syncthreads();
-        int64_t bE = 0, bF = 0, TE = 0, TF = 0;
+        int64_t bE = 0, bF = 0, bC = 0, TE = 0, TF = 0, TC = 0;
 #pragma unroll 8
         for (int w = 0; w < 32; ++w) {
-            const int64_t a = s_warp[0][w], c = s_warp[1][w];
+            const int64_t a = s_warp[0][w], c = s_warp[1][w], k = s_warp[2][w];
             if (w < warp) {
                 bE += a;
                 bF += c;
+                bC += k;
             }
             TE += a;
             TF += c;
+            TC += k;
         }
-        int64_t rE = cE + bE + iE - sE, rF = cF + bF + iF - sF;
+        int64_t rE = cE + bE + iE - sE, rF = cF + bF + iF - sF, rC = cC + bC + iC - sC;
 #pragma unroll
         for (int u = 0; u < kScanPer; ++u) {
             if (b + u < ntiles) {
                 tE[b + u] = rE;
                 tF[b + u] = rF;
+                tC[b + u] = rC;
             }
             rE += vE[u];
             rF += vF[u];
+            rC += mig_cdiv(vE[u], kMigTile);
         }
         cE += TE;
         cF += TF;
+        cC += TC;
         __syncthreads();  // s_warp reused by the next round
     }
-    if (threadIdx.x == 0 && counts != nullptr) {
-        counts[0] = cE;
-        counts[1] = cF;
+    if (threadIdx.x == 0) {
+        tC[ntiles] = cC;
+        if (counts != nullptr) {
+            counts[0] = cE;
+            counts[1] = cF;
+        }
     }
 }
 
@@ -230,59 +245,61 @@ __device__ __forceinline__ void copy_tile_rows(int64_t n, int64_t cpr, int lg, S
     }
 }
 
-// 4c: the tile's extras in NS-15 order.  s_inc[q] = inclusive count of the extras of the
-// tile's particles 0..q; extra j belongs to the first q with s_inc[q] > j, tabulated in s_map
-// when the tile has at most kMapCap extras (binary search otherwise).
-constexpr int kMapCap = 2 * kMigTile;
-
+// 4c: the extras in NS-15 order, cut into work items of kMigTile ranks (a tile's extras are
+// its particles' o_i - 1 copies in order; tile t holds items [tC[t], tC[t+1])).  A persistent
+// grid walks the items, so a tile that holds a heavy particle's thousands of extras is copied
+// by as many CTAs as it has items (one CTA per tile serialised skewed shards).
+// Each item rescans its tile's extras counts and tabulates the owner of each of its ranks.
 template <int CH>
 __global__ void __launch_bounds__(kThreads) k_mig_pack(const char* __restrict__ X, int64_t ld, int64_t row_bytes,
                                                        int lg, int32_t Pl, int64_t p0, const int32_t* __restrict__ o,
-                                                       const int64_t* __restrict__ tE, char* __restrict__ send,
+                                                       const int64_t* __restrict__ tE, const int64_t* __restrict__ tC,
+                                                       int64_t ntiles, char* __restrict__ send,
                                                        int32_t* __restrict__ send_src) {
-    __shared__ int32_t s_inc[kMigTile];
-    __shared__ int16_t s_map[kMapCap];
+    __shared__ int16_t s_map[kMigTile];
     __shared__ int64_t s_warp[kThreads / 32];
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMigTile;
-    int32_t e[kMigItems];
-    int32_t sum = 0;
-#pragma unroll
-    for (int j = 0; j < kMigItems; ++j) {
-        const int64_t i = t0 + threadIdx.x * kMigItems + j;
-        const int32_t v = i < Pl ? __ldg(o + i) : 1;
-        e[j] = v > 1 ? v - 1 : 0;
-        sum += e[j];
-    }
-    int64_t ex;
-    const int64_t Et = block_excl_scan(sum, &ex, s_warp);
-    if (Et == 0) return;
-    const bool mapped = Et <= kMapCap;
-    int32_t run = static_cast<int32_t>(ex);
-#pragma unroll
-    for (int j = 0; j < kMigItems; ++j) {
-        const int q = threadIdx.x * kMigItems + j;
-        if (mapped)
-            for (int c = 0; c < e[j]; ++c) s_map[run + c] = static_cast<int16_t>(q);
-        run += e[j];
-        s_inc[q] = run;
-    }
-    __syncthreads();
-    const int64_t base = tE[blockIdx.x];
-    auto owner = [&](int64_t j) -> int64_t {
-        if (mapped) return s_map[j];
-        int lo = 0, hi = kMigTile - 1;
+    const int64_t items = tC[ntiles];
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+        int64_t lo = 0, hi = ntiles - 1;  // the tile of item w: the last t with tC[t] <= w
         while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_inc[mid] > j) hi = mid;
-            else lo = mid + 1;
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(tC + mid) <= w) lo = mid;
+            else hi = mid - 1;
         }
-        return lo;
-    };
-    if (send_src != nullptr)
-        for (int64_t j = threadIdx.x; j < Et; j += kThreads) send_src[base + j] = static_cast<int32_t>(p0 + t0 + owner(j));
-    if (row_bytes == 0) return;
-    copy_tile_rows<CH>(Et, row_bytes / CH, lg, [&](int64_t j) { return X + (t0 + owner(j)) * ld; },
-                       [&](int64_t j) { return send + (base + j) * row_bytes; });
+        const int64_t t = lo;
+        const int64_t t0 = t * kMigTile;
+        int32_t e[kMigItems];
+        int32_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < kMigItems; ++j) {
+            const int64_t i = t0 + threadIdx.x * kMigItems + j;
+            const int32_t v = i < Pl ? __ldg(o + i) : 1;
+            e[j] = v > 1 ? v - 1 : 0;
+            sum += e[j];
+        }
+        int64_t ex;
+        const int64_t Et = block_excl_scan(sum, &ex, s_warp);
+        const int64_t r0 = (w - __ldg(tC + t)) * kMigTile;
+        const int64_t r1 = min(Et, r0 + kMigTile);
+        int64_t run = ex;
+#pragma unroll
+        for (int j = 0; j < kMigItems; ++j) {
+            const int q = threadIdx.x * kMigItems + j;
+            const int64_t a = max(run, r0), b = min(run + e[j], r1);
+            for (int64_t c = a; c < b; ++c) s_map[c - r0] = static_cast<int16_t>(q);
+            run += e[j];
+        }
+        __syncthreads();
+        const int64_t n = r1 - r0;
+        const int64_t base = __ldg(tE + t) + r0;
+        if (send_src != nullptr)
+            for (int64_t j = threadIdx.x; j < n; j += kThreads)
+                send_src[base + j] = static_cast<int32_t>(p0 + t0 + s_map[j]);
+        if (row_bytes != 0)
+            copy_tile_rows<CH>(n, row_bytes / CH, lg, [&](int64_t j) { return X + (t0 + s_map[j]) * ld; },
+                               [&](int64_t j) { return send + (base + j) * row_bytes; });
+        __syncthreads();  // s_map is rewritten by the next item
+    }
 }
 
 // 4d: the tile's free slots take rows tF[t] + r, r = their rank in the tile.
@@ -339,7 +356,8 @@ int mig_lg(int64_t cpr) {
 
 }  // namespace
 
-size_t mig_plan_bytes(int32_t Pl) { return 2 * sizeof(int64_t) * static_cast<size_t>(mig_cdiv(Pl, kMigTile)); }
+// plan: tE [ntiles], tF [ntiles], tC [ntiles + 1] (int64)
+size_t mig_plan_bytes(int32_t Pl) { return sizeof(int64_t) * (3 * static_cast<size_t>(mig_cdiv(Pl, kMigTile)) + 1); }
 
 cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_t* range, int64_t win0, int32_t Pw,
                                  const float* gmax, const int32_t* gbad, int32_t* o, cudaStream_t s,
@@ -356,7 +374,8 @@ cudaError_t launch_mig_offspring(const int32_t* anc, int64_t n_anc, const int64_
     return cudaPeekAtLastError();
 }
 
-// the plan = the tiles' exclusive prefixes (tE = plan, tF = plan + ntiles); counts nullable
+// the plan = the tiles' exclusive prefixes (tE = plan, tF = plan + ntiles) and the pack work
+// items' prefix (tC = plan + 2 ntiles, ntiles + 1 entries); counts nullable
 cudaError_t launch_mig_plan(const int32_t* o, int32_t Pl, void* plan, int64_t* counts, cudaStream_t s,
                             uint64_t* launches) {
     const int64_t nt = mig_cdiv(Pl, kMigTile);
@@ -368,7 +387,7 @@ cudaError_t launch_mig_plan(const int32_t* o, int32_t Pl, void* plan, int64_t* c
     }
     {
         ProfScope ps_("k_mig_tile_scan", s);
-        k_mig_tile_scan<<<1, 1024, 0, s>>>(tE, tF, nt, counts);
+        k_mig_tile_scan<<<1, 1024, 0, s>>>(tE, tF, tF + nt, nt, counts);
     }
     *launches += 2;
     return cudaPeekAtLastError();
@@ -376,16 +395,21 @@ cudaError_t launch_mig_plan(const int32_t* o, int32_t Pl, void* plan, int64_t* c
 
 cudaError_t launch_mig_pack(const void* X, int64_t row_bytes, int64_t ld, int32_t Pl, int64_t p0, const int32_t* o,
                             const void* plan, void* send, int32_t* send_src, cudaStream_t s, uint64_t* launches) {
+    const int64_t nt = mig_cdiv(Pl, kMigTile);
     const int64_t* tE = static_cast<const int64_t*>(plan);
+    const int64_t* tC = tE + 2 * nt;
     const char* x = static_cast<const char*>(X);
     char* y = static_cast<char*>(send);
     const int ch = row_bytes > 0 ? mig_chunk(x, y, row_bytes, std::max<int64_t>(ld, row_bytes)) : 16;
     const int lg = row_bytes > 0 ? mig_lg(row_bytes / ch) : 0;
-    const unsigned grid = static_cast<unsigned>(mig_cdiv(Pl, kMigTile));
+    // persistent over the work items (their count is on the device): enough CTAs for the
+    // balanced case, and every SM busy when one tile holds most of the extras
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(
+        std::max<int64_t>(nt, static_cast<int64_t>(sm_count()) * 4), static_cast<int64_t>(sm_count()) * 8)));
     ProfScope ps_("k_mig_pack", s);
-    if (ch == 16) k_mig_pack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
-    else if (ch == 4) k_mig_pack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
-    else k_mig_pack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, y, send_src);
+    if (ch == 16) k_mig_pack<16><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, tC, nt, y, send_src);
+    else if (ch == 4) k_mig_pack<4><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, tC, nt, y, send_src);
+    else k_mig_pack<1><<<grid, kThreads, 0, s>>>(x, ld, row_bytes, lg, Pl, p0, o, tE, tC, nt, y, send_src);
     ++*launches;
     return cudaPeekAtLastError();
 }

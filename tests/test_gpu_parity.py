@@ -834,6 +834,10 @@ def test_particle_migration_layouts(pf, dev, orc):
     want[:, :16] = orc.gather_inplace(np.ascontiguousarray(wide[:, :16]), wp)
     assert np.array_equal(Xw.cpu().numpy(), want)
     check(pfinputs.state_matrix(P, 16), np.full(P, P - 2, dtype=np.int32), 4)  # one particle takes all
+    # one particle takes every slot of a 2^20 filter: its shard's 2^20 - 1 extras are split into
+    # work items over many CTAs (the pack side was one CTA per tile)
+    Pd = 1 << 20
+    check(pfinputs.state_matrix(Pd, 16), np.full(Pd, 3, dtype=np.int32), 8)
     check(pfinputs.state_matrix(P, 16), np.arange(P, dtype=np.int32), 4)  # nothing moves
     Pb = 1 << 20
     _, ancb = orc.resample("systematic", pfinputs.gaussian_logw(Pb, 1.0, seed=8), 3)
