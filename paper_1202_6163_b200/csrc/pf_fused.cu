@@ -315,19 +315,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-// non-blocking: has the phase with this parity completed?
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-    return done != 0;
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}" ::"r"(
@@ -1227,6 +1214,9 @@ struct CoopArgs {
     uint64_t* Qtot_out;
     int32_t S;
     uint64_t* g_ptot;   // scratch [G]: packed (extras, free) totals of the chunks (PERM)
+    uint4* heavy;       // scratch [2][heavy_cap]: deferred runs {kind, start, end, particle} per filter parity
+    uint32_t* heavy_n;  // scratch [2]: their counts
+    int32_t heavy_cap;
     // scratch (device): [G] per-CTA values
     float* g_max;
     int32_t* g_bad;
@@ -1300,6 +1290,52 @@ __device__ __forceinline__ void coop_packed_scan(const int32_t* ov, int64_t t0, 
     *total = s_u64[2];
 }
 
+// Slot-balanced expansion under skew (the cooperative kernel): a run of one particle that
+// covers whole kXS-slot expansion chunks of its CTA (o_i >= kXS slots, or o_i - 1 >= kXS extras
+// ranks) is not expanded by that CTA chunk by chunk; its covered chunks [cs, ce) go to a
+// deferred list and, after the filter's closing grid barrier, every CTA of the grid fills a
+// 1/G share of every listed run.  A heavy particle of a skewed filter (sigma^2 = 10 at P = 2^20:
+// one particle ~3.5e4 slots) therefore costs the grid ce - cs stores instead of one CTA
+// (ce - cs) / kXS serial expansion chunks.
+constexpr int kMaxHeavy = 16;  // per sub-tile (more are expanded the ordinary way)
+struct HeavyRun {
+    uint32_t s, e;
+    int32_t id;
+};
+enum { kRunSlots = 0, kRunExtras = 1 };
+
+// the sub-tile's particles with runs of >= kXS (slots or extras ranks) into s_h (tid 0 reads
+// the count after the caller's barrier); run ends are relative to the caller's rank space
+__device__ __forceinline__ void heavy_note(uint32_t s, uint32_t e, int32_t id, HeavyRun* s_h, uint32_t* s_nh) {
+    if (e - s >= static_cast<uint32_t>(kXS)) {
+        const uint32_t k = atomicAdd(s_nh, 1u);
+        if (k < static_cast<uint32_t>(kMaxHeavy)) s_h[k] = {s, e, id};
+    }
+}
+
+// if chunk [q0, q0 + kXS) lies inside a listed run: the end of the run's covered chunks (so the
+// caller jumps there) and the run's particle in *id (the max-scan carry after the jump: its head
+// may sit in a skipped chunk), after listing those chunks for the deferred fill (thread 0);
+// else q0
+__device__ __forceinline__ uint32_t heavy_skip(uint32_t q0, const HeavyRun* s_h, uint32_t nh, const CoopArgs& a,
+                                               int parity, uint32_t kind, uint32_t base, int32_t* id) {
+    for (uint32_t h = 0; h < nh; ++h) {
+        if (s_h[h].s <= q0 && q0 + kXS <= s_h[h].e) {
+            *id = s_h[h].id;
+            const uint32_t nc = (s_h[h].e - q0) / kXS;  // whole chunks covered from q0 on
+            if (threadIdx.x == 0) {
+                // one entry per chunk: the grid then shares the fill evenly however long the run
+                const uint32_t k = atomicAdd(a.heavy_n + parity, nc);
+                for (uint32_t m = 0; m < nc && static_cast<int64_t>(k) + m < a.heavy_cap; ++m)
+                    a.heavy[static_cast<int64_t>(parity) * a.heavy_cap + k + m] =
+                        make_uint4(kind, base + q0 + m * kXS, 0u, static_cast<uint32_t>(s_h[h].id));
+            }
+            return q0 + nc * kXS;
+        }
+    }
+    return q0;
+}
+
 // PERM: 0 ancestors (+ offspring), 1 + the canonical permutation (offspring required)
 template <int SCHEME, bool SUMS, int PERM, int FI>
 __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
@@ -1323,10 +1359,14 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     __shared__ int32_t s_wmax[kFW];
     __shared__ uint64_t s_crho;
     __shared__ double s_cA, s_cBc;
+    __shared__ HeavyRun s_h[kMaxHeavy];
+    __shared__ uint32_t s_nh;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
+    if (c == 0 && tid < 2) a.heavy_n[tid] = 0;  // appended only after the first filter's second grid barrier
     for (int n = 0; n < a.N; ++n) {
+        const int hp = n & 1;  // this filter's deferred-run list
         const float* frow = a.logw + static_cast<int64_t>(n) * a.ld;
         const int64_t c0 = static_cast<int64_t>(c) * a.CH;
         const int64_t c1 = min(static_cast<int64_t>(a.P), c0 + a.CH);
@@ -1366,6 +1406,8 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             a.g_bad[c] = bad;
         }
         grid.sync();
+        // every CTA has filled the previous filter's runs (list 1 - hp) before reaching the barrier
+        if (c == 0 && tid == 0) a.heavy_n[1 - hp] = 0;
         if (warp == 0) {
             float gm = -INFINITY;
             int gb = 0;
@@ -1583,8 +1625,30 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             {
                 int32_t* s_head = &s_buf[0][0];
                 const uint32_t K0 = s_prevE, K1 = s_lastE[kFR - 1][kFW - 1];
+                if (tid == 0) s_nh = 0;
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < kFR; ++j) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        heavy_note((q == 0) ? first[j] : E[j * 4 + q - 1], E[j * 4 + q], idbase + j * (kFT * 4) + q,
+                                   s_h, &s_nh);
+                }
+                __syncthreads();
+                const uint32_t nh = min(s_nh, static_cast<uint32_t>(kMaxHeavy));
                 int32_t cy = -1;
                 for (uint32_t q0 = K0 & ~7u; q0 < K1; q0 += kXS) {
+                    if (nh) {
+                        int32_t hid;
+                        const uint32_t qs = heavy_skip(q0, s_h, nh, a, hp, kRunSlots, 0u, &hid);
+                        if (qs != q0) {
+                            // the skipped chunks all hold the run's particle: it is the max-scan
+                            // carry of the slots that follow (ancestors grow with the slot)
+                            cy = hid;
+                            q0 = qs - kXS;
+                            continue;
+                        }
+                    }
                     cta_clear8(s_head, tid);
                     __syncthreads();
 #pragma unroll
@@ -1687,8 +1751,32 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     const uint32_t XS = static_cast<uint32_t>(run0 >> 31);          // first extras rank
                     const uint32_t XT = static_cast<uint32_t>((run0 + stot) >> 31) - XS;
                     const int32_t idbase = static_cast<int32_t>(t0) + tid * 4;
+                    if (tid == 0) s_nh = 0;
+                    __syncthreads();
+#pragma unroll
+                    for (int j = 0; j < kFR; ++j) {
+                        uint64_t run = run0 + s_wt[j][warp] + pex[j];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int32_t o = ov[j * 4 + q];
+                            const uint32_t r = static_cast<uint32_t>(run >> 31) - XS;
+                            if (o > 1) heavy_note(r, r + static_cast<uint32_t>(o - 1), idbase + j * (kFT * 4) + q, s_h, &s_nh);
+                            run += static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31;
+                        }
+                    }
+                    __syncthreads();
+                    const uint32_t nh = min(s_nh, static_cast<uint32_t>(kMaxHeavy));
                     int32_t cy = -1;
                     for (uint32_t q0 = 0; q0 < XT; q0 += kXS) {
+                        if (nh) {
+                            int32_t hid;
+                            const uint32_t qs = heavy_skip(q0, s_h, nh, a, hp, kRunExtras, XS, &hid);
+                            if (qs != q0) {
+                                cy = hid;
+                                q0 = qs - kXS;
+                                continue;
+                            }
+                        }
                         cta_clear8(s_head, tid);
                         __syncthreads();
 #pragma unroll
@@ -1716,6 +1804,27 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             }
         }
         grid.sync();  // scratch arrays are rewritten by the next filter
+        // the filter's deferred chunks (list hp is complete), round-robin over the grid: chunk
+        // entries {kind, first slot / extras rank, -, particle}, kXS ranks each
+        {
+            const uint32_t nr = min(__ldcg(a.heavy_n + hp), static_cast<uint32_t>(a.heavy_cap));
+            int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
+            int32_t* prow = PERM ? a.perm + static_cast<int64_t>(n) * a.ld_anc : nullptr;
+            for (uint32_t r = c; r < nr; r += G) {
+                const uint4 h = __ldcg(a.heavy + static_cast<int64_t>(hp) * a.heavy_cap + r);
+                const int32_t id = static_cast<int32_t>(h.w);
+                if (h.x == kRunSlots) {
+                    if (a.anc_vec) {  // the chunk grid is 8-slot aligned
+                        int4* dst = reinterpret_cast<int4*>(arow + h.y);
+                        for (int k = tid; k < kXS / 4; k += kFT) __stcs(dst + k, make_int4(id, id, id, id));
+                    } else {
+                        for (int k = tid; k < kXS; k += kFT) arow[h.y + k] = id;
+                    }
+                } else if (PERM) {
+                    for (int k = tid; k < kXS; k += kFT) prow[__ldcg(a.freelist + h.y + k)] = id;
+                }
+            }
+        }
     }
 }
 
@@ -2293,8 +2402,11 @@ bool coop_supported(int scheme, int32_t N, int32_t P) {
     return N == 1 || per_filter_excess_us <= 0.0 || static_cast<double>(N) * per_filter_excess_us < 20.0;
 }
 
+// deferred runs per filter: at most (slots + extras ranks) / kXS of them
+int32_t coop_heavy_cap(int32_t P) { return static_cast<int32_t>(2 * (static_cast<int64_t>(P) / kXS) + 2 * kMaxHeavy); }
 size_t coop_scratch_bytes(int32_t P) {
-    return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(P) * 4 + 256;
+    return static_cast<size_t>(4096) * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(P) * 4 + 256 +
+           2 * static_cast<size_t>(coop_heavy_cap(P)) * sizeof(uint4) + 16;
 }
 
 template <int SCHEME, bool SUMS, int PERM, int FI>
@@ -2401,6 +2513,12 @@ cudaError_t launch_coop_sorted(int scheme, const float* logw, int64_t ld, int32_
     a.g_sw2 = reinterpret_cast<double*>(sc + 4096 * 24);
     a.g_ptot = reinterpret_cast<uint64_t*>(sc + 4096 * 32);
     a.freelist = reinterpret_cast<int32_t*>(sc + 4096 * 40);
+    {
+        const size_t hoff = (static_cast<size_t>(4096) * 40 + static_cast<size_t>(P) * 4 + 255) / 256 * 256;
+        a.heavy_cap = coop_heavy_cap(P);
+        a.heavy = reinterpret_cast<uint4*>(sc + hoff);
+        a.heavy_n = reinterpret_cast<uint32_t*>(sc + hoff + 2 * static_cast<size_t>(a.heavy_cap) * sizeof(uint4));
+    }
     const uint64_t NP = static_cast<uint64_t>(N) * static_cast<uint64_t>(P);
     const uint64_t alg = NP * 4u * (1u + (scheme != kBuckets ? 1u : 0u) + (offspring ? 1u : 0u) + (permuted ? 1u : 0u)) +
                          (scheme == kBuckets ? NP * 8u + static_cast<uint64_t>(N) * static_cast<uint64_t>(a.S) * 4u : 0u);

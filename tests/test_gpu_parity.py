@@ -1045,3 +1045,45 @@ def test_permuted_out(pf, dev, orc, scheme):
                 assert np.array_equal(Pm[n], orc.permute(want)), (scheme, N, P, n, with_off)
                 if with_off:
                     assert np.array_equal(off.cpu().numpy()[n], orc.ancestors_to_offspring(want))
+
+
+def _heavy_logw(P, seed):
+    """Skewed log-weights with runs that cover whole expansion chunks: particle 0 holds 1/32 of
+    the mass (its ~P/32 slots and extras ranks start at 0, a chunk boundary), particles 7, 8 and
+    P/2 (one sub-tile / another CTA) 1/16, 1/64 and 1/8 each, the rest sigma^2 = 1 far below."""
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal(P) - 12.0).astype(np.float32)
+    rest = float(np.sum(np.exp(x.astype(np.float64))))
+    heavy = {0: 1 / 32, 7: 1 / 16, 8: 1 / 64, P // 2: 1 / 8}
+    light = 1.0 - sum(heavy.values())
+    for i, f in heavy.items():
+        x[i] = np.float32(np.log(f / light * rest))
+    return x
+
+
+@pytest.mark.parametrize("P", [1 << 18, (1 << 20) + 3])
+def test_heavy_runs_cooperative_kernel(pf, dev, orc, P):
+    """Slot-balanced expansion (the cooperative kernel's deferred runs, kinds slots and extras
+    ranks): ancestors, offspring and the canonical permutation of filters whose heavy particles'
+    runs cover whole chunks, including one that starts at a chunk boundary, bit-exact vs the
+    oracle; plus the sigma^2 = 10 filter of C2."""
+    import torch
+
+    for x in (_heavy_logw(P, 3), pfinputs.gaussian_logw(P, 10.0, seed=P + 1)):
+        g = _gpu(x, dev)
+        for scheme in ("systematic", "stratified"):
+            off = torch.empty(P, dtype=torch.int32, device=dev)
+            pm = torch.empty(P, dtype=torch.int32, device=dev)
+            a = pf.pf_resample_ex(scheme, g, 77, offspring_out=off, permuted_out=pm)
+            torch.cuda.synchronize()
+            _, want = orc.resample(scheme, x, 77)
+            assert np.array_equal(a.cpu().numpy(), want), (scheme, P)
+            assert np.array_equal(off.cpu().numpy(), orc.ancestors_to_offspring(want)), (scheme, P)
+            assert np.array_equal(pm.cpu().numpy(), orc.permute(want)), (scheme, P)
+        # batched form (several filters through the same deferred lists, both parities)
+        xb = np.stack([x, x[::-1].copy(), x])
+        ab = pf.pf_resample_batched("systematic", _gpu(xb, dev), 5)
+        torch.cuda.synchronize()
+        for n in range(3):
+            _, want = orc.resample("systematic", xb[n], 5, filter_index=n)
+            assert np.array_equal(ab[n].cpu().numpy(), want), n
