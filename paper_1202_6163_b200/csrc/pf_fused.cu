@@ -2671,19 +2671,27 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
     a.ld = ld;
     a.N = N;
     a.P = P;
-    // geometry: 512 threads (8192 particles per CTA) up to 8 CTAs, else 1024 threads (16384);
-    // PF_FUSED_FT=256 (experiment): 256 threads (4096 per CTA), clusters of up to 16
+    // geometry: 512 threads (8192 particles per CTA) up to 8 CTAs, else 1024 threads (16384).
+    // Systematic filters of 16385..65536 particles without the state gather: 256 threads (4096
+    // per CTA, clusters of 5..16, 4 CTAs per SM; C3 resample 0.469 -> 0.452 ms, with the
+    // permutation 0.850 -> 0.773 ms: more, smaller CTAs per SM hide each cluster's barrier
+    // skew).  PF_FUSED_FT=256|512 forces one where both apply (diagnostics).
     static const int ft_env = [] {
         const char* e = std::getenv("PF_FUSED_FT");
         return e ? std::atoi(e) : 0;
     }();
-    const int FT = (ft_env == 256 && !logw64 && P <= 16 * 256 * kFI && scheme != kBuckets)
-                       ? 256
-                       : ((P <= 8 * 512 * kFI) ? 512 : 1024);
-    a.CL = static_cast<int32_t>((P + FT * kFI - 1) / (FT * kFI));
-    int64_t pp = (P + a.CL - 1) / a.CL;
-    pp = (pp + 3) / 4 * 4;
-    a.PP = static_cast<int32_t>(pp);
+    const bool ft256_ok = !logw64 && P <= 16 * 256 * kFI && scheme != kBuckets;
+    const bool ft256_default = ft256_ok && scheme == 3 && !X && P > 4 * 256 * kFI;
+    int FT = ((ft_env == 256 && ft256_ok) || (ft_env != 512 && ft256_default))
+                 ? 256
+                 : ((P <= 8 * 512 * kFI) ? 512 : 1024);
+    auto set_geometry = [&](int ft) {
+        a.CL = static_cast<int32_t>((P + ft * kFI - 1) / (ft * kFI));
+        int64_t pp = (P + a.CL - 1) / a.CL;
+        pp = (pp + 3) / 4 * 4;
+        a.PP = static_cast<int32_t>(pp);
+    };
+    set_geometry(FT);
     const int m = ceil_log2(P);
     a.D = (P <= 1) ? 0 : (((P & (P - 1)) == 0) ? (uint64_t{1} << (64 - m)) : (UINT64_MAX / static_cast<uint64_t>(P)));
     a.S = P;
@@ -2726,9 +2734,15 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
         if (FT != 512) return cudaErrorNotSupported;  // binary64 fused for P <= 65536 only (f64_fused_supported)
         e = launch_fused_ft<512, 16, true>(scheme, pm, a, s);
     } else {
-        e = (FT == 256)   ? launch_fused_ft<256, 16>(scheme, pm, a, s)
-            : (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s)
-                          : launch_fused_ft<1024, 16>(scheme, pm, a, s);
+        if (FT == 256) {
+            e = launch_fused_ft<256, 16>(scheme, pm, a, s);
+            if (e == cudaErrorNotSupported) {  // 16-CTA clusters not schedulable here: 512 threads
+                FT = 512;
+                set_geometry(FT);
+            }
+        }
+        if (FT != 256)
+            e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
     }
     ++*launches;
     if (e != cudaSuccess) return e;

@@ -754,8 +754,18 @@ __global__ void __launch_bounds__(kThreads) k_mexp_vec(const float4* __restrict_
     }
 }
 
+// NS-11's proposal j = (r P) >> 32 is r >> (32 - m) when P = 2^m (m >= 1): the same value
+// without a multiply on the integer-multiply pipe that the Philox rounds saturate (the binding
+// pipe of these kernels, profiles/r02_ncu_metro.md).  PSH = the shift, or 0: general P.
+template <bool POW2>
+__device__ __forceinline__ uint32_t metro_j(uint32_t r, uint32_t P, int sh) {
+    return POW2 ? (r >> sh) : __umulhi(r, P);
+}
+
+template <bool POW2>
 __global__ void __launch_bounds__(kThreads) k_metro(int32_t N, int32_t P, Ws ws, int64_t ldq, Key key,
-                                                    uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc) {
+                                                    uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc,
+                                                    int sh) {
     const int64_t g = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
     if (g >= static_cast<int64_t>(N) * P) return;
     const int n = static_cast<int>(g / P);
@@ -777,9 +787,9 @@ __global__ void __launch_bounds__(kThreads) k_metro(int32_t N, int32_t P, Ws ws,
         for (int t = 0; t < 4; ++t) {
             const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>((b >> 1) + t), 4u, filt,
                                      key.k0, key.k1);
-            j[2 * t] = __umulhi(r.x, static_cast<uint32_t>(P));
+            j[2 * t] = metro_j<POW2>(r.x, static_cast<uint32_t>(P), sh);
             u[2 * t] = __fmul_rn(static_cast<float>(r.y >> 8), kU);
-            j[2 * t + 1] = __umulhi(r.z, static_cast<uint32_t>(P));
+            j[2 * t + 1] = metro_j<POW2>(r.z, static_cast<uint32_t>(P), sh);
             u[2 * t + 1] = __fmul_rn(static_cast<float>(r.w >> 8), kU);
         }
 #pragma unroll
@@ -798,8 +808,10 @@ __global__ void __launch_bounds__(kThreads) k_metro(int32_t N, int32_t P, Ws ws,
 // Filter-per-CTA form: one 1024-thread CTA per SM walks whole filters, so an SM's L1 holds (most
 // of) one filter's weight vector and the B random proposals per chain hit L1 instead of L2
 // (the kernel is launched with the maximum L1 carve-out).  Same chains, same results as k_metro.
+template <bool POW2>
 __global__ void __launch_bounds__(1024, 1) k_metro_fpc(int32_t N, int32_t P, Ws ws, int64_t ldq, Key key,
-                                                        uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc) {
+                                                        uint32_t filt0, int32_t B, int32_t* anc, int64_t ld_anc,
+                                                        int sh) {
     const float kU = __uint_as_float(0x33800000u);  // 2^-24
     for (int n = blockIdx.x; n < N; n += gridDim.x) {
         int32_t* out = anc + static_cast<int64_t>(n) * ld_anc;
@@ -819,9 +831,9 @@ __global__ void __launch_bounds__(1024, 1) k_metro_fpc(int32_t N, int32_t P, Ws 
                 for (int t = 0; t < 4; ++t) {
                     const u32x4 r = philox10(static_cast<uint32_t>(i), static_cast<uint32_t>((b >> 1) + t), 4u, filt,
                                              key.k0, key.k1);
-                    j[2 * t] = __umulhi(r.x, static_cast<uint32_t>(P));
+                    j[2 * t] = metro_j<POW2>(r.x, static_cast<uint32_t>(P), sh);
                     u[2 * t] = __fmul_rn(static_cast<float>(r.y >> 8), kU);
-                    j[2 * t + 1] = __umulhi(r.z, static_cast<uint32_t>(P));
+                    j[2 * t + 1] = metro_j<POW2>(r.z, static_cast<uint32_t>(P), sh);
                     u[2 * t + 1] = __fmul_rn(static_cast<float>(r.w >> 8), kU);
                 }
 #pragma unroll
@@ -2003,20 +2015,18 @@ cudaError_t launch_metropolis(const float* logw, int64_t ld, int32_t N, int32_t 
     }
     // batches that fill the GPU: the filter-per-CTA kernel (L1-resident weights; C3: 6.84 ->
     // 4.28 ms at B = 32, tools/metro_times.py); fewer filters: one thread per chain over all SMs
+    const bool pow2 = P > 1 && (P & (P - 1)) == 0;
+    const int sh = pow2 ? 32 - ceil_log2(P) : 0;
     if (N >= sm_count()) {
-        static std::atomic<int> attr_set[kMaxDevices];
-        cached_per_device(attr_set, [] {
-            cudaFuncSetAttribute(k_metro_fpc, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-            cudaGetLastError();
-            return 1;
-        });
         ProfScope ps_("k_metro", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);  // w read once, ancestors written
-        k_metro_fpc<<<static_cast<unsigned>(std::min<int64_t>(N, sm_count())), 1024, 0, s>>>(
-            N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc);
+        const unsigned g = static_cast<unsigned>(std::min<int64_t>(N, sm_count()));
+        if (pow2) k_metro_fpc<true><<<g, 1024, 0, s>>>(N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc, sh);
+        else k_metro_fpc<false><<<g, 1024, 0, s>>>(N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc, 0);
     } else {
         ProfScope ps_("k_metro", s, static_cast<uint64_t>(N) * static_cast<uint64_t>(P) * 8u);
-        k_metro<<<static_cast<unsigned>(cdiv(total, kThreads)), kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed),
-                                                                               first_filter, B, anc, ld_anc);
+        const unsigned g = static_cast<unsigned>(cdiv(total, kThreads));
+        if (pow2) k_metro<true><<<g, kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc, sh);
+        else k_metro<false><<<g, kThreads, 0, s>>>(N, P, ws, L.ldq, make_key(seed), first_filter, B, anc, ld_anc, 0);
     }
     ++*launches;
     return cudaPeekAtLastError();

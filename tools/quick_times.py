@@ -19,6 +19,20 @@ def main():
     from tools.sweep import time_calls
 
     dev = torch.device("cuda:0")
+    if "--geom" in sys.argv:
+        # systematic batches of N x P = 2^26 by output set (geometry A/B with PF_FUSED_FT)
+        for P in (1 << 14, 1 << 15, 1 << 16, 40000):
+            N = (1 << 26) // P
+            x = pfinputs.gaussian_logw_torch(P, 1.0, pfinputs.BASE_SEED, N, dev)
+            anc = torch.empty((N, P), dtype=torch.int32, device=dev)
+            off = torch.empty_like(anc)
+            pm = torch.empty_like(anc)
+            for name, kw in (("anc", {}), ("perm", {"offspring_out": off, "permuted_out": pm})):
+                ms = time_calls(lambda: pf.pf_resample_batched("systematic", x, 5, ancestors=anc, **kw), 5, dev)
+                print(json.dumps({"P": P, "N": N, "outputs": name, "ms": round(ms, 4),
+                                  "particles_per_s": N * P / (ms / 1e3)}))
+                sys.stdout.flush()
+        return
     if "--c3" in sys.argv:
         # the C3 batch (1024 x 2^16, sigma^2 = 1 unless --var) by output set: resample only,
         # + offspring, + permutation, + in-place gather of a D = 16 state (the bench step)
