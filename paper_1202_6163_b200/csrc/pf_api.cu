@@ -158,6 +158,25 @@ pf_status fused_branch(int scheme, const float* logw, const double* logw64, int6
     return cuda_status(e);
 }
 
+// Canonical permutation (+ the in-place gather) from offspring counts in one cluster-kernel
+// launch when the batch spans the GPU (P <= 65536; pf_fused.cu launch_fused_from_offspring);
+// false: the caller takes the lookback path (k_pscan + k_push, then k_gather_rows16).
+bool fused_permute_preferred(int32_t N, int32_t P) {
+    return !g_no_fusion.load() && pf::fused_from_offspring_supported(P) &&
+           static_cast<int64_t>(N) * pf::fused_cluster_ctas(P) >= pf::sm_count();
+}
+
+cudaError_t permute_gather_from_offspring(const int32_t* off, int64_t ld_off, int32_t N, int32_t P, int32_t* perm,
+                                          int64_t ld_perm, void* state, int64_t x_row, int64_t x_ld, int64_t x_fld,
+                                          cudaStream_t s, uint64_t* nl) {
+    const bool fuse_gather = state && pf::fused_gather_supported(state, x_row, x_ld, x_fld);
+    cudaError_t e = pf::launch_fused_from_offspring(off, ld_off, N, P, perm, ld_perm, fuse_gather ? state : nullptr,
+                                                    x_row, x_ld, x_fld, s, nl);
+    if (e == cudaSuccess && state && !fuse_gather)
+        e = pf::launch_gather_inplace(state, x_row, x_ld, x_fld, N, P, perm, ld_perm, s, nl);
+    return e;
+}
+
 pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, int32_t P, uint64_t seed,
                         uint32_t first_filter, int32_t B, int32_t* anc, int64_t ld_anc, const pf_opts* opts,
                         cudaStream_t s) {
@@ -252,6 +271,13 @@ pf_status resample_core(int scheme, const float* logw, int64_t ld, int32_t N, in
         pf_status st2 = resample_core(scheme, logw, ld, N, P, seed, first_filter, B, anc, ld_anc, &o2, s);
         if (st2 != PF_OK) return st2;
         uint64_t nl = 0;
+        if (!no_fusion && fused_permute_preferred(N, P)) {
+            // a9 + a10 fused: the cluster kernel's phase D on the offspring (one launch)
+            const cudaError_t e = permute_gather_from_offspring(off, ld_anc, N, P, perm, ld_anc, state, x_row, x_ld,
+                                                                x_fld, s, &nl);
+            g_launches += nl;
+            return cuda_status(e);
+        }
         cudaError_t e = cudaMemsetAsync(static_cast<char*>(big) + LP.zero_begin, 0, LP.zero_end - LP.zero_begin, s);
         if (e == cudaSuccess) e = pf::launch_permute_from_offspring(off, ld_anc, N, P, LP, wp, perm, ld_anc, s, &nl);
         if (e == cudaSuccess && state)
@@ -587,6 +613,14 @@ pf_status pf_permute_batched(const int32_t* anc, int64_t ld_anc, int32_t N, int3
     if (st != PF_OK) return st;
     const pf::Ws ws = pf::carve(base, L);
     uint64_t nl = 0;
+    if (fused_permute_preferred(N, P)) {
+        // offspring histogram into the workspace, then the cluster kernel's phase D on it
+        cudaError_t e = pf::launch_offspring(anc, ld_anc, N, P, ws.o, L.ldq, s, &nl);
+        if (e == cudaSuccess)
+            e = pf::launch_fused_from_offspring(ws.o, L.ldq, N, P, permuted, ld_perm, nullptr, 0, 0, 0, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
     if (e == cudaSuccess) e = pf::launch_permute(anc, ld_anc, N, P, L, ws, permuted, ld_perm, s, &nl);
     g_launches += nl;
@@ -603,6 +637,12 @@ pf_status pf_permute_offspring_batched(const int32_t* offspring, int64_t ld_off,
     if (st != PF_OK) return st;
     const pf::Ws ws = pf::carve(base, L);
     uint64_t nl = 0;
+    if (fused_permute_preferred(N, P)) {
+        const cudaError_t e =
+            pf::launch_fused_from_offspring(offspring, ld_off, N, P, permuted, ld_perm, nullptr, 0, 0, 0, s, &nl);
+        g_launches += nl;
+        return cuda_status(e);
+    }
     cudaError_t e = cudaMemsetAsync(static_cast<char*>(base) + L.zero_begin, 0, L.zero_end - L.zero_begin, s);
     if (e == cudaSuccess)
         e = pf::launch_permute_from_offspring(offspring, ld_off, N, P, L, ws, permuted, ld_perm, s, &nl);

@@ -73,6 +73,10 @@ struct Exchange {
 // multinomial search, idx[b] = min{i : Q_i > floor(b Q / NB)} (pf_kernels.cu ModeBuckets), and
 // Q is written
 constexpr int kBuckets = 5;
+// SCHEME value of the permutation-from-offspring mode: phases A-C are replaced by reading the
+// offspring counts (a8's output, e.g. the histogram of the multinomial's or Metropolis' unsorted
+// ancestors); phase D builds the canonical permutation NS-15 and gathers the state NS-16
+constexpr int kFromOffspring = 6;
 
 struct FusedArgs {
     const float* logw;
@@ -97,6 +101,8 @@ struct FusedArgs {
     float* normw;
     int32_t* status_out;
     int32_t* off;   // offspring out (row stride ld_anc), nullable
+    const int32_t* off_in;  // kFromOffspring: the offspring counts (row stride ld_off_in)
+    int64_t ld_off_in;
     int32_t* perm;  // canonical permutation out (row stride ld_anc), nullable
     char* X;        // state rows gathered in place (PERM), nullable: filter n at X + n * xfld
     int64_t xld;    // bytes between rows
@@ -260,11 +266,17 @@ __host__ __device__ constexpr int copy_cu() {
 // phase C leaves no registers for the ticks: its step was 1.96 -> 2.40 ms with them)
 template <int SCHEME, int PERM, int FT, bool F64>
 __host__ __device__ constexpr bool fused_deferred_copy() {
-    return FT <= 512 && !F64 && PERM == 2 && SCHEME == 3;
+#ifndef PF_DC_OFFIN
+#define PF_DC_OFFIN 0  // from offspring the copy has no later phases to hide under: in-line copy (1.59 -> 1.42 ms at C3 multinomial)
+#endif
+    return FT <= 512 && !F64 && PERM == 2 && (SCHEME == 3 || (PF_DC_OFFIN && SCHEME == kFromOffspring));
 }
+#ifndef PF_FT256_DC_BLOCKS
+#define PF_FT256_DC_BLOCKS 3
+#endif
 template <int FT, int PERM>
 __host__ __device__ constexpr int fused_min_blocks() {
-    return (FT == 256 && PERM == 2) ? 3 : 1024 / FT;
+    return (FT == 256 && PERM == 2) ? PF_FT256_DC_BLOCKS : 1024 / FT;
 }
 constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner), P <= 65536
 #ifndef PF_PREFETCH_NEXT
@@ -347,17 +359,22 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
     constexpr int kPP = FT * FI;
     constexpr int kTPL = kFR * kFW / 32;
     constexpr int kXS = kFW * kChunk;
-    constexpr bool MA = fused_max_ahead<FT, F64>();
+    constexpr bool OFFIN = (SCHEME == kFromOffspring);
+    constexpr bool MA = fused_max_ahead<FT, F64>() && !OFFIN;  // the next filter's slice in s_lw
+    constexpr bool MD = fused_max_ahead<FT, F64>();             // phase D with 16-bit lists, one barrier
     constexpr int kCU = copy_cu<FT>();
     static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
     extern __shared__ __align__(16) int32_t s_dyn[];
     float* s_lw = reinterpret_cast<float*>(s_dyn);  // MA: this CTA's slice of the next filter's log-weights
-    // PERM: this CTA's free-slot list (kPP entries; 16-bit slots in the max-ahead mode, P <= 65536)
-    using FsT = std::conditional_t<MA, uint16_t, int32_t>;
+    // PERM: this CTA's free-slot list (kPP entries; 16-bit slots in the max-ahead mode, P <= 65536;
+    // from offspring: two lists, by filter parity, as only one cluster barrier separates filters)
+    using FsT = std::conditional_t<MD, uint16_t, int32_t>;
     constexpr bool DC = fused_deferred_copy<SCHEME, PERM, FT, F64>();  // deferred, asynchronous state copy
-    FsT* s_fs = reinterpret_cast<FsT*>(s_dyn + (MA ? kPP : 0));
-    int32_t* s_pslot = reinterpret_cast<int32_t*>(s_fs + kPP);  // PERM == 2 (not DC): free slot per extras rank
-    uint32_t* s_ring = reinterpret_cast<uint32_t*>(s_fs + kPP);  // DC: kFW rings of kRQ pairs
+    constexpr int kFsN = OFFIN ? 2 : 1;
+    FsT* const s_fs0 = reinterpret_cast<FsT*>(s_dyn + (MA ? kPP : 0));
+    FsT* s_fs = s_fs0;
+    int32_t* s_pslot = reinterpret_cast<int32_t*>(s_fs0 + kFsN * kPP);  // PERM == 2 (not DC): free slot per extras rank
+    uint32_t* s_ring = reinterpret_cast<uint32_t*>(s_fs0 + kFsN * kPP);  // DC: kFW rings of kRQ pairs
     int4* s_stage = reinterpret_cast<int4*>(s_ring + kFW * kRQ); // DC: kFW x kCU x 32 staged chunks
     __shared__ Exchange s_xx[2];                    // MA: double-buffered by filter parity
     __shared__ uint64_t s_mbar;
@@ -540,8 +557,26 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
     }
 
     for (int n = cid; n < a.N; n += num_clusters, ++it) {
-        const int xb = MA ? (it & 1) : 0;
+        const int xb = MD ? (it & 1) : 0;
         Exchange& s_x = s_xx[xb];
+        if (OFFIN) s_fs = s_fs0 + (it & 1) * kPP;
+        uint32_t E[kFI];
+        const int32_t idbase = static_cast<int32_t>(p0) + tid * 4;
+        if constexpr (OFFIN) {
+            // the offspring counts of this CTA's particles (padding: 0, and not a free slot)
+            const int32_t* orow_in = a.off_in + static_cast<int64_t>(n) * a.ld_off_in + p0;
+#pragma unroll
+            for (int j = 0; j < kFR; ++j) {
+                const int i0 = j * (kFT * 4) + tid * 4;
+                if (a.anc_vec && i0 + 3 < np) {
+                    const int4 t = __ldcs(reinterpret_cast<const int4*>(orow_in + i0));
+                    E[j * 4 + 0] = t.x; E[j * 4 + 1] = t.y; E[j * 4 + 2] = t.z; E[j * 4 + 3] = t.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) E[j * 4 + q] = (i0 + q < np) ? __ldcs(orow_in + i0 + q) : 0u;
+                }
+            }
+        } else {
         const float* row = a.logw + static_cast<int64_t>(n) * a.ld + p0;
         const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
         const bool has_next = n + num_clusters < a.N;
@@ -874,7 +909,6 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             continue;
         }
         // ---------------- C: E_i = c(Q_i), heads, max-scan
-        uint32_t E[kFI];
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
             count_row<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
@@ -937,7 +971,6 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             }
         }
         int32_t* arow = a.anc + static_cast<int64_t>(n) * a.ld_anc;
-        const int32_t idbase = static_cast<int32_t>(p0) + tid * 4;
         int32_t* s_head = &s_buf[0][0];
         // The CTA's slots are [k_lo, K1).  Per 8192-slot chunk (8 per thread): heads[E_{i-1}] = i
         // for every particle with o_i > 0, then a CTA-wide max-scan gives
@@ -975,8 +1008,6 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             }
         }
         if (PERM) {
-            // ---------------- D: canonical permutation (NS-15) from o_i = E_i - E_{i-1}
-            // packed value per particle: (extras << 31) | free; padding particles are neither.
             // E becomes the offspring in place (first[] dies here: fewer live registers in D)
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
@@ -984,6 +1015,12 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 for (int q = 3; q > 0; --q) E[j * 4 + q] -= E[j * 4 + q - 1];
                 E[j * 4] -= first[j];
             }
+        }
+        }  // phases A-C (not in the permutation-from-offspring mode)
+        if (PERM) {
+            int32_t* s_head = &s_buf[0][0];
+            // ---------------- D: canonical permutation (NS-15) from the offspring o_i
+            // packed value per particle: (extras << 31) | free; padding particles are neither.
             uint32_t* const O4 = E;  // O4[j * 4 + q] = o of particle (j, q)
             uint64_t pex[kFR];
             if (DC) {
@@ -1043,7 +1080,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 }
             }
             uint64_t poff;
-            if (MA) {
+            if (MD) {
                 // the CTA's free-slot list (local free ranks) before the exchange, so one cluster
                 // barrier publishes both the packed totals and the lists
                 __syncthreads();
@@ -1079,7 +1116,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             }
             __syncthreads();
             poff = s_poff;
-            if (!MA) {
+            if (!MD) {
                 const uint32_t rf_c = s_rf[c];
 #pragma unroll
                 for (int j = 0; j < kFR; ++j) {
@@ -2291,8 +2328,10 @@ constexpr size_t fused_smem() {
     //             PERM 2 otherwise: free slot per extras rank of a chunk, int32]
     // otherwise: [PERM: free-slot list, int32] [PERM 2: free slot per extras rank of a chunk]
     constexpr size_t pslot = (PERM == 2) ? static_cast<size_t>(FT / 32) * kChunk * 4 : 0;
+    constexpr bool offin = SCHEME == kFromOffspring;  // no log-weight slice; two free-slot lists
     return fused_max_ahead<FT, F64>()
-               ? static_cast<size_t>(FT * FI) * 4 + (PERM ? static_cast<size_t>(FT * FI) * 2 : 0) +
+               ? (offin ? 0 : static_cast<size_t>(FT * FI) * 4) +
+                     (PERM ? static_cast<size_t>(FT * FI) * 2 * (offin ? 2 : 1) : 0) +
                      (fused_deferred_copy<SCHEME, PERM, FT, F64>()
                           ? static_cast<size_t>(FT / 32) * (kRQ * 4 + copy_cu<FT>() * 32 * 16)
                           : pslot)
@@ -2368,6 +2407,9 @@ cudaError_t launch_fused_ft(int scheme, int pm, const FusedArgs& a, cudaStream_t
     if constexpr (FT == 512 && !F64) {
         if (scheme == kBuckets)
             return a.sums ? launch_fused_t<kBuckets, true, 0, FT, FI>(a, s) : launch_fused_t<kBuckets, false, 0, FT, FI>(a, s);
+        if (scheme == kFromOffspring)
+            return pm == 2 ? launch_fused_t<kFromOffspring, false, 2, FT, FI>(a, s)
+                           : launch_fused_t<kFromOffspring, false, 1, FT, FI>(a, s);
     }
     if (scheme == 2) {
         if (pm == 2)
@@ -2744,6 +2786,40 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
         if (FT != 256)
             e = (FT == 512) ? launch_fused_ft<512, 16>(scheme, pm, a, s) : launch_fused_ft<1024, 16>(scheme, pm, a, s);
     }
+    ++*launches;
+    if (e != cudaSuccess) return e;
+    return cudaPeekAtLastError();
+}
+
+// The canonical permutation (NS-15) and the in-place state gather (NS-16) of a batch from its
+// offspring counts, in one cluster-kernel launch (phase D of k_fused_sorted on counts read from
+// memory): the fused a9 + a10 for the schemes whose ancestors are unsorted (multinomial,
+// Metropolis) and for pf_permute_offspring.  X nullable (permutation only).
+bool fused_from_offspring_supported(int32_t P) { return P >= 1 && P <= 8 * 512 * kFI; }
+
+cudaError_t launch_fused_from_offspring(const int32_t* off, int64_t ld_off, int32_t N, int32_t P, int32_t* perm,
+                                        int64_t ld_perm, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
+                                        cudaStream_t s, uint64_t* launches) {
+    FusedArgs a{};
+    a.N = N;
+    a.P = P;
+    a.CL = static_cast<int32_t>((P + 512 * kFI - 1) / (512 * kFI));
+    int64_t pp = (P + a.CL - 1) / a.CL;
+    a.PP = static_cast<int32_t>((pp + 3) / 4 * 4);
+    a.off_in = off;
+    a.ld_off_in = ld_off;
+    a.perm = perm;
+    a.ld_anc = ld_perm;
+    a.anc_vec = ((reinterpret_cast<uintptr_t>(perm) & 15) == 0 && ld_perm % 4 == 0 &&
+                 (reinterpret_cast<uintptr_t>(off) & 15) == 0 && ld_off % 4 == 0) ? 1 : 0;
+    a.X = static_cast<char*>(X);
+    a.xld = x_ld;
+    a.xfld = x_fld;
+    a.xlg = 0;
+    while ((int64_t{16} << a.xlg) < x_row_bytes) ++a.xlg;
+    const uint64_t NP = static_cast<uint64_t>(N) * static_cast<uint64_t>(P);
+    ProfScope ps_("k_fused_perm", s, NP * 8u, X ? 2u * static_cast<uint64_t>(x_row_bytes) : 0u);
+    const cudaError_t e = launch_fused_ft<512, 16>(kFromOffspring, X ? 2 : 1, a, s);
     ++*launches;
     if (e != cudaSuccess) return e;
     return cudaPeekAtLastError();

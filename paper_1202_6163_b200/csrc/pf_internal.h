@@ -164,6 +164,10 @@ cudaError_t launch_fused_sorted(int scheme, const float* logw, int64_t ld, int32
                                 cudaStream_t s, uint64_t* launches, const double* logw64 = nullptr,
                                 uint64_t* Qout = nullptr, int64_t ldq = 0, uint64_t* Qtot_out = nullptr);
 // scheme id of launch_fused_sorted's multinomial bucket mode (Q + bucket index, pf_fused.cu)
+bool fused_from_offspring_supported(int32_t P);
+cudaError_t launch_fused_from_offspring(const int32_t* off, int64_t ld_off, int32_t N, int32_t P, int32_t* perm,
+                                        int64_t ld_perm, void* X, int64_t x_row_bytes, int64_t x_ld, int64_t x_fld,
+                                        cudaStream_t s, uint64_t* launches);
 constexpr int kFusedBuckets = 5;
 bool buckets_fused_supported(int32_t P);
 cudaError_t launch_bsearch_buckets(int32_t N, int32_t P, const Layout& L, const Ws& ws, uint64_t seed,

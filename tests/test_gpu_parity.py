@@ -1087,3 +1087,38 @@ def test_heavy_runs_cooperative_kernel(pf, dev, orc, P):
         for n in range(3):
             _, want = orc.resample("systematic", xb[n], 5, filter_index=n)
             assert np.array_equal(ab[n].cpu().numpy(), want), n
+
+
+@pytest.mark.parametrize("N,P", [(24, 1 << 16), (160, 4099), (40, 40001)])
+def test_fused_permutation_from_offspring(pf, dev, orc, N, P):
+    """a9 + a10 from offspring counts in one cluster-kernel launch (the multinomial / Metropolis
+    step, pf_permute_batched, pf_permute_offspring_batched) for batches that span the GPU:
+    permutations and gathered states bit-exact vs the oracle, incl. ragged P and an invalid
+    filter (identity)."""
+    import torch
+
+    xb = pfinputs.gaussian_logw(P, 1.0, seed=N + P, N=N)
+    xb[1, 5] = np.nan  # NS-1: this filter's ancestors, offspring and permutation are the identity
+    X = np.stack([pfinputs.state_matrix(P, 16, seed=n) for n in range(N)])
+    for scheme, B in (("multinomial", 0), ("metropolis", 9)):
+        gX = _gpu(X, dev)
+        off = torch.empty((N, P), dtype=torch.int32, device=dev)
+        pm = torch.empty((N, P), dtype=torch.int32, device=dev)
+        n0 = pf.pf_launch_count()
+        a = pf.pf_resample_batched(scheme, _gpu(xb, dev), 41, B=B, offspring_out=off, permuted_out=pm, state=gX)
+        torch.cuda.synchronize()
+        _, want = orc.resample_batched(scheme, xb, 41, B=B)
+        assert np.array_equal(a.cpu().numpy(), want), scheme
+        pmh, Xh = pm.cpu().numpy(), gX.cpu().numpy()
+        for n in range(N):
+            wp = orc.permute(want[n])
+            assert np.array_equal(pmh[n], wp), (scheme, n)
+            assert np.array_equal(Xh[n], orc.gather_inplace(X[n], wp)), (scheme, n)
+        assert pf.pf_launch_count() > n0
+        # the standalone conversions take the same kernel
+        p2 = pf.pf_permute(_gpu(want, dev))
+        p3 = pf.pf_permute_offspring(_gpu(np.stack([orc.ancestors_to_offspring(want[n]) for n in range(N)]), dev))
+        torch.cuda.synchronize()
+        for n in (0, 1, N - 1):
+            wp = orc.permute(want[n])
+            assert np.array_equal(p2[n].cpu().numpy(), wp) and np.array_equal(p3[n].cpu().numpy(), wp), (scheme, n)
