@@ -274,12 +274,40 @@ pf_status pf_shard_scan(const float* logw, int32_t Pl, int64_t P_global, const f
  * k_hi).  Stratified/systematic: positions are sorted, the slot range is found
  * by search and merged with d_Q (work ~ Pl + slots).  Multinomial: every shard
  * regenerates all P_global positions and keeps its own (replicated position
- * generation; exact, not work-optimal).  An invalid global filter (bad or all
+ * generation; exact, not work-optimal: the routed stages below are).  An invalid global filter (bad or all
  * -inf) writes the identity for slots [p0, p0 + Pl).  P_global <= 2^31 - 1. */
 pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
                           const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
                           const int32_t* d_gbad, uint64_t seed, uint32_t filter_index, int32_t* anc_out,
                           int64_t* d_slot_range, pf_stream_t stream);
+
+/*
+ * Routed unsorted multinomial (Fig. 1(a)): the
+ * work-optimal alternative to pf_shard_search's replicated position generation.  Shard g
+ * generates only the positions x_k (NS-8) of its own SLOT shard [g ceil(P/G), ...) and each goes
+ * to the shard whose cumulative-weight range [off_h, off_h + T_h) holds it:
+ *   pf_shard_route_count   d_counts[nshards] (int64, device) = this slot shard's positions per
+ *                          owner shard (all zero for an invalid filter)
+ *   (caller: all_gather of the counts -> the split sizes of one variable all_to_all)
+ *   pf_shard_route_pack    send_x (u64) / send_k (int32) = the pairs (x_k, k) grouped by owner in
+ *                          shard order (group h starts at sum_{h' < h} d_counts[h']; the order
+ *                          inside a group is unspecified); d_counts from pf_shard_route_count
+ *   (caller: all_to_all of the pairs)
+ *   pf_shard_route_search  for the nrecv received pairs: anc_out[k] = p0 + min{i : Q_i > x - off}
+ *                          (the same value pf_shard_search writes); an invalid filter writes the
+ *                          identity for slots [p0, p0 + Pl).
+ * Work per rank ~ P_global / nshards generated positions + its received ones.  nshards <= 64,
+ * P_global <= 2^31 - 1.  d_totals / d_gmax / d_gbad as for pf_shard_search. */
+pf_status pf_shard_route_count(const uint64_t* d_totals, int32_t nshards, int32_t shard, int64_t P_global,
+                               const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                               int64_t* d_counts, pf_stream_t stream);
+pf_status pf_shard_route_pack(const uint64_t* d_totals, int32_t nshards, int32_t shard, int64_t P_global,
+                              const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                              const int64_t* d_counts, uint64_t* send_x, int32_t* send_k, pf_stream_t stream);
+pf_status pf_shard_route_search(const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
+                                const int32_t* d_gbad, const uint64_t* recv_x, const int32_t* recv_k, int64_t nrecv,
+                                int32_t* anc_out, pf_stream_t stream);
 /*
  * Sorted-uniform multinomial (a6, NS-12) over shards: work-optimal.
  * The P_global + 1 spacings e_0..e_P are split into nshards contiguous SPACING

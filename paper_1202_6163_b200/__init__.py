@@ -79,6 +79,9 @@ _SIGS = {
     "pf_gather_state_out": ([_V, _V, _I64, _I64, _I64, _I32, _V, _V], ctypes.c_int),
     "pf_shard_max": ([_V, _I32, _V, _V, _V], ctypes.c_int),
     "pf_shard_scan": ([_V, _I32, _I64, _V, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_route_count": ([_V, _I32, _I32, _I64, _V, _V, _U64, _U32, _V, _V], ctypes.c_int),
+    "pf_shard_route_pack": ([_V, _I32, _I32, _I64, _V, _V, _U64, _U32, _V, _V, _V, _V], ctypes.c_int),
+    "pf_shard_route_search": ([_V, _I32, _I64, _I64, _V, _I32, _I32, _V, _V, _V, _V, _I64, _V, _V], ctypes.c_int),
     "pf_shard_search": ([ctypes.c_int, _V, _I32, _I64, _I64, _V, _I32, _I32, _V, _V, _U64, _U32, _V, _V, _V],
                         ctypes.c_int),
     "pf_shard_spacings_total": ([_I64, _I32, _I32, _U64, _U32, _V, _V], ctypes.c_int),
@@ -517,6 +520,41 @@ def pf_shard_search(scheme, Q, p0: int, P_global: int, totals, shard: int, gmax,
                                  filter_index, anc_out.data_ptr(), rng.data_ptr(), _stream(Q, stream)),
            "pf_shard_search")
     return rng
+
+
+def pf_shard_route_count(totals, shard: int, P_global: int, gmax, gbad, seed: int, filter_index: int,
+                         stream=None):
+    """Routed multinomial, stage 3a (include/pf.h): int64 [nshards] positions of this rank's slot
+    shard per owner shard."""
+    torch = _torch()
+    cnt = torch.empty(totals.shape[0], dtype=torch.int64, device=totals.device)
+    _check(lib().pf_shard_route_count(totals.data_ptr(), totals.shape[0], shard, P_global, gmax.data_ptr(),
+                                      gbad.data_ptr(), seed & (2 ** 64 - 1), filter_index, cnt.data_ptr(),
+                                      _stream(totals, stream)), "pf_shard_route_count")
+    return cnt
+
+
+def pf_shard_route_pack(totals, shard: int, P_global: int, gmax, gbad, seed: int, filter_index: int, counts,
+                        n_send: int, stream=None):
+    """Stage 3b: (x u64 as int64 [n_send], k int32 [n_send]) grouped by owner shard."""
+    torch = _torch()
+    sx = torch.empty(max(n_send, 1), dtype=torch.int64, device=totals.device)
+    sk = torch.empty(max(n_send, 1), dtype=torch.int32, device=totals.device)
+    _check(lib().pf_shard_route_pack(totals.data_ptr(), totals.shape[0], shard, P_global, gmax.data_ptr(),
+                                     gbad.data_ptr(), seed & (2 ** 64 - 1), filter_index, counts.data_ptr(),
+                                     sx.data_ptr(), sk.data_ptr(), _stream(totals, stream)), "pf_shard_route_pack")
+    return sx[:n_send], sk[:n_send]
+
+
+def pf_shard_route_search(Q, p0: int, P_global: int, totals, shard: int, gmax, gbad, recv_x, recv_k, anc_out,
+                          stream=None):
+    """Stage 3c: anc_out[k] for the received pairs (identity over the shard if the filter is invalid)."""
+    n = recv_x.shape[0]
+    _check(lib().pf_shard_route_search(Q.data_ptr(), Q.shape[0], p0, P_global, totals.data_ptr(), totals.shape[0],
+                                       shard, gmax.data_ptr(), gbad.data_ptr(), recv_x.data_ptr() if n else None,
+                                       recv_k.data_ptr() if n else None, n, anc_out.data_ptr(), _stream(Q, stream)),
+           "pf_shard_route_search")
+    return anc_out
 
 
 def pf_shard_spacings_total(P_global: int, nshards: int, shard: int, seed: int, filter_index: int, device,

@@ -746,6 +746,55 @@ pf_status pf_shard_search(pf_scheme scheme, const uint64_t* d_Q, int32_t Pl, int
     return cuda_status(e);
 }
 
+pf_status pf_shard_route_count(const uint64_t* d_totals, int32_t nshards, int32_t shard, int64_t P_global,
+                               const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                               int64_t* d_counts, pf_stream_t stream) {
+    if (!d_totals || !d_gmax || !d_gbad || !d_counts) return PF_ERR_INVALID_ARG;
+    if (P_global < 1 || P_global > INT32_MAX || nshards < 1 || nshards > pf::kMaxRouteShards || shard < 0 ||
+        shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_route(d_totals, nshards, shard, d_gmax, d_gbad, P_global, seed, filter_index,
+                                           d_counts, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_route_pack(const uint64_t* d_totals, int32_t nshards, int32_t shard, int64_t P_global,
+                              const float* d_gmax, const int32_t* d_gbad, uint64_t seed, uint32_t filter_index,
+                              const int64_t* d_counts, uint64_t* send_x, int32_t* send_k, pf_stream_t stream) {
+    if (!d_totals || !d_gmax || !d_gbad || !d_counts || !send_x || !send_k) return PF_ERR_INVALID_ARG;
+    if (P_global < 1 || P_global > INT32_MAX || nshards < 1 || nshards > pf::kMaxRouteShards || shard < 0 ||
+        shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void* cur = nullptr;
+    const pf_status st = pool_get(sizeof(int64_t) * pf::kMaxRouteShards, s, &cur);
+    if (st != PF_OK) return st;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_route(d_totals, nshards, shard, d_gmax, d_gbad, P_global, seed, filter_index,
+                                           const_cast<int64_t*>(d_counts), static_cast<int64_t*>(cur), send_x, send_k,
+                                           s, &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
+pf_status pf_shard_route_search(const uint64_t* d_Q, int32_t Pl, int64_t p0, int64_t P_global,
+                                const uint64_t* d_totals, int32_t nshards, int32_t shard, const float* d_gmax,
+                                const int32_t* d_gbad, const uint64_t* recv_x, const int32_t* recv_k, int64_t nrecv,
+                                int32_t* anc_out, pf_stream_t stream) {
+    if (!d_Q || !d_totals || !d_gmax || !d_gbad || !anc_out || nrecv < 0 || (nrecv > 0 && (!recv_x || !recv_k)))
+        return PF_ERR_INVALID_ARG;
+    if (Pl < 1 || p0 < 0 || P_global < p0 + Pl || P_global > INT32_MAX || nshards < 1 ||
+        nshards > pf::kMaxRouteShards || shard < 0 || shard >= nshards)
+        return PF_ERR_INVALID_ARG;
+    uint64_t nl = 0;
+    const cudaError_t e = pf::launch_route_search(d_Q, Pl, p0, d_totals, nshards, shard, d_gmax, d_gbad, recv_x, recv_k,
+                                                  nrecv, anc_out, static_cast<cudaStream_t>(stream), &nl);
+    g_launches += nl;
+    return cuda_status(e);
+}
+
 pf_status pf_shard_spacings_total(int64_t P_global, int32_t nshards, int32_t shard, uint64_t seed,
                                   uint32_t filter_index, uint64_t* d_etotal, pf_stream_t stream) {
     if (!d_etotal || P_global < 1 || P_global > INT32_MAX || nshards < 1 || shard < 0 || shard >= nshards)

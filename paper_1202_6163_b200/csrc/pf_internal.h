@@ -134,6 +134,13 @@ cudaError_t launch_shard_weights(const float* logw, int32_t Pl, const float* gma
 cudaError_t launch_metro_slots(const float* w, int64_t P_global, int64_t slot0, int32_t nslots, uint64_t seed,
                                int32_t B, uint32_t filt, const float* gmax, const int32_t* gbad, int32_t* anc,
                                cudaStream_t s, uint64_t* launches);
+constexpr int kMaxRouteShards = 64;  // ranks of a routed multinomial (one node and beyond)
+cudaError_t launch_route(const uint64_t* totals, int nshards, int shard, const float* gmax, const int32_t* gbad,
+                         int64_t P_global, uint64_t seed, uint32_t filt, int64_t* counts, int64_t* cursor,
+                         uint64_t* send_x, int32_t* send_k, cudaStream_t s, uint64_t* launches);
+cudaError_t launch_route_search(const uint64_t* Q, int32_t Pl, int64_t p0, const uint64_t* totals, int nshards,
+                                int shard, const float* gmax, const int32_t* gbad, const uint64_t* rx,
+                                const int32_t* rk, int64_t nrecv, int32_t* anc, cudaStream_t s, uint64_t* launches);
 size_t shard_ctx_bytes();
 // a6 (sorted multinomial) shards.
 cudaError_t launch_spacings_total(int64_t P_global, int nshards, int shard, uint64_t seed, uint32_t filt,

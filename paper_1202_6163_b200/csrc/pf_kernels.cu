@@ -1437,6 +1437,112 @@ __global__ void __launch_bounds__(kThreads) k_shard_multinomial(const uint64_t* 
     }
 }
 
+// ---- Routed multinomial: rank g generates only the positions of
+// its own slot shard [k0, k1) (NS-8) and sends each to the shard whose cumulative-weight range
+// holds it (one variable all-to-all); the owner searches its local Q.  Work per rank ~ P/G.
+struct RouteRanges {
+    uint64_t off[kMaxRouteShards + 1];  // exclusive prefix of the shard totals
+    uint64_t Qtot;
+    int32_t invalid;
+};
+
+__device__ __forceinline__ void route_ranges(const uint64_t* totals, int nshards, const float* gmax,
+                                             const int32_t* gbad, RouteRanges* r) {
+    uint64_t c = 0;
+    for (int h = 0; h < nshards; ++h) {
+        r->off[h] = c;
+        c += totals[h];
+    }
+    r->off[nshards] = c;
+    r->Qtot = c;
+    r->invalid = (*gbad != 0 || *gmax == -INFINITY) ? 1 : 0;
+}
+
+// owner shard of position x: the h with off[h] <= x < off[h + 1] (empty ranges never match)
+__device__ __forceinline__ int route_owner(const RouteRanges& r, int nshards, uint64_t x) {
+    int h = 0;
+    for (int g = 1; g < nshards; ++g) h = (r.off[g] <= x) ? g : h;
+    return h;
+}
+
+// pass 1: positions of the slot shard per owner (counts[nshards], zeroed by the caller);
+// pass 2 (cursor != nullptr): (x, k) pairs grouped by owner, group h starting at the exclusive
+// prefix of counts (order inside a group is arbitrary; each pair carries its slot)
+__global__ void __launch_bounds__(kThreads) k_route(const uint64_t* totals, int nshards, const float* gmax,
+                                                    const int32_t* gbad, int64_t P_global, int64_t k0, int64_t k1,
+                                                    Key key, uint32_t filt, unsigned long long* counts,
+                                                    unsigned long long* cursor, uint64_t* send_x, int32_t* send_k) {
+    __shared__ RouteRanges s_r;
+    __shared__ unsigned long long s_base[kMaxRouteShards];
+    if (threadIdx.x == 0) route_ranges(totals, nshards, gmax, gbad, &s_r);
+    if (cursor != nullptr && threadIdx.x < nshards) {
+        unsigned long long b = 0;
+        for (int h = 0; h < static_cast<int>(threadIdx.x); ++h) b += counts[h];
+        s_base[threadIdx.x] = b;
+    }
+    __syncthreads();
+    if (s_r.invalid) return;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    // pairs of slots (one Philox call, NS-8); the loop is warp-uniform for the aggregation
+    const int64_t pr0 = k0 >> 1, pr1 = (k1 + 1) >> 1;
+    const int64_t rounds = (pr1 - pr0 + stride - 1) / stride;
+    for (int64_t rr = 0; rr < rounds; ++rr) {
+        const int64_t pr = pr0 + rr * stride + blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+        u32x4 r = {0u, 0u, 0u, 0u};
+        if (pr < pr1) r = philox10(static_cast<uint32_t>(pr), 0u, 1u, filt, key.k0, key.k1);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int64_t k = 2 * pr + hh;
+            const bool mine = pr < pr1 && k >= k0 && k < k1;
+            const uint64_t x = mine ? mulhi64(hh ? hi_word(r) : lo_word(r), s_r.Qtot) : 0;
+            const int h = mine ? route_owner(s_r, nshards, x) : -1;
+            // warp-aggregated: one atomic per (warp, owner)
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, h);
+            const int leader = __ffs(peers) - 1;
+            const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+            unsigned long long base = 0;
+            if (mine && (threadIdx.x & 31) == leader)
+                base = atomicAdd(cursor ? cursor + h : counts + h, static_cast<unsigned long long>(__popc(peers)));
+            base = __shfl_sync(0xFFFFFFFFu, base, leader);
+            if (mine && cursor) {
+                const unsigned long long at = s_base[h] + base + rank;
+                send_x[at] = x;
+                send_k[at] = static_cast<int32_t>(k);
+            }
+        }
+    }
+}
+
+// received (x, k): anc[k] = p0 + min{i : Q_i > x - off_shard}; invalid filter: the identity over
+// the shard's own particles (every rank writes its own, as the other schemes do)
+__global__ void __launch_bounds__(kThreads) k_route_search(const uint64_t* __restrict__ Q, int32_t Pl, int64_t p0,
+                                                           const uint64_t* totals, int nshards, int shard,
+                                                           const float* gmax, const int32_t* gbad,
+                                                           const uint64_t* __restrict__ rx,
+                                                           const int32_t* __restrict__ rk, int64_t nrecv,
+                                                           int32_t* anc) {
+    __shared__ RouteRanges s_r;
+    if (threadIdx.x == 0) route_ranges(totals, nshards, gmax, gbad, &s_r);
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    const int64_t g0 = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x;
+    if (s_r.invalid) {
+        for (int64_t i = g0; i < Pl; i += stride) anc[p0 + i] = static_cast<int32_t>(p0 + i);
+        return;
+    }
+    const uint64_t off = s_r.off[shard];
+    for (int64_t t = g0; t < nrecv; t += stride) {
+        const uint64_t xl = __ldg(rx + t) - off;
+        int64_t lo = 0, hi = Pl - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(Q + mid) > xl) hi = mid;
+            else lo = mid + 1;
+        }
+        anc[__ldg(rk + t)] = static_cast<int32_t>(p0 + lo);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_shard_weights(const float* __restrict__ logw, int32_t Pl,
                                                             const float* gmax, float* w) {
     const float lm = *gmax;
@@ -2253,6 +2359,44 @@ static SpacShardLayout spac_shard_layout(int64_t P_global) {
 }
 
 size_t spac_shard_workspace_bytes(int64_t P_global) { return spac_shard_layout(P_global).total; }
+
+// slot shard of rank `shard`: [shard ceil(P/G), ...) as shard_range in paper_1202_6163_b200/shard.py
+static void route_slots(int64_t P_global, int nshards, int shard, int64_t* k0, int64_t* k1) {
+    const int64_t per = (P_global + nshards - 1) / nshards;
+    *k0 = std::min<int64_t>(P_global, static_cast<int64_t>(shard) * per);
+    *k1 = std::min<int64_t>(P_global, *k0 + per);
+}
+
+cudaError_t launch_route(const uint64_t* totals, int nshards, int shard, const float* gmax, const int32_t* gbad,
+                         int64_t P_global, uint64_t seed, uint32_t filt, int64_t* counts, int64_t* cursor,
+                         uint64_t* send_x, int32_t* send_k, cudaStream_t s, uint64_t* launches) {
+    int64_t k0, k1;
+    route_slots(P_global, nshards, shard, &k0, &k1);
+    const int64_t pairs = std::max<int64_t>(1, ((k1 + 1) >> 1) - (k0 >> 1));
+    const unsigned grid = static_cast<unsigned>(grid_for(pairs, 4));
+    cudaError_t e = cudaMemsetAsync(cursor ? cursor : counts, 0, sizeof(int64_t) * nshards, s);
+    if (e != cudaSuccess) return e;
+    {
+        ProfScope ps_(cursor ? "k_route_pack" : "k_route_count", s, cursor ? static_cast<uint64_t>(k1 - k0) * 12u : 0u);
+        k_route<<<grid, kThreads, 0, s>>>(totals, nshards, gmax, gbad, P_global, k0, k1, make_key(seed), filt,
+                                          reinterpret_cast<unsigned long long*>(counts),
+                                          reinterpret_cast<unsigned long long*>(cursor), send_x, send_k);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_route_search(const uint64_t* Q, int32_t Pl, int64_t p0, const uint64_t* totals, int nshards,
+                                int shard, const float* gmax, const int32_t* gbad, const uint64_t* rx,
+                                const int32_t* rk, int64_t nrecv, int32_t* anc, cudaStream_t s, uint64_t* launches) {
+    const unsigned grid = static_cast<unsigned>(grid_for(std::max<int64_t>(std::max<int64_t>(nrecv, Pl), 1), 4));
+    {
+        ProfScope ps_("k_route_search", s, static_cast<uint64_t>(nrecv) * 16u);  // (x, k) read, ancestor written
+        k_route_search<<<grid, kThreads, 0, s>>>(Q, Pl, p0, totals, nshards, shard, gmax, gbad, rx, rk, nrecv, anc);
+    }
+    ++*launches;
+    return cudaPeekAtLastError();
+}
 
 cudaError_t launch_shard_search_sorted(const uint64_t* Q, int32_t Pl, int64_t p0, int64_t P_global,
                                        const uint64_t* totals, const uint64_t* etotals, int nshards, int shard,

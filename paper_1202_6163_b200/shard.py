@@ -10,6 +10,10 @@ into a per-GPU scan plus an 8-byte-per-rank exchange):
                        search: every rank computes its own slot range from the
                        totals (positions are functions of the slot index) and
                        writes the ancestors of those slots.
+  unsorted multinomial routed (NEXT-4): rank g generates only the positions of its own
+                       slot shard, all-gathers the per-owner counts (G x G int64) and sends
+                       each position to the shard whose weight range holds it in one
+                       variable all_to_all; the owner searches its local Q (work ~ P/G).
   sorted multinomial   (a6, ``flags=PF_SORTED``) additionally all-gathers the
                        8-byte totals of the exponential spacings of each
                        spacing shard; each rank then regenerates
@@ -185,6 +189,15 @@ class GpuStages:
         return self.pf.pf_shard_search(scheme, Q, p0, P_global, totals, shard, gmax, gbad, seed, filter_index,
                                        anc_out)
 
+    def route_count(self, totals, shard, P_global, gmax, gbad, seed, filter_index):
+        return self.pf.pf_shard_route_count(totals, shard, P_global, gmax, gbad, seed, filter_index)
+
+    def route_pack(self, totals, shard, P_global, gmax, gbad, seed, filter_index, counts, n_send):
+        return self.pf.pf_shard_route_pack(totals, shard, P_global, gmax, gbad, seed, filter_index, counts, n_send)
+
+    def route_search(self, Q, p0, P_global, totals, shard, gmax, gbad, rx, rk, anc_out):
+        return self.pf.pf_shard_route_search(Q, p0, P_global, totals, shard, gmax, gbad, rx, rk, anc_out)
+
     def spacings_total(self, P_global, nshards, shard, seed, filter_index, device):
         return self.pf.pf_shard_spacings_total(P_global, nshards, shard, seed, filter_index, device)
 
@@ -271,6 +284,9 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
         etot = stages.spacings_total(P_global, world, rank, seed, filter_index, logw_local.device)
         etotals = comm.all_gather_cat(etot)
         rng = stages.search_sorted(Q, p0, P_global, totals, etotals, rank, gmax, gbad, seed, filter_index, anc)
+    elif scheme_id == 1:
+        rng = _route_multinomial(Q, p0, P_global, totals, world, rank, gmax, gbad, seed, filter_index, anc,
+                                 comm, stages)
     else:
         rng = stages.search(scheme_id, Q, p0, P_global, totals, rank, gmax, gbad, seed, filter_index, anc)
     info["slot_range_dev"] = rng
@@ -295,6 +311,30 @@ def resample_sharded(scheme, logw_local, P_global: int, seed: int, B: int = 0, f
         out = anc
     _raise_if(shape_err)
     return out, info
+
+
+def route_splits(counts_matrix, rank: int):
+    """(send_splits, recv_splits) of ``rank`` from the all-gathered G x G matrix of per-owner
+    position counts (row g = what rank g's slot shard sends to each owner)."""
+    send = [int(v) for v in counts_matrix[rank]]
+    recv = [int(row[rank]) for row in counts_matrix]
+    return send, recv
+
+
+def _route_multinomial(Q, p0, P_global, totals, world, rank, gmax, gbad, seed, filter_index, anc, comm, stages):
+    """Routed unsorted multinomial (include/pf.h 3a-3c): this rank's slot shard's positions to
+    their owners, one variable all_to_all of (x, k); the owners' searches write anc[k].  One host
+    read of the G x G counts sizes the exchange.  Returns an empty slot range (slots scatter)."""
+    import torch
+
+    cnt = stages.route_count(totals, rank, P_global, gmax, gbad, seed, filter_index)
+    M = comm.all_gather_cat(cnt).cpu().view(world, world).tolist()
+    send, recv = route_splits(M, rank)
+    sx, sk = stages.route_pack(totals, rank, P_global, gmax, gbad, seed, filter_index, cnt, sum(send))
+    rx = comm.all_to_all_v(sx, send, recv)
+    rk = comm.all_to_all_v(sk, send, recv)
+    stages.route_search(Q, p0, P_global, totals, rank, gmax, gbad, rx, rk, anc)
+    return torch.zeros(2, dtype=torch.int64, device=anc.device)
 
 
 def _raise_if(msg):
@@ -422,6 +462,20 @@ def resample_sharded_local(scheme, logw_full, nshards: int, seed: int, B: int = 
                              for g in range(nshards)])
         for g, ((p0, Pl), (Q, _, _)) in enumerate(zip(parts, scans)):
             stages.search_sorted(Q, p0, P_global, totals, etotals, g, gmax, gbad, seed, filter_index, anc)
+        return anc
+    if scheme_id == 1:
+        # routed: every slot shard's positions to their owners (the all-to-all by slicing)
+        cnts = [stages.route_count(totals, g, P_global, gmax, gbad, seed, filter_index) for g in range(nshards)]
+        M = torch.stack(cnts).cpu().tolist()
+        packs = [stages.route_pack(totals, g, P_global, gmax, gbad, seed, filter_index, cnts[g], sum(M[g]))
+                 for g in range(nshards)]
+        for h, ((p0, Pl), (Q, _, _)) in enumerate(zip(parts, scans)):
+            xs, ks = [], []
+            for g in range(nshards):
+                a = sum(M[g][:h])
+                xs.append(packs[g][0][a:a + M[g][h]])
+                ks.append(packs[g][1][a:a + M[g][h]])
+            stages.route_search(Q, p0, P_global, totals, h, gmax, gbad, torch.cat(xs), torch.cat(ks), anc)
         return anc
     for g, ((p0, Pl), (Q, _, _)) in enumerate(zip(parts, scans)):
         stages.search(scheme_id, Q, p0, P_global, totals, g, gmax, gbad, seed, filter_index, anc)

@@ -44,6 +44,52 @@ class CpuOracleStages:
         rng = (min(ks), max(ks) + 1) if ks else (0, 0)
         return torch.tensor(rng, dtype=torch.int64)
 
+    # routed unsorted multinomial (include/pf.h 3a-3c): slot shard g = [g ceil(P/G), ...)
+    @staticmethod
+    def _owner(x, tot):
+        c = 0
+        for h, t in enumerate(tot):
+            if c <= x < c + t:
+                return h, c
+            c += t
+        raise AssertionError("position outside [0, Q)")
+
+    def _slot_positions(self, totals, shard, P_global, gmax, gbad, seed, filter_index):
+        if int(gbad.item()) or float(gmax.item()) == -np.inf:
+            return []
+        tot = [int(v) for v in totals.numpy().view(np.uint64)]
+        per = -(-P_global // len(tot))
+        k0, k1 = min(P_global, shard * per), min(P_global, (shard + 1) * per)
+        out = []
+        for k in range(k0, k1):
+            x = oracle.position(1, P_global, sum(tot), seed, filter_index, k)
+            out.append((self._owner(x, tot)[0], x, k))
+        return out
+
+    def route_count(self, totals, shard, P_global, gmax, gbad, seed, filter_index):
+        c = np.zeros(totals.shape[0], dtype=np.int64)
+        for h, _, _ in self._slot_positions(totals, shard, P_global, gmax, gbad, seed, filter_index):
+            c[h] += 1
+        return torch.from_numpy(c)
+
+    def route_pack(self, totals, shard, P_global, gmax, gbad, seed, filter_index, counts, n_send):
+        pos = sorted(self._slot_positions(totals, shard, P_global, gmax, gbad, seed, filter_index))
+        assert len(pos) == n_send
+        xs = np.array([x for _, x, _ in pos], dtype=np.uint64).view(np.int64)
+        ks = np.array([k for _, _, k in pos], dtype=np.int32)
+        return torch.from_numpy(xs), torch.from_numpy(ks)
+
+    def route_search(self, Q, p0, P_global, totals, shard, gmax, gbad, rx, rk, anc_out):
+        Ql = Q.numpy().view(np.uint64)
+        if int(gbad.item()) or float(gmax.item()) == -np.inf:
+            anc_out[p0:p0 + len(Ql)] = torch.arange(p0, p0 + len(Ql), dtype=torch.int32)
+            return anc_out
+        tot = [int(v) for v in totals.numpy().view(np.uint64)]
+        off = sum(tot[:shard])
+        for x, k in zip(rx.numpy().view(np.uint64), rk.numpy()):
+            anc_out[int(k)] = p0 + int(np.searchsorted(Ql, np.uint64(int(x) - off), side="right"))
+        return anc_out
+
     # a6 sorted multinomial (NS-12): spacing totals per spacing shard, positions
     # x_k = floor(G_k Q / G_P) in exact Python integers from the oracle's G.
     @staticmethod

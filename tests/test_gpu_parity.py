@@ -1122,3 +1122,30 @@ def test_fused_permutation_from_offspring(pf, dev, orc, N, P):
         for n in (0, 1, N - 1):
             wp = orc.permute(want[n])
             assert np.array_equal(p2[n].cpu().numpy(), wp) and np.array_equal(p3[n].cpu().numpy(), wp), (scheme, n)
+
+
+def test_routed_multinomial_matches_replicated(pf, dev, orc):
+    """The routed multinomial stages (pf_shard_route_count / pack / search) and the replicated
+    pf_shard_search give the same ancestors, shard by shard (fake shards), and the oracle's."""
+    import torch
+
+    from paper_1202_6163_b200.shard import GpuStages, resample_sharded_local, shard_range
+
+    st = GpuStages()
+    for P, G in ((20011, 4), (1 << 18, 8)):
+        x = pfinputs.gaussian_logw(P, 1.0, seed=P)
+        g = _gpu(x, dev)
+        routed = resample_sharded_local("multinomial", g, G, 99, filter_index=2)
+        parts = [shard_range(P, G, h) for h in range(G)]
+        mx = [st.max(g[p0:p0 + Pl]) for p0, Pl in parts]
+        gmax = torch.stack([m for m, _ in mx]).max(dim=0).values
+        gbad = torch.stack([b for _, b in mx]).max(dim=0).values
+        scans = [st.scan(g[p0:p0 + Pl], P, gmax) for p0, Pl in parts]
+        totals = torch.cat([t for _, t, _ in scans])
+        rep = torch.full((P,), -1, dtype=torch.int32, device=dev)
+        for h, ((p0, _), (Q, _, _)) in enumerate(zip(parts, scans)):
+            st.search(1, Q, p0, P, totals, h, gmax, gbad, 99, 2, rep)
+        torch.cuda.synchronize()
+        _, want = orc.resample("multinomial", x, 99, filter_index=2)
+        assert np.array_equal(routed.cpu().numpy(), want), (P, G)
+        assert np.array_equal(rep.cpu().numpy(), want), (P, G)
