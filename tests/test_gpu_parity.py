@@ -1149,3 +1149,29 @@ def test_routed_multinomial_matches_replicated(pf, dev, orc):
         _, want = orc.resample("multinomial", x, 99, filter_index=2)
         assert np.array_equal(routed.cpu().numpy(), want), (P, G)
         assert np.array_equal(rep.cpu().numpy(), want), (P, G)
+
+
+@pytest.mark.parametrize("D", [16, 3, 6])
+def test_lg_step_elementwise(pf, dev, orc, D):
+    """C4 propagate + weight kernel (k_lg_step, k_lg_init) element by element against the
+    oracle/lg_model.py step from the same input state (NS-18): states within 1e-5 (1 + |x|),
+    log-weights within 1e-5 (1 + |logw|) of the binary64 oracle (the kernel's binary32 arithmetic
+    and <= 2-ulp library functions), for the float4 rows (D = 16) and the scalar rows."""
+    import torch
+
+    from oracle import lg_model
+
+    P, phi, sx, sy, seed = 3001, 0.9, 1.0, 1.0, 0x5EED
+    X = torch.empty((P, D), device=dev)
+    pf.pf_lg_init(X, phi, sx, seed)
+    torch.cuda.synchronize()
+    X0 = lg_model.lg_init(P, D, phi, sx, seed)
+    assert np.allclose(X.cpu().numpy(), X0, rtol=0, atol=1e-5 * (1 + np.abs(X0).max()))
+    for t, y in ((0, 0.3), (17, -2.5)):
+        Xin = X.cpu().numpy().astype(np.float64)
+        logw = pf.pf_lg_propagate_weight(X, phi, sx, sy, y, seed, t)
+        torch.cuda.synchronize()
+        Xw, lw = lg_model.lg_step(Xin, y, t, phi, sx, sy, seed)
+        got = X.cpu().numpy()
+        assert np.all(np.abs(got - Xw) <= 1e-5 * (1 + np.abs(Xw))), (D, t)
+        assert np.all(np.abs(logw.cpu().numpy() - lw) <= 1e-5 * (1 + np.abs(lw))), (D, t)

@@ -811,3 +811,31 @@ def test_sorted_weights_laws(orc):
         for s in SORTED_SCHEMES:
             st, a = orc.resample_sorted_weights(s, bad, 3)
             assert st == 1 and list(a) == [0, 1, 2]
+
+
+# --------------------------------------------------------------------------- C4 model (NS-18)
+def test_lg_model_noise_is_standard_normal(orc):
+    """oracle/lg_model.py: the Box-Muller noise of the C4 step is N(0, 1) (KS test against the
+    normal CDF over 4 x 4096 draws; pairs uncorrelated), and one step of the AR(1) from x has mean
+    phi x and variance sigma_x^2 per dimension (R-20), the weight the Gaussian log-density."""
+    from scipy import stats
+
+    from oracle import lg_model
+
+    z = np.concatenate([lg_model.noise(i, 3, 6, 12345) for i in range(4096)])
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+    zz = z.reshape(-1, 4)
+    assert abs(np.corrcoef(zz[:, 0], zz[:, 1])[0, 1]) < 0.05
+    assert abs(np.corrcoef(zz[:, 0], zz[:, 2])[0, 1]) < 0.05
+    P, D, phi, sx, sy = 4000, 5, 0.9, 0.7, 1.3
+    X = np.full((P, D), 2.0)
+    Xn, logw = lg_model.lg_step(X, 0.4, 7, phi, sx, sy, 99)
+    d = Xn - phi * X
+    se = sx / math.sqrt(P)
+    assert np.all(np.abs(d.mean(axis=0)) < 5 * se)
+    assert np.all(np.abs(d.std(axis=0) / sx - 1.0) < 0.06)
+    assert np.allclose(logw, -((0.4 - Xn[:, 0]) ** 2) / (2 * sy * sy))
+    # distinct time steps and particles draw distinct noise (the Philox counter layout)
+    assert not np.allclose(lg_model.noise(5, 1, 6, 99), lg_model.noise(5, 2, 6, 99))
+    X0 = lg_model.lg_init(3000, 4, phi, sx, 7)
+    assert abs(X0.var() / (sx * sx / (1 - phi * phi)) - 1.0) < 0.06
