@@ -251,47 +251,21 @@ void pfo_systematic_from_R(const uint64_t* Q, int32_t P, uint64_t R, int32_t* an
 /* ------------------------------------------------------------------------ */
 /* NS-11  Metropolis resampler.                      */
 /* ------------------------------------------------------------------------ */
-/* NS-11b (R-23, "the rate at which random numbers can be generated"):
- * for P = 2^m with 1 <= m <= 16 one Philox call feeds THREE proposals instead of two:
- * proposal b uses call c1 = b / 3 and t = b % 3, word r = x_t for u (its top 24 bits) and,
- * for j, the low byte of x_t followed by byte t of x_3 (16 bits, the top m of them).  Same
- * law (j uniform on the P indices, u on the 24-bit grid, disjoint bits). */
-static int pack3_bits(int64_t P)
-{
-    if (P < 2 || P > 65536 || (P & (P - 1)) != 0) return 0;
-    int m = 0;
-    while ((INT64_C(1) << m) < P) ++m;
-    return m;
-}
-
 void pfo_metropolis_chains(const float* w, int32_t P, int64_t slot0, int32_t nslots,
                            uint64_t seed, int32_t B, uint32_t filter_index, int32_t* anc)
 {
-    const int m3 = pack3_bits(P);
     for (int32_t s = 0; s < nslots; ++s) {
         int64_t i = slot0 + s;
         int64_t k = i;       /* G3: chain starts at its own particle */
         float wk = w[k];
         uint32_t x[4] = { 0, 0, 0, 0 };
         for (int32_t b = 0; b < B; ++b) {
-            int64_t j;
-            uint32_t ru;
-            if (m3) {
-                /* NS-11b */
-                int t = b % 3;
-                if (t == 0)
-                    philox_draw(seed, (uint32_t)i, (uint32_t)(b / 3), PFO_METROPOLIS, filter_index, x);
-                ru = x[t];
-                uint32_t j16 = ((x[t] & 0xFFu) << 8) | ((x[3] >> (8 * t)) & 0xFFu);
-                j = (int64_t)(j16 >> (16 - m3));
-            } else {
-                if ((b & 1) == 0)
-                    philox_draw(seed, (uint32_t)i, (uint32_t)(b >> 1), PFO_METROPOLIS, filter_index, x);
-                uint32_t rj = (b & 1) ? x[2] : x[0];
-                ru = (b & 1) ? x[3] : x[1];
-                /* proposal: uniform over all particle indices (line:proposal) */
-                j = (int64_t)(((uint64_t)rj * (uint64_t)P) >> 32);
-            }
+            if ((b & 1) == 0)
+                philox_draw(seed, (uint32_t)i, (uint32_t)(b >> 1), PFO_METROPOLIS, filter_index, x);
+            uint32_t rj = (b & 1) ? x[2] : x[0];
+            uint32_t ru = (b & 1) ? x[3] : x[1];
+            /* proposal: uniform over all particle indices (line:proposal) */
+            int64_t j = (int64_t)(((uint64_t)rj * (uint64_t)P) >> 32);
             /* u on the 24-bit grid of [0,1) */
             float u = (float)(ru >> 8) * f32_from_bits(0x33800000u); /* 2^-24 */
             float wj = w[j];

@@ -435,11 +435,10 @@ def _metro_kernel(w, P):
 
 
 def test_metropolis_exact_small(orc):
-    """P <= 4 brute force: each chain's ancestor law equals row i of K^B (NS-11; P = 2, 4 take
-    NS-11b's three proposals per Philox call, B = 5, 7 crossing call boundaries); catches a wrong
+    """P <= 4 brute force: each chain's ancestor law equals row i of K^B (NS-11); catches a wrong
     proposal map, a flipped comparison or a reused random word."""
     n = 20000
-    for P, B, seed in ((3, 1, 4), (3, 5, 5), (4, 3, 6), (4, 7, 7), (2, 5, 8)):
+    for P, B, seed in ((3, 1, 4), (3, 5, 5), (4, 3, 6)):
         x = pfinputs.gaussian_logw(P, 1.0, seed=seed)
         st, w = orc.weights(x)
         KB = np.linalg.matrix_power(_metro_kernel(w, P), B)
