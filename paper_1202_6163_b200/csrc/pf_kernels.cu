@@ -198,12 +198,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const float* __restrict__ 
         }
         if (lane < kThreads / 32) s_off[lane] = prefix + wi - wv;
         if (j == T - 1) {
-            // last tile of the filter: every predecessor's partial sums are visible
-            // (written before its first status release; acquire chain of the lookback).
-            __threadfence();
+            // last tile of the filter: every predecessor wrote its partial sums before its first
+            // status release; an acquire load of each predecessor's (non-empty) status word
+            // synchronises with that release directly, so the sums read after it are visible
+            // (no reliance on transitive relaxed chains through the lookback).
+            __syncwarp();  // this tile's own sums (lane 0's stores) for the lane that reads them
             double a = 0.0, b = 0.0;
             const int64_t t0 = static_cast<int64_t>(n) * T;
-            for (int t = lane; t < T; t += 32) { a += __ldcg(ws.tsum + t0 + t); b += __ldcg(ws.tsum2 + t0 + t); }
+            for (int t = lane; t < T; t += 32) {
+                if (t != j)
+                    while ((ld_acquire(st + t) >> kFlagShift) == 0) {
+                    }
+                a += __ldcg(ws.tsum + t0 + t);
+                b += __ldcg(ws.tsum2 + t0 + t);
+            }
             a = warp_sum_f64(a);
             b = warp_sum_f64(b);
             if (lane == 0) {
