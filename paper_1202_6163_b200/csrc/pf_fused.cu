@@ -279,6 +279,12 @@ __host__ __device__ constexpr int fused_min_blocks() {
     return (FT == 256 && PERM == 2) ? PF_FT256_DC_BLOCKS : 1024 / FT;
 }
 constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner), P <= 65536
+#ifndef PF_TICK_B
+#define PF_TICK_B 1  // a tick after each row of phase B
+#endif
+#ifndef PF_TICK_C
+#define PF_TICK_C 1  // a tick after each row's slot counts in phase C
+#endif
 #ifndef PF_PREFETCH_NEXT
 #define PF_PREFETCH_NEXT 1
 #endif
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             ex[j] = incl - loc;
             const uint64_t wt = __shfl_sync(kFull, incl, 31);
             if (lane == 0) s_wt[j][warp] = wt;
-            tick();
+            if (PF_TICK_B) tick();
         }
         if (SUMS) {
             sw = warp_sum_f64(sw);
@@ -933,7 +939,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 }
             }
             if (lane == 31) s_lastE[j][warp] = E[j * 4 + 3];
-            tick();
+            if (PF_TICK_C) tick();
         }
         if (tid == 0) s_klo = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O);
         if (SCHEME == kBuckets && c == 0 && tid == 0) a.Qtot_out[n] = z.Qtot;
