@@ -80,6 +80,74 @@ __device__ __forceinline__ float dexp(float t) {
     return fminf(w, 1.0f);
 }
 
+// NS-4 for two weights at once with the Blackwell packed FP32 instructions (FFMA2 / FMUL2 /
+// FADD2: fma.rn / mul.rn / add.rn .f32x2, each lane an IEEE round-to-nearest operation), so the
+// result is bit-identical to two dexp() calls while the polynomial issues half the
+// instructions.  Same steps as dexp(); the selects stay per lane.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_splat(uint32_t bits) {
+    return (static_cast<uint64_t>(bits) << 32) | bits;
+}
+
+// w = dexp(fl(logw - lmax)) for two log-weights (NS-3 + NS-4), bit-identical to weight()
+__device__ __forceinline__ void weight2(float l0, float l1, float lmax, float& w0, float& w1) {
+    const float kTiny = __uint_as_float(0x00800000u);  // 2^-126
+    float t0, t1;
+    f2_unpack(f2_add(f2_pack(l0, l1), f2_pack(-lmax, -lmax)), t0, t1);  // fl(logw - lmax): exact negation
+    const bool k0 = !(t0 >= -88.0f), k1 = !(t1 >= -88.0f);              // step 1 (also -inf)
+    float a0 = k0 ? 0.0f : t0, a1 = k1 ? 0.0f : t1;
+    a0 = (fabsf(a0) < kTiny) ? 0.0f : a0;                               // step 2
+    a1 = (fabsf(a1) < kTiny) ? 0.0f : a1;
+    const uint64_t tt = f2_pack(a0, a1);
+    float n0, n1;
+    f2_unpack(f2_mul(tt, f2_splat(0x3FB8AA3Bu)), n0, n1);                // step 3
+    n0 = rintf(n0);
+    n1 = rintf(n1);
+    const uint64_t n = f2_pack(n0, n1);
+    // step 4: fma(-n, c, t) == fma(n, -c, t) exactly (negation is exact)
+    uint64_t r = f2_fma(n, f2_splat(0x3F317200u ^ 0x80000000u), tt);
+    r = f2_fma(n, f2_splat(0x35BFBE8Eu ^ 0x80000000u), r);
+    uint64_t p = f2_splat(0x39500D01u);                                  // step 5
+    p = f2_fma(p, r, f2_splat(0x3AB60B61u));
+    p = f2_fma(p, r, f2_splat(0x3C088889u));
+    p = f2_fma(p, r, f2_splat(0x3D2AAAABu));
+    p = f2_fma(p, r, f2_splat(0x3E2AAAABu));
+    p = f2_fma(p, r, f2_splat(0x3F000000u));                             // 0.5
+    p = f2_fma(p, r, f2_splat(0x3F800000u));                             // 1
+    p = f2_fma(p, r, f2_splat(0x3F800000u));                             // 1
+    const int i0 = static_cast<int>(n0), i1 = static_cast<int>(n1);      // step 6
+    const uint32_t s0 = (i0 >= -126) ? (static_cast<uint32_t>(i0 + 127) << 23) : 0u;
+    const uint32_t s1 = (i1 >= -126) ? (static_cast<uint32_t>(i1 + 127) << 23) : 0u;
+    float x0, x1;
+    f2_unpack(f2_mul(p, (static_cast<uint64_t>(s1) << 32) | s0), x0, x1);
+    x0 = (k0 || x0 < kTiny) ? 0.0f : x0;                                 // step 7
+    x1 = (k1 || x1 < kTiny) ? 0.0f : x1;
+    w0 = fminf(x0, 1.0f);
+    w1 = fminf(x1, 1.0f);
+}
+
 // ---------------------------------------------------------------- NS-5
 // q = trunc(w * 2^kfx): w is 0 or a normal float in [2^-126, 1] (NS-4 flushes).
 __device__ __forceinline__ uint64_t quantise(float w, int kfx) {

@@ -279,6 +279,9 @@ __host__ __device__ constexpr int fused_min_blocks() {
     return (FT == 256 && PERM == 2) ? PF_FT256_DC_BLOCKS : 1024 / FT;
 }
 constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner), P <= 65536
+#ifndef PF_FFMA2
+#define PF_FFMA2 1  // phase B's dexp on packed f32x2 (FFMA2 / FMUL2)
+#endif
 #ifndef PF_TICK_B
 #define PF_TICK_B 1  // a tick after each row of phase B
 #endif
@@ -782,9 +785,14 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
             uint64_t loc = 0;
+            if (PF_FFMA2) {
+                // two weights per packed f32x2 evaluation (bit-identical to weight())
+                weight2(v[j * 4 + 0], v[j * 4 + 1], lm, v[j * 4 + 0], v[j * 4 + 1]);
+                weight2(v[j * 4 + 2], v[j * 4 + 3], lm, v[j * 4 + 2], v[j * 4 + 3]);
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float w = weight(v[j * 4 + q], lm);
+                const float w = PF_FFMA2 ? v[j * 4 + q] : weight(v[j * 4 + q], lm);
                 v[j * 4 + q] = w;
                 if (SUMS) {
                     sw += static_cast<double>(w);
@@ -1492,9 +1500,13 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) v4[q] = (i0 + q < c1) ? __ldg(frow + i0 + q) : -INFINITY;
                 }
+                if (PF_FFMA2) {
+                    weight2(v4[0], v4[1], lm, v4[0], v4[1]);
+                    weight2(v4[2], v4[3], lm, v4[2], v4[3]);
+                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float w = weight(v4[q], lm);
+                    const float w = PF_FFMA2 ? v4[q] : weight(v4[q], lm);
                     tot += quantise(w, a.kfx);
                     if (SUMS) {
                         sw += static_cast<double>(w);
@@ -1574,9 +1586,13 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
                 uint64_t loc = 0;
+                if (PF_FFMA2) {
+                    weight2(v[j * 4 + 0], v[j * 4 + 1], lm, v[j * 4 + 0], v[j * 4 + 1]);
+                    weight2(v[j * 4 + 2], v[j * 4 + 3], lm, v[j * 4 + 2], v[j * 4 + 3]);
+                }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float w = weight(v[j * 4 + q], lm);
+                    const float w = PF_FFMA2 ? v[j * 4 + q] : weight(v[j * 4 + q], lm);
                     v[j * 4 + q] = w;
                     loc += quantise(w, a.kfx);
                 }
