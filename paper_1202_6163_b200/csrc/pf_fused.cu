@@ -279,6 +279,9 @@ __host__ __device__ constexpr int fused_min_blocks() {
     return (FT == 256 && PERM == 2) ? PF_FT256_DC_BLOCKS : 1024 / FT;
 }
 constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner), P <= 65536
+#ifndef PF_ROW_SKIP
+#define PF_ROW_SKIP 1  // expansion marks: skip a thread's rows whose slots miss the chunk
+#endif
 #ifndef PF_FFMA2
 #define PF_FFMA2 1  // phase B's dexp on packed f32x2 (FFMA2 / FMUL2)
 #endif
@@ -997,6 +1000,8 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 __syncthreads();
 #pragma unroll
                 for (int j = 0; j < kFR; ++j) {
+                    // the row's heads lie in [first[j], E[j*4+3]): skip rows outside this chunk
+                    if (PF_ROW_SKIP && (E[j * 4 + 3] <= c0 || first[j] >= c0 + static_cast<uint32_t>(kXS))) continue;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
@@ -1712,6 +1717,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     __syncthreads();
 #pragma unroll
                     for (int j = 0; j < kFR; ++j) {
+                        if (PF_ROW_SKIP && (E[j * 4 + 3] <= q0 || first[j] >= q0 + static_cast<uint32_t>(kXS))) continue;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const uint32_t pe = (q == 0) ? first[j] : E[j * 4 + q - 1];
