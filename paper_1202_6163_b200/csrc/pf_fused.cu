@@ -282,6 +282,12 @@ constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner),
 #ifndef PF_ROW_SKIP
 #define PF_ROW_SKIP 1  // expansion marks: skip a thread's rows whose slots miss the chunk
 #endif
+#ifndef PF_PF_L2
+#define PF_PF_L2 1  // deferred copy: L2 prefetch of each pair's owner row when the pair is queued
+                    // (C3 step 1.350 -> 1.333 ms; prefetching every owner at once instead -- at
+                    // the end of phase C, or before the in-line copies of other schemes -- floods
+                    // L2 and the memory system: 1.58 ms, stratified step 2.0 -> 2.4 ms)
+#endif
 #ifndef PF_FFMA2
 #define PF_FFMA2 1  // phase B's dexp on packed f32x2 (FFMA2 / FMUL2)
 #endif
@@ -1201,11 +1207,18 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                                 }
                                 const int32_t slot = static_cast<int32_t>(rfs[R - rb]);
                                 prow[slot] = h[t];
-                                if (DC)
+                                if (DC) {
                                     ring[(rq_tail + 8 * lane + t) & (kRQ - 1)] =
                                         (static_cast<uint32_t>(slot) << 16) | static_cast<uint32_t>(h[t]);
-                                else if (PERM == 2)
+                                    if (PF_PF_L2 && (t == 0 || h[t] != h[t - 1])) {
+                                        const char* src = a.X + static_cast<int64_t>(n) * a.xfld +
+                                                          static_cast<int64_t>(h[t]) * a.xld;
+                                        for (int b = 0; b < (16 << cxl); b += 128)
+                                            asm volatile("prefetch.global.L2 [%0];" ::"l"(src + b));
+                                    }
+                                } else if (PERM == 2) {
                                     s_pslot[8 * tid + t] = slot;
+                                }
                                 ++R;
                             }
                         }
