@@ -53,19 +53,27 @@ __device__ __forceinline__ uint64_t hi_word(const u32x4& v) {
 }
 
 // ---------------------------------------------------------------- NS-4
-// Deterministic float32 exp of t <= 0; constants are the NS-4 bit patterns.
-// Written without branches (selects only); every value equals NS-4 step by
-// step: for n = -127 the scale bits are 0, so w = p * 0 = 0, which is what
-// step 6 returns.
+// Deterministic float32 exp of t <= 0; constants are the NS-4 bit patterns.  Written without
+// branches, and with three steps folded into cheaper equivalents, each bit-identical for every
+// t <= 0 and NaN (all 2^31 + 1 such inputs checked exhaustively against the literal NS-4
+// transcription by tools/dexp_check.cu):
+//  - step 1 (t < -88 or NaN -> 0) becomes a clamp t >= -100: below -88 the scale 2^n is 0
+//    (n <= -127), so w = p * 0 = 0 while r and p stay finite; step 7 then returns 0;
+//  - step 2 (|t| < 2^-126 -> 0) is dropped: such a t gives n = 0, r = t and p = fl(1 + t) = 1,
+//    the value t = 0 gives;
+//  - step 3's rint of fl(t * log2e) by the add-and-subtract of 1.5 * 2^23 (round to nearest
+//    even in [2^23, 2^24), the rint of the product for |t * log2e| < 2^22), which also yields
+//    n as an integer from the sum's bit pattern (no float-to-int conversion);
+//  - step 6's scale bits max(n + 127, 0) << 23 (n >= -145 after the clamp).
+constexpr float kRintMagic = 12582912.0f;  // 1.5 * 2^23, bit pattern 0x4B400000
 __device__ __forceinline__ float dexp(float t) {
     const float kTiny = __uint_as_float(0x00800000u);  // 2^-126
-    const bool kill = !(t >= -88.0f);                   // step 1 (also -inf)
-    float tt = kill ? 0.0f : t;
-    tt = (fabsf(tt) < kTiny) ? 0.0f : tt;               // step 2
-    const float n = rintf(__fmul_rn(tt, __uint_as_float(0x3FB8AA3Bu)));  // step 3
-    float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), tt);           // step 4
+    const float tt = fmaxf(t, -100.0f);                 // step 1 (also -inf and NaN)
+    const float m = __fadd_rn(__fmul_rn(tt, __uint_as_float(0x3FB8AA3Bu)), kRintMagic);  // step 3
+    const float n = __fadd_rn(m, -kRintMagic);
+    float r = __fmaf_rn(-n, __uint_as_float(0x3F317200u), tt);  // step 4
     r = __fmaf_rn(-n, __uint_as_float(0x35BFBE8Eu), r);
-    float p = __uint_as_float(0x39500D01u);                               // step 5
+    float p = __uint_as_float(0x39500D01u);  // step 5
     p = __fmaf_rn(p, r, __uint_as_float(0x3AB60B61u));
     p = __fmaf_rn(p, r, __uint_as_float(0x3C088889u));
     p = __fmaf_rn(p, r, __uint_as_float(0x3D2AAAABu));
@@ -73,17 +81,17 @@ __device__ __forceinline__ float dexp(float t) {
     p = __fmaf_rn(p, r, 0.5f);
     p = __fmaf_rn(p, r, 1.0f);
     p = __fmaf_rn(p, r, 1.0f);
-    const int ni = static_cast<int>(n);                                   // step 6
-    const uint32_t sbits = (ni >= -126) ? (static_cast<uint32_t>(ni + 127) << 23) : 0u;
-    float w = __fmul_rn(p, __uint_as_float(sbits));
-    w = (kill || w < kTiny) ? 0.0f : w;                                   // step 7
+    // step 6: n + 127 = bits(m) - (0x4B400000 - 127)
+    const int e = max(static_cast<int>(__float_as_uint(m)) - (0x4B400000 - 127), 0);
+    float w = __fmul_rn(p, __uint_as_float(static_cast<uint32_t>(e) << 23));
+    w = (w < kTiny) ? 0.0f : w;  // step 7
     return fminf(w, 1.0f);
 }
 
 // NS-4 for two weights at once with the Blackwell packed FP32 instructions (FFMA2 / FMUL2 /
 // FADD2: fma.rn / mul.rn / add.rn .f32x2, each lane an IEEE round-to-nearest operation), so the
-// result is bit-identical to two dexp() calls while the polynomial issues half the
-// instructions.  Same steps as dexp(); the selects stay per lane.
+// result is bit-identical to two dexp() calls while the arithmetic issues half the
+// instructions.  Same steps as dexp(); the clamps and selects stay per lane.
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
     uint64_t r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -116,16 +124,16 @@ __device__ __forceinline__ void weight2(float l0, float l1, float lmax, float& w
     const float kTiny = __uint_as_float(0x00800000u);  // 2^-126
     float t0, t1;
     f2_unpack(f2_add(f2_pack(l0, l1), f2_pack(-lmax, -lmax)), t0, t1);  // fl(logw - lmax): exact negation
-    const bool k0 = !(t0 >= -88.0f), k1 = !(t1 >= -88.0f);              // step 1 (also -inf)
-    float a0 = k0 ? 0.0f : t0, a1 = k1 ? 0.0f : t1;
-    a0 = (fabsf(a0) < kTiny) ? 0.0f : a0;                               // step 2
-    a1 = (fabsf(a1) < kTiny) ? 0.0f : a1;
-    const uint64_t tt = f2_pack(a0, a1);
-    float n0, n1;
-    f2_unpack(f2_mul(tt, f2_splat(0x3FB8AA3Bu)), n0, n1);                // step 3
-    n0 = rintf(n0);
-    n1 = rintf(n1);
-    const uint64_t n = f2_pack(n0, n1);
+    const uint64_t tt = f2_pack(fmaxf(t0, -100.0f), fmaxf(t1, -100.0f));  // step 1
+    // step 3: m = fl(fl(t log2e) + 1.5 2^23), n = m - 1.5 2^23 (exact).  Per lane: ptxas
+    // contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2 (a single rounding,
+    // which changes the rint of half-way products; tools/dexp_check.cu caught it)
+    float s0, s1;
+    f2_unpack(tt, s0, s1);
+    const float m0 = __fadd_rn(__fmul_rn(s0, __uint_as_float(0x3FB8AA3Bu)), kRintMagic);
+    const float m1 = __fadd_rn(__fmul_rn(s1, __uint_as_float(0x3FB8AA3Bu)), kRintMagic);
+    const uint64_t m = f2_pack(m0, m1);
+    const uint64_t n = f2_add(m, f2_splat(0xCB400000u));
     // step 4: fma(-n, c, t) == fma(n, -c, t) exactly (negation is exact)
     uint64_t r = f2_fma(n, f2_splat(0x3F317200u ^ 0x80000000u), tt);
     r = f2_fma(n, f2_splat(0x35BFBE8Eu ^ 0x80000000u), r);
@@ -137,13 +145,15 @@ __device__ __forceinline__ void weight2(float l0, float l1, float lmax, float& w
     p = f2_fma(p, r, f2_splat(0x3F000000u));                             // 0.5
     p = f2_fma(p, r, f2_splat(0x3F800000u));                             // 1
     p = f2_fma(p, r, f2_splat(0x3F800000u));                             // 1
-    const int i0 = static_cast<int>(n0), i1 = static_cast<int>(n1);      // step 6
-    const uint32_t s0 = (i0 >= -126) ? (static_cast<uint32_t>(i0 + 127) << 23) : 0u;
-    const uint32_t s1 = (i1 >= -126) ? (static_cast<uint32_t>(i1 + 127) << 23) : 0u;
+    // step 6: the scale bits max(n + 127, 0) << 23 from the bit patterns of m
+    const int e0 = max(static_cast<int>(static_cast<uint32_t>(m)) - (0x4B400000 - 127), 0);
+    const int e1 = max(static_cast<int>(static_cast<uint32_t>(m >> 32)) - (0x4B400000 - 127), 0);
     float x0, x1;
-    f2_unpack(f2_mul(p, (static_cast<uint64_t>(s1) << 32) | s0), x0, x1);
-    x0 = (k0 || x0 < kTiny) ? 0.0f : x0;                                 // step 7
-    x1 = (k1 || x1 < kTiny) ? 0.0f : x1;
+    f2_unpack(f2_mul(p, (static_cast<uint64_t>(static_cast<uint32_t>(e1) << 23) << 32) |
+                            (static_cast<uint32_t>(e0) << 23)),
+              x0, x1);
+    x0 = (x0 < kTiny) ? 0.0f : x0;  // step 7
+    x1 = (x1 < kTiny) ? 0.0f : x1;
     w0 = fminf(x0, 1.0f);
     w1 = fminf(x1, 1.0f);
 }
