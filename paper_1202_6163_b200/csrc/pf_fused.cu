@@ -288,6 +288,9 @@ constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner),
                     // the end of phase C, or before the in-line copies of other schemes -- floods
                     // L2 and the memory system: 1.58 ms, stratified step 2.0 -> 2.4 ms)
 #endif
+#ifndef PF_COOP_RESIDENT
+#define PF_COOP_RESIDENT 1  // cooperative kernel: one sub-tile per CTA keeps its values in registers
+#endif
 #ifndef PF_FFMA2
 #define PF_FFMA2 1  // phase B's dexp on packed f32x2 (FFMA2 / FMUL2)
 #endif
@@ -1443,6 +1446,11 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         // ---------------- A: chunk max
         float m = -INFINITY;
         int bad = 0;
+        // resident (a CTA's chunk is one sub-tile): the values stay in registers from A to C,
+        // and phase C reuses phase B's weights (one load and one dexp per particle, not three / two)
+        // (8 particles per thread only: with 16 the live values cost registers on every path)
+        const bool resident = PF_COOP_RESIDENT && kFI == 8 && a.CH <= kPP;
+        float rv[kFI];
         for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
@@ -1459,6 +1467,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 for (int q = 0; q < 4; ++q) {
                     bad |= (isnan(v4[q]) || v4[q] == INFINITY) ? 1 : 0;
                     m = fmaxf(m, v4[q]);
+                    if (kFI == 8) rv[j * 4 + q] = v4[q];
                 }
             }
         }
@@ -1511,7 +1520,10 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             for (int j = 0; j < kFR; ++j) {
                 const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
                 float v4[4];
-                if (a.vec && i0 + 3 < c1) {
+                if (resident) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v4[q] = rv[j * 4 + q];
+                } else if (a.vec && i0 + 3 < c1) {
                     const float4 t = __ldg(reinterpret_cast<const float4*>(frow + i0));
                     v4[0] = t.x; v4[1] = t.y; v4[2] = t.z; v4[3] = t.w;
                 } else {
@@ -1525,6 +1537,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float w = PF_FFMA2 ? v4[q] : weight(v4[q], lm);
+                    if (kFI == 8) rv[j * 4 + q] = w;
                     tot += quantise(w, a.kfx);
                     if (SUMS) {
                         sw += static_cast<double>(w);
@@ -1592,7 +1605,10 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
                 const int64_t i0 = t0 + j * (kFT * 4) + tid * 4;
-                if (a.vec && i0 + 3 < c1) {
+                if (resident) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[j * 4 + q] = rv[j * 4 + q];  // phase B's weights
+                } else if (a.vec && i0 + 3 < c1) {
                     const float4 t = __ldg(reinterpret_cast<const float4*>(frow + i0));
                     v[j * 4 + 0] = t.x; v[j * 4 + 1] = t.y; v[j * 4 + 2] = t.z; v[j * 4 + 3] = t.w;
                 } else {
@@ -1604,13 +1620,13 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
                 uint64_t loc = 0;
-                if (PF_FFMA2) {
+                if (PF_FFMA2 && !resident) {
                     weight2(v[j * 4 + 0], v[j * 4 + 1], lm, v[j * 4 + 0], v[j * 4 + 1]);
                     weight2(v[j * 4 + 2], v[j * 4 + 3], lm, v[j * 4 + 2], v[j * 4 + 3]);
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float w = PF_FFMA2 ? v[j * 4 + q] : weight(v[j * 4 + q], lm);
+                    const float w = (PF_FFMA2 || resident) ? v[j * 4 + q] : weight(v[j * 4 + q], lm);
                     v[j * 4 + q] = w;
                     loc += quantise(w, a.kfx);
                 }
