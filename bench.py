@@ -664,10 +664,10 @@ def run_ours(args):
 
         h_logw = logw.cpu().pin_memory()
         h_out = torch.empty((N, P), dtype=torch.int32).pin_memory()
-        pipe = HostPipeline(N, P, dev, chunks=16)
+        pipe = HostPipeline(N, P, dev, chunks=8)
 
         def e2e_step():
-            pipe.run(scheme, h_logw, seed, h_out, B=B, first_filter=first, state=X, stream=stream)
+            pipe.run(scheme, h_logw, seed, h_out, B=B, first_filter=first, state=X, stream=stream, chain=True)
 
         for _ in range(2):
             e2e_step()
@@ -687,8 +687,13 @@ def run_ours(args):
         e2e = {"value": N * P * world * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": N * P * 4, "d2h_bytes_per_step": N * P * 4,
                "note": "host logw (pinned) -> H2D -> resample/permute/gather -> D2H permuted ancestors, "
-                       "16 chunks of filters overlapped on three streams (paper_1202_6163_b200.pipeline); "
-                       "state X stays resident"}
+                       "8 chunks of filters overlapped on three streams, consecutive steps chained "
+                       "(paper_1202_6163_b200.pipeline, chain=True); state X stays resident"}
+        # the link's own ceiling: both copy directions at once, same bytes, same pinned buffers
+        link = link_rates(dev, h_logw, h_out, pipe.d_logw, pipe.perm)
+        e2e["link"] = link
+        e2e["frac_of_link"] = round(e2e["value"] / (N * P * world / (max(
+            N * P * 4 / (link["both_h2d_gbs"] * 1e9), N * P * 4 / (link["both_d2h_gbs"] * 1e9)))), 3)
     clocks = sampler.stop()
 
     cpu = None
@@ -724,6 +729,47 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------------------------- CPU oracle legs
+def link_rates(dev, h_in, h_out, d_in, d_out, reps: int = 5):
+    """Host<->device copy rates over the e2e step's own pinned buffers (GB/s): H2D alone,
+    D2H alone, and each direction while both run at once (two streams)."""
+    import torch
+
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    out = {}
+    for name, h2d, d2h in (("h2d", True, False), ("d2h", False, True), ("both", True, True)):
+        cur = torch.cuda.current_stream(dev)
+        ev = {}
+        for tag, s in (("h2d", s1), ("d2h", s2)):
+            ev[tag] = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        torch.cuda.synchronize(dev)
+        for s in (s1, s2):
+            s.wait_stream(cur)
+        for it in range(reps + 1):
+            if it == 1:
+                if h2d:
+                    ev["h2d"][0].record(s1)
+                if d2h:
+                    ev["d2h"][0].record(s2)
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_in.copy_(h_in, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_out.copy_(d_out, non_blocking=True)
+        if h2d:
+            ev["h2d"][1].record(s1)
+        if d2h:
+            ev["d2h"][1].record(s2)
+        torch.cuda.synchronize(dev)
+        for tag, on in (("h2d", h2d), ("d2h", d2h)):
+            if on:
+                ms = ev[tag][0].elapsed_time(ev[tag][1]) / reps
+                key = f"{tag}_gbs" if name != "both" else f"both_{tag}_gbs"
+                nbytes = h_in.numel() * h_in.element_size() if tag == "h2d" else d_out.numel() * d_out.element_size()
+                out[key] = round(nbytes / (ms / 1e3) / 1e9, 2)
+    return out
+
+
 def _oracle_pass(scheme, logw_np, X_np, seed, first, B, threads):
     """Oracle pipeline (resample -> permute -> in-place gather) over the given filters, one filter
     per task on `threads` host threads (ctypes releases the GIL; each call is single-threaded C)."""

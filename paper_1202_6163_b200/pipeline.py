@@ -4,8 +4,11 @@ Filters are independent (the Philox counter carries the global filter index, NS-
 batch split into chunks of filters gives the same results as one call.  Each chunk's
 host->device copy, its `pf_resample_batched` call and the device->host copy of its
 permutation run on three CUDA streams ordered by events, so chunk k+1's input copy and chunk
-k-1's output copy overlap chunk k's kernel (each copy direction has its own engine).  Plumbing
-only: every step of the method runs in libpfresample.
+k-1's output copy overlap chunk k's kernel (each copy direction has its own engine).  With
+``chain=True`` consecutive calls also overlap each other: a call's input copies wait only for the
+previous call's kernel on the same chunk (the device buffer they overwrite), not for the caller's
+stream, so the next batch streams in while the previous one streams out and both PCIe
+directions stay busy.  Plumbing only: every step of the method runs in libpfresample.
 """
 from __future__ import annotations
 
@@ -36,10 +39,17 @@ class HostPipeline:
         self.s_in = torch.cuda.Stream(self.dev)
         self.s_run = torch.cuda.Stream(self.dev)
         self.s_out = torch.cuda.Stream(self.dev)
+        self._consumed = [None] * self.chunks  # per chunk: the last call's kernel (reads d_logw)
 
     def run(self, scheme, h_logw, seed: int, h_out, B: int = 0, first_filter: int = 0, state=None,
-            output: str = "permutation", stream=None):
-        """Enqueue the whole batch; the caller's stream (default: current) waits for the last copy."""
+            output: str = "permutation", stream=None, chain: bool = False):
+        """Enqueue the whole batch; the caller's stream (default: current) waits for the last copy.
+
+        The kernels and the output copies follow everything already enqueued on the caller's
+        stream (e.g. a propagate step writing ``state``).  The input copies do too, unless
+        ``chain``: then h_logw must be complete on the host when run() is called (not produced by
+        work pending on the caller's stream), and each chunk's input copy waits only for the
+        previous call's kernel on that chunk."""
         import torch
 
         if not (h_logw.is_pinned() and h_out.is_pinned()):
@@ -51,13 +61,15 @@ class HostPipeline:
         # the streams start after everything already enqueued on the caller's stream
         start = torch.cuda.Event()
         start.record(caller)
-        for s in (self.s_in, self.s_run, self.s_out):
+        for s in ((self.s_run, self.s_out) if chain else (self.s_in, self.s_run, self.s_out)):
             s.wait_event(start)
         done = None
-        for a, b in self.bounds:
+        for c, (a, b) in enumerate(self.bounds):
             e_in = torch.cuda.Event()
             e_run = torch.cuda.Event()
             with torch.cuda.stream(self.s_in):
+                if chain and self._consumed[c] is not None:
+                    self.s_in.wait_event(self._consumed[c])
                 self.d_logw[a:b].copy_(h_logw[a:b], non_blocking=True)
                 e_in.record(self.s_in)
             self.s_run.wait_event(e_in)
@@ -66,6 +78,7 @@ class HostPipeline:
                                 ancestors=self.anc[a:b], offspring_out=self.off[a:b],
                                 permuted_out=self.perm[a:b], state=X, stream=self.s_run)
             e_run.record(self.s_run)
+            self._consumed[c] = e_run
             self.s_out.wait_event(e_run)
             with torch.cuda.stream(self.s_out):
                 h_out[a:b].copy_(src[a:b], non_blocking=True)

@@ -366,6 +366,18 @@ def test_host_pipeline_matches_direct_call(pf, dev, orc):
             torch.cuda.synchronize()
             assert torch.equal(h_out, ref_perm.cpu()), (scheme, chunks)
             assert torch.equal(Xp, Xd), (scheme, chunks)
+            # chained calls (the next batch's input copies overlap this one's output copies):
+            # two different batches back to back, each equal to its own direct call
+            h2 = torch.from_numpy(pfinputs.gaussian_logw(P, 10.0, seed=22, N=N)).pin_memory()
+            ref2 = torch.empty((N, P), dtype=torch.int32, device=dev)
+            pf.pf_resample_batched(scheme, h2.to(dev), 78, first_filter=5, permuted_out=ref2)
+            o1 = torch.empty((N, P), dtype=torch.int32).pin_memory()
+            o2 = torch.empty((N, P), dtype=torch.int32).pin_memory()
+            for _ in range(2):
+                pipe.run(scheme, h_logw, 77, o1, first_filter=5, chain=True)
+                pipe.run(scheme, h2, 78, o2, first_filter=5, chain=True)
+            torch.cuda.synchronize()
+            assert torch.equal(o1, ref_perm.cpu()) and torch.equal(o2, ref2.cpu()), (scheme, chunks)
         for n in (0, 36):
             _, want = orc.resample(scheme, x[n], 77, filter_index=5 + n)
             assert np.array_equal(ref_perm[n].cpu().numpy(), orc.permute(want))
