@@ -47,8 +47,6 @@ def main():
             for name, kw in (("anc", {}), ("off", {"offspring_out": off}),
                              ("perm", {"offspring_out": off, "permuted_out": pm}),
                              ("step", {"offspring_out": off, "permuted_out": pm, "state": X})):
-                if scheme == "multinomial" and name != "anc":
-                    continue
                 ms = time_calls(lambda: pf.pf_resample_batched(scheme, x, 5, ancestors=anc, **kw), 5, dev)
                 print(json.dumps({"c3": scheme, "var": var, "outputs": name, "ms": round(ms, 4),
                                   "particles_per_s": N * P / (ms / 1e3)}))
