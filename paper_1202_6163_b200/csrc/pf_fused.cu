@@ -341,6 +341,12 @@ __host__ __device__ constexpr bool fused_max_ahead() {
     return FT <= 512 && !F64;
 }
 
+// IEEE max that propagates NaN (max.NaN.f32): the max of a set is NaN iff a member is
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -465,11 +471,9 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 for (int q = 0; q < 4; ++q) x[q] = (i0 + q < np) ? s_lw[i0 + q] : -INFINITY;
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                bad |= !(x[q] <= FLT_MAX);  // NaN or +inf
-                m = fmaxf(m, x[q]);
-            }
+            for (int q = 0; q < 4; ++q) m = fmax_nan(m, x[q]);  // a NaN anywhere stays NaN
         }
+        bad = !(m <= FLT_MAX);  // NaN or +inf among the values (one test, not one per value)
         int b = bad ? 1 : 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
