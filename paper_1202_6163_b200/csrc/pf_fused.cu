@@ -291,6 +291,9 @@ constexpr int kRQ = 256;  // ring entries per warp: packed (slot << 16 | owner),
 #ifndef PF_COOP_RESIDENT
 #define PF_COOP_RESIDENT 1  // cooperative kernel: one sub-tile per CTA keeps its values in registers
 #endif
+#ifndef PF_ROWSCAN
+#define PF_ROWSCAN 1  // the four row scans of phases B and D as one transposed warp scan
+#endif
 #ifndef PF_FFMA2
 #define PF_FFMA2 1  // phase B's dexp on packed f32x2 (FFMA2 / FMUL2)
 #endif
@@ -339,6 +342,50 @@ __device__ __forceinline__ void copy_rows_warp(const Args& a, int n, const int32
 template <int FT, bool F64>
 __host__ __device__ constexpr bool fused_max_ahead() {
     return FT <= 512 && !F64;
+}
+
+// Exclusive prefix sums across the warp's lanes of R rows at once (R = 2 or 4): ex[j] = sum
+// over lanes l' < lane of loc[j] (what R warp_incl_scan_u64 calls give), through the warp's
+// R x 256 B of shared memory buf (16-byte aligned, warp-private): lane l sums the R-lane
+// segment l % (32 / R) of row l / (32 / R) serially, a (32 / R)-lane shuffle scan runs over the
+// segments, and the prefixes go back through buf.  One 3- (4-) step 64-bit shuffle scan
+// instead of four (two) 5-step ones.  *rowtot: the total of row l / (32 / R), valid on the last
+// lane of each row's group.
+template <int R>
+__device__ __forceinline__ void warp_rows_excl_scan(const uint64_t* loc, uint64_t* ex, uint64_t* buf, int lane,
+                                                    uint64_t* rowtot) {
+    static_assert(R == 2 || R == 4, "two or four rows");
+    constexpr int kSeg = 32 / R;  // segments per row = lanes per row group
+#pragma unroll
+    for (int j = 0; j < R; ++j) buf[j * 32 + lane] = loc[j];
+    __syncwarp();
+    const int seg = lane % kSeg;
+    ulonglong2* p = reinterpret_cast<ulonglong2*>(buf + (lane / kSeg) * 32 + seg * R);
+    uint64_t e[R];  // inclusive partial sums of the segment
+    const ulonglong2 a = p[0];
+    e[0] = a.x;
+    e[1] = a.x + a.y;
+    if (R == 4) {
+        const ulonglong2 b = p[1];
+        e[2 % R] = e[1] + b.x;
+        e[3 % R] = e[2 % R] + b.y;
+    }
+    const uint64_t T = e[R - 1];
+    uint64_t inc = T;
+#pragma unroll
+    for (int o = 1; o < kSeg; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o, kSeg);
+        if (seg >= o) inc += t;
+    }
+    *rowtot = inc;
+    const uint64_t base = inc - T;
+    __syncwarp();
+    p[0] = make_ulonglong2(base, base + e[0]);
+    if (R == 4) p[1] = make_ulonglong2(base + e[1], base + e[2 % R]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < R; ++j) ex[j] = buf[j * 32 + lane];
+    __syncwarp();
 }
 
 // IEEE max that propagates NaN (max.NaN.f32): the max of a set is NaN iff a member is
@@ -391,6 +438,10 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
     constexpr bool MD = fused_max_ahead<FT, F64>();             // phase D with 16-bit lists, one barrier
     constexpr int kCU = copy_cu<FT>();
     static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
+    static_assert((kFR == 2 || kFR == 4) && kChunk * 4 >= kFR * 32 * 8, "warp_rows_excl_scan: rows of s_buf per warp");
+    // phase D's packed scan transposed too, except in the gather-from-offspring form (measured
+    // 0.02 ms slower at the C3 multinomial step: its registers spill more)
+    constexpr bool RS_D = PF_ROWSCAN && !(SCHEME == kFromOffspring && PERM == 2);
     extern __shared__ __align__(16) int32_t s_dyn[];
     float* s_lw = reinterpret_cast<float*>(s_dyn);  // MA: this CTA's slice of the next filter's log-weights
     // PERM: this CTA's free-slot list (kPP entries; 16-bit slots in the max-ahead mode, P <= 65536;
@@ -798,6 +849,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
         // ---------------- B: weights, quantise, block scan, cluster offsets
         double sw = 0.0, sw2 = 0.0;
         uint64_t ex[kFR];
+        uint64_t locs[kFR];
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
             uint64_t loc = 0;
@@ -816,11 +868,20 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 }
                 loc += quantise(w, a.kfx);
             }
-            const uint64_t incl = warp_incl_scan_u64(loc, lane);
-            ex[j] = incl - loc;
-            const uint64_t wt = __shfl_sync(kFull, incl, 31);
-            if (lane == 0) s_wt[j][warp] = wt;
+            if (PF_ROWSCAN) {
+                locs[j] = loc;
+            } else {
+                const uint64_t incl = warp_incl_scan_u64(loc, lane);
+                ex[j] = incl - loc;
+                const uint64_t wt = __shfl_sync(kFull, incl, 31);
+                if (lane == 0) s_wt[j][warp] = wt;
+            }
             if (PF_TICK_B) tick();
+        }
+        if (PF_ROWSCAN) {
+            uint64_t rt;
+            warp_rows_excl_scan<kFR>(locs, ex, reinterpret_cast<uint64_t*>(&s_buf[warp][0]), lane, &rt);
+            if (lane % (32 / kFR) == 32 / kFR - 1) s_wt[lane / (32 / kFR)][warp] = rt;
         }
         if (SUMS) {
             sw = warp_sum_f64(sw);
@@ -1060,6 +1121,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 rq_n = n;
             }
             __syncthreads();  // s_wt is reused
+            uint64_t plocs[kFR];
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
                 uint64_t loc = 0;
@@ -1069,10 +1131,19 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                     const bool real = (j * (kFT * 4) + tid * 4 + q) < np;
                     loc += (static_cast<uint64_t>(o > 1 ? o - 1 : 0) << 31) | ((o == 0 && real) ? 1ull : 0ull);
                 }
-                const uint64_t incl = warp_incl_scan_u64(loc, lane);
-                pex[j] = incl - loc;
-                const uint64_t wt = __shfl_sync(kFull, incl, 31);
-                if (lane == 0) s_wt[j][warp] = wt;
+                if (RS_D) {
+                    plocs[j] = loc;
+                } else {
+                    const uint64_t incl = warp_incl_scan_u64(loc, lane);
+                    pex[j] = incl - loc;
+                    const uint64_t wt = __shfl_sync(kFull, incl, 31);
+                    if (lane == 0) s_wt[j][warp] = wt;
+                }
+            }
+            if (RS_D) {
+                uint64_t rt;
+                warp_rows_excl_scan<kFR>(plocs, pex, reinterpret_cast<uint64_t*>(&s_buf[warp][0]), lane, &rt);
+                if (lane % (32 / kFR) == 32 / kFR - 1) s_wt[lane / (32 / kFR)][warp] = rt;
             }
             __syncthreads();
             if (warp == 0) {
@@ -1422,6 +1493,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
     constexpr int kPP = kFT * FI;
     constexpr int kTPL = kFR * kFW / 32;
     static_assert(kFR * kFW % 32 == 0, "phase-B totals scan assumes a multiple of 32 (row, warp) totals");
+    static_assert((kFR == 2 || kFR == 4) && kChunk * 4 >= kFR * 32 * 8, "warp_rows_excl_scan: rows of s_buf per warp");
     __shared__ float s_f[kFW];
     __shared__ int s_i[kFW];
     __shared__ double s_d[2][kFW];
@@ -1621,6 +1693,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 }
             }
             uint64_t ex[kFR];
+            uint64_t locs[kFR];
 #pragma unroll
             for (int j = 0; j < kFR; ++j) {
                 uint64_t loc = 0;
@@ -1634,10 +1707,21 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     v[j * 4 + q] = w;
                     loc += quantise(w, a.kfx);
                 }
-                const uint64_t incl = warp_incl_scan_u64(loc, lane);
-                ex[j] = incl - loc;
-                const uint64_t wt = __shfl_sync(kFull, incl, 31);
-                if (lane == 0) s_wt[j][warp] = wt;
+                if (PF_ROWSCAN) {
+                    locs[j] = loc;
+                } else {
+                    const uint64_t incl = warp_incl_scan_u64(loc, lane);
+                    ex[j] = incl - loc;
+                    const uint64_t wt = __shfl_sync(kFull, incl, 31);
+                    if (lane == 0) s_wt[j][warp] = wt;
+                }
+            }
+            if (PF_ROWSCAN) {
+                // s_buf's last readers (the previous sub-tile's expansion) passed the barrier
+                // inside its final max-scan
+                uint64_t rt;
+                warp_rows_excl_scan<kFR>(locs, ex, reinterpret_cast<uint64_t*>(&s_buf[warp][0]), lane, &rt);
+                if (lane % (32 / kFR) == 32 / kFR - 1) s_wt[lane / (32 / kFR)][warp] = rt;
             }
             __syncthreads();
             if (warp == 0) {
