@@ -116,6 +116,7 @@ struct Pos {
     uint32_t filt;
     int64_t P;
     double A, Bc;  // k* = v * A - Bc
+    double C;      // A 2^kfx: k* advances by about w C per particle of weight w (PF_KF_RUN)
 };
 
 template <int SCHEME>
@@ -184,19 +185,42 @@ __device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_
     return (n < 0) ? 0u : (n >= P ? static_cast<uint32_t>(P) : static_cast<uint32_t>(n) + below);
 }
 
+#ifndef PF_KF_RUN
+#define PF_KF_RUN 1  // systematic slot counts: k* estimate advanced by w C (count_row<3, true>)
+#endif
 // E for the 4 particles of a row: running sum from run0, fast paths with an exact redo of the
 // (rare) rows holding a near-integer k*
-template <int SCHEME>
+template <int SCHEME, bool KFR = false>
 __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const float* w4, int kfx, uint32_t* E4) {
     if (SCHEME == 3) {
         bool any_slow = false;
         uint64_t run = run0;
+        if (KFR && z.A < 0x1p-16) {
+            // the estimate of k* from the row's exact start, advanced by w C per particle
+            // instead of quantising each weight and converting each Q_i: it differs from the
+            // per-particle estimate by the quantiser's truncations (< 1 unit of q each, i.e.
+            // < A in k*; A = 2^64 / (D Q) <= S 2^-kfx, at most 2^-23 for S <= 2^18, and the
+            // filter-uniform test A < 2^-16 keeps four of them below 2^-14 at any P) and by
+            // roundings (<= 2^-20 for k* < 2^31): inside the 2^-12 margin that sends
+            // near-integer k* to the exact recount below
+            double kf = fma(static_cast<double>(run0), z.A, -z.Bc);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            run += quantise(w4[q], kfx);
-            bool sl;
-            E4[q] = count_below_sys_fast(z, run, &sl);
-            any_slow |= sl;
+            for (int q = 0; q < 4; ++q) {
+                kf = fma(static_cast<double>(w4[q]), z.C, kf);
+                const double fl = floor(kf);
+                const double fr = kf - fl;
+                any_slow |= !(fr > 0x1p-12 && fr < 1.0 - 0x1p-12);
+                const int n1 = static_cast<int>(fl) + 1;
+                E4[q] = static_cast<uint32_t>(min(max(n1, 0), static_cast<int>(z.P)));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                run += quantise(w4[q], kfx);
+                bool sl;
+                E4[q] = count_below_sys_fast(z, run, &sl);
+                any_slow |= sl;
+            }
         }
         if (any_slow) {
             run = run0;
@@ -975,6 +999,7 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
         z.P = (SCHEME == kBuckets) ? a.S : a.P;  // slots: the P resampled particles, or the NB buckets
         z.rho = s_rho;
         z.A = s_zA;
+        z.C = ldexp(s_zA, a.kfx);
         z.Bc = s_zBc;
         if (c == 0 && tid == 0) {
             if (a.lse_out) a.lse_out[n] = (F64 ? s_lmax64 : static_cast<double>(lm)) + log(s_S);
@@ -1002,7 +1027,11 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
         // ---------------- C: E_i = c(Q_i), heads, max-scan
 #pragma unroll
         for (int j = 0; j < kFR; ++j) {
-            count_row<(SCHEME == kBuckets ? 3 : SCHEME)>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
+            // the w C estimate: measured faster without the permutation in CTAs of <= 512
+            // threads (C3 resample 0.3845 -> 0.381 ms, bucket mode 1.116 -> 1.10 ms) and slower
+            // with it, in 1024-thread CTAs or in the cooperative kernel (more live registers)
+            count_row<(SCHEME == kBuckets ? 3 : SCHEME), PF_KF_RUN && PERM == 0 && FT <= 512>(z, O + s_wt[j][warp] + ex[j], v + j * 4,
+                                                                              a.kfx, E + j * 4);
             if (SCHEME == kBuckets) {
                 // the multinomial's search structure: Q_i of every particle (u64, 2 x 16-byte stores)
                 uint64_t r = O + s_wt[j][warp] + ex[j];
@@ -1672,6 +1701,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         z.P = (SCHEME == kBuckets) ? a.S : a.P;  // slots: the particles, or the NB buckets
         z.rho = s_crho;
         z.A = s_cA;
+        z.C = ldexp(s_cA, a.kfx);
         z.Bc = s_cBc;
         uint64_t carry = s_u64[0];
         if (tid == 0) s_prevE = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, carry);
