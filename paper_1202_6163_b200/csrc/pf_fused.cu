@@ -185,6 +185,9 @@ __device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_
     return (n < 0) ? 0u : (n >= P ? static_cast<uint32_t>(P) : static_cast<uint32_t>(n) + below);
 }
 
+#ifndef PF_EARLY_RHO
+#define PF_EARLY_RHO 1
+#endif
 #ifndef PF_KF_RUN
 #define PF_KF_RUN 1  // systematic slot counts: k* estimate advanced by w C (count_row<3, true>)
 #endif
@@ -462,6 +465,11 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
     constexpr bool MD = fused_max_ahead<FT, F64>();             // phase D with 16-bit lists, one barrier
     constexpr int kCU = copy_cu<FT>();
     static_assert(kXS == 8 * kFT && kFW <= 32 && kFR * kFW % 32 == 0, "fused kernel geometry");
+    // rho and rho / D at the top of each filter by the last warp (PF_EARLY_RHO), except in the
+    // ancestors-only 256-thread form, where the 8 warps cannot hide that warp's extra latency
+    // (measured: step 1.312 -> 1.281 ms, permutation 0.701 -> 0.688 ms, ancestors-only
+    // 0.382 -> 0.391 ms, which therefore keeps them after the exchange)
+    constexpr bool kEarlyRho = PF_EARLY_RHO && !(FT == 256 && PERM == 0);
     static_assert((kFR == 2 || kFR == 4) && kChunk * 4 >= kFR * 32 * 8, "warp_rows_excl_scan: rows of s_buf per warp");
     // phase D's packed scan transposed too, except in the gather-from-offspring form (measured
     // 0.02 ms slower at the C3 multinomial step: its registers spill more)
@@ -679,6 +687,16 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
         } else {
         const float* row = a.logw + static_cast<int64_t>(n) * a.ld + p0;
         const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+        if (kEarlyRho && warp == kFW - 1 && lane == 0) {
+            // the filter's weight-free position constants rho and rho / D (a Philox call and a
+            // double division), by one thread of the last warp while the filter starts: read
+            // after the scan exchange's barriers, so off the path that every warp waits on there
+            // (computed after the exchange by warp 0 they were 14% of the stall samples)
+            const uint64_t rho =
+                (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+            s_rho = rho;
+            s_zBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+        }
         const bool has_next = n + num_clusters < a.N;
 
         // ---------------- A: load + max
@@ -978,14 +996,22 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
                 s_Qtot = tot;
                 s_S = Sr;
                 s_S2 = S2r;
-                // the filter's position constants, once per CTA (not per thread: a Philox call
-                // and two double divisions on the FP64 pipe by 512 threads)
-                const uint64_t rho =
-                    (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
-                s_rho = rho;
-                // A = 2^64 / (D Q), Bc = rho / D  (the double estimate of k*)
-                s_zA = 0x1p64 / (static_cast<double>(a.D) * static_cast<double>(tot));
-                s_zBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+                if (!kEarlyRho) {
+                    const uint64_t rho = (SCHEME == 3)
+                                             ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D)
+                                             : 0ull;
+                    s_rho = rho;
+                    s_zBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+                }
+                // A = 2^64 / (D Q) (the double estimate k* = v A - rho / D): a float reciprocal
+                // refined by two Newton steps (relative error ~2^-52) instead of a double
+                // division on the path every warp waits on; A only steers the estimate, whose
+                // near-integer cases the exact recount decides
+                const double den = static_cast<double>(a.D) * static_cast<double>(tot);
+                double r = static_cast<double>(__frcp_rn(static_cast<float>(den)));
+                r = fma(r, fma(-den, r, 1.0), r);
+                r = fma(r, fma(-den, r, 1.0), r);
+                s_zA = 0x1p64 * r;
             }
             if (MA && has_next) lw_cluster_reduce(xb);  // the next filter's lmax / flag
         }

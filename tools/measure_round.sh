@@ -12,3 +12,5 @@ ncu -i /tmp/ro_sys.ncu-rep --page raw --csv > gpurun_out/m/ro_raw.csv 2>/dev/nul
 ncu -i /tmp/step_sys.ncu-rep --page raw --csv > gpurun_out/m/step_raw.csv 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m/launches.csv python bench.py --steps 2 --warmup 1 --no-extras > gpurun_out/m/ncu_launch.log 2>&1
 ls -la gpurun_out/m
+python tools/sass_lines.py /tmp/ro_sys.ncu-rep k_fused_sorted k_fused_sortedILi3ELb0ELi0ELi256 --outer --top 60 > gpurun_out/m/ro_sys_outer.txt 2>&1
+python tools/sass_lines.py /tmp/ro_sys.ncu-rep k_fused_sorted k_fused_sortedILi3ELb0ELi0ELi256 --top 60 > gpurun_out/m/ro_sys_lines.txt 2>&1
