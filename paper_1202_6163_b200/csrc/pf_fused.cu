@@ -1574,6 +1574,14 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         const int64_t c0 = static_cast<int64_t>(c) * a.CH;
         const int64_t c1 = min(static_cast<int64_t>(a.P), c0 + a.CH);
         const uint32_t filt = a.filt0 + static_cast<uint32_t>(n);
+        if (PF_EARLY_RHO && warp == kFW - 1 && lane == 0) {
+            // rho and rho / D (weight-free) while phase A loads, not after the scan's grid barrier
+            // where every warp waits for them (as in k_fused_sorted); read after that barrier
+            const uint64_t rho =
+                (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
+            s_crho = rho;
+            s_cBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+        }
         // ---------------- A: chunk max
         float m = -INFINITY;
         int bad = 0;
@@ -1596,12 +1604,12 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    bad |= (isnan(v4[q]) || v4[q] == INFINITY) ? 1 : 0;
-                    m = fmaxf(m, v4[q]);
+                    m = fmax_nan(m, v4[q]);  // a NaN anywhere stays NaN
                     if (kFI == 8) rv[j * 4 + q] = v4[q];
                 }
             }
         }
+        bad = !(m <= FLT_MAX) ? 1 : 0;  // NaN or +inf among this thread's values
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
@@ -1703,11 +1711,18 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                 s_u64[0] = off;
                 s_u64[1] = all;
                 // the filter's position constants, once per CTA (as in k_fused_sorted)
-                const uint64_t rho =
-                    (SCHEME == 3) ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D) : 0ull;
-                s_crho = rho;
-                s_cA = 0x1p64 / (static_cast<double>(a.D) * static_cast<double>(all));
-                s_cBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+                if (!PF_EARLY_RHO) {
+                    const uint64_t rho = (SCHEME == 3)
+                                             ? mulhi64(lo_word(philox10(0u, 0u, 3u, filt, a.key.k0, a.key.k1)), a.D)
+                                             : 0ull;
+                    s_crho = rho;
+                    s_cBc = (SCHEME == 3) ? static_cast<double>(rho) / static_cast<double>(a.D) : 0.0;
+                }
+                const double den = static_cast<double>(a.D) * static_cast<double>(all);
+                double r = static_cast<double>(__frcp_rn(static_cast<float>(den)));
+                r = fma(r, fma(-den, r, 1.0), r);
+                r = fma(r, fma(-den, r, 1.0), r);
+                s_cA = 0x1p64 * r;
                 if (SUMS && c == 0) {
                     double S = 0.0, S2 = 0.0;
                     for (int r = 0; r < G; ++r) { S += __ldcg(a.g_sw + r); S2 += __ldcg(a.g_sw2 + r); }
