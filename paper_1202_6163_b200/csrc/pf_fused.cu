@@ -1455,18 +1455,29 @@ __device__ __forceinline__ void coop_load_o(const int32_t* orow, int64_t t0, int
 template <int FI>
 __device__ __forceinline__ void coop_packed_scan(const int32_t* ov, int64_t t0, int64_t c1, int tid, int warp,
                                                  int lane, uint64_t (*s_wt)[kFW], uint64_t* s_u64, uint64_t* pex,
-                                                 uint64_t* total) {
+                                                 uint64_t* total, uint64_t* wbuf) {
+    // wbuf: this warp's 1 KB of free shared memory (the row scans as one transposed scan)
     constexpr int kFR = FI / 4;
     constexpr int kTPL = kFR * kFW / 32;
+    uint64_t locs[kFR];
 #pragma unroll
     for (int j = 0; j < kFR; ++j) {
         uint64_t loc = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) loc += packed_of(ov[j * 4 + q], t0 + j * (kFT * 4) + tid * 4 + q < c1);
-        const uint64_t incl = warp_incl_scan_u64(loc, lane);
-        pex[j] = incl - loc;
-        const uint64_t wt = __shfl_sync(kFull, incl, 31);
-        if (lane == 0) s_wt[j][warp] = wt;
+        if (PF_ROWSCAN) {
+            locs[j] = loc;
+        } else {
+            const uint64_t incl = warp_incl_scan_u64(loc, lane);
+            pex[j] = incl - loc;
+            const uint64_t wt = __shfl_sync(kFull, incl, 31);
+            if (lane == 0) s_wt[j][warp] = wt;
+        }
+    }
+    if (PF_ROWSCAN) {
+        uint64_t rt;
+        warp_rows_excl_scan<kFR>(locs, pex, wbuf, lane, &rt);
+        if (lane % (32 / kFR) == 32 / kFR - 1) s_wt[lane / (32 / kFR)][warp] = rt;
     }
     __syncthreads();
     if (warp == 0) {
@@ -1972,7 +1983,8 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     int32_t ov[kFI];
                     coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
                     uint64_t pex[kFR], stot;
-                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot,
+                                         reinterpret_cast<uint64_t*>(&s_buf[warp][0]));
 #pragma unroll
                     for (int j = 0; j < kFR; ++j) {
                         uint64_t run = run0 + s_wt[j][warp] + pex[j];
@@ -2000,7 +2012,8 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     int32_t ov[kFI];
                     coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
                     uint64_t pex[kFR], stot;
-                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot);
+                    coop_packed_scan<FI>(ov, t0, c1, tid, warp, lane, s_wt, s_u64, pex, &stot,
+                                         reinterpret_cast<uint64_t*>(&s_buf[warp][0]));
                     const uint32_t XS = static_cast<uint32_t>(run0 >> 31);          // first extras rank
                     const uint32_t XT = static_cast<uint32_t>((run0 + stot) >> 31) - XS;
                     const int32_t idbase = static_cast<int32_t>(t0) + tid * 4;
