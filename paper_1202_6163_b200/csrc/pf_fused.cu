@@ -1758,6 +1758,7 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
         uint64_t carry = s_u64[0];
         if (tid == 0) s_prevE = count_below<(SCHEME == kBuckets ? 3 : SCHEME)>(z, carry);
         // ---------------- C: sub-tiles in order
+        uint64_t ploc_c = 0;  // PERM: packed (extras << 31 | free) total of this thread's particles
         for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
             float v[kFI];
 #pragma unroll
@@ -1873,8 +1874,13 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
                     const int32_t o1 = static_cast<int32_t>(E[j * 4 + 1] - E[j * 4 + 0]);
                     const int32_t o2 = static_cast<int32_t>(E[j * 4 + 2] - E[j * 4 + 1]);
                     const int32_t o3 = static_cast<int32_t>(E[j * 4 + 3] - E[j * 4 + 2]);
+                    if (PERM)
+                        ploc_c += packed_of(o0, i0 + 0 < c1) + packed_of(o1, i0 + 1 < c1) + packed_of(o2, i0 + 2 < c1) +
+                                  packed_of(o3, i0 + 3 < c1);
                     if (a.anc_vec && i0 + 3 < c1) {
-                        __stcs(reinterpret_cast<int4*>(orow + i0), make_int4(o0, o1, o2, o3));
+                        // phase D reads them back: keep them in L2 (streaming stores otherwise)
+                        if (PERM) __stcg(reinterpret_cast<int4*>(orow + i0), make_int4(o0, o1, o2, o3));
+                        else __stcs(reinterpret_cast<int4*>(orow + i0), make_int4(o0, o1, o2, o3));
                     } else {
                         if (i0 + 0 < c1) orow[i0 + 0] = o0;
                         if (i0 + 1 < c1) orow[i0 + 1] = o1;
@@ -1952,15 +1958,9 @@ __global__ void __launch_bounds__(kFT, 1024 / kFT) k_coop_sorted(CoopArgs a) {
             __syncthreads();
             const int32_t* orow = a.off + static_cast<int64_t>(n) * a.ld_anc;
             int32_t* prow = a.perm + static_cast<int64_t>(n) * a.ld_anc;
-            // D1: packed (extras << 31 | free) total of the chunk
-            uint64_t ploc = 0;
-            for (int64_t t0 = c0; t0 < c1; t0 += kPP) {
-                int32_t ov[kFI];
-                coop_load_o<FI>(orow, t0, c1, tid, a.anc_vec, ov);
-#pragma unroll
-                for (int t = 0; t < kFI; ++t) ploc += packed_of(ov[t], t0 + (t >> 2) * (kFT * 4) + tid * 4 + (t & 3) < c1);
-            }
-            ploc = warp_sum_u64(ploc);
+            // D1: packed (extras << 31 | free) total of the chunk (each thread's part summed in
+            // phase C from the offspring in registers)
+            uint64_t ploc = warp_sum_u64(ploc_c);
             if (lane == 0) s_wt[0][warp] = ploc;
             __syncthreads();
             if (tid == 0) {
