@@ -14,3 +14,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 ls -la gpurun_out/m
 python tools/sass_lines.py /tmp/ro_sys.ncu-rep k_fused_sorted k_fused_sortedILi3ELb0ELi0ELi256 --outer --top 60 > gpurun_out/m/ro_sys_outer.txt 2>&1
 python tools/sass_lines.py /tmp/ro_sys.ncu-rep k_fused_sorted k_fused_sortedILi3ELb0ELi0ELi256 --top 60 > gpurun_out/m/ro_sys_lines.txt 2>&1
+python tools/sass_lines.py /tmp/step_sys.ncu-rep k_fused_sorted k_fused_sortedILi3ELb0ELi2ELi512ELi16ELb0 --outer --top 60 > gpurun_out/m/step_outer.txt 2>&1
