@@ -110,6 +110,9 @@ struct FusedArgs {
     int xlg;        // log2 of the 16-byte chunks per row (row bytes = 16 << xlg)
 };
 
+#ifndef PF_STRAT_DBL
+#define PF_STRAT_DBL 1  // stratified check decided in double away from the boundary
+#endif
 struct Pos {
     uint64_t D, Qtot, rho;
     Key key;
@@ -171,6 +174,7 @@ __device__ __forceinline__ uint32_t count_below_sys_fast(const Pos& z, uint64_t 
 
 // Stratified: the common case (k* not within 2^-12 of an integer), branch-free: stratum n
 // decides itself by one exact position check (strata below n lie below v, above n above).
+template <bool SD = false>
 __device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_t v, bool* slow) {
     const double kf = fma(static_cast<double>(v), z.A, -z.Bc);
     const double fl = floor(kf);
@@ -180,8 +184,20 @@ __device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_
     const int n = static_cast<int>(fl);
     const int nc = min(max(n, 0), P - 1);
     const u32x4 r = philox10(static_cast<uint32_t>(nc >> 1), 0u, 2u, z.filt, z.key.k0, z.key.k1);
-    const uint64_t rho = mulhi64((nc & 1) ? hi_word(r) : lo_word(r), z.D);
-    const uint32_t below = (mulhi64(static_cast<uint64_t>(nc) * z.D + rho, z.Qtot) < v) ? 1u : 0u;
+    const uint64_t R = (nc & 1) ? hi_word(r) : lo_word(r);
+    // x_n < v  <=>  rho_n < fr D  <=>  rho_n / D < fr, and rho_n / D = mulhi(R, D) / D lies in
+    // (R 2^-64 - 1/D, R 2^-64]: decided in double away from the boundary (|kf| error < 2^-19 for
+    // k* < 2^31, 1/D <= 2^-33, so a 2^-18 band is safe), exactly within it (rare)
+    uint32_t below;
+    const double u = static_cast<double>(R) * 0x1p-64;
+    if (SD && u + 0x1p-18 < fr) {
+        below = 1u;
+    } else if (SD && u > fr + 0x1p-18) {
+        below = 0u;
+    } else {
+        const uint64_t rho = mulhi64(R, z.D);
+        below = (mulhi64(static_cast<uint64_t>(nc) * z.D + rho, z.Qtot) < v) ? 1u : 0u;
+    }
     return (n < 0) ? 0u : (n >= P ? static_cast<uint32_t>(P) : static_cast<uint32_t>(n) + below);
 }
 
@@ -193,7 +209,7 @@ __device__ __forceinline__ uint32_t count_below_strat_fast(const Pos& z, uint64_
 #endif
 // E for the 4 particles of a row: running sum from run0, fast paths with an exact redo of the
 // (rare) rows holding a near-integer k*
-template <int SCHEME, bool KFR = false>
+template <int SCHEME, bool KFR = false, bool SD = false>
 __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const float* w4, int kfx, uint32_t* E4) {
     if (SCHEME == 3) {
         bool any_slow = false;
@@ -240,7 +256,7 @@ __device__ __forceinline__ void count_row(const Pos& z, uint64_t run0, const flo
         for (int q = 0; q < 4; ++q) {
             run += quantise(w4[q], kfx);
             bool sl;
-            E4[q] = count_below_strat_fast(z, run, &sl);
+            E4[q] = count_below_strat_fast<SD>(z, run, &sl);
             any_slow |= sl;
         }
         if (any_slow) {
@@ -1056,8 +1072,10 @@ __global__ void __launch_bounds__(FT, (fused_min_blocks<FT, PERM>())) k_fused_so
             // the w C estimate: measured faster without the permutation in CTAs of <= 512
             // threads (C3 resample 0.3845 -> 0.381 ms, bucket mode 1.116 -> 1.10 ms) and slower
             // with it, in 1024-thread CTAs or in the cooperative kernel (more live registers)
-            count_row<(SCHEME == kBuckets ? 3 : SCHEME), PF_KF_RUN && PERM == 0 && FT <= 512>(z, O + s_wt[j][warp] + ex[j], v + j * 4,
-                                                                              a.kfx, E + j * 4);
+            // (and the stratified check in double away from its boundary, without the state
+            // gather: C3 stratified resample 0.775 -> 0.738 ms, with the gather 1.905 -> 2.12 ms)
+            count_row<(SCHEME == kBuckets ? 3 : SCHEME), PF_KF_RUN && PERM == 0 && FT <= 512,
+                      PF_STRAT_DBL && PERM < 2>(z, O + s_wt[j][warp] + ex[j], v + j * 4, a.kfx, E + j * 4);
             if (SCHEME == kBuckets) {
                 // the multinomial's search structure: Q_i of every particle (u64, 2 x 16-byte stores)
                 uint64_t r = O + s_wt[j][warp] + ex[j];
